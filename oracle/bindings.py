@@ -1,0 +1,165 @@
+"""oracle/bindings.py — TEST INFRASTRUCTURE ONLY.
+
+ctypes access to the two CPU checkers:
+  * "oracle": liboracle.so, the C restatement (oracle/auxamg_oracle.c)
+  * "ref":    _ref/libauxamg_ref.so, the unmodified reference headers
+              compiled through oracle/ref_shim.cpp
+
+Only tests/, __graft_entry__.smoke() and bench.py's CPU legs import this.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import sys
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(_HERE))
+from paper_1209_5421_b200 import _abi  # noqa: E402
+
+_LIBS = {}
+
+
+def lib_path(kind: str) -> str:
+    return os.path.join(_HERE, "liboracle.so") if kind == "oracle" else \
+        os.path.join(_HERE, "_ref", "libauxamg_ref.so")
+
+
+def available(kind: str) -> bool:
+    return os.path.exists(lib_path(kind))
+
+
+def _load(kind: str):
+    if kind in _LIBS:
+        return _LIBS[kind]
+    lib = C.CDLL(lib_path(kind))
+    p = "orc_" if kind == "oracle" else "ref_"
+    f = lambda name: getattr(lib, p + name)  # noqa: E731
+    f("setup").argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.POINTER(C.c_void_p), C.c_char_p, C.c_size_t]
+    f("solve").argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_char_p, C.c_size_t]
+    f("destroy").argtypes = [C.c_void_p]
+    f("n_levels").argtypes = [C.c_void_p]
+    for name in ("grid", "stats", "level_info_get", "export_level", "export_coarsest"):
+        f(name).restype = C.c_int
+    f("grid").argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+    f("stats").argtypes = [C.c_void_p, C.c_void_p]
+    f("locality").argtypes = [C.c_void_p, C.c_void_p]
+    f("level_info_get").argtypes = [C.c_void_p, C.c_int32, C.c_void_p]
+    f("export_level").argtypes = [C.c_void_p, C.c_int32, C.c_void_p]
+    f("export_coarsest").argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+    f("choose_depth").argtypes = [C.c_long, C.POINTER(C.c_int)]
+    f("subregion_of_point").argtypes = [C.c_double, C.c_double, C.c_void_p, C.c_int, C.POINTER(C.c_int)]
+    f("point_gs_sweep_ell").argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_char_p, C.c_size_t]
+    f("dot").argtypes = [C.c_void_p, C.c_void_p, C.c_int64]
+    f("dot").restype = C.c_double
+    if kind == "ref":
+        lib.ref_set_num_threads.argtypes = [C.c_int]
+    _LIBS[kind] = (lib, p)
+    return _LIBS[kind]
+
+
+def csr_view(A):
+    v = _abi.CsrView(A.n_rows, A.n_cols, A.nnz, A.row_ptr.ctypes.data, A.col_idx.ctypes.data,
+                     A.values.ctypes.data)
+    return v
+
+
+def setup_opts(coarsest_size=64, strict_locality=False, lump_locality=False, symmetry_tol=1e-10):
+    return _abi.SetupOpts(coarsest_size, int(strict_locality), int(lump_locality), symmetry_tol)
+
+
+def cycle_opts(n_inner=2, pre_sweeps=1, post_sweeps=1, max_outer=100, rtol=1e-6, max_directions=0):
+    return _abi.CycleOpts(n_inner, pre_sweeps, post_sweeps, max_outer, rtol, max_directions)
+
+
+class CpuHierarchy:
+    """Handle to a hierarchy built by one of the CPU checkers."""
+
+    def __init__(self, kind, A, coords, opts=None):
+        self.kind = kind
+        self.lib, self.p = _load(kind)
+        self._A = A
+        coords = np.ascontiguousarray(coords, dtype=np.float64)
+        self._xy = coords
+        self.h = C.c_void_p()
+        msg = C.create_string_buffer(512)
+        o = opts if opts is not None else setup_opts()
+        s = self._f("setup")(C.byref(csr_view(A)), coords.ctypes.data, coords.shape[0] if coords.ndim == 2 else coords.size // 2,
+                             C.byref(o), C.byref(self.h), msg, 512)
+        _abi.raise_for(s, msg.raw)
+
+    def _f(self, name):
+        return getattr(self.lib, self.p + name)
+
+    def __del__(self):
+        try:
+            if self.h:
+                self._f("destroy")(self.h)
+                self.h = C.c_void_p()
+        except Exception:
+            pass
+
+    def solve(self, b, opts=None, A=None):
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        o = opts if opts is not None else cycle_opts()
+        n = self._A.n_rows
+        u = np.zeros(max(n, 1), np.float64)
+        hist = np.zeros(o.max_outer + 2, np.float64)
+        res = _abi.SolveResultC(u.ctypes.data, hist.ctypes.data, hist.size, 0, 0, 0, 0.0, 0.0, 0.0)
+        msg = C.create_string_buffer(512)
+        av = C.byref(csr_view(A)) if A is not None else None
+        s = self._f("solve")(self.h, av, b.ctypes.data, b.size, C.byref(o), C.byref(res), msg, 512)
+        _abi.raise_for(s, msg.raw)
+        return {"u": u[:n], "residual_history": hist[: res.history_len].copy(), "iterations": res.iterations,
+                "converged": bool(res.converged), "solve_seconds": res.solve_seconds}
+
+    def export(self):
+        f = self._f
+        return _abi.collect_hierarchy(
+            lambda: f("n_levels")(self.h),
+            lambda i, o: f("level_info_get")(self.h, i, o),
+            lambda i, o: f("export_level")(self.h, i, o),
+            lambda box, d: f("grid")(self.h, box, d),
+            lambda o: f("locality")(self.h, o),
+            lambda o: f("stats")(self.h, o),
+            lambda n, lu, perm: f("export_coarsest")(self.h, n, lu, perm),
+        )
+
+
+def set_ref_threads(n: int) -> None:
+    lib, _ = _load("ref")
+    lib.ref_set_num_threads(n)
+
+
+def choose_depth(kind, n):
+    lib, p = _load(kind)
+    d = C.c_int()
+    s = getattr(lib, p + "choose_depth")(n, C.byref(d))
+    _abi.raise_for(s, b"choose_depth")
+    return d.value
+
+
+def subregion_of_point(kind, x, y, box, k):
+    lib, p = _load(kind)
+    b = (C.c_double * 4)(*box)
+    c = C.c_int()
+    s = getattr(lib, p + "subregion_of_point")(x, y, b, k, C.byref(c))
+    _abi.raise_for(s, b"subregion_of_point")
+    return c.value
+
+
+def point_gs_sweep_ell(kind, k, col, val, b, x, dir_):
+    lib, p = _load(kind)
+    x = np.array(x, dtype=np.float64, copy=True)
+    msg = C.create_string_buffer(256)
+    s = getattr(lib, p + "point_gs_sweep_ell")(k, col.ctypes.data, val.ctypes.data, b.ctypes.data,
+                                               x.ctypes.data, dir_, msg, 256)
+    _abi.raise_for(s, msg.raw)
+    return x
+
+
+def dot(kind, a, b):
+    lib, p = _load(kind)
+    return getattr(lib, p + "dot")(a.ctypes.data, b.ctypes.data, a.size)

@@ -1,0 +1,227 @@
+// oracle/ref_shim.cpp — TEST INFRASTRUCTURE ONLY.
+//
+// Exposes the UNMODIFIED reference library (/root/reference/proj/include/auxamg,
+// header-only C++20) through the same plain C ABI as oracle/auxamg_oracle.c
+// (ref_ prefix), so tests can pin the C restatement against the reference
+// itself and bench.py can time the reference's own CPU path.  Built by
+// oracle/Makefile into oracle/_ref/libauxamg_ref.so (git-ignored; the .so
+// travels to the GPU box, the reference sources do not).
+#include <cstring>
+#include <exception>
+#include <span>
+#include <string>
+#include <vector>
+
+#include "auxamg/auxamg.hpp"
+#include "../include/auxamg_b200.h"
+
+namespace {
+
+struct RefH {
+    auxamg::Hierarchy h;
+};
+
+template <class F>
+int guarded(char* msg, size_t len, F&& f) {
+    auto put = [&](const std::exception& ex) {
+        if (msg && len) std::snprintf(msg, len, "%s", ex.what());
+    };
+    try {
+        f();
+        return AUX_OK;
+    } catch (const auxamg::size_error& e) { put(e); return AUX_SIZE_ERROR; }
+    catch (const auxamg::capacity_error& e) { put(e); return AUX_CAPACITY_ERROR; }
+    catch (const auxamg::structure_error& e) { put(e); return AUX_STRUCTURE_ERROR; }
+    catch (const auxamg::argument_error& e) { put(e); return AUX_ARGUMENT_ERROR; }
+    catch (const auxamg::geometry_error& e) { put(e); return AUX_GEOMETRY_ERROR; }
+    catch (const auxamg::definiteness_error& e) { put(e); return AUX_DEFINITENESS_ERROR; }
+    catch (const auxamg::singular_error& e) { put(e); return AUX_SINGULAR_ERROR; }
+    catch (const auxamg::io_error& e) { put(e); return AUX_IO_ERROR; }
+    catch (const auxamg::parse_error& e) { put(e); return AUX_PARSE_ERROR; }
+    catch (const std::exception& e) { put(e); return AUX_INTERNAL_ERROR; }
+}
+
+auxamg::CsrMatrix to_csr(const aux_csr_view* v) {
+    auxamg::CsrMatrix A;
+    A.n_rows = v->n_rows;
+    A.n_cols = v->n_cols;
+    A.row_ptr.assign(v->row_ptr, v->row_ptr + v->n_rows + 1);
+    A.col_idx.assign(v->col_idx, v->col_idx + v->nnz);
+    A.values.assign(v->values, v->values + v->nnz);
+    return A;
+}
+
+}  // namespace
+
+extern "C" {
+
+void ref_set_num_threads(int n) { auxamg::set_num_threads(n); }
+
+int ref_setup(const aux_csr_view* Av, const double* xy, int64_t n_points, const aux_setup_opts* o,
+              void** out, char* msg, size_t len) {
+    *out = nullptr;
+    return guarded(msg, len, [&] {
+        auxamg::CsrMatrix A = to_csr(Av);
+        std::vector<auxamg::Point> pts(static_cast<std::size_t>(n_points));
+        for (int64_t i = 0; i < n_points; ++i) pts[i] = {xy[2 * i], xy[2 * i + 1]};
+        auxamg::SetupOptions so;
+        so.coarsest_size = o->coarsest_size;
+        so.strict_locality = o->strict_locality != 0;
+        so.lump_locality = o->lump_locality != 0;
+        so.symmetry_tol = o->symmetry_tol;
+        auto* r = new RefH{auxamg::setup_hierarchy(A, pts, so)};
+        *out = r;
+    });
+}
+
+void ref_destroy(void* h) { delete static_cast<RefH*>(h); }
+
+int ref_solve(void* hp, const aux_csr_view* Av, const double* b, int64_t n_b, const aux_cycle_opts* o,
+              aux_solve_result* res, char* msg, size_t len) {
+    auto* H = static_cast<RefH*>(hp);
+    return guarded(msg, len, [&] {
+        auxamg::CycleOptions co;
+        co.n_inner = o->n_inner;
+        co.pre_sweeps = o->pre_sweeps;
+        co.post_sweeps = o->post_sweeps;
+        co.max_outer = o->max_outer;
+        co.rtol = o->rtol;
+        co.max_directions = o->max_directions;
+        std::span<const double> bs(b, static_cast<std::size_t>(n_b));
+        auxamg::SolveResult r;
+        if (Av) {
+            const auxamg::CsrMatrix A = to_csr(Av);
+            r = auxamg::solve(A, bs, H->h, co);
+        } else {
+            r = auxamg::solve(H->h.levels.front().csr, bs, H->h, co);
+        }
+        if (res->u) std::memcpy(res->u, r.u.data(), r.u.size() * sizeof(double));
+        res->history_len = static_cast<int32_t>(r.residual_history.size());
+        for (std::size_t i = 0; i < r.residual_history.size() && static_cast<int>(i) < res->history_capacity; ++i)
+            res->residual_history[i] = r.residual_history[i];
+        res->iterations = r.iterations;
+        res->converged = r.converged ? 1 : 0;
+        res->setup_seconds = r.setup_seconds;
+        res->solve_seconds = r.solve_seconds;
+        res->total_seconds = r.total_seconds;
+    });
+}
+
+int ref_n_levels(void* hp) { return static_cast<RefH*>(hp)->h.n_levels(); }
+
+int ref_grid(void* hp, double box[4], int32_t* depth) {
+    const auto& g = static_cast<RefH*>(hp)->h.grid;
+    box[0] = g.a1; box[1] = g.b1; box[2] = g.a2; box[3] = g.b2;
+    *depth = g.depth;
+    return AUX_OK;
+}
+
+int ref_locality(void* hp, aux_locality* out) {
+    const auto& l = static_cast<RefH*>(hp)->h.locality;
+    out->dropped = l.dropped; out->dropped_mass = l.dropped_mass;
+    out->lumped = l.lumped; out->lumped_mass = l.lumped_mass;
+    return AUX_OK;
+}
+
+int ref_stats(void* hp, aux_stats_out* s) {
+    const auxamg::HierarchyStats st = auxamg::stats(static_cast<RefH*>(hp)->h);
+    s->levels = st.levels;
+    for (int i = 0; i < st.levels && i < AUX_MAX_LEVELS; ++i) { s->sizes[i] = st.sizes[i]; s->nnz[i] = st.nnz[i]; }
+    s->operator_complexity = st.operator_complexity;
+    return AUX_OK;
+}
+
+int ref_level_info_get(void* hp, int32_t l, aux_level_info* o) {
+    const auto& h = static_cast<RefH*>(hp)->h;
+    if (l < 0 || l >= h.n_levels()) return AUX_ARGUMENT_ERROR;
+    const auxamg::Level& lv = h.levels[l];
+    std::memset(o, 0, sizeof *o);
+    o->k = lv.k; o->structured = lv.structured; o->n = lv.n; o->nnz = lv.nnz;
+    o->has_map = lv.to_coarser.agg_of.empty() ? 0 : 1;
+    o->map_level = lv.to_coarser.level;
+    o->n_aggregates = lv.to_coarser.n_aggregates;
+    o->n_items = lv.schedule.n_items();
+    long pool = 0;
+    for (int s : lv.blocks.block_size) pool += static_cast<long>(s) * s;
+    o->block_pool = pool;
+    return AUX_OK;
+}
+
+int ref_export_level(void* hp, int32_t l, aux_level_export* x) {
+    const auto& h = static_cast<RefH*>(hp)->h;
+    if (l < 0 || l >= h.n_levels()) return AUX_ARGUMENT_ERROR;
+    const auxamg::Level& lv = h.levels[l];
+    const auto& m = lv.to_coarser;
+    if (!m.agg_of.empty()) {
+        if (x->agg_of) std::memcpy(x->agg_of, m.agg_of.data(), 4 * m.agg_of.size());
+        if (x->member_ptr) std::memcpy(x->member_ptr, m.member_ptr.data(), 4 * m.member_ptr.size());
+        if (x->member_idx) std::memcpy(x->member_idx, m.member_idx.data(), 4 * m.member_idx.size());
+    }
+    if (x->active) std::memcpy(x->active, lv.active.data(), lv.active.size());
+    if (x->item_color && !lv.schedule.item_color.empty())
+        std::memcpy(x->item_color, lv.schedule.item_color.data(), 4 * lv.schedule.item_color.size());
+    if (lv.structured) {
+        if (x->ell_col) std::memcpy(x->ell_col, lv.ell.col_idx.data(), 4 * lv.ell.col_idx.size());
+        if (x->ell_val) std::memcpy(x->ell_val, lv.ell.values.data(), 8 * lv.ell.values.size());
+    }
+    if (!lv.blocks.block_size.empty()) {
+        long off = 0, poff = 0;
+        const int nb = static_cast<int>(lv.blocks.block_size.size());
+        for (int g = 0; g < nb; ++g) {
+            const int s = lv.blocks.block_size[g];
+            if (x->block_size) x->block_size[g] = s;
+            if (x->block_offset) x->block_offset[g] = off;
+            if (s && x->block_lu) std::memcpy(x->block_lu + off, lv.blocks.factors[g].lu.data.data(), 8 * static_cast<size_t>(s) * s);
+            if (s && x->block_perm) std::memcpy(x->block_perm + poff, lv.blocks.factors[g].perm.data(), 4 * static_cast<size_t>(s));
+            off += static_cast<long>(s) * s;
+            poff += s;
+        }
+        if (x->block_offset) x->block_offset[nb] = off;
+    }
+    return AUX_OK;
+}
+
+int ref_export_coarsest(void* hp, int32_t* n, double* lu, int32_t* perm) {
+    const auto& c = static_cast<RefH*>(hp)->h.coarsest;
+    *n = c.lu.n_rows;
+    if (lu) std::memcpy(lu, c.lu.data.data(), 8 * c.lu.data.size());
+    if (perm) std::memcpy(perm, c.perm.data(), 4 * c.perm.size());
+    return AUX_OK;
+}
+
+// Kernel-level hooks used by the KAT tests.
+int ref_choose_depth(long n, int* depth) {
+    char m[8];
+    return guarded(m, sizeof m, [&] { *depth = auxamg::choose_depth(n); });
+}
+
+int ref_subregion_of_point(double x, double y, const double box[4], int k, int* cell) {
+    char m[8];
+    return guarded(m, sizeof m, [&] {
+        auxamg::AuxGrid g;
+        g.a1 = box[0]; g.b1 = box[1]; g.a2 = box[2]; g.b2 = box[3];
+        g.depth = k;
+        *cell = auxamg::subregion_of_point(x, y, g, k);
+    });
+}
+
+int ref_point_gs_sweep_ell(int k, const int* col, const double* val, const double* b, double* x, int dir,
+                           char* msg, size_t len) {
+    return guarded(msg, len, [&] {
+        const int n = 1 << (2 * k);
+        auxamg::EllMatrix A(n, 9);
+        A.col_idx.assign(col, col + 9 * n);
+        A.values.assign(val, val + 9 * n);
+        const auxamg::ColorSchedule s = auxamg::make_schedule(k, std::vector<std::uint8_t>(n, 1));
+        std::span<const double> bs(b, n);
+        std::span<double> xs(x, n);
+        auxamg::point_gs_sweep(A, bs, xs, s, dir == 0 ? auxamg::SweepDirection::forward
+                                                      : auxamg::SweepDirection::transposed);
+    });
+}
+
+double ref_dot(const double* a, const double* b, int64_t n) {
+    return auxamg::dot(std::span<const double>(a, n), std::span<const double>(b, n));
+}
+
+}  // extern "C"
