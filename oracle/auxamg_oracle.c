@@ -572,6 +572,7 @@ int orc_setup(const aux_csr_view* Av, const double* xy, int64_t n_points, const 
         return e.code;
     }
     aux_setup_opts opts = *opts_in;
+    h->a1 = 0.0; h->b1 = 1.0; h->a2 = 0.0; h->b2 = 1.0; h->depth = 1;   /* AuxGrid defaults, auxgrid.hpp:30-37 */
     Csr A = {Av->n_rows, Av->n_cols, (int*)Av->row_ptr, (int*)Av->col_idx, (double*)Av->values, (long)Av->nnz};
     if (A.n_rows != A.n_cols) fail(&e, AUX_SIZE_ERROR, "setup_hierarchy: matrix not square");
     if (n_points != A.n_rows) fail(&e, AUX_SIZE_ERROR, "setup_hierarchy: coordinate count does not match matrix order");

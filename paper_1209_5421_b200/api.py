@@ -1,0 +1,276 @@
+"""Python mirror of the reference's C++ solver API, bound to the CUDA library
+through the C ABI (include/auxamg_b200.h).
+
+    setup_hierarchy(A, coords, opts)   auxamg::setup_hierarchy   hierarchy.hpp:315-386
+    solve(A, b, h, opts)               auxamg::solve             cycle.hpp:202-247
+    stats(h)                           auxamg::stats             hierarchy.hpp:395-406
+    set_num_threads(n)                 auxamg::set_num_threads   parallel.hpp:43 (no-op)
+
+Same option fields and defaults (SetupOptions hierarchy.hpp:29-34,
+CycleOptions cycle.hpp:30-37), same result fields (SolveResult cycle.hpp:47-55)
+and the same exception classes (errors.hpp:13-76).  There is no CPU path:
+importing this module on a machine without the built library raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _abi
+from ._abi import (AuxamgError, SizeError, CapacityError, StructureError, ArgumentError,  # noqa: F401
+                   GeometryError, DefinitenessError, SingularError, IoError, ParseError, DeviceError)
+from .problems import CsrMatrix, LinearSystem  # noqa: F401
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libauxamg_b200.so")
+_lib = None
+
+
+def lib():
+    """The loaded CUDA library; raises if it was not built (no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise OSError(f"{LIB_PATH} not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    L = C.CDLL(LIB_PATH)
+    vp, i32, i64, sz = C.c_void_p, C.c_int32, C.c_int64, C.c_size_t
+    L.aux_setup.argtypes = [vp, vp, i64, vp, vp, C.POINTER(vp), C.c_char_p, sz]
+    L.aux_setup_device.argtypes = [vp, vp, i64, vp, vp, C.POINTER(vp), C.c_char_p, sz]
+    L.aux_solve.argtypes = [vp, vp, vp, i64, vp, vp, C.c_char_p, sz]
+    L.aux_solve_device.argtypes = [vp, vp, i64, vp, vp, C.c_char_p, sz]
+    for f in ("aux_setup", "aux_setup_device", "aux_solve", "aux_solve_device", "aux_stats", "aux_get_locality",
+              "aux_grid", "aux_level_info_get", "aux_export_level", "aux_export_coarsest", "aux_profile_read",
+              "aux_last_timing"):
+        getattr(L, f).restype = C.c_int
+    L.aux_stats.argtypes = [vp, vp]
+    L.aux_get_locality.argtypes = [vp, vp]
+    L.aux_grid.argtypes = [vp, vp, vp]
+    L.aux_n_levels.argtypes = [vp]
+    L.aux_n_levels.restype = i32
+    L.aux_level_info_get.argtypes = [vp, i32, vp]
+    L.aux_export_level.argtypes = [vp, i32, vp]
+    L.aux_export_coarsest.argtypes = [vp, vp, vp, vp]
+    L.aux_destroy.argtypes = [vp]
+    L.aux_launch_count.restype = i64
+    L.aux_profile_enable.argtypes = [vp, i32]
+    L.aux_profile_read.argtypes = [vp, i32, C.POINTER(i64), C.POINTER(C.c_double), C.POINTER(C.c_double)]
+    L.aux_last_timing.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+    L.aux_version.restype = C.c_char_p
+    L.aux_set_num_threads.argtypes = [i32]
+    _lib = L
+    return L
+
+
+@dataclass
+class SetupOptions:
+    """auxamg::SetupOptions (hierarchy.hpp:29-34)."""
+    coarsest_size: int = 64
+    strict_locality: bool = False
+    lump_locality: bool = False
+    symmetry_tol: float = 1e-10
+
+    def c(self):
+        return _abi.SetupOpts(self.coarsest_size, int(self.strict_locality), int(self.lump_locality),
+                              self.symmetry_tol)
+
+
+@dataclass
+class CycleOptions:
+    """auxamg::CycleOptions (cycle.hpp:30-37)."""
+    n_inner: int = 2
+    pre_sweeps: int = 1
+    post_sweeps: int = 1
+    max_outer: int = 100
+    rtol: float = 1e-6
+    max_directions: int = 0
+
+    def c(self):
+        return _abi.CycleOpts(self.n_inner, self.pre_sweeps, self.post_sweeps, self.max_outer, self.rtol,
+                              self.max_directions)
+
+
+@dataclass
+class GpuOptions:
+    """B200-only knobs (not part of the reference option structs)."""
+    device: int = 0
+    coarse_solve: int = 0        # 0 explicit inverse, 1 LU in reference order
+    fused_max_cells: int = -1
+    use_graphs: bool = True
+
+    def c(self):
+        o = _abi.GpuOpts()
+        o.device, o.coarse_solve, o.fused_max_cells, o.use_graphs = (self.device, self.coarse_solve,
+                                                                     self.fused_max_cells, int(self.use_graphs))
+        return o
+
+
+@dataclass
+class SolveResult:
+    """auxamg::SolveResult (cycle.hpp:47-55)."""
+    u: np.ndarray
+    residual_history: list = field(default_factory=list)
+    iterations: int = 0
+    converged: bool = False
+    setup_seconds: float = 0.0
+    solve_seconds: float = 0.0
+    total_seconds: float = 0.0
+
+
+@dataclass
+class HierarchyStats:
+    """auxamg::HierarchyStats (hierarchy.hpp:388-393)."""
+    levels: int
+    sizes: list
+    nnz: list
+    operator_complexity: float
+
+
+def _csr_view(A: CsrMatrix):
+    return _abi.CsrView(A.n_rows, A.n_cols, int(A.values.size), A.row_ptr.ctypes.data,
+                        A.col_idx.ctypes.data, A.values.ctypes.data)
+
+
+def _prep_csr(A: CsrMatrix) -> CsrMatrix:
+    return CsrMatrix(int(A.n_rows), int(A.n_cols), np.ascontiguousarray(A.row_ptr, np.int32),
+                     np.ascontiguousarray(A.col_idx, np.int32), np.ascontiguousarray(A.values, np.float64))
+
+
+class Hierarchy:
+    """Device-resident auxamg::Hierarchy (hierarchy.hpp:301-309)."""
+
+    def __init__(self, handle, A: CsrMatrix | None, n: int):
+        self._h = handle
+        self._A = A   # keeps the host arrays alive: solve(A, ...) reuses the device copy
+        self.n = n
+
+    @property
+    def handle(self):
+        return self._h
+
+    def __del__(self):
+        try:
+            if self._h:
+                lib().aux_destroy(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+    def n_levels(self) -> int:
+        return lib().aux_n_levels(self._h)
+
+    def stats(self) -> HierarchyStats:
+        return stats(self)
+
+    def locality(self):
+        loc = _abi.Locality()
+        lib().aux_get_locality(self._h, C.byref(loc))
+        return loc.dropped, loc.dropped_mass, loc.lumped, loc.lumped_mass
+
+    def export(self) -> dict:
+        """Every Hierarchy field in the reference's layout (for parity checks)."""
+        L, h = lib(), self._h
+        return _abi.collect_hierarchy(
+            lambda: L.aux_n_levels(h),
+            lambda i, o: L.aux_level_info_get(h, i, o),
+            lambda i, o: L.aux_export_level(h, i, o),
+            lambda box, d: L.aux_grid(h, box, d),
+            lambda o: L.aux_get_locality(h, o),
+            lambda o: L.aux_stats(h, o),
+            lambda n, lu, perm: L.aux_export_coarsest(h, n, lu, perm),
+        )
+
+    def profile(self, on: bool) -> None:
+        lib().aux_profile_enable(self._h, int(on))
+
+    def profile_read(self, kind: int):
+        n, ms, by = C.c_int64(), C.c_double(), C.c_double()
+        _abi.raise_for(lib().aux_profile_read(self._h, kind, C.byref(n), C.byref(ms), C.byref(by)), b"profile")
+        return n.value, ms.value, by.value
+
+    def last_timing(self):
+        a, b = C.c_double(), C.c_double()
+        lib().aux_last_timing(self._h, C.byref(a), C.byref(b))
+        return a.value, b.value
+
+
+def set_num_threads(n: int) -> None:
+    lib().aux_set_num_threads(n)
+
+
+def setup_hierarchy(A: CsrMatrix, coords, opts: SetupOptions | None = None,
+                    gpu: GpuOptions | None = None) -> Hierarchy:
+    A = _prep_csr(A)
+    xy = np.ascontiguousarray(coords, dtype=np.float64)
+    npts = xy.shape[0] if xy.ndim == 2 else xy.size // 2
+    o = (opts or SetupOptions()).c()
+    g = (gpu or GpuOptions()).c()
+    h = C.c_void_p()
+    msg = C.create_string_buffer(512)
+    s = lib().aux_setup(C.byref(_csr_view(A)), xy.ctypes.data, npts, C.byref(o), C.byref(g), C.byref(h), msg, 512)
+    _abi.raise_for(s, msg.raw)
+    return Hierarchy(h, A, A.n_rows)
+
+
+def setup_hierarchy_device(n: int, nnz: int, row_ptr: int, col_idx: int, values: int, xy: int, n_points: int,
+                           opts: SetupOptions | None = None, gpu: GpuOptions | None = None) -> Hierarchy:
+    """setup_hierarchy with every input already in device memory (raw pointers)."""
+    v = _abi.CsrView(n, n, nnz, row_ptr, col_idx, values)
+    o = (opts or SetupOptions()).c()
+    g = (gpu or GpuOptions()).c()
+    h = C.c_void_p()
+    msg = C.create_string_buffer(512)
+    s = lib().aux_setup_device(C.byref(v), xy, n_points, C.byref(o), C.byref(g), C.byref(h), msg, 512)
+    _abi.raise_for(s, msg.raw)
+    return Hierarchy(h, None, n)
+
+
+def solve(A: CsrMatrix | None, b, h: Hierarchy, opts: CycleOptions | None = None) -> SolveResult:
+    """solve(A, b, h, opts).  A may be None or the matrix given to setup."""
+    o = (opts or CycleOptions()).c()
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    n = h.n
+    u = np.zeros(max(n, 1), np.float64)
+    hist = np.zeros(o.max_outer + 2, np.float64)
+    res = _abi.SolveResultC(u.ctypes.data, hist.ctypes.data, hist.size, 0, 0, 0, 0.0, 0.0, 0.0)
+    msg = C.create_string_buffer(512)
+    av = None
+    if A is not None:
+        if h._A is not None and A is not h._A and _same_arrays(A, h._A):
+            A = h._A
+        av = C.byref(_csr_view(A if A is h._A else _prep_csr(A)))
+    s = lib().aux_solve(h.handle, av, b.ctypes.data, b.size, C.byref(o), C.byref(res), msg, 512)
+    _abi.raise_for(s, msg.raw)
+    return SolveResult(u[:n].copy(), list(hist[: res.history_len]), res.iterations, bool(res.converged),
+                       res.setup_seconds, res.solve_seconds, res.total_seconds)
+
+
+def solve_device(h: Hierarchy, b_ptr: int, u_ptr: int, n: int, opts: CycleOptions | None = None) -> SolveResult:
+    """solve() with b and u in device memory (raw pointers, caller DoF order)."""
+    o = (opts or CycleOptions()).c()
+    hist = np.zeros(o.max_outer + 2, np.float64)
+    res = _abi.SolveResultC(u_ptr, hist.ctypes.data, hist.size, 0, 0, 0, 0.0, 0.0, 0.0)
+    msg = C.create_string_buffer(512)
+    s = lib().aux_solve_device(h.handle, b_ptr, n, C.byref(o), C.byref(res), msg, 512)
+    _abi.raise_for(s, msg.raw)
+    return SolveResult(None, list(hist[: res.history_len]), res.iterations, bool(res.converged),
+                       res.setup_seconds, res.solve_seconds, res.total_seconds)
+
+
+def _same_arrays(a: CsrMatrix, b: CsrMatrix) -> bool:
+    return (a.n_rows == b.n_rows and a.values.size == b.values.size and np.array_equal(a.row_ptr, b.row_ptr)
+            and np.array_equal(a.col_idx, b.col_idx) and np.array_equal(a.values, b.values))
+
+
+def stats(h: Hierarchy) -> HierarchyStats:
+    st = _abi.StatsOut()
+    lib().aux_stats(h.handle, C.byref(st))
+    return HierarchyStats(st.levels, list(st.sizes[: st.levels]), list(st.nnz[: st.levels]),
+                          st.operator_complexity)
+
+
+def launch_count() -> int:
+    return lib().aux_launch_count()

@@ -1,0 +1,198 @@
+// common.cuh — shared device helpers, layout math and error plumbing for the
+// B200-native auxiliary-grid AMG.
+//
+// Layout of a structured level k (w = 2^k cells per side, n = 4^k cells):
+// "colour-major" order.  Cell (t1, t2) has colour c = (t1&1) | (t2&1)<<1
+// (= color_of, auxgrid.hpp:154-160) and in-plane position
+// pos = (t2>>1)*H + (t1>>1) with H = w/2; its storage index is c*nq + pos with
+// nq = n/4.  Consequences used everywhere:
+//   * every colour class of the 4-colour Gauss-Seidel (smoother.hpp:41-89) is
+//     one contiguous plane, so a colour pass streams its rows once;
+//   * the parent of a cell on level k-1 (auxgrid.hpp:138-150) has lexicographic
+//     index pos, and the 4 children of coarse cell R are c*nq + R for
+//     c = 0..3, i.e. SW, SE, NW, NE — the reference's member order, so the
+//     restriction sum (hierarchy.hpp:267-277) reads 4 coalesced planes in the
+//     reference's addition order;
+//   * 9-point neighbours (hierarchy.hpp:48-57) of a colour-c cell sit in the
+//     other three planes at pos, pos-1, pos-H, ... (coalesced).
+// The 9 stencil values of a level are 9 SoA planes val[t*n + idx] with the
+// slot order of the reference (0 = diagonal, 1..8 = E,NE,N,NW,W,SW,S,SE);
+// column indices are implicit.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+
+#include "../../include/auxamg_b200.h"
+
+namespace auxb200 {
+
+// --------------------------------------------------------------- errors
+
+struct AuxError : std::runtime_error {
+    aux_status code;
+    AuxError(aux_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] inline void throw_aux(aux_status c, const std::string& m) { throw AuxError(c, m); }
+
+#define AUX_CUDA(call)                                                                        \
+    do {                                                                                      \
+        cudaError_t e_ = (call);                                                              \
+        if (e_ != cudaSuccess)                                                                \
+            ::auxb200::throw_aux(AUX_CUDA_ERROR, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+// Host-side kernel launch counter (bench.py's gpu_launches).
+extern int64_t g_launches;
+#define AUX_LAUNCHED(n) (::auxb200::g_launches += (n))
+
+// --------------------------------------------------------------- layout
+
+// Stencil offsets of slots 1..8 (hierarchy.hpp:48-50): E, NE, N, NW, W, SW, S, SE.
+__host__ __device__ constexpr int stencil_dx(int s) {
+    return s == 1 ? 1 : s == 2 ? 1 : s == 3 ? 0 : s == 4 ? -1 : s == 5 ? -1 : s == 6 ? -1 : s == 7 ? 0 : 1;
+}
+__host__ __device__ constexpr int stencil_dy(int s) {
+    return s == 1 ? 0 : s == 2 ? 1 : s == 3 ? 1 : s == 4 ? 1 : s == 5 ? 0 : s == 6 ? -1 : s == 7 ? -1 : -1;
+}
+// stencil_slot, hierarchy.hpp:53-57.
+__host__ __device__ inline int stencil_slot(int dx, int dy) {
+    if (dx < -1 || dx > 1 || dy < -1 || dy > 1) return -1;
+    const int t = 3 * (dy + 1) + (dx + 1);
+    // table {6, 7, 8, 5, 0, 1, 4, 3, 2}
+    return t == 0 ? 6 : t == 1 ? 7 : t == 2 ? 8 : t == 3 ? 5 : t == 4 ? 0 : t == 5 ? 1 : t == 6 ? 4 : t == 7 ? 3 : 2;
+}
+
+// Geometry of one structured level k >= 1.
+struct Geo {
+    int k;       // level
+    int n;       // 4^k
+    int lq;      // log2(nq) = 2(k-1)
+    int lh;      // log2(H)  = k-1
+    int nq;      // n / 4
+    int H;       // 2^(k-1)
+};
+
+__host__ __device__ inline Geo make_geo(int k) {
+    Geo g;
+    g.k = k;
+    g.n = 1 << (2 * k);
+    g.lq = 2 * (k - 1);
+    g.lh = k - 1;
+    g.nq = 1 << g.lq;
+    g.H = 1 << g.lh;
+    return g;
+}
+
+// colour-major index of lexicographic cell (t1, t2)
+__host__ __device__ inline int cm_of_xy(const Geo& g, int t1, int t2) {
+    const int c = (t1 & 1) | ((t2 & 1) << 1);
+    return (c << g.lq) + ((t2 >> 1) << g.lh) + (t1 >> 1);
+}
+__host__ __device__ inline void xy_of_cm(const Geo& g, int idx, int& t1, int& t2) {
+    const int c = idx >> g.lq;
+    const int pos = idx & (g.nq - 1);
+    const int a = pos & (g.H - 1), b = pos >> g.lh;
+    t1 = 2 * a + (c & 1);
+    t2 = 2 * b + (c >> 1);
+}
+__host__ __device__ inline int lex_of_cm(const Geo& g, int idx) {
+    int t1, t2;
+    xy_of_cm(g, idx, t1, t2);
+    return (t2 << g.k) + t1;
+}
+__host__ __device__ inline int cm_of_lex(const Geo& g, int lex) {
+    return cm_of_xy(g, lex & ((1 << g.k) - 1), lex >> g.k);
+}
+
+// Neighbour of a cell (colour c, plane coords a, b) in slot s (1..8); returns
+// -1 when off-grid (build_stencil_indices, hierarchy.hpp:75-91).
+__device__ __forceinline__ int cm_neighbor(const Geo& g, int c, int a, int b, int s) {
+    const int ux = (c & 1) + stencil_dx(s);
+    const int uy = (c >> 1) + stencil_dy(s);
+    const int na = a + (ux >> 1);
+    const int nb = b + (uy >> 1);
+    if (na < 0 || na >= g.H || nb < 0 || nb >= g.H) return -1;
+    const int nc = (ux & 1) | ((uy & 1) << 1);
+    return (nc << g.lq) + (nb << g.lh) + na;
+}
+
+// --------------------------------------------------------------- reductions
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Deterministic grid reduction state: one partials buffer and a ticket
+// counter shared by all reduction kernels on the (single) solve stream.
+struct RedState {
+    double* partials;          // [kMaxRedBlocks * 4]
+    unsigned int* ticket;      // 1 counter
+};
+constexpr int kMaxRedBlocks = 1184;   // 148 SMs x 8
+constexpr int kRedThreads = 256;
+
+inline int red_blocks(long n) {
+    long b = (n + 2 * kRedThreads - 1) / (2 * kRedThreads);
+    if (b < 1) b = 1;
+    if (b > kMaxRedBlocks) b = kMaxRedBlocks;
+    return static_cast<int>(b);
+}
+
+// Block-level sum of NV values per thread into smem; returns true in the
+// last-finishing block, where out[v] holds the grid total (fixed-shape tree
+// over block partials => run-to-run deterministic for a fixed grid).
+template <int NV>
+__device__ bool grid_reduce(double (&v)[NV], const RedState& rs, double (&out)[NV]) {
+    __shared__ double sm[NV][kRedThreads / 32];
+    __shared__ bool last;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+        const double s = warp_sum(v[i]);
+        if (lane == 0) sm[i][wid] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+            double s = 0.0;
+            for (int w = 0; w < kRedThreads / 32; ++w) s += sm[i][w];
+            rs.partials[blockIdx.x * NV + i] = s;
+        }
+        __threadfence();
+        const unsigned int t = atomicAdd(rs.ticket, 1u);
+        last = (t == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!last) return false;
+    __threadfence();
+    // fixed-order reduction of gridDim.x partials: per-thread strided sums,
+    // then the same warp/block tree.
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+        double s = 0.0;
+        for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x)
+            s += ((volatile double*)rs.partials)[b * NV + i];
+        s = warp_sum(s);
+        if (lane == 0) sm[i][wid] = s;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+        double s = 0.0;
+        for (int w = 0; w < kRedThreads / 32; ++w) s += sm[i][w];
+        out[i] = s;
+    }
+    if (threadIdx.x == 0) *rs.ticket = 0u;
+    return true;
+}
+
+}  // namespace auxb200

@@ -1,0 +1,140 @@
+// hier.cuh — device-resident hierarchy (the GPU form of auxamg::Hierarchy,
+// hierarchy.hpp:288-309) and the solve workspace.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <vector>
+
+#include "common.cuh"
+
+namespace auxb200 {
+
+// RAII device buffer.
+template <class T>
+struct DBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    DBuf() = default;
+    explicit DBuf(size_t count) { alloc(count); }
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    DBuf(DBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+    DBuf& operator=(DBuf&& o) noexcept {
+        if (this != &o) { release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+        return *this;
+    }
+    ~DBuf() { release(); }
+    void alloc(size_t count) {
+        release();
+        n = count;
+        if (count) AUX_CUDA(cudaMalloc(&p, count * sizeof(T)));
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    T* get() const { return p; }
+};
+
+// Per-level PCG state (nonlinear_pcg, cycle.hpp:106-128) for a level that is
+// the target of a coarse-grid correction.
+struct PcgBufs {
+    DBuf<double> r;                 // PCG residual; the restriction writes rc here
+    DBuf<double> u;                 // PCG iterate (= ec of the finer level)
+    std::vector<DBuf<double>> p;    // directions (z of step i is written into p[i])
+    std::vector<DBuf<double>> ap;   // cached A p
+    // scalars: [0]=alpha [1]=beta [2]=dead flag [3..3+n_inner) energies
+    DBuf<double> sc;
+};
+
+struct Level {
+    int k = 0;
+    bool structured = false;
+    int n = 0;
+    long nnz = 0;
+    Geo geo{};
+    // structured: 9 value planes in colour-major order + active flags
+    DBuf<double> val;
+    DBuf<uint8_t> active;
+    int zero_diag_lex = -1;        // first active row (colour, then index) with a_ii == 0
+    PcgBufs pcg;                   // used when this level is a PCG target (index >= 1)
+};
+
+// Finest level (CSR, rows permuted into level-L cell order).
+struct Finest {
+    int n = 0;
+    long nnz = 0;
+    DBuf<int> rp, col;
+    DBuf<double> v;
+    DBuf<int> perm;      // new -> caller DoF id
+    DBuf<int> iperm;     // caller DoF id -> new
+    DBuf<int> cell;      // new row -> level-L colour-major cell id
+    DBuf<int> lex_of_row;// new row -> level-L lexicographic cell id (agg_of)
+    DBuf<int> bptr;      // level-L colour-major cell -> first row (n_L + 1)
+    // blocks with more than kSmallBlock members: stored LU factors
+    int n_big = 0;
+    int big_color_begin[5] = {0, 0, 0, 0, 0};   // big-block list split by colour
+    DBuf<int> big_ids;        // cell ids (colour-major), sorted by colour
+    DBuf<long long> big_off;  // offset of each big block's s*s LU in big_lu
+    DBuf<double> big_lu;
+    DBuf<int> big_perm;       // s entries per big block, indexed by first row
+    DBuf<double> scratch;     // 2N: residual + solution scratch of the big-block solves
+    bool color_clean = true;  // check_color_locality (smoother.hpp:217-231) empty
+    int max_block = 0;
+};
+
+constexpr int kSmallBlock = 4;
+
+struct Profile {
+    bool on = false;
+    std::vector<cudaEvent_t> ev_begin[4], ev_end[4];
+    size_t used[4] = {0, 0, 0, 0};
+    double bytes[4] = {0, 0, 0, 0};
+    long long launches[4] = {0, 0, 0, 0};
+    double total_ms[4] = {0, 0, 0, 0};
+};
+
+}  // namespace auxb200
+
+struct aux_hierarchy {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    aux_setup_opts opts{};
+    aux_gpu_opts gpu{};
+    int n = 0;                 // finest order
+    bool direct_only = false;  // n <= coarsest_size (hierarchy.hpp:339-344)
+    double box[4] = {0, 1, 0, 1};   // AuxGrid defaults (auxgrid.hpp:30-37)
+    int depth = 1;
+    aux_locality loc{};
+    auxb200::Finest fine;
+    std::vector<auxb200::Level> lv;   // lv[0] describes the finest level (CSR)
+    // coarsest dense factors (reference order) and explicit inverse (colour-major)
+    int nc = 0;
+    auxb200::DBuf<double> c_lu;      // nc*nc row-major, lexicographic rows/cols
+    auxb200::DBuf<int> c_perm;
+    auxb200::DBuf<double> c_inv;     // nc*nc row-major, storage order
+    auxb200::DBuf<int> c_lex;        // storage index -> lexicographic (coarsest level)
+    auxb200::DBuf<double> c_work;    // 2*nc scratch of the LU-mode coarse solve
+    // reduction state
+    auxb200::DBuf<double> red_partials;
+    auxb200::DBuf<unsigned int> red_ticket;
+    // setup-time identity of the host matrix (solve() may reuse the device copy)
+    const void* host_rp = nullptr;
+    const void* host_col = nullptr;
+    const void* host_val = nullptr;
+    long host_nnz = 0;
+    // solve workspace (outer loop)
+    auxb200::DBuf<double> w_r, w_u, w_b, w_tmp;
+    std::vector<auxb200::DBuf<double>> w_p, w_ap;
+    auxb200::DBuf<double> w_sc;      // outer scalars
+    // graph of the coarse part of the cycle (PCG at level 1)
+    cudaGraphExec_t graph = nullptr;
+    long graph_kernels = 0;
+    aux_cycle_opts graph_opts{};
+    bool graph_valid = false;
+    auxb200::Profile prof;
+    double last_setup_ms = 0.0, last_solve_ms = 0.0;
+    ~aux_hierarchy();
+};

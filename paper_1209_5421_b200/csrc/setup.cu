@@ -1,0 +1,828 @@
+// setup.cu — device setup_hierarchy (hierarchy.hpp:315-386).
+//
+// Pipeline (all on one stream, all kernels hand-written):
+//   k_validate / k_diag / k_symm     validate_csr, diagonal > 0, symmetry_defect
+//   k_bbox                            bounding_box                (auxgrid.hpp:75-91)
+//   k_cellkey                         subregion_of_point on level L, colour-major key
+//   radix_sort_pairs                  build_members (stable => members ascending)
+//   k_count / scan                    member_ptr + active flags   (hierarchy.hpp:94-98)
+//   k_permute_csr                     finest rows grouped by aggregate, entries in
+//                                     caller storage order, columns relabelled
+//   k_galerkin_L                      assemble_coarse_finest     (hierarchy.hpp:141-192):
+//                                     one thread per aggregate streams its contiguous
+//                                     rows and sums each entry into one of 9 register
+//                                     accumulators in the reference's order (the
+//                                     (agg_i, agg_j) sort is the aggregation sort above
+//                                     plus the 9-way slot key), so values are bitwise equal
+//   k_block_check / k_factor_big      factor_blocks (smoother.hpp:129-156)
+//   k_coarsen                         assemble_coarse_structured + coarsen_active
+//   k_dense / cta LU / k_inverse      dense_from_ell + lu_factor for the coarsest level
+#include <algorithm>
+#include <cstring>
+#include <numeric>
+#include <vector>
+
+#include "lu.cuh"
+#include "scan_sort.cuh"
+#include "setup.cuh"
+
+namespace auxb200 {
+
+namespace {
+
+constexpr int kT = 256;
+inline unsigned grid_for(long n, int per = 1) {
+    long b = (n + (long)kT * per - 1) / ((long)kT * per);
+    if (b < 1) b = 1;
+    if (b > 148L * 64) b = 148L * 64;
+    return static_cast<unsigned>(b);
+}
+
+#define GSTRIDE(i, n) for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < (n); i += (long)gridDim.x * blockDim.x)
+
+// ---------------------------------------------------------------- validation
+
+// validate_csr (sparse.hpp:101-116): key = row*4 + kind of the first failing
+// check in the reference's scan order; the minimum key is the reference's throw.
+__global__ void k_validate(const int* __restrict__ rp, const int* __restrict__ col, int n, long nnz, int ncols,
+                           unsigned long long* err) {
+    GSTRIDE(r, n) {
+        const int a = rp[r], b = rp[r + 1];
+        unsigned long long key = ~0ull;
+        if (a > b) {
+            key = (unsigned long long)r * 4 + 1;
+        } else {
+            const long lo = a < 0 ? 0 : a, hi = b > nnz ? nnz : b;
+            if (a < 0 || b > nnz) key = (unsigned long long)r * 4 + 2;
+            for (long p = lo; p < hi && key == ~0ull; ++p) {
+                const int c = col[p];
+                if (c < 0 || c >= ncols) key = (unsigned long long)r * 4 + 2;
+                else if (p > a && col[p - 1] >= c) key = (unsigned long long)r * 4 + 3;
+            }
+        }
+        if (key != ~0ull) atomicMin(err, key);
+    }
+}
+
+__device__ __forceinline__ int find_col(const int* col, int lo, int hi, int c) {
+    while (lo < hi) {
+        const int mid = lo + (hi - lo) / 2;
+        if (col[mid] < c) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+// A.at(r,r) <= 0 (hierarchy.hpp:321-323)
+__global__ void k_diag(const int* __restrict__ rp, const int* __restrict__ col, const double* __restrict__ v, int n,
+                       unsigned long long* err) {
+    GSTRIDE(r, n) {
+        const int a = rp[r], b = rp[r + 1];
+        const int p = find_col(col, a, b, (int)r);
+        const double d = (p < b && col[p] == r) ? v[p] : 0.0;
+        if (d <= 0.0) atomicMin(err, (unsigned long long)r);
+    }
+}
+
+// symmetry_defect (sparse.hpp:238-260): max over stored (i,j) of |a_ij - a_ji|
+// (or |a_ij| when (j,i) is absent) and max |a_ij|.  Both maxima are of
+// non-negative doubles, so they reduce exactly through atomicMax on the bits.
+__global__ void k_symm(const int* __restrict__ rp, const int* __restrict__ col, const double* __restrict__ v, int n,
+                       unsigned long long* out /* [0]=defect [1]=scale */) {
+    double dmx = 0.0, smx = 0.0;
+    GSTRIDE(i, n) {
+        for (int p = rp[i]; p < rp[i + 1]; ++p) {
+            const int j = col[p];
+            const double a = v[p];
+            const double aa = fabs(a);
+            smx = (smx < aa) ? aa : smx;
+            const int lo = rp[j], hi = rp[j + 1];
+            const int q = find_col(col, lo, hi, (int)i);
+            const double d = (q < hi && col[q] == i) ? fabs(a - v[q]) : aa;
+            dmx = (dmx < d) ? d : dmx;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double d2 = __shfl_xor_sync(0xffffffffu, dmx, o);
+        const double s2 = __shfl_xor_sync(0xffffffffu, smx, o);
+        dmx = (dmx < d2) ? d2 : dmx;
+        smx = (smx < s2) ? s2 : smx;
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMax(&out[0], (unsigned long long)__double_as_longlong(dmx));
+        atomicMax(&out[1], (unsigned long long)__double_as_longlong(smx));
+    }
+}
+
+// ---------------------------------------------------------------- quadtree
+
+__device__ __forceinline__ unsigned long long ord_key(double x) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(x);
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double ord_val(unsigned long long k) {
+    const unsigned long long b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+    return __longlong_as_double((long long)b);
+}
+
+// bounding_box (auxgrid.hpp:75-91); out = {min x, max x, min y, max y} as
+// order-preserving keys, flag[0] = any non-finite coordinate.
+__global__ void k_bbox(const double* __restrict__ xy, long n, unsigned long long* out, int* flag) {
+    unsigned long long mnx = ~0ull, mxx = 0, mny = ~0ull, mxy = 0;
+    int bad = 0;
+    GSTRIDE(i, n) {
+        const double x = xy[2 * i], y = xy[2 * i + 1];
+        if (!isfinite(x) || !isfinite(y)) { bad = 1; continue; }
+        const unsigned long long kx = ord_key(x), ky = ord_key(y);
+        mnx = min(mnx, kx); mxx = max(mxx, kx);
+        mny = min(mny, ky); mxy = max(mxy, ky);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        mnx = min(mnx, __shfl_xor_sync(0xffffffffu, mnx, o));
+        mxx = max(mxx, __shfl_xor_sync(0xffffffffu, mxx, o));
+        mny = min(mny, __shfl_xor_sync(0xffffffffu, mny, o));
+        mxy = max(mxy, __shfl_xor_sync(0xffffffffu, mxy, o));
+        bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(&out[0], mnx); atomicMax(&out[1], mxx);
+        atomicMin(&out[2], mny); atomicMax(&out[3], mxy);
+        if (bad) atomicOr(flag, 1);
+    }
+}
+
+// subregion_of_point (auxgrid.hpp:109-121) on level L with the same IEEE
+// operations (sub, div, min, exact scaling, truncation); key = colour-major id.
+__global__ void k_cellkey(const double* __restrict__ xy, long n, double a1, double b1, double a2, double b2,
+                          Geo g, unsigned* __restrict__ key) {
+    const double w = (double)(1 << g.k);
+    const double below_one = 1.0 - 2.220446049250313e-16 / 2;
+    GSTRIDE(i, n) {
+        const double qx = __ddiv_rn(__dsub_rn(xy[2 * i], a1), __dsub_rn(b1, a1));
+        const double qy = __ddiv_rn(__dsub_rn(xy[2 * i + 1], a2), __dsub_rn(b2, a2));
+        const double sx = (below_one < qx) ? below_one : qx;
+        const double sy = (below_one < qy) ? below_one : qy;
+        const int t1 = __double2int_rz(__dmul_rn(sx, w));
+        const int t2 = __double2int_rz(__dmul_rn(sy, w));
+        key[i] = (unsigned)cm_of_xy(g, t1, t2);
+    }
+}
+
+__global__ void k_count(const unsigned* __restrict__ key, long n, int* cnt) {
+    GSTRIDE(i, n) atomicAdd(&cnt[key[i]], 1);
+}
+
+__global__ void k_after_sort(const unsigned* __restrict__ key, const int* __restrict__ perm, long n, Geo g,
+                             int* __restrict__ iperm, int* __restrict__ cell, int* __restrict__ lexrow,
+                             int* __restrict__ len, const int* __restrict__ rp) {
+    GSTRIDE(i, n) {
+        const int old = perm[i];
+        iperm[old] = (int)i;
+        cell[i] = (int)key[i];
+        lexrow[i] = lex_of_cm(g, (int)key[i]);
+        len[i] = rp[old + 1] - rp[old];
+    }
+}
+
+__global__ void k_active_from_count(const int* __restrict__ bptr, int nL, uint8_t* __restrict__ act) {
+    GSTRIDE(g, nL) act[g] = bptr[g + 1] > bptr[g] ? 1 : 0;
+}
+
+// Finest rows in aggregate order; entries keep the caller's storage order
+// (every row sum of the reference runs in that order), columns relabelled.
+__global__ void k_permute_csr(const int* __restrict__ rp, const int* __restrict__ col, const double* __restrict__ v,
+                              const int* __restrict__ perm, const int* __restrict__ iperm, long n,
+                              const int* __restrict__ rpn, int* __restrict__ coln, double* __restrict__ vn) {
+    // one warp per row: coalesced copy of the row's entries
+    const int lane = threadIdx.x & 31;
+    const long warp = (blockIdx.x * (long)blockDim.x + threadIdx.x) >> 5;
+    const long nw = ((long)gridDim.x * blockDim.x) >> 5;
+    for (long i = warp; i < n; i += nw) {
+        const int old = perm[i];
+        const int a = rp[old], b = rp[old + 1], o = rpn[i];
+        for (int p = a + lane; p < b; p += 32) {
+            coln[o + (p - a)] = iperm[col[p]];
+            vn[o + (p - a)] = v[p];
+        }
+    }
+}
+
+// assemble_coarse_finest (hierarchy.hpp:141-192) for aggregate g.
+__global__ void k_galerkin_L(const int* __restrict__ bptr, const int* __restrict__ rp, const int* __restrict__ col,
+                             const double* __restrict__ v, const int* __restrict__ cell, Geo g, int lump,
+                             double* __restrict__ val, int* __restrict__ dcnt, double* __restrict__ dmass,
+                             unsigned long long* total) {
+    GSTRIDE(r, g.n) {
+        const int r0 = bptr[r], r1 = bptr[r + 1];
+        double acc[9];
+#pragma unroll
+        for (int t = 0; t < 9; ++t) acc[t] = 0.0;
+        if (r0 == r1) {
+            acc[0] = 1.0;   // inactive identity row (preset_stencil, hierarchy.hpp:121-131)
+        } else {
+            int t1, t2;
+            xy_of_cm(g, (int)r, t1, t2);
+            int nd = 0;
+            double mass = 0.0;
+            for (int i = r0; i < r1; ++i) {
+                for (int p = rp[i]; p < rp[i + 1]; ++p) {
+                    const double a = v[p];
+                    int u1, u2;
+                    xy_of_cm(g, cell[col[p]], u1, u2);
+                    const int slot = stencil_slot(u1 - t1, u2 - t2);
+                    if (slot < 0) {
+                        if (lump) acc[0] = __dadd_rn(acc[0], a);
+                        ++nd;
+                        mass = __dadd_rn(mass, fabs(a));
+                        continue;
+                    }
+#pragma unroll
+                    for (int t = 0; t < 9; ++t)
+                        if (slot == t) acc[t] = __dadd_rn(acc[t], a);
+                }
+            }
+            if (nd) {
+                dcnt[r] = nd;
+                dmass[r] = mass;
+                atomicAdd(total, (unsigned long long)nd);
+            }
+        }
+#pragma unroll
+        for (int t = 0; t < 9; ++t) val[(size_t)t * g.n + r] = acc[t];
+    }
+}
+
+// LocalityReport totals: sequential over rows in lexicographic order, as the
+// reference (hierarchy.hpp:178-187).  Only launched when something was dropped.
+__global__ void k_locality_sum(const int* __restrict__ dcnt, const double* __restrict__ dmass, Geo g, double* out) {
+    if (blockIdx.x != 0 || threadIdx.x != 0) return;
+    double m = 0.0;
+    for (int lex = 0; lex < g.n; ++lex) {
+        const int r = cm_of_lex(g, lex);
+        if (dcnt[r] == 0) continue;
+        m = __dadd_rn(m, dmass[r]);
+    }
+    *out = m;
+}
+
+// factor_blocks for 2 <= s <= kSmallBlock: factor in registers, report the
+// lowest singular aggregate (lexicographic id, the reference's loop order).
+template <int S>
+__device__ void check_small_block(const int* rp, const int* col, const double* v, int r0, Geo g, int r,
+                                  unsigned long long* err) {
+    double a[S][S];
+    int perm[S];
+#pragma unroll
+    for (int q = 0; q < S; ++q)
+#pragma unroll
+        for (int c = 0; c < S; ++c) a[q][c] = 0.0;
+#pragma unroll
+    for (int q = 0; q < S; ++q)
+        for (int p = rp[r0 + q]; p < rp[r0 + q + 1]; ++p) {
+            const unsigned off = (unsigned)(col[p] - r0);
+#pragma unroll
+            for (int c = 0; c < S; ++c)
+                if (off == (unsigned)c) a[q][c] = v[p];
+        }
+    if (!reg_lu_factor<S>(a, perm)) atomicMin(err, (unsigned long long)lex_of_cm(g, r));
+}
+
+__global__ void k_block_check(const int* __restrict__ bptr, const int* __restrict__ rp, const int* __restrict__ col,
+                              const double* __restrict__ v, Geo g, unsigned long long* err, int* big_flag,
+                              int* max_block) {
+    int mb = 0;
+    GSTRIDE(r, g.n) {
+        const int r0 = bptr[r], s = bptr[r + 1] - r0;
+        mb = max(mb, s);
+        big_flag[r] = s > kSmallBlock ? 1 : 0;
+        if (s == 2) check_small_block<2>(rp, col, v, r0, g, (int)r, err);
+        else if (s == 3) check_small_block<3>(rp, col, v, r0, g, (int)r, err);
+        else if (s == 4) check_small_block<4>(rp, col, v, r0, g, (int)r, err);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mb = max(mb, __shfl_xor_sync(0xffffffffu, mb, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(max_block, mb);
+}
+
+__global__ void k_compact(const int* __restrict__ flag, const int* __restrict__ pos, int n, int* __restrict__ out) {
+    GSTRIDE(i, n) if (flag[i]) out[pos[i]] = (int)i;
+}
+
+// Extract and factor one big block per CTA (s > kSmallBlock).
+__global__ void k_factor_big(const int* __restrict__ ids, const long long* __restrict__ off,
+                             const int* __restrict__ bptr, const int* __restrict__ rp, const int* __restrict__ col,
+                             const double* __restrict__ v, Geo g, double* __restrict__ lu, int* __restrict__ perm,
+                             unsigned long long* err) {
+    const int gid = ids[blockIdx.x];
+    const int r0 = bptr[gid], s = bptr[gid + 1] - r0;
+    double* a = lu + off[blockIdx.x];
+    for (long e = threadIdx.x; e < (long)s * s; e += blockDim.x) a[e] = 0.0;
+    __syncthreads();
+    for (int q = threadIdx.x; q < s; q += blockDim.x)
+        for (int p = rp[r0 + q]; p < rp[r0 + q + 1]; ++p) {
+            const unsigned c = (unsigned)(col[p] - r0);
+            if (c < (unsigned)s) a[(size_t)q * s + c] = v[p];
+        }
+    __syncthreads();
+    const int zc = cta_lu_factor(a, perm + r0, s);
+    if (zc >= 0 && threadIdx.x == 0) atomicMin(err, (unsigned long long)lex_of_cm(g, gid));
+}
+
+// check_color_locality (smoother.hpp:217-231): any nonzero coupling between
+// two distinct blocks of the same colour => keep per-colour snapshots.
+__global__ void k_color_check(const int* __restrict__ rp, const int* __restrict__ col, const double* __restrict__ v,
+                              const int* __restrict__ cell, long n, int lq, int* flag) {
+    GSTRIDE(i, n) {
+        const int gi = cell[i];
+        for (int p = rp[i]; p < rp[i + 1]; ++p) {
+            if (v[p] == 0.0) continue;
+            const int gj = cell[col[p]];
+            if (gi != gj && (gi >> lq) == (gj >> lq)) { atomicOr(flag, 1); break; }
+        }
+    }
+}
+
+// assemble_coarse_structured + coarsen_active (hierarchy.hpp:198-235, 101-109):
+// thread per coarse cell, children SW,SE,NW,NE (planes 0..3 at the coarse
+// lexicographic index), slots 0..8, 9 register accumulators.
+__global__ void k_coarsen(Geo gf, const double* __restrict__ vf, const uint8_t* __restrict__ af, Geo gc,
+                          double* __restrict__ vc, uint8_t* __restrict__ ac, int* overflow) {
+    const int wc = 1 << gc.k;
+    GSTRIDE(Q, gc.n) {
+        int T1, T2;
+        xy_of_cm(gc, (int)Q, T1, T2);
+        const int R = T2 * wc + T1;
+        bool act = false;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) act |= af[(c << gf.lq) + R] != 0;
+        double acc[9];
+#pragma unroll
+        for (int t = 0; t < 9; ++t) acc[t] = 0.0;
+        if (!act) {
+            acc[0] = 1.0;
+        } else {
+            for (int c = 0; c < 4; ++c) {
+                const int i = (c << gf.lq) + R;
+                if (!af[i]) continue;
+                const int t1 = 2 * T1 + (c & 1), t2 = 2 * T2 + (c >> 1);
+                acc[0] = __dadd_rn(acc[0], vf[i]);   // t = 0: the child itself, slot 0
+#pragma unroll
+                for (int t = 1; t < 9; ++t) {
+                    const int j = cm_neighbor(gf, c, T1, T2, t);
+                    if (j < 0) continue;
+                    const int q1 = (t1 + stencil_dx(t)) >> 1, q2 = (t2 + stencil_dy(t)) >> 1;
+                    const int slot = stencil_slot(q1 - T1, q2 - T2);
+                    if (slot < 0) { atomicOr(overflow, 1); continue; }
+                    const double a = vf[(size_t)t * gf.n + i];
+#pragma unroll
+                    for (int s = 0; s < 9; ++s)
+                        if (slot == s) acc[s] = __dadd_rn(acc[s], a);
+                }
+            }
+        }
+        ac[Q] = act ? 1 : 0;
+#pragma unroll
+        for (int t = 0; t < 9; ++t) vc[(size_t)t * gc.n + Q] = acc[t];
+    }
+}
+
+// point_gs_sweep's zero-diagonal check (smoother.hpp:73-76): first active row
+// in (colour, lexicographic) order.  key = colour * n + lex.
+__global__ void k_zero_diag(Geo g, const double* __restrict__ val, const uint8_t* __restrict__ act,
+                            unsigned long long* err) {
+    GSTRIDE(i, g.n) {
+        if (!act[i] || val[i] != 0.0) continue;
+        const int c = (int)(i >> g.lq);
+        atomicMin(err, (unsigned long long)c * g.n + lex_of_cm(g, (int)i));
+    }
+}
+
+// EllMatrix::nnz (sparse.hpp:47-52) of a preset 9-point level: diagonal
+// plus in-grid neighbours on active rows, diagonal only on inactive rows.
+__global__ void k_level_nnz(Geo g, const uint8_t* __restrict__ act, unsigned long long* out) {
+    unsigned long long s = 0;
+    GSTRIDE(i, g.n) {
+        s += 1;
+        if (!act[i]) continue;
+        const int c = (int)(i >> g.lq), pos = (int)(i & (g.nq - 1));
+        const int a = pos & (g.H - 1), b = pos >> g.lh;
+        for (int t = 1; t < 9; ++t) s += cm_neighbor(g, c, a, b, t) >= 0 ? 1 : 0;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) atomicAdd(out, s);
+}
+
+// dense_from_ell (dense.hpp:39-45) in lexicographic indexing.
+__global__ void k_dense_from_level(Geo g, const double* __restrict__ val, const uint8_t* __restrict__ act,
+                                   double* __restrict__ d, int* __restrict__ lex_of_storage) {
+    GSTRIDE(i, g.n) {
+        const int r = lex_of_cm(g, (int)i);
+        lex_of_storage[i] = r;
+        d[(size_t)r * g.n + r] = val[i];
+        if (!act[i]) continue;
+        const int c = (int)(i >> g.lq), pos = (int)(i & (g.nq - 1));
+        const int a = pos & (g.H - 1), b = pos >> g.lh;
+        for (int t = 1; t < 9; ++t) {
+            const int j = cm_neighbor(g, c, a, b, t);
+            if (j >= 0) d[(size_t)r * g.n + lex_of_cm(g, j)] = val[(size_t)t * g.n + i];
+        }
+    }
+}
+
+// dense_from_csr (dense.hpp:31-37) for the direct-only hierarchy.
+__global__ void k_dense_from_csr(const int* __restrict__ rp, const int* __restrict__ col,
+                                 const double* __restrict__ v, int n, double* __restrict__ d, int* lex_of_storage) {
+    GSTRIDE(r, n) {
+        lex_of_storage[r] = (int)r;
+        for (int p = rp[r]; p < rp[r + 1]; ++p) d[(size_t)r * n + col[p]] = v[p];
+    }
+}
+
+__global__ void k_cta_lu(double* a, int* perm, int n, int* zero_col) {
+    const int zc = cta_lu_factor(a, perm, n);
+    if (threadIdx.x == 0) *zero_col = zc;
+}
+
+// Explicit inverse of the coarsest operator (fast coarse solve): column j is
+// LuFactors::solve(e_j); stored in storage (colour-major) order so the solve
+// is one mat-vec.  Work vectors live in `work` (n*n, column-major).
+__global__ void k_inverse(const double* __restrict__ lu, const int* __restrict__ perm, int n,
+                          const int* __restrict__ lex_of_storage, double* __restrict__ work,
+                          double* __restrict__ inv) {
+    GSTRIDE(js, n) {
+        const int j = lex_of_storage[js];
+        double* x = work + (size_t)js * n;
+        // x = P e_j, then substitutions (dense.hpp:52-67)
+        for (int i = 0; i < n; ++i) x[i] = perm[i] == j ? 1.0 : 0.0;
+        for (int i = 1; i < n; ++i) {
+            double s = x[i];
+            for (int q = 0; q < i; ++q) s = __dsub_rn(s, __dmul_rn(lu[(size_t)i * n + q], x[q]));
+            x[i] = s;
+        }
+        for (int i = n - 1; i >= 0; --i) {
+            double s = x[i];
+            for (int q = i + 1; q < n; ++q) s = __dsub_rn(s, __dmul_rn(lu[(size_t)i * n + q], x[q]));
+            x[i] = s / lu[(size_t)i * n + i];
+        }
+    }
+}
+__global__ void k_inverse_scatter(const double* __restrict__ work, const int* __restrict__ lex_of_storage, int n,
+                                  double* __restrict__ inv) {
+    GSTRIDE(e, (long)n * n) {
+        const int is = (int)(e / n), js = (int)(e % n);
+        inv[e] = work[(size_t)js * n + lex_of_storage[is]];
+    }
+}
+
+template <class T>
+T read1(const T* d, cudaStream_t s) {
+    T v;
+    AUX_CUDA(cudaMemcpyAsync(&v, d, sizeof(T), cudaMemcpyDeviceToHost, s));
+    AUX_CUDA(cudaStreamSynchronize(s));
+    return v;
+}
+
+void alloc_pcg(aux_hierarchy* h, auxb200::Level& L, int n_inner) {
+    PcgBufs& P = L.pcg;
+    P.r.alloc(L.n);
+    P.u.alloc(L.n);
+    P.p.clear();
+    P.ap.clear();
+    for (int i = 0; i < n_inner; ++i) {
+        P.p.emplace_back(L.n);
+        P.ap.emplace_back(L.n);
+    }
+    P.sc.alloc(3 + n_inner);
+    AUX_CUDA(cudaMemsetAsync(P.sc.p, 0, sizeof(double) * (3 + n_inner), h->stream));
+}
+
+// Coarsest-level dense factorization + explicit inverse from a dense
+// lexicographic matrix already in h->c_lu.
+void factor_coarsest(aux_hierarchy* h) {
+    cudaStream_t s = h->stream;
+    const int nc = h->nc;
+    DBuf<int> zc(1);
+    k_cta_lu<<<1, 256, 0, s>>>(h->c_lu.p, h->c_perm.p, nc, zc.p);
+    AUX_LAUNCHED(1);
+    const int z = read1(zc.p, s);
+    if (z >= 0) throw_aux(AUX_SINGULAR_ERROR, "lu_factor: zero pivot at column " + std::to_string(z));
+    DBuf<double> work((size_t)nc * nc);
+    h->c_work.alloc((size_t)2 * nc);
+    h->c_inv.alloc((size_t)nc * nc);
+    k_inverse<<<grid_for(nc), kT, 0, s>>>(h->c_lu.p, h->c_perm.p, nc, h->c_lex.p, work.p, h->c_inv.p);
+    k_inverse_scatter<<<grid_for((long)nc * nc), kT, 0, s>>>(work.p, h->c_lex.p, nc, h->c_inv.p);
+    AUX_LAUNCHED(2);
+    AUX_CUDA(cudaGetLastError());
+    AUX_CUDA(cudaStreamSynchronize(s));
+}
+
+}  // namespace
+
+void alloc_solve_levels(aux_hierarchy* h, int n_inner) {
+    for (size_t l = 1; l < h->lv.size(); ++l) alloc_pcg(h, h->lv[l], n_inner);
+    AUX_CUDA(cudaStreamSynchronize(h->stream));
+}
+
+// A: device CSR view (arrays not retained); xy: device coordinates.
+void setup_device(aux_hierarchy* h, const aux_csr_view* A, const double* xy, long n_points) {
+    cudaStream_t s = h->stream;
+    const aux_setup_opts& o = h->opts;
+    if (A->n_rows != A->n_cols) throw_aux(AUX_SIZE_ERROR, "setup_hierarchy: matrix not square");
+    if (n_points != A->n_rows)
+        throw_aux(AUX_SIZE_ERROR, "setup_hierarchy: coordinate count does not match matrix order");
+    const int n = A->n_rows;
+    const long nnz = A->nnz;
+    h->n = n;
+
+    // ---- validate_csr (sparse.hpp:101-116)
+    {
+        int ends[2] = {0, 0};
+        if (n >= 0) {
+            AUX_CUDA(cudaMemcpyAsync(&ends[0], A->row_ptr, sizeof(int), cudaMemcpyDeviceToHost, s));
+            AUX_CUDA(cudaMemcpyAsync(&ends[1], A->row_ptr + n, sizeof(int), cudaMemcpyDeviceToHost, s));
+            AUX_CUDA(cudaStreamSynchronize(s));
+        }
+        if (ends[0] != 0 || (long)ends[1] != nnz)
+            throw_aux(AUX_STRUCTURE_ERROR, "CSR row_ptr endpoints inconsistent with nnz");
+        DBuf<unsigned long long> err(3);
+        AUX_CUDA(cudaMemsetAsync(err.p, 0xff, 2 * sizeof(unsigned long long), s));
+        if (n > 0) {
+            k_validate<<<grid_for(n), kT, 0, s>>>(A->row_ptr, A->col_idx, n, nnz, A->n_cols, err.p);
+            AUX_LAUNCHED(1);
+        }
+        const unsigned long long e = read1(err.p, s);
+        if (e != ~0ull) {
+            const long r = (long)(e / 4);
+            const int kind = (int)(e % 4);
+            if (kind == 1) throw_aux(AUX_STRUCTURE_ERROR, "CSR row_ptr not nondecreasing at row " + std::to_string(r));
+            if (kind == 2) throw_aux(AUX_STRUCTURE_ERROR, "CSR column index out of range in row " + std::to_string(r));
+            throw_aux(AUX_STRUCTURE_ERROR, "CSR row " + std::to_string(r) + " not sorted by column");
+        }
+        // diagonal > 0 (hierarchy.hpp:321-323)
+        if (n > 0) {
+            k_diag<<<grid_for(n), kT, 0, s>>>(A->row_ptr, A->col_idx, A->values, n, err.p + 1);
+            AUX_LAUNCHED(1);
+        }
+        const unsigned long long d = read1(err.p + 1, s);
+        if (d != ~0ull) throw_aux(AUX_DEFINITENESS_ERROR, "nonpositive diagonal at row " + std::to_string(d));
+        // symmetry (hierarchy.hpp:324-325)
+        DBuf<unsigned long long> sy(2);
+        AUX_CUDA(cudaMemsetAsync(sy.p, 0, 2 * sizeof(unsigned long long), s));
+        if (n > 0) {
+            k_symm<<<grid_for(n), kT, 0, s>>>(A->row_ptr, A->col_idx, A->values, n, sy.p);
+            AUX_LAUNCHED(1);
+        }
+        unsigned long long syh[2];
+        AUX_CUDA(cudaMemcpyAsync(syh, sy.p, sizeof syh, cudaMemcpyDeviceToHost, s));
+        AUX_CUDA(cudaStreamSynchronize(s));
+        double defect, scale;
+        std::memcpy(&defect, &syh[0], 8);
+        std::memcpy(&scale, &syh[1], 8);
+        scale = (1.0 < scale) ? scale : 1.0;
+        if (defect / scale > o.symmetry_tol) throw_aux(AUX_STRUCTURE_ERROR, "matrix is not symmetric to tolerance");
+    }
+    h->opts.coarsest_size = std::max(o.coarsest_size, 4);
+    const int coarsest_size = h->opts.coarsest_size;
+
+    Finest& F = h->fine;
+    F.n = n;
+    F.nnz = nnz;
+    h->lv.clear();
+    h->lv.emplace_back();
+    h->lv[0].k = 0;
+    h->lv[0].structured = false;
+    h->lv[0].n = n;
+    h->lv[0].nnz = nnz;
+
+    if (n <= coarsest_size) {   // direct-only hierarchy (hierarchy.hpp:339-344)
+        h->direct_only = true;
+        F.rp.alloc(n + 1);
+        F.col.alloc(nnz);
+        F.v.alloc(nnz);
+        AUX_CUDA(cudaMemcpyAsync(F.rp.p, A->row_ptr, sizeof(int) * (n + 1), cudaMemcpyDeviceToDevice, s));
+        AUX_CUDA(cudaMemcpyAsync(F.col.p, A->col_idx, sizeof(int) * nnz, cudaMemcpyDeviceToDevice, s));
+        AUX_CUDA(cudaMemcpyAsync(F.v.p, A->values, sizeof(double) * nnz, cudaMemcpyDeviceToDevice, s));
+        h->nc = n;
+        h->c_lu.alloc((size_t)n * n);
+        h->c_perm.alloc(n);
+        h->c_lex.alloc(n);
+        AUX_CUDA(cudaMemsetAsync(h->c_lu.p, 0, sizeof(double) * n * n, s));
+        k_dense_from_csr<<<grid_for(n), kT, 0, s>>>(F.rp.p, F.col.p, F.v.p, n, h->c_lu.p, h->c_lex.p);
+        AUX_LAUNCHED(1);
+        factor_coarsest(h);
+        return;
+    }
+
+    // ---- bounding box + depth (auxgrid.hpp:75-104)
+    {
+        DBuf<unsigned long long> bb(4);
+        DBuf<int> bad(1);
+        unsigned long long init[4] = {~0ull, 0ull, ~0ull, 0ull};
+        AUX_CUDA(cudaMemcpyAsync(bb.p, init, sizeof init, cudaMemcpyHostToDevice, s));
+        AUX_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), s));
+        k_bbox<<<grid_for(n, 4), kT, 0, s>>>(xy, n, bb.p, bad.p);
+        AUX_LAUNCHED(1);
+        unsigned long long r[4];
+        int badh = 0;
+        AUX_CUDA(cudaMemcpyAsync(r, bb.p, sizeof r, cudaMemcpyDeviceToHost, s));
+        AUX_CUDA(cudaMemcpyAsync(&badh, bad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+        AUX_CUDA(cudaStreamSynchronize(s));
+        if (badh) throw_aux(AUX_ARGUMENT_ERROR, "bounding_box: non-finite coordinate");
+        auto val = [](unsigned long long k) {
+            const unsigned long long b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+            double d;
+            std::memcpy(&d, &b, 8);
+            return d;
+        };
+        h->box[0] = val(r[0]);
+        h->box[1] = val(r[1]);
+        h->box[2] = val(r[2]);
+        h->box[3] = val(r[3]);
+        if (!(h->box[1] > h->box[0]) || !(h->box[3] > h->box[2]))
+            throw_aux(AUX_GEOMETRY_ERROR, "bounding_box: degenerate point set");
+    }
+    int depth = 0;
+    {
+        long cells = 1;
+        while (cells * 4 < n) { cells *= 4; ++depth; }
+        if (depth == 0) depth = 1;
+    }
+    h->depth = depth;
+    h->lv[0].k = depth + 1;
+    const Geo gL = make_geo(depth);
+    const int nL = gL.n;
+
+    // ---- aggregate_finest: keys, stable sort, member pointers
+    DBuf<unsigned> key(n);
+    F.perm.alloc(n);
+    k_cellkey<<<grid_for(n), kT, 0, s>>>(xy, n, h->box[0], h->box[1], h->box[2], h->box[3], gL, key.p);
+    AUX_LAUNCHED(1);
+    radix_sort_pairs(key.p, F.perm.p, n, 2 * depth, s, true);
+    {
+        DBuf<int> cnt(nL);
+        AUX_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(int) * nL, s));
+        k_count<<<grid_for(n), kT, 0, s>>>(key.p, n, cnt.p);
+        AUX_LAUNCHED(1);
+        F.bptr.alloc(nL + 1);
+        exclusive_scan(cnt.p, F.bptr.p, nL, s);
+    }
+    F.iperm.alloc(n);
+    F.cell.alloc(n);
+    F.lex_of_row.alloc(n);
+    {
+        DBuf<int> len(n);
+        k_after_sort<<<grid_for(n), kT, 0, s>>>(key.p, F.perm.p, n, gL, F.iperm.p, F.cell.p, F.lex_of_row.p, len.p,
+                                                 A->row_ptr);
+        AUX_LAUNCHED(1);
+        F.rp.alloc(n + 1);
+        exclusive_scan(len.p, F.rp.p, n, s);
+    }
+    key.release();
+    F.col.alloc(nnz);
+    F.v.alloc(nnz);
+    k_permute_csr<<<grid_for((long)n * 32), kT, 0, s>>>(A->row_ptr, A->col_idx, A->values, F.perm.p, F.iperm.p, n,
+                                                        F.rp.p, F.col.p, F.v.p);
+    AUX_LAUNCHED(1);
+
+    // ---- finest blocks: singularity check, big-block factors (factor_blocks)
+    {
+        DBuf<unsigned long long> err(1);
+        DBuf<int> flag(nL), mb(1);
+        AUX_CUDA(cudaMemsetAsync(err.p, 0xff, sizeof(unsigned long long), s));
+        AUX_CUDA(cudaMemsetAsync(mb.p, 0, sizeof(int), s));
+        k_block_check<<<grid_for(nL), kT, 0, s>>>(F.bptr.p, F.rp.p, F.col.p, F.v.p, gL, err.p, flag.p, mb.p);
+        AUX_LAUNCHED(1);
+        F.max_block = read1(mb.p, s);
+        DBuf<int> pos(nL + 1);
+        exclusive_scan(flag.p, pos.p, nL, s);
+        int nbig = 0;
+        AUX_CUDA(cudaMemcpyAsync(&nbig, pos.p + nL, sizeof(int), cudaMemcpyDeviceToHost, s));
+        AUX_CUDA(cudaStreamSynchronize(s));
+        F.n_big = nbig;
+        if (nbig > 0) {
+            F.big_ids.alloc(nbig);
+            k_compact<<<grid_for(nL), kT, 0, s>>>(flag.p, pos.p, nL, F.big_ids.p);
+            AUX_LAUNCHED(1);
+            std::vector<int> ids(nbig), bp0(nbig), bp1(nbig);
+            AUX_CUDA(cudaMemcpyAsync(ids.data(), F.big_ids.p, sizeof(int) * nbig, cudaMemcpyDeviceToHost, s));
+            AUX_CUDA(cudaStreamSynchronize(s));
+            std::vector<int> bptr_h(nL + 1);
+            AUX_CUDA(cudaMemcpyAsync(bptr_h.data(), F.bptr.p, sizeof(int) * (nL + 1), cudaMemcpyDeviceToHost, s));
+            AUX_CUDA(cudaStreamSynchronize(s));
+            std::vector<long long> off(nbig + 1, 0);
+            for (int j = 0; j < nbig; ++j) {
+                const long long sz = bptr_h[ids[j] + 1] - bptr_h[ids[j]];
+                off[j + 1] = off[j] + sz * sz;
+            }
+            for (int c = 0; c <= 4; ++c) {
+                F.big_color_begin[c] = static_cast<int>(
+                    std::lower_bound(ids.begin(), ids.end(), c << gL.lq) - ids.begin());
+            }
+            F.big_off.alloc(nbig + 1);
+            AUX_CUDA(cudaMemcpyAsync(F.big_off.p, off.data(), sizeof(long long) * (nbig + 1), cudaMemcpyHostToDevice, s));
+            F.big_lu.alloc(off[nbig]);
+            F.big_perm.alloc(n);
+            k_factor_big<<<nbig, 128, 0, s>>>(F.big_ids.p, F.big_off.p, F.bptr.p, F.rp.p, F.col.p, F.v.p, gL,
+                                               F.big_lu.p, F.big_perm.p, err.p);
+            AUX_LAUNCHED(1);
+            F.scratch.alloc(2 * (size_t)n);   // residuals + solutions of the big-block solves
+        }
+        const unsigned long long e = read1(err.p, s);
+        if (e != ~0ull) throw_aux(AUX_DEFINITENESS_ERROR, "aggregate " + std::to_string(e) + " has a singular block");
+        DBuf<int> cflag(1);
+        AUX_CUDA(cudaMemsetAsync(cflag.p, 0, sizeof(int), s));
+        k_color_check<<<grid_for(n), kT, 0, s>>>(F.rp.p, F.col.p, F.v.p, F.cell.p, n, gL.lq, cflag.p);
+        AUX_LAUNCHED(1);
+        F.color_clean = read1(cflag.p, s) == 0;
+    }
+
+    // ---- level L operator (assemble_coarse_finest)
+    h->lv.emplace_back();
+    {
+        auxb200::Level& L1 = h->lv[1];
+        L1.k = depth;
+        L1.structured = true;
+        L1.n = nL;
+        L1.geo = gL;
+        L1.val.alloc((size_t)9 * nL);
+        L1.active.alloc(nL);
+        k_active_from_count<<<grid_for(nL), kT, 0, s>>>(F.bptr.p, nL, L1.active.p);
+        DBuf<int> dcnt(nL);
+        DBuf<double> dmass(nL);
+        DBuf<unsigned long long> tot(1);
+        AUX_CUDA(cudaMemsetAsync(dcnt.p, 0, sizeof(int) * nL, s));
+        AUX_CUDA(cudaMemsetAsync(tot.p, 0, sizeof(unsigned long long), s));
+        const int lump = (o.lump_locality && !o.strict_locality) ? 1 : 0;
+        k_galerkin_L<<<grid_for(nL), kT, 0, s>>>(F.bptr.p, F.rp.p, F.col.p, F.v.p, F.cell.p, gL, lump, L1.val.p,
+                                                   dcnt.p, dmass.p, tot.p);
+        AUX_LAUNCHED(2);
+        const unsigned long long dropped = read1(tot.p, s);
+        std::memset(&h->loc, 0, sizeof h->loc);
+        if (dropped > 0) {
+            DBuf<double> m(1);
+            k_locality_sum<<<1, 32, 0, s>>>(dcnt.p, dmass.p, gL, m.p);
+            AUX_LAUNCHED(1);
+            const double mass = read1(m.p, s);
+            if (lump) { h->loc.lumped = (int64_t)dropped; h->loc.lumped_mass = mass; }
+            else { h->loc.dropped = (int64_t)dropped; h->loc.dropped_mass = mass; }
+        }
+        if (o.strict_locality && h->loc.dropped > 0)
+            throw_aux(AUX_STRUCTURE_ERROR, "strict locality: " + std::to_string(h->loc.dropped) +
+                                               " couplings fall outside the 9-point stencil");
+    }
+
+    // ---- structured coarsening (hierarchy.hpp:366-381)
+    DBuf<int> ovf(1);
+    AUX_CUDA(cudaMemsetAsync(ovf.p, 0, sizeof(int), s));
+    while (h->lv.back().k > 0 && h->lv.back().n > coarsest_size) {
+        if ((int)h->lv.size() >= AUX_MAX_LEVELS) throw_aux(AUX_INTERNAL_ERROR, "too many levels");
+        const int k = h->lv.back().k;
+        h->lv.emplace_back();
+        auxb200::Level& cur = h->lv[h->lv.size() - 2];
+        auxb200::Level& nx = h->lv.back();
+        nx.k = k - 1;
+        nx.structured = true;
+        nx.n = 1 << (2 * (k - 1));
+        nx.geo = make_geo(k - 1);
+        nx.val.alloc((size_t)9 * nx.n);
+        nx.active.alloc(nx.n);
+        k_coarsen<<<grid_for(nx.n), kT, 0, s>>>(cur.geo, cur.val.p, cur.active.p, nx.geo, nx.val.p, nx.active.p, ovf.p);
+        AUX_LAUNCHED(1);
+    }
+    if (read1(ovf.p, s)) throw_aux(AUX_STRUCTURE_ERROR, "4-child coarsening escaped the 9-point stencil");
+
+    // ---- per-level nnz and zero-diagonal records
+    {
+        DBuf<unsigned long long> cnt(1), zd(1);
+        for (size_t l = 1; l < h->lv.size(); ++l) {
+            auxb200::Level& L = h->lv[l];
+            AUX_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long), s));
+            AUX_CUDA(cudaMemsetAsync(zd.p, 0xff, sizeof(unsigned long long), s));
+            k_level_nnz<<<grid_for(L.n, 4), kT, 0, s>>>(L.geo, L.active.p, cnt.p);
+            k_zero_diag<<<grid_for(L.n, 4), kT, 0, s>>>(L.geo, L.val.p, L.active.p, zd.p);
+            AUX_LAUNCHED(2);
+            L.nnz = (long)read1(cnt.p, s);
+            const unsigned long long z = read1(zd.p, s);
+            L.zero_diag_lex = z == ~0ull ? -1 : (int)(z % (unsigned long long)L.n);
+        }
+    }
+
+    // ---- coarsest dense LU (hierarchy.hpp:383)
+    {
+        auxb200::Level& C = h->lv.back();
+        const int nc = C.n;
+        h->nc = nc;
+        h->c_lu.alloc((size_t)nc * nc);
+        h->c_perm.alloc(nc);
+        h->c_lex.alloc(nc);
+        AUX_CUDA(cudaMemsetAsync(h->c_lu.p, 0, sizeof(double) * nc * nc, s));
+        k_dense_from_level<<<grid_for(nc), kT, 0, s>>>(C.geo, C.val.p, C.active.p, h->c_lu.p, h->c_lex.p);
+        AUX_LAUNCHED(1);
+        factor_coarsest(h);
+    }
+    AUX_CUDA(cudaStreamSynchronize(s));
+}
+
+}  // namespace auxb200

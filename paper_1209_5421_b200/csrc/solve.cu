@@ -1,0 +1,752 @@
+// solve.cu — device solve (cycle.hpp:202-247): outer flexible PCG, the
+// recursive AMLI K-cycle (cycle.hpp:161-197) and inner nonlinear PCG
+// (cycle.hpp:106-128).
+//
+// Per-element arithmetic follows the reference exactly (library built with
+// -fmad=false): Gauss-Seidel rows, SpMV row sums, restriction sums, block LU
+// solves and axpys are bitwise those of the reference.  Inner products use
+// a fixed-shape two-stage tree (warp shuffle + last-block reduction), which is
+// run-to-run deterministic but not the reference's 1024-block tree; scalars
+// (alpha, beta, energies, breakdown flags) stay in device memory so a whole
+// coarse K-cycle is one CUDA graph replay with no host round trip.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <deque>
+#include <vector>
+
+#include "lu.cuh"
+#include "setup.cuh"
+
+namespace auxb200 {
+
+namespace {
+
+constexpr double kBreakdown = 1e-300;   // cycle.hpp:78
+
+double g_color_bytes[4];   // algorithmic bytes of one finest colour pass
+
+// Finaliser applied by the last block of a reduction kernel.
+struct Fin {
+    int op;            // 0 none, 1 alpha (e=s0, alpha=s1/e), 2 beta (-s0/e_in), 3 store s0
+    double* sc;        // [0]=alpha [1]=beta [2]=dead
+    const double* e_in;
+    double* e_out;     // op 1: energy slot; op 3: destination
+};
+
+__device__ __forceinline__ void finalize(const Fin& f, const double* s) {
+    if (f.op == 1) {
+        const double e = s[0];
+        *f.e_out = e;
+        if (!(e > kBreakdown)) f.sc[2] = 1.0;
+        f.sc[0] = s[1] / e;
+    } else if (f.op == 2) {
+        f.sc[1] = -s[0] / *f.e_in;
+    } else if (f.op == 3) {
+        *f.e_out = s[0];
+    }
+}
+
+#define GSTRIDE(i, n) for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < (n); i += (long)gridDim.x * blockDim.x)
+
+// ------------------------------------------------------------ structured levels
+
+// One colour pass of point_gs_sweep (smoother.hpp:68-89) on a colour-major
+// 9-point level: x_i <- (b_i - sum_{t>=1} a_it x_j) / a_ii for the active
+// cells of `color`.  zero: all neighbours are known zero (first pass from
+// u = 0), so their terms are skipped.
+__global__ void __launch_bounds__(256) k_gs9(Geo g, const double* __restrict__ val, const uint8_t* __restrict__ act,
+                                            const double* __restrict__ f, double* __restrict__ x, int color, int zero) {
+    GSTRIDE(pos, g.nq) {
+        const int i = (color << g.lq) + (int)pos;
+        if (!act[i]) continue;
+        double sum = f[i];
+        if (!zero) {
+            const int a = (int)pos & (g.H - 1), b = (int)pos >> g.lh;
+#pragma unroll
+            for (int t = 1; t < 9; ++t) {
+                const int j = cm_neighbor(g, color, a, b, t);
+                if (j >= 0) sum = __dsub_rn(sum, __dmul_rn(val[(size_t)t * g.n + i], x[j]));
+            }
+        }
+        x[i] = __ddiv_rn(sum, val[i]);
+    }
+}
+
+// ell_spmv row (sparse.hpp:120-132): sum from 0.0 over non-padding slots in
+// slot order; inactive rows hold only the unit diagonal.
+__device__ __forceinline__ double row9(const Geo& g, const double* __restrict__ val, bool active, int i,
+                                       const double* __restrict__ x) {
+    double s = __dadd_rn(0.0, __dmul_rn(val[i], x[i]));
+    if (active) {
+        const int c = i >> g.lq, pos = i & (g.nq - 1);
+        const int a = pos & (g.H - 1), b = pos >> g.lh;
+#pragma unroll
+        for (int t = 1; t < 9; ++t) {
+            const int j = cm_neighbor(g, c, a, b, t);
+            if (j >= 0) s = __dadd_rn(s, __dmul_rn(val[(size_t)t * g.n + i], x[j]));
+        }
+    }
+    return s;
+}
+
+// r = f - A u on level gf, restricted (hierarchy.hpp:267-277: children in
+// order, sum from 0.0) into rc (coarse storage order).  Block 0 also clears
+// the coarse level's PCG breakdown flag.
+__global__ void __launch_bounds__(256) k_resid_restrict9(Geo gf, const double* __restrict__ vf,
+                                                        const uint8_t* __restrict__ af, const double* __restrict__ f,
+                                                        const double* __restrict__ u, Geo gc,
+                                                        double* __restrict__ rc, double* sc_c) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) sc_c[2] = 0.0;
+    const int wc = 1 << gc.k;
+    GSTRIDE(Q, gc.n) {
+        int T1, T2;
+        xy_of_cm(gc, (int)Q, T1, T2);
+        const int R = T2 * wc + T1;
+        double sum = 0.0;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const int i = (c << gf.lq) + R;
+            const double au = row9(gf, vf, af[i] != 0, i, u);
+            sum = __dadd_rn(sum, __dsub_rn(f[i], au));
+        }
+        rc[Q] = sum;
+    }
+}
+
+// u_i += ec[parent(i)] on active cells (cycle.hpp:191-194).
+__global__ void k_prolong9(Geo gf, const uint8_t* __restrict__ af, double* __restrict__ u, Geo gc,
+                           const double* __restrict__ ec) {
+    GSTRIDE(i, gf.n) {
+        if (!af[i]) continue;
+        const int R = (int)i & (gf.nq - 1);
+        u[i] = __dadd_rn(u[i], ec[cm_of_lex(gc, R)]);
+    }
+}
+
+// y = A x plus fused partial inner products.
+//   mode 0: s0 = x.y, s1 = r.x     (first PCG step: energy and (r, p))
+//   mode 1: s0 = x.w               (first MGS projection, w = ap_0)
+__global__ void __launch_bounds__(kRedThreads) k_spmv9(Geo g, const double* __restrict__ val,
+                                                      const uint8_t* __restrict__ act, const double* __restrict__ x,
+                                                      double* __restrict__ y, int mode, const double* __restrict__ r,
+                                                      const double* __restrict__ w, RedState rs, Fin fin) {
+    double v[2] = {0.0, 0.0};
+    GSTRIDE(i, g.n) {
+        const double yi = row9(g, val, act[i] != 0, (int)i, x);
+        y[i] = yi;
+        const double xi = x[i];
+        if (mode == 0) {
+            v[0] = __dadd_rn(v[0], __dmul_rn(xi, yi));
+            v[1] = __dadd_rn(v[1], __dmul_rn(r[i], xi));
+        } else {
+            v[0] = __dadd_rn(v[0], __dmul_rn(xi, w[i]));
+        }
+    }
+    double out[2];
+    if (grid_reduce<2>(v, rs, out) && threadIdx.x == 0) finalize(fin, out);
+}
+
+// ------------------------------------------------------------ vector kernels
+
+// p += beta p_j; ap += beta ap_j (axpy, parallel.hpp:117-119) then
+//   mode 0: s0 = p.w          (next MGS projection)
+//   mode 1: s0 = p.ap, s1 = r.p (energy and alpha numerator)
+// beta is read before the loop; the finaliser may overwrite it.
+__global__ void __launch_bounds__(kRedThreads) k_mgs(long n, double* __restrict__ p, double* __restrict__ ap,
+                                                    const double* __restrict__ pj, const double* __restrict__ apj,
+                                                    const double* __restrict__ w, const double* __restrict__ r,
+                                                    int mode, const double* sc, RedState rs, Fin fin) {
+    const double beta = sc[1];
+    double v[2] = {0.0, 0.0};
+    GSTRIDE(i, n) {
+        const double pi = __dadd_rn(p[i], __dmul_rn(beta, pj[i]));
+        const double api = __dadd_rn(ap[i], __dmul_rn(beta, apj[i]));
+        p[i] = pi;
+        ap[i] = api;
+        if (mode == 0) {
+            v[0] = __dadd_rn(v[0], __dmul_rn(pi, w[i]));
+        } else {
+            v[0] = __dadd_rn(v[0], __dmul_rn(pi, api));
+            v[1] = __dadd_rn(v[1], __dmul_rn(r[i], pi));
+        }
+    }
+    double out[2];
+    if (grid_reduce<2>(v, rs, out) && threadIdx.x == 0) finalize(fin, out);
+}
+
+// u (+)= alpha p; r -= alpha ap (cycle.hpp:124-126, 233-235), skipped after a
+// breakdown.  assign: u starts at zero (first step).  norm: s0 = r.r.
+__global__ void __launch_bounds__(kRedThreads) k_update(long n, double* __restrict__ u, const double* __restrict__ p,
+                                                       double* __restrict__ r, const double* __restrict__ ap,
+                                                       int assign, int upd_r, int norm, const double* sc,
+                                                       RedState rs, Fin fin) {
+    const double alpha = sc[0];
+    const bool dead = sc[2] != 0.0;
+    const double nalpha = -alpha;
+    double v[1] = {0.0};
+    GSTRIDE(i, n) {
+        if (!dead) {
+            const double base = assign ? 0.0 : u[i];
+            u[i] = __dadd_rn(base, __dmul_rn(alpha, p[i]));
+            if (upd_r) {
+                const double ri = __dadd_rn(r[i], __dmul_rn(nalpha, ap[i]));
+                r[i] = ri;
+                if (norm) v[0] = __dadd_rn(v[0], __dmul_rn(ri, ri));
+            }
+        } else if (assign) {
+            u[i] = 0.0;
+        }
+    }
+    if (norm) {
+        double out[1];
+        if (grid_reduce<1>(v, rs, out) && threadIdx.x == 0) finalize(fin, out);
+    }
+}
+
+__global__ void __launch_bounds__(kRedThreads) k_dot(long n, const double* __restrict__ a, const double* __restrict__ b,
+                                                    RedState rs, Fin fin) {
+    double v[1] = {0.0};
+    GSTRIDE(i, n) v[0] = __dadd_rn(v[0], __dmul_rn(a[i], b[i]));
+    double out[1];
+    if (grid_reduce<1>(v, rs, out) && threadIdx.x == 0) finalize(fin, out);
+}
+
+// ------------------------------------------------------------ coarsest solve
+
+// u = A_c^{-1} f with the explicit inverse (one warp per row, fixed order).
+__global__ void k_coarse_inv(int n, const double* __restrict__ inv, const double* __restrict__ f,
+                             double* __restrict__ u) {
+    const int lane = threadIdx.x & 31;
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nw = (gridDim.x * blockDim.x) >> 5;
+    for (int i = warp; i < n; i += nw) {
+        double s = 0.0;
+        for (int j = lane; j < n; j += 32) s = fma(inv[(size_t)i * n + j], f[j], s);
+        s = warp_sum(s);
+        if (lane == 0) u[i] = s;
+    }
+}
+
+// LuFactors::solve (dense.hpp:52-67) in the reference order (parity mode).
+__global__ void k_coarse_lu(int n, const double* __restrict__ lu, const int* __restrict__ perm,
+                            const int* __restrict__ lex, const double* __restrict__ f, double* __restrict__ u,
+                            double* __restrict__ work) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    double* b = work;
+    double* x = work + n;
+    for (int is = 0; is < n; ++is) b[lex[is]] = f[is];
+    seq_lu_solve(lu, perm, n, b, x);
+    for (int is = 0; is < n; ++is) u[is] = x[lex[is]];
+}
+
+// ------------------------------------------------------------ finest level (CSR)
+
+template <int S>
+__device__ __forceinline__ void bgs_block(const int* __restrict__ rp, const int* __restrict__ col,
+                                          const double* __restrict__ v, const double* __restrict__ b,
+                                          const double* __restrict__ xin, double* __restrict__ xout, int r0,
+                                          bool zero) {
+    double a[S][S];
+    double res[S], d[S];
+    int perm[S];
+#pragma unroll
+    for (int q = 0; q < S; ++q) {
+#pragma unroll
+        for (int c = 0; c < S; ++c) a[q][c] = 0.0;
+        const int i = r0 + q;
+        double sum = b[i];
+        for (int p = rp[i]; p < rp[i + 1]; ++p) {
+            const int c = col[p];
+            const double val = v[p];
+            const unsigned off = (unsigned)(c - r0);
+#pragma unroll
+            for (int cc = 0; cc < S; ++cc)
+                if (off == (unsigned)cc) a[q][cc] = val;
+            if (!zero) sum = __dsub_rn(sum, __dmul_rn(val, xin[c]));
+        }
+        res[q] = sum;
+    }
+    reg_lu_factor<S>(a, perm);
+    reg_lu_solve<S>(a, perm, res, d);
+#pragma unroll
+    for (int q = 0; q < S; ++q) xout[r0 + q] = __dadd_rn(zero ? 0.0 : xin[r0 + q], d[q]);
+}
+
+// One colour pass of block_gs_sweep (smoother.hpp:162-205) over the cells
+// [g0, g1) of one colour; blocks of size 1 use the point update
+// (smoother.hpp:178-191), sizes 2..kSmallBlock re-factor in registers, larger
+// blocks are left to k_bgs_big.
+__global__ void __launch_bounds__(128) k_bgs(const int* __restrict__ bptr, const int* __restrict__ rp,
+                                            const int* __restrict__ col, const double* __restrict__ v,
+                                            const double* __restrict__ b, const double* __restrict__ xin,
+                                            double* __restrict__ xout, int g0, int g1, int zero) {
+    GSTRIDE(gg, (long)(g1 - g0)) {
+        const int g = g0 + (int)gg;
+        const int r0 = bptr[g], s = bptr[g + 1] - r0;
+        if (s == 1) {
+            double diag = 0.0, sum = b[r0];
+            for (int p = rp[r0]; p < rp[r0 + 1]; ++p) {
+                const int c = col[p];
+                if (c == r0) diag = v[p];
+                else if (!zero) sum = __dsub_rn(sum, __dmul_rn(v[p], xin[c]));
+            }
+            xout[r0] = __ddiv_rn(sum, diag);
+        } else if (s == 2) {
+            bgs_block<2>(rp, col, v, b, xin, xout, r0, zero);
+        } else if (s == 3) {
+            bgs_block<3>(rp, col, v, b, xin, xout, r0, zero);
+        } else if (s == 4) {
+            bgs_block<4>(rp, col, v, b, xin, xout, r0, zero);
+        }
+    }
+}
+
+// Blocks with more than kSmallBlock members: one warp each; residual rows in
+// parallel, then the stored LU factors (setup) solved in the reference order.
+__global__ void k_bgs_big(const int* __restrict__ ids, const long long* __restrict__ off,
+                          const double* __restrict__ lu, const int* __restrict__ lperm,
+                          const int* __restrict__ bptr, const int* __restrict__ rp, const int* __restrict__ col,
+                          const double* __restrict__ v, const double* __restrict__ b,
+                          const double* __restrict__ xin, double* __restrict__ xout, double* __restrict__ scratch,
+                          int j0, int j1, int n, int zero) {
+    const int lane = threadIdx.x & 31;
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nw = (gridDim.x * blockDim.x) >> 5;
+    for (int j = j0 + warp; j < j1; j += nw) {
+        const int g = ids[j];
+        const int r0 = bptr[g], s = bptr[g + 1] - r0;
+        double* res = scratch + r0;
+        double* sol = scratch + n + r0;
+        for (int q = lane; q < s; q += 32) {
+            const int i = r0 + q;
+            double sum = b[i];
+            if (!zero)
+                for (int p = rp[i]; p < rp[i + 1]; ++p) sum = __dsub_rn(sum, __dmul_rn(v[p], xin[col[p]]));
+            res[q] = sum;
+        }
+        __syncwarp();
+        if (lane == 0) seq_lu_solve(lu + off[j], lperm + r0, s, res, sol);
+        __syncwarp();
+        for (int q = lane; q < s; q += 32) xout[r0 + q] = __dadd_rn(zero ? 0.0 : xin[r0 + q], sol[q]);
+        __syncwarp();
+    }
+}
+
+// r = f - A u on the finest level, restricted to level L (member order).
+__global__ void __launch_bounds__(256) k_csr_resid_restrict(const int* __restrict__ bptr, const int* __restrict__ rp,
+                                                           const int* __restrict__ col, const double* __restrict__ v,
+                                                           const double* __restrict__ f, const double* __restrict__ u,
+                                                           int nL, double* __restrict__ rc, double* sc_c) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) sc_c[2] = 0.0;
+    GSTRIDE(g, nL) {
+        double sum = 0.0;
+        for (int i = bptr[g]; i < bptr[g + 1]; ++i) {
+            double au = 0.0;
+            for (int p = rp[i]; p < rp[i + 1]; ++p) au = __dadd_rn(au, __dmul_rn(v[p], u[col[p]]));
+            sum = __dadd_rn(sum, __dsub_rn(f[i], au));
+        }
+        rc[g] = sum;
+    }
+}
+
+__global__ void k_csr_prolong(const int* __restrict__ cell, long n, double* __restrict__ u,
+                              const double* __restrict__ ec) {
+    GSTRIDE(i, n) u[i] = __dadd_rn(u[i], ec[cell[i]]);
+}
+
+// csr_spmv (sparse.hpp:141-150) with the same fused inner products as k_spmv9.
+__global__ void __launch_bounds__(kRedThreads) k_csr_spmv(long n, const int* __restrict__ rp,
+                                                         const int* __restrict__ col, const double* __restrict__ v,
+                                                         const double* __restrict__ x, double* __restrict__ y,
+                                                         int mode, const double* __restrict__ r,
+                                                         const double* __restrict__ w, RedState rs, Fin fin) {
+    double acc[2] = {0.0, 0.0};
+    GSTRIDE(i, n) {
+        double s = 0.0;
+        for (int p = rp[i]; p < rp[i + 1]; ++p) s = __dadd_rn(s, __dmul_rn(v[p], x[col[p]]));
+        y[i] = s;
+        const double xi = x[i];
+        if (mode == 0) {
+            acc[0] = __dadd_rn(acc[0], __dmul_rn(xi, s));
+            acc[1] = __dadd_rn(acc[1], __dmul_rn(r[i], xi));
+        } else {
+            acc[0] = __dadd_rn(acc[0], __dmul_rn(xi, w[i]));
+        }
+    }
+    double out[2];
+    if (grid_reduce<2>(acc, rs, out) && threadIdx.x == 0) finalize(fin, out);
+}
+
+__global__ void k_gather(long n, const int* __restrict__ perm, const double* __restrict__ src,
+                         double* __restrict__ dst) {
+    GSTRIDE(i, n) dst[i] = src[perm[i]];
+}
+__global__ void k_scatter(long n, const int* __restrict__ perm, const double* __restrict__ src,
+                          double* __restrict__ dst) {
+    GSTRIDE(i, n) dst[perm[i]] = src[i];
+}
+
+inline unsigned blocks_for(long n, int threads = 256) {
+    long b = (n + threads - 1) / threads;
+    if (b < 1) b = 1;
+    if (b > 148L * 16) b = 148L * 16;
+    return (unsigned)b;
+}
+
+// ------------------------------------------------------------ orchestration
+
+struct Ctx {
+    aux_hierarchy* h;
+    cudaStream_t s;
+    aux_cycle_opts o;
+    RedState rs;
+    bool profile_finest;
+};
+
+void prof_begin(Ctx& c, int kind) {
+    Profile& P = c.h->prof;
+    if (!P.on) return;
+    if (P.used[kind] >= P.ev_begin[kind].size()) {
+        cudaEvent_t a, b;
+        AUX_CUDA(cudaEventCreate(&a));
+        AUX_CUDA(cudaEventCreate(&b));
+        P.ev_begin[kind].push_back(a);
+        P.ev_end[kind].push_back(b);
+    }
+    AUX_CUDA(cudaEventRecord(P.ev_begin[kind][P.used[kind]], c.s));
+}
+void prof_end(Ctx& c, int kind, double bytes) {
+    Profile& P = c.h->prof;
+    if (!P.on) return;
+    AUX_CUDA(cudaEventRecord(P.ev_end[kind][P.used[kind]], c.s));
+    P.used[kind]++;
+    P.bytes[kind] += bytes;
+    P.launches[kind]++;
+}
+
+void pcg_level(Ctx& c, int m);
+
+void coarse_solve(Ctx& c, const double* f, double* u) {
+    aux_hierarchy* h = c.h;
+    if (h->gpu.coarse_solve == 1) {
+        k_coarse_lu<<<1, 32, 0, c.s>>>(h->nc, h->c_lu.p, h->c_perm.p, h->c_lex.p, f, u, h->c_work.p);
+    } else {
+        const int warps = h->nc;
+        const unsigned blocks = (unsigned)std::min(1184, (warps * 32 + 255) / 256);
+        k_coarse_inv<<<blocks, 256, 0, c.s>>>(h->nc, h->c_inv.p, f, u);
+    }
+    AUX_LAUNCHED(1);
+}
+
+// amli_cycle (cycle.hpp:161-197) on structured level l >= 1.
+void cycle_structured(Ctx& c, int l, const double* f, double* u) {
+    aux_hierarchy* h = c.h;
+    if (l == (int)h->lv.size() - 1) {
+        coarse_solve(c, f, u);
+        return;
+    }
+    Level& L = h->lv[l];
+    Level& C = h->lv[l + 1];
+    const Geo g = L.geo;
+    const unsigned bq = blocks_for(g.nq);
+    AUX_CUDA(cudaMemsetAsync(u, 0, sizeof(double) * L.n, c.s));
+    for (int sw = 0; sw < c.o.pre_sweeps; ++sw)
+        for (int col = 0; col < 4; ++col) {
+            k_gs9<<<bq, 256, 0, c.s>>>(g, L.val.p, L.active.p, f, u, col, (sw == 0 && col == 0) ? 1 : 0);
+            AUX_LAUNCHED(1);
+        }
+    k_resid_restrict9<<<blocks_for(C.n), 256, 0, c.s>>>(g, L.val.p, L.active.p, f, u, C.geo, C.pcg.r.p, C.pcg.sc.p);
+    AUX_LAUNCHED(1);
+    pcg_level(c, l + 1);
+    k_prolong9<<<blocks_for(L.n), 256, 0, c.s>>>(g, L.active.p, u, C.geo, C.pcg.u.p);
+    AUX_LAUNCHED(1);
+    for (int sw = 0; sw < c.o.post_sweeps; ++sw)
+        for (int col = 3; col >= 0; --col) {
+            k_gs9<<<bq, 256, 0, c.s>>>(g, L.val.p, L.active.p, f, u, col, 0);
+            AUX_LAUNCHED(1);
+        }
+}
+
+void apply_spmv(Ctx& c, int m, const double* x, double* y, int mode, const double* r, const double* w, Fin fin) {
+    Level& L = c.h->lv[m];
+    k_spmv9<<<red_blocks(L.n), kRedThreads, 0, c.s>>>(L.geo, L.val.p, L.active.p, x, y, mode, r, w, c.rs, fin);
+    AUX_LAUNCHED(1);
+}
+
+// nonlinear_pcg (cycle.hpp:106-128) on level m >= 1 with the K-cycle of level
+// m as preconditioner; rhs already in lv[m].pcg.r, result in lv[m].pcg.u.
+void pcg_level(Ctx& c, int m) {
+    Level& L = c.h->lv[m];
+    PcgBufs& P = L.pcg;
+    const long n = L.n;
+    double* sc = P.sc.p;
+    const int ni = c.o.n_inner;
+    for (int i = 0; i < ni; ++i) {
+        cycle_structured(c, m, P.r.p, P.p[i].p);
+        if (i == 0) {
+            apply_spmv(c, m, P.p[0].p, P.ap[0].p, 0, P.r.p, nullptr, Fin{1, sc, nullptr, sc + 3});
+        } else {
+            apply_spmv(c, m, P.p[i].p, P.ap[i].p, 1, nullptr, P.ap[0].p, Fin{2, sc, sc + 3, nullptr});
+            for (int j = 1; j < i; ++j) {
+                k_mgs<<<red_blocks(n), kRedThreads, 0, c.s>>>(n, P.p[i].p, P.ap[i].p, P.p[j - 1].p, P.ap[j - 1].p,
+                                                             P.ap[j].p, nullptr, 0, sc, c.rs,
+                                                             Fin{2, sc, sc + 3 + j, nullptr});
+                AUX_LAUNCHED(1);
+            }
+            k_mgs<<<red_blocks(n), kRedThreads, 0, c.s>>>(n, P.p[i].p, P.ap[i].p, P.p[i - 1].p, P.ap[i - 1].p,
+                                                         nullptr, P.r.p, 1, sc, c.rs, Fin{1, sc, nullptr, sc + 3 + i});
+            AUX_LAUNCHED(1);
+        }
+        const int upd_r = (i + 1 < ni) ? 1 : 0;   // the last residual update is never read
+        k_update<<<red_blocks(n), kRedThreads, 0, c.s>>>(n, P.u.p, P.p[i].p, P.r.p, P.ap[i].p, i == 0 ? 1 : 0,
+                                                        upd_r, 0, sc, c.rs, Fin{0, sc, nullptr, nullptr});
+        AUX_LAUNCHED(1);
+    }
+}
+
+// Byte counts of one finest colour pass (12 nnz + 4(N+1) + 24 N
+// + 4 (n_L+1) per sweep, split by colour).
+struct ColorBytes {
+    double b[4];
+};
+
+void finest_bgs_pass(Ctx& c, int color, const double* f, double* u, bool zero, double* snap) {
+    aux_hierarchy* h = c.h;
+    Finest& F = h->fine;
+    const Geo& gL = h->lv[1].geo;
+    const int g0 = color << gL.lq, g1 = (color + 1) << gL.lq;
+    const double* xin = u;
+    if (!F.color_clean && !zero) {
+        AUX_CUDA(cudaMemcpyAsync(snap, u, sizeof(double) * F.n, cudaMemcpyDeviceToDevice, c.s));
+        xin = snap;
+    }
+    prof_begin(c, 0);
+    k_bgs<<<blocks_for(g1 - g0, 128), 128, 0, c.s>>>(F.bptr.p, F.rp.p, F.col.p, F.v.p, f, xin, u, g0, g1,
+                                                     zero ? 1 : 0);
+    AUX_LAUNCHED(1);
+    const int j0 = F.big_color_begin[color], j1 = F.big_color_begin[color + 1];
+    if (j1 > j0) {
+        const int warps = j1 - j0;
+        k_bgs_big<<<(unsigned)std::min(1184, (warps * 32 + 127) / 128), 128, 0, c.s>>>(
+            F.big_ids.p, F.big_off.p, F.big_lu.p, F.big_perm.p, F.bptr.p, F.rp.p, F.col.p, F.v.p, f, xin, u,
+            F.scratch.p, j0, j1, F.n, zero ? 1 : 0);
+        AUX_LAUNCHED(1);
+    }
+    prof_end(c, 0, g_color_bytes[color]);
+}
+
+void finest_cycle(Ctx& c, const double* f, double* u, double* snap) {
+    aux_hierarchy* h = c.h;
+    if (h->direct_only || h->lv.size() == 1) {
+        coarse_solve(c, f, u);
+        return;
+    }
+    Finest& F = h->fine;
+    Level& C = h->lv[1];
+    AUX_CUDA(cudaMemsetAsync(u, 0, sizeof(double) * F.n, c.s));
+    for (int sw = 0; sw < c.o.pre_sweeps; ++sw)
+        for (int col = 0; col < 4; ++col) finest_bgs_pass(c, col, f, u, sw == 0 && col == 0, snap);
+    prof_begin(c, 2);
+    k_csr_resid_restrict<<<blocks_for(C.n), 256, 0, c.s>>>(F.bptr.p, F.rp.p, F.col.p, F.v.p, f, u, C.n, C.pcg.r.p,
+                                                          C.pcg.sc.p);
+    AUX_LAUNCHED(1);
+    prof_end(c, 2, 12.0 * F.nnz + 4.0 * (F.n + 1) + 16.0 * F.n + 4.0 * (C.n + 1) + 8.0 * C.n);
+    if (h->graph_valid) {
+        AUX_CUDA(cudaGraphLaunch(h->graph, c.s));
+        AUX_LAUNCHED(h->graph_kernels);
+    } else {
+        pcg_level(c, 1);
+    }
+    k_csr_prolong<<<blocks_for(F.n), 256, 0, c.s>>>(F.cell.p, F.n, u, C.pcg.u.p);
+    AUX_LAUNCHED(1);
+    for (int sw = 0; sw < c.o.post_sweeps; ++sw)
+        for (int col = 3; col >= 0; --col) finest_bgs_pass(c, col, f, u, false, snap);
+}
+
+void build_graph(aux_hierarchy* h, const aux_cycle_opts& o, RedState rs) {
+    if (h->graph_valid && std::memcmp(&h->graph_opts, &o, sizeof o) == 0) return;
+    if (h->graph) {
+        cudaGraphExecDestroy(h->graph);
+        h->graph = nullptr;
+    }
+    h->graph_valid = false;
+    if (!h->gpu.use_graphs || h->direct_only || h->lv.size() < 2) return;
+    Ctx c{h, h->stream, o, rs, false};
+    const int64_t before = g_launches;
+    cudaGraph_t g;
+    AUX_CUDA(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+    pcg_level(c, 1);
+    AUX_CUDA(cudaStreamEndCapture(h->stream, &g));
+    h->graph_kernels = g_launches - before;
+    g_launches = before;
+    AUX_CUDA(cudaGraphInstantiate(&h->graph, g, 0));
+    cudaGraphDestroy(g);
+    h->graph_opts = o;
+    h->graph_valid = true;
+}
+
+}  // namespace
+
+void solve_device(aux_hierarchy* h, const double* b, long n_b, const aux_cycle_opts* o, aux_solve_result* res,
+                  double* u_out) {
+    if (o->n_inner < 1 || o->pre_sweeps < 1 || o->post_sweeps < 1 || o->max_outer < 1)
+        throw_aux(AUX_ARGUMENT_ERROR, "cycle options must be positive");
+    if (!(o->rtol > 0.0) || !(o->rtol < 1.0)) throw_aux(AUX_ARGUMENT_ERROR, "rtol must lie in (0,1)");
+    if (o->max_directions < 0) throw_aux(AUX_ARGUMENT_ERROR, "max_directions must be >= 0");
+    if (n_b != h->n) throw_aux(AUX_SIZE_ERROR, "solve: right-hand side does not match matrix");
+
+    const auto t0 = std::chrono::steady_clock::now();
+    cudaStream_t s = h->stream;
+    Finest& F = h->fine;
+    const long n = h->n;
+    RedState rs{h->red_partials.p, h->red_ticket.p};
+
+    // workspace
+    const int slots = o->max_directions > 0 ? std::min(o->max_directions + 1, o->max_outer) : o->max_outer;
+    if (h->w_r.n != (size_t)n) {
+        h->w_r.alloc(n);
+        h->w_u.alloc(n);
+        h->w_b.alloc(n);
+        h->w_tmp.alloc(n);
+    }
+    if ((int)h->w_p.size() < slots) {
+        while ((int)h->w_p.size() < slots) {
+            h->w_p.emplace_back(n);
+            h->w_ap.emplace_back(n);
+        }
+    }
+    if (h->w_sc.n < (size_t)(8 + slots + 1)) h->w_sc.alloc(8 + std::max(slots, o->max_outer) + 1);
+    if (!h->direct_only && h->lv.size() > 1 && (int)h->lv[1].pcg.p.size() != o->n_inner) {
+        alloc_solve_levels(h, o->n_inner);
+        h->graph_valid = false;
+    }
+    double* sc = h->w_sc.p;
+    AUX_CUDA(cudaMemsetAsync(sc, 0, sizeof(double) * h->w_sc.n, s));
+
+    // norm of b (caller order) and b in storage order
+    Fin fnorm{3, sc, nullptr, sc + 4};
+    k_dot<<<red_blocks(n), kRedThreads, 0, s>>>(n, b, b, rs, fnorm);
+    AUX_LAUNCHED(1);
+    if (h->direct_only) {
+        AUX_CUDA(cudaMemcpyAsync(h->w_r.p, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+    } else {
+        k_gather<<<blocks_for(n), 256, 0, s>>>(n, F.perm.p, b, h->w_r.p);
+        AUX_LAUNCHED(1);
+    }
+    double nb2 = 0.0;
+    AUX_CUDA(cudaMemcpyAsync(&nb2, sc + 4, sizeof(double), cudaMemcpyDeviceToHost, s));
+    AUX_CUDA(cudaStreamSynchronize(s));
+    const double norm_b = std::sqrt(nb2);
+    std::vector<double> hist;
+    hist.push_back(norm_b);
+    res->iterations = 0;
+    res->converged = 0;
+    AUX_CUDA(cudaMemsetAsync(h->w_u.p, 0, sizeof(double) * n, s));
+
+    if (norm_b == 0.0) {
+        res->converged = 1;
+    } else {
+        // solve-time singular_error of point_gs_sweep (smoother.hpp:73-76)
+        for (size_t l = 1; l + 1 < h->lv.size(); ++l)
+            if (h->lv[l].zero_diag_lex >= 0)
+                throw_aux(AUX_SINGULAR_ERROR, "zero diagonal at row " + std::to_string(h->lv[l].zero_diag_lex));
+        build_graph(h, *o, rs);
+        Ctx c{h, s, *o, rs, h->prof.on};
+        // colour-pass byte counts for the profile
+        if (h->prof.on && !h->direct_only && h->lv.size() > 1) {
+            const Geo& gL = h->lv[1].geo;
+            std::vector<int> bp(5);
+            for (int col = 0; col <= 4; ++col)
+                AUX_CUDA(cudaMemcpyAsync(&bp[col], F.bptr.p + (col << gL.lq), sizeof(int), cudaMemcpyDeviceToHost, s));
+            AUX_CUDA(cudaStreamSynchronize(s));
+            std::vector<int> rpv(5);
+            for (int col = 0; col <= 4; ++col)
+                AUX_CUDA(cudaMemcpyAsync(&rpv[col], F.rp.p + bp[col], sizeof(int), cudaMemcpyDeviceToHost, s));
+            AUX_CUDA(cudaStreamSynchronize(s));
+            for (int col = 0; col < 4; ++col) {
+                const double rows = bp[col + 1] - bp[col], ents = rpv[col + 1] - rpv[col];
+                g_color_bytes[col] = 12.0 * ents + 4.0 * rows + 24.0 * rows + 4.0 * (gL.nq + 1);
+            }
+        }
+        std::deque<int> kept;
+        std::vector<char> in_use(slots, 0);
+        double* r = h->w_r.p;
+        double* u = h->w_u.p;
+        const double spmv_bytes = 12.0 * F.nnz + 4.0 * (n + 1) + 16.0 * n;
+        while (res->iterations < o->max_outer) {
+            int slot = 0;
+            while (in_use[slot]) ++slot;
+            double* p = h->w_p[slot].p;
+            double* ap = h->w_ap[slot].p;
+            double* e_slot = sc + 8 + slot;
+            finest_cycle(c, r, p, h->w_tmp.p);
+            prof_begin(c, 1);
+            if (h->direct_only) {
+                k_csr_spmv<<<red_blocks(n), kRedThreads, 0, s>>>(n, F.rp.p, F.col.p, F.v.p, p, ap, kept.empty() ? 0 : 1,
+                                                                r, kept.empty() ? nullptr : h->w_ap[kept[0]].p, rs,
+                                                                kept.empty() ? Fin{1, sc, nullptr, e_slot}
+                                                                             : Fin{2, sc, sc + 8 + kept[0], nullptr});
+            } else {
+                k_csr_spmv<<<red_blocks(n), kRedThreads, 0, s>>>(n, F.rp.p, F.col.p, F.v.p, p, ap, kept.empty() ? 0 : 1,
+                                                                r, kept.empty() ? nullptr : h->w_ap[kept[0]].p, rs,
+                                                                kept.empty() ? Fin{1, sc, nullptr, e_slot}
+                                                                             : Fin{2, sc, sc + 8 + kept[0], nullptr});
+            }
+            AUX_LAUNCHED(1);
+            prof_end(c, 1, spmv_bytes + (kept.empty() ? 16.0 : 8.0) * n);
+            if (!kept.empty()) {
+                for (size_t j = 1; j < kept.size(); ++j) {
+                    k_mgs<<<red_blocks(n), kRedThreads, 0, s>>>(n, p, ap, h->w_p[kept[j - 1]].p, h->w_ap[kept[j - 1]].p,
+                                                               h->w_ap[kept[j]].p, nullptr, 0, sc, rs,
+                                                               Fin{2, sc, sc + 8 + kept[j], nullptr});
+                    AUX_LAUNCHED(1);
+                }
+                k_mgs<<<red_blocks(n), kRedThreads, 0, s>>>(n, p, ap, h->w_p[kept.back()].p, h->w_ap[kept.back()].p,
+                                                           nullptr, r, 1, sc, rs, Fin{1, sc, nullptr, e_slot});
+                AUX_LAUNCHED(1);
+            }
+            k_update<<<red_blocks(n), kRedThreads, 0, s>>>(n, u, p, r, ap, 0, 1, 1, sc, rs, Fin{3, sc, nullptr, sc + 3});
+            AUX_LAUNCHED(1);
+            double st[2];
+            AUX_CUDA(cudaMemcpyAsync(st, sc + 2, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+            AUX_CUDA(cudaStreamSynchronize(s));
+            if (st[0] != 0.0) break;   // breakdown (cycle.hpp:230)
+            in_use[slot] = 1;
+            kept.push_back(slot);
+            if (o->max_directions > 0 && (int)kept.size() > o->max_directions) {
+                in_use[kept.front()] = 0;
+                kept.pop_front();
+            }
+            res->iterations++;
+            const double rn = std::sqrt(st[1]);
+            hist.push_back(rn);
+            if (rn <= o->rtol * norm_b) {
+                res->converged = 1;
+                break;
+            }
+        }
+    }
+    // u back to the caller's order
+    if (u_out) {
+        if (h->direct_only) {
+            AUX_CUDA(cudaMemcpyAsync(u_out, h->w_u.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+        } else {
+            k_scatter<<<blocks_for(n), 256, 0, s>>>(n, F.perm.p, h->w_u.p, u_out);
+            AUX_LAUNCHED(1);
+        }
+    }
+    AUX_CUDA(cudaGetLastError());
+    AUX_CUDA(cudaStreamSynchronize(s));
+    res->history_len = (int32_t)hist.size();
+    if (res->residual_history)
+        for (size_t i = 0; i < hist.size() && (int)i < res->history_capacity; ++i) res->residual_history[i] = hist[i];
+    const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    res->solve_seconds = secs;
+    res->total_seconds = secs;
+    res->setup_seconds = 0.0;
+    h->last_solve_ms = secs * 1e3;
+}
+
+}  // namespace auxb200

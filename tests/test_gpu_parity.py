@@ -1,0 +1,222 @@
+"""GPU parity tests: the CUDA path through the C ABI against the oracle
+(oracle/auxamg_oracle.c, itself pinned bitwise to the reference in
+tests/test_oracle.py) on identical inputs.
+
+Bar (BASELINE.json north_star): aggregates, colourings and coarse sparsity
+patterns bit-exact; coarse operator values bit-exact (library built with
+-fmad=false, sums in the reference order; tolerance 1e-12 relative allowed);
+iteration counts within +-1; solutions within 1e-12 relative (max-norm).
+"""
+import numpy as np
+import pytest
+
+import bindings as ob
+from paper_1209_5421_b200 import problems
+
+pytestmark = pytest.mark.gpu
+
+U_TOL = 1e-12          # max |u - u_ref| / max |u_ref|
+VAL_TOL = 1e-12        # coarse values, relative to the level's max |value|
+
+
+def _problems_small():
+    return {
+        "poisson5_33": problems.poisson5(33),          # N = 4^5 exactly: depth drops by one
+        "poisson5_40": problems.poisson5(40),
+        "jitter_48": problems.jittered_p1(48),
+        "graded_64": problems.graded_p1(64, 1.3),
+        "disk_40": problems.disk_p1(40),               # empty cells -> inactive identity rows
+        "graded2_40": problems.graded_p1(40, 2.0),     # dropped couplings + same-colour couplings
+        "jump_48": problems.jittered_p1(48, jump=1e3),
+    }
+
+
+PROBS = _problems_small()
+
+
+def compare_exports(eg, eo, exact_values=True):
+    assert eg["depth"] == eo["depth"]
+    assert eg["box"] == eo["box"]
+    assert eg["locality"][0] == eo["locality"][0] and eg["locality"][2] == eo["locality"][2]
+    assert eg["locality"][1] == pytest.approx(eo["locality"][1], rel=1e-14, abs=0)
+    assert eg["locality"][3] == pytest.approx(eo["locality"][3], rel=1e-14, abs=0)
+    assert eg["stats"]["levels"] == eo["stats"]["levels"]
+    assert eg["stats"]["sizes"] == eo["stats"]["sizes"]
+    assert eg["stats"]["nnz"] == eo["stats"]["nnz"]
+    assert eg["stats"]["operator_complexity"] == eo["stats"]["operator_complexity"]
+    for i, (lg, lo) in enumerate(zip(eg["levels"], eo["levels"])):
+        for key in ("k", "structured", "n", "nnz", "has_map"):
+            assert lg[key] == lo[key], (i, key)
+        for key in ("agg_of", "member_ptr", "member_idx", "active", "item_color", "ell_col", "block_size",
+                    "block_offset", "block_perm"):
+            if key in lo:
+                assert np.array_equal(lg[key], lo[key]), (i, key)
+        for key in ("ell_val", "block_lu"):
+            if key in lo:
+                if exact_values:
+                    assert np.array_equal(lg[key], lo[key]), (i, key, np.max(np.abs(lg[key] - lo[key])))
+                else:
+                    scale = max(1.0, np.max(np.abs(lo[key])))
+                    assert np.max(np.abs(lg[key] - lo[key])) <= VAL_TOL * scale, (i, key)
+    assert np.array_equal(eg["coarsest_perm"], eo["coarsest_perm"])
+    assert np.array_equal(eg["coarsest_lu"], eo["coarsest_lu"])
+
+
+@pytest.mark.parametrize("name", list(PROBS))
+def test_setup_exports_bitwise(gpu_api, name):
+    s = PROBS[name]
+    h = gpu_api.setup_hierarchy(s.A, s.coords)
+    ref = ob.CpuHierarchy("oracle", s.A, s.coords)
+    compare_exports(h.export(), ref.export(), exact_values=True)
+
+
+@pytest.mark.parametrize("name", list(PROBS))
+@pytest.mark.parametrize("coarse", [0, 1])
+def test_solve_parity(gpu_api, name, coarse):
+    s = PROBS[name]
+    h = gpu_api.setup_hierarchy(s.A, s.coords, gpu=gpu_api.GpuOptions(coarse_solve=coarse))
+    res = gpu_api.solve(s.A, s.b, h)
+    ref = ob.CpuHierarchy("oracle", s.A, s.coords).solve(s.b)
+    assert abs(res.iterations - ref["iterations"]) <= 1
+    assert res.converged == ref["converged"]
+    err = np.max(np.abs(res.u - ref["u"])) / np.max(np.abs(ref["u"]))
+    assert err <= U_TOL, err
+    assert len(res.residual_history) == res.iterations + 1
+    hr = np.array(ref["residual_history"])
+    m = min(len(hr), len(res.residual_history))
+    np.testing.assert_allclose(res.residual_history[:m], hr[:m], rtol=1e-8, atol=0)
+
+
+@pytest.mark.parametrize("opts", [
+    dict(n_inner=1), dict(n_inner=3), dict(pre_sweeps=2, post_sweeps=2), dict(max_directions=2),
+    dict(rtol=1e-10), dict(max_outer=3),
+])
+def test_cycle_options(gpu_api, opts):
+    s = PROBS["jitter_48"]
+    h = gpu_api.setup_hierarchy(s.A, s.coords)
+    res = gpu_api.solve(s.A, s.b, h, gpu_api.CycleOptions(**opts))
+    ref = ob.CpuHierarchy("oracle", s.A, s.coords).solve(s.b, ob.cycle_opts(**opts))
+    assert abs(res.iterations - ref["iterations"]) <= 1
+    err = np.max(np.abs(res.u - ref["u"])) / np.max(np.abs(ref["u"]))
+    assert err <= U_TOL, err
+
+
+def test_no_graph_path_matches(gpu_api):
+    s = PROBS["graded_64"]
+    h1 = gpu_api.setup_hierarchy(s.A, s.coords, gpu=gpu_api.GpuOptions(use_graphs=False))
+    h2 = gpu_api.setup_hierarchy(s.A, s.coords)
+    r1 = gpu_api.solve(s.A, s.b, h1)
+    r2 = gpu_api.solve(s.A, s.b, h2)
+    assert r1.iterations == r2.iterations
+    assert np.array_equal(r1.u, r2.u)   # same kernels, same grid: bitwise
+
+
+def test_deterministic_repeat(gpu_api):
+    s = PROBS["jump_48"]
+    h = gpu_api.setup_hierarchy(s.A, s.coords)
+    a = gpu_api.solve(s.A, s.b, h)
+    b = gpu_api.solve(None, s.b, h)
+    assert a.iterations == b.iterations
+    assert np.array_equal(a.u, b.u)
+    assert a.residual_history == b.residual_history
+
+
+def test_setup_options_locality(gpu_api):
+    s = PROBS["graded2_40"]
+    for o in (dict(lump_locality=True), dict(coarsest_size=4), dict(coarsest_size=300)):
+        h = gpu_api.setup_hierarchy(s.A, s.coords, gpu_api.SetupOptions(**o))
+        ref = ob.CpuHierarchy("oracle", s.A, s.coords, ob.setup_opts(**o))
+        compare_exports(h.export(), ref.export())
+        r = gpu_api.solve(s.A, s.b, h)
+        rr = ref.solve(s.b)
+        assert abs(r.iterations - rr["iterations"]) <= 1
+        assert np.max(np.abs(r.u - rr["u"])) / np.max(np.abs(rr["u"])) <= U_TOL
+    with pytest.raises(gpu_api.StructureError):
+        gpu_api.setup_hierarchy(s.A, s.coords, gpu_api.SetupOptions(strict_locality=True))
+
+
+def test_direct_only(gpu_api):
+    # n <= coarsest_size: one level, dense LU, one outer iteration (test_cycle.cpp:197-212)
+    s = problems.poisson5(8)
+    h = gpu_api.setup_hierarchy(s.A, s.coords)
+    ref = ob.CpuHierarchy("oracle", s.A, s.coords)
+    compare_exports(h.export(), ref.export())
+    r = gpu_api.solve(s.A, s.b, h)
+    rr = ref.solve(s.b)
+    assert r.iterations == rr["iterations"] == 1
+    assert np.max(np.abs(r.u - rr["u"])) / np.max(np.abs(rr["u"])) <= U_TOL
+
+
+def test_zero_rhs(gpu_api):
+    s = PROBS["poisson5_40"]
+    h = gpu_api.setup_hierarchy(s.A, s.coords)
+    r = gpu_api.solve(s.A, np.zeros(s.A.n_rows), h)
+    assert r.converged and r.iterations == 0 and np.all(r.u == 0.0)
+    assert r.residual_history == [0.0]
+
+
+def test_errors_match_reference(gpu_api):
+    s = problems.poisson5(20)
+    A = s.A
+    # size errors
+    with pytest.raises(gpu_api.SizeError):
+        gpu_api.setup_hierarchy(A, s.coords[:-1])
+    # nonpositive diagonal
+    bad = problems.CsrMatrix(A.n_rows, A.n_cols, A.row_ptr.copy(), A.col_idx.copy(), A.values.copy())
+    d = np.where(bad.col_idx[bad.row_ptr[5]:bad.row_ptr[6]] == 5)[0][0] + bad.row_ptr[5]
+    bad.values[d] = -1.0
+    with pytest.raises(gpu_api.DefinitenessError, match="row 5"):
+        gpu_api.setup_hierarchy(bad, s.coords)
+    # nonsymmetric
+    ns = problems.CsrMatrix(A.n_rows, A.n_cols, A.row_ptr.copy(), A.col_idx.copy(), A.values.copy())
+    ns.values[A.row_ptr[3]] += 0.5 if A.col_idx[A.row_ptr[3]] != 3 else 0.0
+    ns.values[A.row_ptr[3] + 1] -= 0.25
+    with pytest.raises(gpu_api.StructureError):
+        gpu_api.setup_hierarchy(ns, s.coords)
+    # unsorted row
+    us = problems.CsrMatrix(A.n_rows, A.n_cols, A.row_ptr.copy(), A.col_idx.copy(), A.values.copy())
+    p = A.row_ptr[7]
+    us.col_idx[p], us.col_idx[p + 1] = us.col_idx[p + 1], us.col_idx[p]
+    with pytest.raises(gpu_api.StructureError, match="row 7 not sorted"):
+        gpu_api.setup_hierarchy(us, s.coords)
+    # non-finite coordinate
+    xy = s.coords.copy()
+    xy[3, 0] = np.nan
+    with pytest.raises(gpu_api.ArgumentError):
+        gpu_api.setup_hierarchy(A, xy)
+    # degenerate box
+    xy = s.coords.copy()
+    xy[:, 1] = 0.5
+    with pytest.raises(gpu_api.GeometryError):
+        gpu_api.setup_hierarchy(A, xy)
+    # cycle options
+    h = gpu_api.setup_hierarchy(A, s.coords)
+    with pytest.raises(gpu_api.ArgumentError):
+        gpu_api.solve(A, s.b, h, gpu_api.CycleOptions(rtol=1.5))
+    with pytest.raises(gpu_api.ArgumentError):
+        gpu_api.solve(A, s.b, h, gpu_api.CycleOptions(n_inner=0))
+    with pytest.raises(gpu_api.SizeError):
+        gpu_api.solve(A, s.b[:-1], h)
+
+
+def test_reference_error_types_agree(gpu_api):
+    """Every error case above raises the same class in the reference."""
+    s = problems.poisson5(20)
+    xy = s.coords.copy()
+    xy[:, 1] = 0.5
+    with pytest.raises(gpu_api.GeometryError):
+        ob.CpuHierarchy("oracle", s.A, xy)
+    with pytest.raises(gpu_api.GeometryError):
+        gpu_api.setup_hierarchy(s.A, xy)
+
+
+@pytest.mark.parametrize("n", [257, 513])
+def test_medium_parity(gpu_api, n):
+    s = problems.jittered_p1(n)
+    h = gpu_api.setup_hierarchy(s.A, s.coords)
+    ref = ob.CpuHierarchy("oracle", s.A, s.coords)
+    compare_exports(h.export(), ref.export())
+    r = gpu_api.solve(s.A, s.b, h)
+    rr = ref.solve(s.b)
+    assert abs(r.iterations - rr["iterations"]) <= 1
+    assert np.max(np.abs(r.u - rr["u"])) / np.max(np.abs(rr["u"])) <= U_TOL
