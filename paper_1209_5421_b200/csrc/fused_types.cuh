@@ -1,0 +1,42 @@
+#pragma once
+#include "common.cuh"
+
+namespace auxb200 {
+
+constexpr int kFusedMaxInner = 8;
+constexpr int kMaxFusedLevels = 8;
+constexpr int kFusedSmemMax = 232448 - 2048;   // 227 KB per CTA minus the static reduction buffer
+
+// Global-memory descriptor of one level for the fused coarse kernel (fused.cu).
+struct FLevel {
+    Geo g;
+    const double* val;
+    const uint8_t* act;
+    double* r;
+    double* u;
+    double* p[kFusedMaxInner];
+    double* ap[kFusedMaxInner];
+};
+
+struct FusedArgs {
+    int m0;          // first level handled by the kernel (its nonlinear_pcg)
+    int last;        // coarsest level index
+    int ni, pre, post;
+    int coarse_mode; // 0 inverse, 1 LU
+    int nc;
+    const FLevel* lv;   // device array indexed by absolute level index (global buffers)
+    const double* inv;
+    const double* lu;
+    const int* perm;
+    const int* lex;
+    double* work;
+    // shared-memory layout (bytes) of fused level q = m - m0
+    unsigned off_val[kMaxFusedLevels];
+    unsigned off_act[kMaxFusedLevels];
+    unsigned off_vec[kMaxFusedLevels];   // r, u, p[0..ni), ap[0..ni), n doubles each
+    unsigned off_inv;                    // explicit inverse, if staged
+    int inv_in_smem;
+    unsigned smem_bytes;
+};
+
+}  // namespace auxb200

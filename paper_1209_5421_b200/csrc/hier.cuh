@@ -7,8 +7,18 @@
 #include <vector>
 
 #include "common.cuh"
+#include "fused_types.cuh"
 
 namespace auxb200 {
+
+// Process-wide caching device allocator: setup/solve allocate and release the
+// same sizes over and over (every bench step rebuilds the hierarchy), and
+// cudaMalloc/cudaFree are synchronous and slow.  Blocks are cached by exact
+// rounded size and reused; all users of one block are stream-ordered on the
+// hierarchy's single stream, and a hierarchy synchronises its stream before
+// returning its blocks.
+void* dev_alloc(size_t bytes);
+void dev_free(void* p, size_t bytes);
 
 // RAII device buffer.
 template <class T>
@@ -28,10 +38,10 @@ struct DBuf {
     void alloc(size_t count) {
         release();
         n = count;
-        if (count) AUX_CUDA(cudaMalloc(&p, count * sizeof(T)));
+        if (count) p = static_cast<T*>(dev_alloc(count * sizeof(T)));
     }
     void release() {
-        if (p) cudaFree(p);
+        if (p) dev_free(p, n * sizeof(T));
         p = nullptr;
         n = 0;
     }
@@ -76,6 +86,7 @@ struct Finest {
     // blocks with more than kSmallBlock members: stored LU factors
     int n_big = 0;
     int big_color_begin[5] = {0, 0, 0, 0, 0};   // big-block list split by colour
+    int big_cta_begin[4] = {0, 0, 0, 0};        // within a colour: first block with > 32 members
     DBuf<int> big_ids;        // cell ids (colour-major), sorted by colour
     DBuf<long long> big_off;  // offset of each big block's s*s LU in big_lu
     DBuf<double> big_lu;
@@ -85,7 +96,7 @@ struct Finest {
     int max_block = 0;
 };
 
-constexpr int kSmallBlock = 4;
+constexpr int kSmallBlock = 8;   // blocks up to this size re-factor in registers every sweep
 
 struct Profile {
     bool on = false;
@@ -134,6 +145,9 @@ struct aux_hierarchy {
     long graph_kernels = 0;
     aux_cycle_opts graph_opts{};
     bool graph_valid = false;
+    int fused_m0 = 1 << 30;          // first level run by the single-CTA kernel
+    auxb200::DBuf<auxb200::FLevel> d_flv;
+    auxb200::FusedArgs fused_args{};
     auxb200::Profile prof;
     double last_setup_ms = 0.0, last_solve_ms = 0.0;
     ~aux_hierarchy();

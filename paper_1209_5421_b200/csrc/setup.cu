@@ -711,14 +711,25 @@ void setup_device(aux_hierarchy* h, const aux_csr_view* A, const double* xy, lon
             std::vector<int> bptr_h(nL + 1);
             AUX_CUDA(cudaMemcpyAsync(bptr_h.data(), F.bptr.p, sizeof(int) * (nL + 1), cudaMemcpyDeviceToHost, s));
             AUX_CUDA(cudaStreamSynchronize(s));
+            // order: per colour, the warp class (<= 32 members) then the CTA class
+            auto bsize = [&](int g) { return bptr_h[g + 1] - bptr_h[g]; };
+            std::vector<int> ord;
+            ord.reserve(nbig);
+            for (int c = 0; c < 4; ++c) {
+                F.big_color_begin[c] = (int)ord.size();
+                for (int g : ids)
+                    if ((g >> gL.lq) == c && bsize(g) <= 32) ord.push_back(g);
+                F.big_cta_begin[c] = (int)ord.size();
+                for (int g : ids)
+                    if ((g >> gL.lq) == c && bsize(g) > 32) ord.push_back(g);
+            }
+            F.big_color_begin[4] = (int)ord.size();
+            ids.swap(ord);
+            AUX_CUDA(cudaMemcpyAsync(F.big_ids.p, ids.data(), sizeof(int) * nbig, cudaMemcpyHostToDevice, s));
             std::vector<long long> off(nbig + 1, 0);
             for (int j = 0; j < nbig; ++j) {
-                const long long sz = bptr_h[ids[j] + 1] - bptr_h[ids[j]];
+                const long long sz = bsize(ids[j]);
                 off[j + 1] = off[j] + sz * sz;
-            }
-            for (int c = 0; c <= 4; ++c) {
-                F.big_color_begin[c] = static_cast<int>(
-                    std::lower_bound(ids.begin(), ids.end(), c << gL.lq) - ids.begin());
             }
             F.big_off.alloc(nbig + 1);
             AUX_CUDA(cudaMemcpyAsync(F.big_off.p, off.data(), sizeof(long long) * (nbig + 1), cudaMemcpyHostToDevice, s));

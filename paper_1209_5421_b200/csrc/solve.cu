@@ -12,11 +12,13 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <deque>
 #include <vector>
 
 #include "lu.cuh"
+#include "fused.cuh"
 #include "setup.cuh"
 
 namespace auxb200 {
@@ -60,6 +62,11 @@ __global__ void __launch_bounds__(256) k_gs9(Geo g, const double* __restrict__ v
                                             const double* __restrict__ f, double* __restrict__ x, int color, int zero) {
     GSTRIDE(pos, g.nq) {
         const int i = (color << g.lq) + (int)pos;
+        if (zero) {   // u = 0 on the other three colour planes (cycle.hpp:170)
+#pragma unroll
+            for (int c = 1; c < 4; ++c) x[(((color + c) & 3) << g.lq) + pos] = 0.0;
+            if (!act[i]) x[i] = 0.0;
+        }
         if (!act[i]) continue;
         double sum = f[i];
         if (!zero) {
@@ -275,9 +282,11 @@ __device__ __forceinline__ void bgs_block(const int* __restrict__ rp, const int*
 }
 
 // One colour pass of block_gs_sweep (smoother.hpp:162-205) over the cells
-// [g0, g1) of one colour; blocks of size 1 use the point update
-// (smoother.hpp:178-191), sizes 2..kSmallBlock re-factor in registers, larger
-// blocks are left to k_bgs_big.
+// [g0, g1) of one colour, for the blocks with LO <= size <= HI: size 1 uses the
+// point update (smoother.hpp:178-191), sizes up to kSmallBlock re-factor in
+// registers (one thread per block).  The <1,4> instance also clears the
+// sibling rows on the first pass from zero.
+template <int LO, int HI>
 __global__ void __launch_bounds__(128) k_bgs(const int* __restrict__ bptr, const int* __restrict__ rp,
                                             const int* __restrict__ col, const double* __restrict__ v,
                                             const double* __restrict__ b, const double* __restrict__ xin,
@@ -285,6 +294,14 @@ __global__ void __launch_bounds__(128) k_bgs(const int* __restrict__ bptr, const
     GSTRIDE(gg, (long)(g1 - g0)) {
         const int g = g0 + (int)gg;
         const int r0 = bptr[g], s = bptr[g + 1] - r0;
+        if (LO == 1 && zero) {   // u = 0 on the rows of the sibling cells of the other colours
+            const int nq = g1 - g0;
+            for (int cc = 1; cc < 4; ++cc) {
+                const int gs = g + cc * nq;
+                for (int i = bptr[gs]; i < bptr[gs + 1]; ++i) xout[i] = 0.0;
+            }
+        }
+        if (s < LO || s > HI) continue;
         if (s == 1) {
             double diag = 0.0, sum = b[r0];
             for (int p = rp[r0]; p < rp[r0 + 1]; ++p) {
@@ -297,41 +314,117 @@ __global__ void __launch_bounds__(128) k_bgs(const int* __restrict__ bptr, const
             bgs_block<2>(rp, col, v, b, xin, xout, r0, zero);
         } else if (s == 3) {
             bgs_block<3>(rp, col, v, b, xin, xout, r0, zero);
-        } else if (s == 4) {
-            bgs_block<4>(rp, col, v, b, xin, xout, r0, zero);
+        } else if (HI >= 4 && s == 4) {
+            bgs_block<(HI >= 4 ? 4 : 1)>(rp, col, v, b, xin, xout, r0, zero);
+        } else if (HI >= 5 && s == 5) {
+            bgs_block<(HI >= 5 ? 5 : 1)>(rp, col, v, b, xin, xout, r0, zero);
+        } else if (HI >= 6 && s == 6) {
+            bgs_block<(HI >= 6 ? 6 : 1)>(rp, col, v, b, xin, xout, r0, zero);
+        } else if (HI >= 7 && s == 7) {
+            bgs_block<(HI >= 7 ? 7 : 1)>(rp, col, v, b, xin, xout, r0, zero);
+        } else if (HI >= 8 && s == 8) {
+            bgs_block<(HI >= 8 ? 8 : 1)>(rp, col, v, b, xin, xout, r0, zero);
         }
     }
 }
 
-// Blocks with more than kSmallBlock members: one warp each; residual rows in
-// parallel, then the stored LU factors (setup) solved in the reference order.
-__global__ void k_bgs_big(const int* __restrict__ ids, const long long* __restrict__ off,
-                          const double* __restrict__ lu, const int* __restrict__ lperm,
-                          const int* __restrict__ bptr, const int* __restrict__ rp, const int* __restrict__ col,
-                          const double* __restrict__ v, const double* __restrict__ b,
-                          const double* __restrict__ xin, double* __restrict__ xout, double* __restrict__ scratch,
-                          int j0, int j1, int n, int zero) {
-    const int lane = threadIdx.x & 31;
+// Residual row b_i - sum_p a_p x_p over the whole row in storage order
+// (smoother.hpp:196-199).
+__device__ __forceinline__ double block_res_row(const int* __restrict__ rp, const int* __restrict__ col,
+                                                const double* __restrict__ v, const double* __restrict__ b,
+                                                const double* __restrict__ xin, int i, bool zero) {
+    double sum = b[i];
+    if (!zero)
+        for (int p = rp[i]; p < rp[i + 1]; ++p) sum = __dsub_rn(sum, __dmul_rn(v[p], xin[col[p]]));
+    return sum;
+}
+
+// Blocks of kSmallBlock+1 .. 32 members: one warp per block, lane q owns row q.
+// The stored LU factors (setup, factor_blocks) are staged in shared memory;
+// the forward substitution runs column by column across lanes (every row
+// still subtracts in ascending column order, dense.hpp:57-61); the backward
+// substitution is the reference's row loop (dense.hpp:62-66) on one lane.
+__global__ void __launch_bounds__(128) k_bgs_warp(const int* __restrict__ ids, const long long* __restrict__ off,
+                                                 const double* __restrict__ lu, const int* __restrict__ lperm,
+                                                 const int* __restrict__ bptr, const int* __restrict__ rp,
+                                                 const int* __restrict__ col, const double* __restrict__ v,
+                                                 const double* __restrict__ b, const double* __restrict__ xin,
+                                                 double* __restrict__ xout, int j0, int j1, int zero) {
+    __shared__ double sLU[4][32 * 32];
+    __shared__ double sx[4][32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int nw = (gridDim.x * blockDim.x) >> 5;
+    double* U = sLU[w];
+    double* X = sx[w];
     for (int j = j0 + warp; j < j1; j += nw) {
         const int g = ids[j];
         const int r0 = bptr[g], s = bptr[g + 1] - r0;
-        double* res = scratch + r0;
-        double* sol = scratch + n + r0;
-        for (int q = lane; q < s; q += 32) {
-            const int i = r0 + q;
-            double sum = b[i];
-            if (!zero)
-                for (int p = rp[i]; p < rp[i + 1]; ++p) sum = __dsub_rn(sum, __dmul_rn(v[p], xin[col[p]]));
-            res[q] = sum;
+        const double* F = lu + off[j];
+        for (int e = lane; e < s * s; e += 32) U[e] = F[e];
+        const double res = lane < s ? block_res_row(rp, col, v, b, xin, r0 + lane, zero) : 0.0;
+        const int pm = lane < s ? lperm[r0 + lane] : 0;
+        __syncwarp();
+        double x = __shfl_sync(0xffffffffu, res, pm);
+        for (int c = 0; c + 1 < s; ++c) {
+            const double xc = __shfl_sync(0xffffffffu, x, c);
+            if (lane > c && lane < s) x = __dsub_rn(x, __dmul_rn(U[lane * s + c], xc));
+        }
+        if (lane < s) X[lane] = x;
+        __syncwarp();
+        if (lane == 0) {
+            for (int i = s - 1; i >= 0; --i) {
+                double t = X[i];
+                for (int c = i + 1; c < s; ++c) t = __dsub_rn(t, __dmul_rn(U[i * s + c], X[c]));
+                X[i] = __ddiv_rn(t, U[i * s + i]);
+            }
         }
         __syncwarp();
-        if (lane == 0) seq_lu_solve(lu + off[j], lperm + r0, s, res, sol);
-        __syncwarp();
-        for (int q = lane; q < s; q += 32) xout[r0 + q] = __dadd_rn(zero ? 0.0 : xin[r0 + q], sol[q]);
+        if (lane < s) xout[r0 + lane] = __dadd_rn(zero ? 0.0 : xin[r0 + lane], X[lane]);
         __syncwarp();
     }
+}
+
+// Blocks of more than 32 members: one CTA per block, factors in dynamic
+// shared memory when they fit (smem_lu), otherwise read from global memory.
+__global__ void __launch_bounds__(128) k_bgs_cta(const int* __restrict__ ids, const long long* __restrict__ off,
+                                                const double* __restrict__ lu, const int* __restrict__ lperm,
+                                                const int* __restrict__ bptr, const int* __restrict__ rp,
+                                                const int* __restrict__ col, const double* __restrict__ v,
+                                                const double* __restrict__ b, const double* __restrict__ xin,
+                                                double* __restrict__ xout, double* __restrict__ scratch, int j0,
+                                                int zero, int smem_lu) {
+    extern __shared__ double dyn[];
+    const int j = j0 + blockIdx.x;
+    const int g = ids[j];
+    const int r0 = bptr[g], s = bptr[g + 1] - r0;
+    const double* F = lu + off[j];
+    double* X = smem_lu ? dyn + (size_t)s * s : scratch + r0;   // solution vector
+    const double* U = F;
+    if (smem_lu) {
+        double* d = dyn;
+        for (int e = threadIdx.x; e < s * s; e += blockDim.x) d[e] = F[e];
+        U = d;
+    }
+    double* R = scratch + r0;   // residuals (global scratch, row r0..)
+    for (int q = threadIdx.x; q < s; q += blockDim.x) R[q] = block_res_row(rp, col, v, b, xin, r0 + q, zero);
+    __syncthreads();
+    for (int q = threadIdx.x; q < s; q += blockDim.x) X[q] = R[lperm[r0 + q]];
+    __syncthreads();
+    for (int c = 0; c + 1 < s; ++c) {   // column-oriented forward substitution
+        const double xc = X[c];
+        for (int q = c + 1 + threadIdx.x; q < s; q += blockDim.x) X[q] = __dsub_rn(X[q], __dmul_rn(U[(size_t)q * s + c], xc));
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        for (int i = s - 1; i >= 0; --i) {
+            double t = X[i];
+            for (int c = i + 1; c < s; ++c) t = __dsub_rn(t, __dmul_rn(U[(size_t)i * s + c], X[c]));
+            X[i] = __ddiv_rn(t, U[(size_t)i * s + i]);
+        }
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < s; q += blockDim.x) xout[r0 + q] = __dadd_rn(zero ? 0.0 : xin[r0 + q], X[q]);
 }
 
 // r = f - A u on the finest level, restricted to level L (member order).
@@ -426,6 +519,42 @@ void prof_end(Ctx& c, int kind, double bytes) {
     P.launches[kind]++;
 }
 
+// AUX_TRACE=1: device-time breakdown of each solve by phase, printed to stderr.
+struct Trace {
+    bool on = false;
+    std::vector<cudaEvent_t> ev;
+    std::vector<int> cat;
+    void mark(cudaStream_t s, int c) {
+        if (!on) return;
+        cudaEvent_t e;
+        AUX_CUDA(cudaEventCreate(&e));
+        AUX_CUDA(cudaEventRecord(e, s));
+        ev.push_back(e);
+        cat.push_back(c);
+    }
+    void report() {
+        if (!on || ev.empty()) return;
+        AUX_CUDA(cudaEventSynchronize(ev.back()));
+        static const char* names[] = {"start", "finest pre-smooth+restrict", "coarse K-cycle (levels>=1)",
+                                      "finest prolong+post-smooth", "outer A z + MGS + update", "host sync"};
+        double t[6] = {0, 0, 0, 0, 0, 0};
+        for (size_t i = 1; i < ev.size(); ++i) {
+            float ms = 0.f;
+            AUX_CUDA(cudaEventElapsedTime(&ms, ev[i - 1], ev[i]));
+            t[cat[i]] += ms;
+        }
+        double tot = 0;
+        for (int k = 1; k < 6; ++k) tot += t[k];
+        std::fprintf(stderr, "[aux trace] device time %.3f ms:", tot);
+        for (int k = 1; k < 6; ++k) std::fprintf(stderr, " %s %.3f;", names[k], t[k]);
+        std::fprintf(stderr, "\n");
+        for (auto e : ev) cudaEventDestroy(e);
+        ev.clear();
+        cat.clear();
+    }
+};
+Trace g_trace;
+
 void pcg_level(Ctx& c, int m);
 
 void coarse_solve(Ctx& c, const double* f, double* u) {
@@ -451,7 +580,6 @@ void cycle_structured(Ctx& c, int l, const double* f, double* u) {
     Level& C = h->lv[l + 1];
     const Geo g = L.geo;
     const unsigned bq = blocks_for(g.nq);
-    AUX_CUDA(cudaMemsetAsync(u, 0, sizeof(double) * L.n, c.s));
     for (int sw = 0; sw < c.o.pre_sweeps; ++sw)
         for (int col = 0; col < 4; ++col) {
             k_gs9<<<bq, 256, 0, c.s>>>(g, L.val.p, L.active.p, f, u, col, (sw == 0 && col == 0) ? 1 : 0);
@@ -478,6 +606,11 @@ void apply_spmv(Ctx& c, int m, const double* x, double* y, int mode, const doubl
 // nonlinear_pcg (cycle.hpp:106-128) on level m >= 1 with the K-cycle of level
 // m as preconditioner; rhs already in lv[m].pcg.r, result in lv[m].pcg.u.
 void pcg_level(Ctx& c, int m) {
+    aux_hierarchy* h = c.h;
+    if (m == h->fused_m0) {   // this level and everything below: one single-CTA kernel
+        launch_fused_pcg(h->fused_args, c.s);
+        return;
+    }
     Level& L = c.h->lv[m];
     PcgBufs& P = L.pcg;
     const long n = L.n;
@@ -523,15 +656,33 @@ void finest_bgs_pass(Ctx& c, int color, const double* f, double* u, bool zero, d
         xin = snap;
     }
     prof_begin(c, 0);
-    k_bgs<<<blocks_for(g1 - g0, 128), 128, 0, c.s>>>(F.bptr.p, F.rp.p, F.col.p, F.v.p, f, xin, u, g0, g1,
-                                                     zero ? 1 : 0);
+    const int z = zero ? 1 : 0;
+    k_bgs<1, 4><<<blocks_for(g1 - g0, 128), 128, 0, c.s>>>(F.bptr.p, F.rp.p, F.col.p, F.v.p, f, xin, u, g0, g1, z);
     AUX_LAUNCHED(1);
-    const int j0 = F.big_color_begin[color], j1 = F.big_color_begin[color + 1];
-    if (j1 > j0) {
-        const int warps = j1 - j0;
-        k_bgs_big<<<(unsigned)std::min(1184, (warps * 32 + 127) / 128), 128, 0, c.s>>>(
-            F.big_ids.p, F.big_off.p, F.big_lu.p, F.big_perm.p, F.bptr.p, F.rp.p, F.col.p, F.v.p, f, xin, u,
-            F.scratch.p, j0, j1, F.n, zero ? 1 : 0);
+    if (F.max_block >= 5) {
+        k_bgs<5, kSmallBlock><<<blocks_for(g1 - g0, 128), 128, 0, c.s>>>(F.bptr.p, F.rp.p, F.col.p, F.v.p, f, xin,
+                                                                          u, g0, g1, z);
+        AUX_LAUNCHED(1);
+    }
+    const int j0 = F.big_color_begin[color], jc = F.big_cta_begin[color], j1 = F.big_color_begin[color + 1];
+    if (jc > j0) {   // 9..32 members: warp per block
+        const int warps = jc - j0;
+        k_bgs_warp<<<(unsigned)std::min(4736, (warps + 3) / 4), 128, 0, c.s>>>(
+            F.big_ids.p, F.big_off.p, F.big_lu.p, F.big_perm.p, F.bptr.p, F.rp.p, F.col.p, F.v.p, f, xin, u, j0, jc,
+            z);
+        AUX_LAUNCHED(1);
+    }
+    if (j1 > jc) {   // more than 32 members: CTA per block
+        const size_t need = ((size_t)F.max_block * F.max_block + F.max_block) * sizeof(double);
+        const int smem_lu = need <= (size_t)200 * 1024 ? 1 : 0;
+        static bool attr = false;
+        if (!attr) {
+            AUX_CUDA(cudaFuncSetAttribute(k_bgs_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+            attr = true;
+        }
+        k_bgs_cta<<<(unsigned)(j1 - jc), 128, smem_lu ? need : 0, c.s>>>(F.big_ids.p, F.big_off.p, F.big_lu.p,
+                                                                         F.big_perm.p, F.bptr.p, F.rp.p, F.col.p,
+                                                                         F.v.p, f, xin, u, F.scratch.p, jc, z, smem_lu);
         AUX_LAUNCHED(1);
     }
     prof_end(c, 0, g_color_bytes[color]);
@@ -545,7 +696,6 @@ void finest_cycle(Ctx& c, const double* f, double* u, double* snap) {
     }
     Finest& F = h->fine;
     Level& C = h->lv[1];
-    AUX_CUDA(cudaMemsetAsync(u, 0, sizeof(double) * F.n, c.s));
     for (int sw = 0; sw < c.o.pre_sweeps; ++sw)
         for (int col = 0; col < 4; ++col) finest_bgs_pass(c, col, f, u, sw == 0 && col == 0, snap);
     prof_begin(c, 2);
@@ -553,12 +703,14 @@ void finest_cycle(Ctx& c, const double* f, double* u, double* snap) {
                                                           C.pcg.sc.p);
     AUX_LAUNCHED(1);
     prof_end(c, 2, 12.0 * F.nnz + 4.0 * (F.n + 1) + 16.0 * F.n + 4.0 * (C.n + 1) + 8.0 * C.n);
+    g_trace.mark(c.s, 1);
     if (h->graph_valid) {
         AUX_CUDA(cudaGraphLaunch(h->graph, c.s));
         AUX_LAUNCHED(h->graph_kernels);
     } else {
         pcg_level(c, 1);
     }
+    g_trace.mark(c.s, 2);
     k_csr_prolong<<<blocks_for(F.n), 256, 0, c.s>>>(F.cell.p, F.n, u, C.pcg.u.p);
     AUX_LAUNCHED(1);
     for (int sw = 0; sw < c.o.post_sweeps; ++sw)
@@ -587,6 +739,57 @@ void build_graph(aux_hierarchy* h, const aux_cycle_opts& o, RedState rs) {
     h->graph_valid = true;
 }
 
+// Choose the first level handled by the single-CTA kernel and publish the
+// level descriptors it reads.
+void setup_fused(aux_hierarchy* h, const aux_cycle_opts& o) {
+    int m0 = 1 << 30;
+    const int cap = h->gpu.fused_max_cells < 0 ? (1 << 30) : h->gpu.fused_max_cells;
+    FusedArgs fa;
+    std::memset(&fa, 0, sizeof fa);
+    if (!h->direct_only && cap > 0 && o.n_inner <= kFusedMaxInner) {
+        // the largest tail of levels whose data fits in one CTA's shared memory
+        for (int l = 1; l < (int)h->lv.size(); ++l)
+            if (h->lv[l].n <= cap && fused_layout(h, l, o.n_inner, &fa) > 0) { m0 = l; break; }
+    }
+    if (m0 != h->fused_m0) h->graph_valid = false;
+    h->fused_m0 = m0;
+    if (m0 < (int)h->lv.size()) {
+        fa.m0 = m0;
+        fa.last = (int)h->lv.size() - 1;
+        fa.ni = o.n_inner;
+        fa.pre = o.pre_sweeps;
+        fa.post = o.post_sweeps;
+        fa.coarse_mode = h->gpu.coarse_solve;
+        fa.nc = h->nc;
+        fa.inv = h->c_inv.p;
+        fa.lu = h->c_lu.p;
+        fa.perm = h->c_perm.p;
+        fa.lex = h->c_lex.p;
+        fa.work = h->c_work.p;
+    }
+    if (m0 >= (int)h->lv.size()) return;
+    std::vector<FLevel> d(h->lv.size());
+    for (size_t l = 1; l < h->lv.size(); ++l) {
+        Level& L = h->lv[l];
+        FLevel& f = d[l];
+        std::memset(&f, 0, sizeof f);
+        f.g = L.geo;
+        f.val = L.val.p;
+        f.act = L.active.p;
+        f.r = L.pcg.r.p;
+        f.u = L.pcg.u.p;
+        for (int i = 0; i < o.n_inner && i < kFusedMaxInner; ++i) {
+            f.p[i] = L.pcg.p[i].p;
+            f.ap[i] = L.pcg.ap[i].p;
+        }
+    }
+    if (h->d_flv.n < d.size()) h->d_flv.alloc(d.size());
+    AUX_CUDA(cudaMemcpyAsync(h->d_flv.p, d.data(), sizeof(FLevel) * d.size(), cudaMemcpyHostToDevice, h->stream));
+    AUX_CUDA(cudaStreamSynchronize(h->stream));
+    fa.lv = h->d_flv.p;
+    h->fused_args = fa;
+}
+
 }  // namespace
 
 void solve_device(aux_hierarchy* h, const double* b, long n_b, const aux_cycle_opts* o, aux_solve_result* res,
@@ -611,17 +814,12 @@ void solve_device(aux_hierarchy* h, const double* b, long n_b, const aux_cycle_o
         h->w_b.alloc(n);
         h->w_tmp.alloc(n);
     }
-    if ((int)h->w_p.size() < slots) {
-        while ((int)h->w_p.size() < slots) {
-            h->w_p.emplace_back(n);
-            h->w_ap.emplace_back(n);
-        }
-    }
-    if (h->w_sc.n < (size_t)(8 + slots + 1)) h->w_sc.alloc(8 + std::max(slots, o->max_outer) + 1);
+    if (h->w_sc.n < (size_t)(8 + o->max_outer + 1)) h->w_sc.alloc(8 + o->max_outer + 1);
     if (!h->direct_only && h->lv.size() > 1 && (int)h->lv[1].pcg.p.size() != o->n_inner) {
         alloc_solve_levels(h, o->n_inner);
         h->graph_valid = false;
     }
+    setup_fused(h, *o);
     double* sc = h->w_sc.p;
     AUX_CUDA(cudaMemsetAsync(sc, 0, sizeof(double) * h->w_sc.n, s));
 
@@ -675,13 +873,21 @@ void solve_device(aux_hierarchy* h, const double* b, long n_b, const aux_cycle_o
         double* r = h->w_r.p;
         double* u = h->w_u.p;
         const double spmv_bytes = 12.0 * F.nnz + 4.0 * (n + 1) + 16.0 * n;
+        g_trace.on = std::getenv("AUX_TRACE") != nullptr;
+        g_trace.mark(s, 0);
         while (res->iterations < o->max_outer) {
             int slot = 0;
             while (in_use[slot]) ++slot;
+            while ((int)h->w_p.size() <= slot) {   // direction storage grows on demand
+                h->w_p.emplace_back(n);
+                h->w_ap.emplace_back(n);
+            }
             double* p = h->w_p[slot].p;
             double* ap = h->w_ap[slot].p;
             double* e_slot = sc + 8 + slot;
+            g_trace.mark(s, 5);
             finest_cycle(c, r, p, h->w_tmp.p);
+            g_trace.mark(s, 3);
             prof_begin(c, 1);
             if (h->direct_only) {
                 k_csr_spmv<<<red_blocks(n), kRedThreads, 0, s>>>(n, F.rp.p, F.col.p, F.v.p, p, ap, kept.empty() ? 0 : 1,
@@ -709,6 +915,7 @@ void solve_device(aux_hierarchy* h, const double* b, long n_b, const aux_cycle_o
             }
             k_update<<<red_blocks(n), kRedThreads, 0, s>>>(n, u, p, r, ap, 0, 1, 1, sc, rs, Fin{3, sc, nullptr, sc + 3});
             AUX_LAUNCHED(1);
+            g_trace.mark(s, 4);
             double st[2];
             AUX_CUDA(cudaMemcpyAsync(st, sc + 2, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
             AUX_CUDA(cudaStreamSynchronize(s));
@@ -747,6 +954,7 @@ void solve_device(aux_hierarchy* h, const double* b, long n_b, const aux_cycle_o
     res->total_seconds = secs;
     res->setup_seconds = 0.0;
     h->last_solve_ms = secs * 1e3;
+    g_trace.report();
 }
 
 }  // namespace auxb200
