@@ -92,9 +92,14 @@ typedef struct orc_hierarchy orc_hierarchy;
 
 /* ------------------------------------------------------ parallel.hpp:86-119 */
 
-/* dot: 1024-element sequential blocks + fixed pairwise tree, parallel.hpp:88-112 */
+/* dot: 1024-element sequential blocks + fixed pairwise tree, parallel.hpp:88-112.
+ * ORC_BLK != 1024 builds a sensitivity variant (tests only: it measures how
+ * far the reference's own results move under a different summation order). */
+#ifndef ORC_BLK
+#define ORC_BLK 1024
+#endif
 static double dot(const double* a, const double* b, size_t n) {
-    const size_t blk = 1024;
+    const size_t blk = ORC_BLK;
     size_t nb = (n + blk - 1) / blk;
     if (nb <= 1) {
         double s = 0.0;

