@@ -37,6 +37,67 @@ namespace auxb200 {
 
 namespace {
 
+
+// AUX_FUSED_CLOCKS (debug builds only): per (call type, level) clock64 totals,
+// printed once by the third launch.  Types: 0 cycle_down, 1 coarse_solve,
+// 2 pcg_step, 3 cycle_up.
+#ifdef AUX_FUSED_CLOCKS
+__device__ int g_fclk_launch;
+#define FCLK_DECL                                   \
+    __shared__ unsigned long long s_clk[16];        \
+    __shared__ unsigned s_cnt[16];                  \
+    if (threadIdx.x < 16) { s_clk[threadIdx.x] = 0; s_cnt[threadIdx.x] = 0; } \
+    __syncthreads();                                \
+    long long fclk_t0 = 0;
+#define FCLK_BEGIN fclk_t0 = clock64();
+#define FCLK_END(T, Q)                                                        \
+    if (threadIdx.x == 0) { s_clk[(T) * 4 + ((Q) & 3)] += clock64() - fclk_t0; s_cnt[(T) * 4 + ((Q) & 3)]++; }
+#define FCLK_REPORT                                                           \
+    if (threadIdx.x == 0 && atomicAdd(&g_fclk_launch, 1) == 2) {            \
+        for (int k = 0; k < 16; ++k)                                          \
+            if (s_cnt[k]) printf("fused clk type %d level %d: calls %u avg %llu cycles\n", k / 4, k % 4, s_cnt[k], \
+                                 s_clk[k] / s_cnt[k]);                        \
+    }
+#else
+#define FCLK_DECL
+#define FCLK_BEGIN
+#define FCLK_END(T, Q)
+#define FCLK_REPORT
+#endif
+
+// ---- TMA bulk copy (cp.async.bulk) + mbarrier helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+// global -> shared bulk copy; 16-byte aligned addresses, size a multiple of 16
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
 constexpr double kBreak = 1e-300;
 #ifndef AUX_FUSED_THREADS
 #define AUX_FUSED_THREADS 256
@@ -174,7 +235,8 @@ __device__ __forceinline__ void gs_sweep(const SLevel& L, const double* f, doubl
 
 // Coarsest solve (cycle.hpp:152-155).  The coarsest level's vectors are padded
 // too; the inverse is stored in colour-major (compact) order.
-__device__ void coarse_solve(const FusedArgs& a, const double* inv, const SLevel& L, PState& ps, double* u) {
+__device__ void coarse_solve(const FusedArgs& a, const double* inv, double* part, const SLevel& L, PState& ps,
+                             double* u) {
     double* r = L.r;
     if (ps.pend) {
         const double na = -ps.alpha[ps.step - 1];
@@ -202,18 +264,24 @@ __device__ void coarse_solve(const FusedArgs& a, const double* inv, const SLevel
             }
         }
     } else {
-        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-        for (int row = wid; row < a.nc; row += kWarps) {
+        // column-major inverse: thread (row, quarter) sums its quarter of j
+        // sequentially (conflict-free shared loads, r broadcast), then the four
+        // partials combine in order — the order of k_coarse_inv.
+        const int nc = a.nc, cs = (nc + 3) / 4;
+        for (int idx = threadIdx.x; idx < 4 * nc; idx += kThreads) {
+            const int row = idx % nc, k = idx / nc;
             double s = 0.0;
-            for (int j = lane; j < a.nc; j += 32) {
+            for (int j = k * cs; j < min(nc, (k + 1) * cs); ++j) {
                 const int c = j >> (2 * L.lh), pos = j & (L.nq - 1);
-                s = fma(inv[row * a.nc + j], r[pidx(L, c, pos & (L.H - 1), pos >> L.lh)], s);
+                s = fma(inv[j * nc + row], r[pidx(L, c, pos & (L.H - 1), pos >> L.lh)], s);
             }
-            s = warp_sum(s);
-            if (lane == 0) {
-                const int c = row >> (2 * L.lh), pos = row & (L.nq - 1);
-                u[pidx(L, c, pos & (L.H - 1), pos >> L.lh)] = s;
-            }
+            part[k * nc + row] = s;
+        }
+        __syncthreads();
+        for (int row = threadIdx.x; row < nc; row += kThreads) {
+            const int c = row >> (2 * L.lh), pos = row & (L.nq - 1);
+            u[pidx(L, c, pos & (L.H - 1), pos >> L.lh)] =
+                ((part[row] + part[nc + row]) + part[2 * nc + row]) + part[3 * nc + row];
         }
     }
     __syncthreads();
@@ -367,27 +435,47 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_pcg(const __grid_constant
     __shared__ double red[2 * 2 * kWarps];
     const int nl = a.last - a.m0 + 1;
 
-    // ---- stage read-only data, zero the padded vectors (ghost rings), load r
+    // ---- stage read-only data with TMA bulk copies (cp.async.bulk, all in
+    // flight at once, completion on one mbarrier); meanwhile zero the padded
+    // vectors (ghost rings) with 16-byte stores.
+    __shared__ __align__(8) uint64_t bar;
+    const double* inv = a.inv;
+    if (a.inv_in_smem) inv = reinterpret_cast<const double*>(sm + a.off_inv);
+    if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t bytes = 0;
+        for (int q = 0; q < nl; ++q) {
+            const int n = a.lv[a.m0 + q].g.n;
+            bytes += 9u * n * 8u;
+            if ((n & 15) == 0) bytes += (uint32_t)n;
+        }
+        if (a.inv_in_smem) bytes += (uint32_t)a.nc * a.nc * 8u;
+        mbar_arrive_expect_tx(&bar, bytes);
+        for (int q = 0; q < nl; ++q) {
+            const FLevel& G = a.lv[a.m0 + q];
+            const int n = G.g.n;
+            bulk_g2s(sm + a.off_val[q], G.val, 9u * n * 8u, &bar);
+            if ((n & 15) == 0) bulk_g2s(sm + a.off_act[q], G.act, (uint32_t)n, &bar);
+        }
+        if (a.inv_in_smem) bulk_g2s(sm + a.off_inv, a.inv, (uint32_t)a.nc * a.nc * 8u, &bar);
+    }
     for (int q = 0; q < nl; ++q) {
         const FLevel& G = a.lv[a.m0 + q];
         const int n = G.g.n;
-        const double2* src = reinterpret_cast<const double2*>(G.val);
-        double2* dst = reinterpret_cast<double2*>(sm + a.off_val[q]);
-        for (int i = threadIdx.x; i < 9 * n / 2; i += kThreads) dst[i] = src[i];
-        if (((9 * n) & 1) && threadIdx.x == 0)
-            reinterpret_cast<double*>(sm + a.off_val[q])[9 * n - 1] = G.val[9 * n - 1];
-        uint8_t* act = sm + a.off_act[q];
-        for (int i = threadIdx.x; i < n; i += kThreads) act[i] = G.act[i];
+        if (n & 15) {   // too small for a bulk copy
+            uint8_t* act = sm + a.off_act[q];
+            for (int i = threadIdx.x; i < n; i += kThreads) act[i] = G.act[i];
+        }
         const int W2 = G.g.H + 2;
-        double* v = reinterpret_cast<double*>(sm + a.off_vec[q]);
-        for (int i = threadIdx.x; i < (1 + 2 * a.ni) * 4 * W2 * W2; i += kThreads) v[i] = 0.0;
+        double2* v = reinterpret_cast<double2*>(sm + a.off_vec[q]);
+        const int nv2 = (1 + 2 * a.ni) * 2 * W2 * W2;   // doubles / 2 (4*W2*W2 is even)
+        for (int i = threadIdx.x; i < nv2; i += kThreads) v[i] = make_double2(0.0, 0.0);
     }
-    const double* inv = a.inv;
-    if (a.inv_in_smem) {
-        double* d = reinterpret_cast<double*>(sm + a.off_inv);
-        for (int i = threadIdx.x; i < a.nc * a.nc; i += kThreads) d[i] = a.inv[i];
-        inv = d;
-    }
+    mbar_wait(&bar, 0);
     __syncthreads();
     {
         const SLevel L0 = slev(a, sm, 0);
@@ -407,23 +495,31 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_pcg(const __grid_constant
     ps[0].nval = 0;
     ps[0].pend = 0;
     bool resume = false;   // false: start cycle(q) for step; true: cycle(q) just finished
+    double* part = reinterpret_cast<double*>(sm + a.off_part);
+    FCLK_DECL
     while (true) {
         const SLevel L = slev(a, sm, q);
         if (!resume) {
             double* u = L.p + ps[q].step * 4 * L.PP;
             if (q == nl - 1) {
-                coarse_solve(a, inv, L, ps[q], u);
+                FCLK_BEGIN
+                coarse_solve(a, inv, part, L, ps[q], u);
+                FCLK_END(1, q)
                 resume = true;
                 continue;
             }
+            FCLK_BEGIN
             cycle_down(a, L, ps[q], slev(a, sm, q + 1), u);
+            FCLK_END(0, q)
             ++q;
             ps[q].step = 0;
             ps[q].nval = 0;
             ps[q].pend = 0;
             continue;
         }
+        FCLK_BEGIN
         const bool done = pcg_step(a, L, ps[q], red, par);
+        FCLK_END(2, q)
         if (!done) {
             ps[q].pend = 1;
             ++ps[q].step;
@@ -433,9 +529,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_pcg(const __grid_constant
         if (q == 0) break;
         --q;
         const SLevel P = slev(a, sm, q);
+        FCLK_BEGIN
         cycle_up(a, P, L, ps[q + 1], P.p + ps[q].step * 4 * P.PP);
+        FCLK_END(3, q)
         resume = true;
     }
+    FCLK_REPORT
 
     // ---- u of nonlinear_pcg(m0) = ((0 + alpha_0 p_0) + alpha_1 p_1) ... to global memory
     {
@@ -470,6 +569,7 @@ unsigned fused_layout(const aux_hierarchy* h, int m0, int ni, FusedArgs* a) {
         a->off_vec[q] = take((1 + 2 * (size_t)ni) * 4 * W2 * W2 * sizeof(double));
         a->off_act[q] = take(n);
     }
+    a->off_part = take(4 * (size_t)h->nc * sizeof(double));
     const size_t need = off;
     if (need > (size_t)kFusedSmemMax) return 0;
     const size_t inv_bytes = (size_t)h->nc * h->nc * sizeof(double);

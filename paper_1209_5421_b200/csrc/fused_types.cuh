@@ -35,6 +35,7 @@ struct FusedArgs {
     unsigned off_act[kMaxFusedLevels];
     unsigned off_vec[kMaxFusedLevels];   // r, u, p[0..ni), ap[0..ni), n doubles each
     unsigned off_inv;                    // explicit inverse, if staged
+    unsigned off_part;                   // 4*nc partial sums of the coarse mat-vec
     int inv_in_smem;
     unsigned smem_bytes;
 };

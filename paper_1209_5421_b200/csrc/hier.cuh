@@ -83,20 +83,24 @@ struct Finest {
     DBuf<int> cell;      // new row -> level-L colour-major cell id
     DBuf<int> lex_of_row;// new row -> level-L lexicographic cell id (agg_of)
     DBuf<int> bptr;      // level-L colour-major cell -> first row (n_L + 1)
-    // blocks with more than kSmallBlock members: stored LU factors
+    // LU factors of every block with >= 2 members, stored once at setup as in
+    // factor_blocks (smoother.hpp:129-156): row-major s*s at cell_lu_off[g],
+    // pivot permutation at big_perm[first row of g ...]
+    DBuf<int> cell_lu_off;    // n_L + 1
+    DBuf<double> big_lu;
+    DBuf<int> big_perm;       // N
+    // blocks with more than kTileBlock members, solved by the warp / CTA kernels
     int n_big = 0;
     int big_color_begin[5] = {0, 0, 0, 0, 0};   // big-block list split by colour
     int big_cta_begin[4] = {0, 0, 0, 0};        // within a colour: first block with > 32 members
     DBuf<int> big_ids;        // cell ids (colour-major), sorted by colour
-    DBuf<long long> big_off;  // offset of each big block's s*s LU in big_lu
-    DBuf<double> big_lu;
-    DBuf<int> big_perm;       // s entries per big block, indexed by first row
-    DBuf<double> scratch;     // 2N: residual + solution scratch of the big-block solves
+    DBuf<double> scratch;     // 2N: colour-pass residuals + big-block solutions
+    int color_row[5] = {0, 0, 0, 0, 0};   // first finest row of each colour class (+ N)
     bool color_clean = true;  // check_color_locality (smoother.hpp:217-231) empty
     int max_block = 0;
 };
 
-constexpr int kSmallBlock = 8;   // blocks up to this size re-factor in registers every sweep
+constexpr int kTileBlock = 8;   // blocks up to this size: one thread per block
 
 struct Profile {
     bool on = false;

@@ -266,39 +266,14 @@ __global__ void k_locality_sum(const int* __restrict__ dcnt, const double* __res
     *out = m;
 }
 
-// factor_blocks for 2 <= s <= kSmallBlock: factor in registers, report the
-// lowest singular aggregate (lexicographic id, the reference's loop order).
-template <int S>
-__device__ void check_small_block(const int* rp, const int* col, const double* v, int r0, Geo g, int r,
-                                  unsigned long long* err) {
-    double a[S][S];
-    int perm[S];
-#pragma unroll
-    for (int q = 0; q < S; ++q)
-#pragma unroll
-        for (int c = 0; c < S; ++c) a[q][c] = 0.0;
-#pragma unroll
-    for (int q = 0; q < S; ++q)
-        for (int p = rp[r0 + q]; p < rp[r0 + q + 1]; ++p) {
-            const unsigned off = (unsigned)(col[p] - r0);
-#pragma unroll
-            for (int c = 0; c < S; ++c)
-                if (off == (unsigned)c) a[q][c] = v[p];
-        }
-    if (!reg_lu_factor<S>(a, perm)) atomicMin(err, (unsigned long long)lex_of_cm(g, r));
-}
-
-__global__ void k_block_check(const int* __restrict__ bptr, const int* __restrict__ rp, const int* __restrict__ col,
-                              const double* __restrict__ v, Geo g, unsigned long long* err, int* big_flag,
-                              int* max_block) {
+// Block-size census: blocks with more than kTileBlock members are solved by
+// the warp / CTA kernels and listed; the maximum size is recorded.
+__global__ void k_block_check(const int* __restrict__ bptr, Geo g, int* big_flag, int* max_block) {
     int mb = 0;
     GSTRIDE(r, g.n) {
-        const int r0 = bptr[r], s = bptr[r + 1] - r0;
+        const int s = bptr[r + 1] - bptr[r];
         mb = max(mb, s);
-        big_flag[r] = s > kSmallBlock ? 1 : 0;
-        if (s == 2) check_small_block<2>(rp, col, v, r0, g, (int)r, err);
-        else if (s == 3) check_small_block<3>(rp, col, v, r0, g, (int)r, err);
-        else if (s == 4) check_small_block<4>(rp, col, v, r0, g, (int)r, err);
+        big_flag[r] = s > kTileBlock ? 1 : 0;
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mb = max(mb, __shfl_xor_sync(0xffffffffu, mb, o));
@@ -309,14 +284,42 @@ __global__ void k_compact(const int* __restrict__ flag, const int* __restrict__ 
     GSTRIDE(i, n) if (flag[i]) out[pos[i]] = (int)i;
 }
 
-// Extract and factor one big block per CTA (s > kSmallBlock).
-__global__ void k_factor_big(const int* __restrict__ ids, const long long* __restrict__ off,
+// LU factor pool offsets: blocks with s >= 2 store s*s factors (singletons use
+// the point update and need none, smoother.hpp:178-191).
+__global__ void k_lu_sizes(const int* __restrict__ bptr, int nL, int* __restrict__ cnt) {
+    GSTRIDE(g, nL) {
+        const int s = bptr[g + 1] - bptr[g];
+        cnt[g] = s >= 2 ? s * s : 0;
+    }
+}
+
+// factor_blocks (smoother.hpp:129-156) for 2 <= s <= 16: one thread extracts the
+// principal block into the pool and factors it in place (lu_factor order).
+__global__ void k_factor_cells(const int* __restrict__ bptr, const int* __restrict__ rp, const int* __restrict__ col,
+                               const double* __restrict__ v, Geo g, const int* __restrict__ off,
+                               double* __restrict__ lu, int* __restrict__ perm, unsigned long long* err) {
+    GSTRIDE(gid, g.n) {
+        const int r0 = bptr[gid], s = bptr[gid + 1] - r0;
+        if (s < 2 || s > 16) continue;
+        double* a = lu + off[gid];
+        for (int e = 0; e < s * s; ++e) a[e] = 0.0;
+        for (int q = 0; q < s; ++q)
+            for (int p = rp[r0 + q]; p < rp[r0 + q + 1]; ++p) {
+                const unsigned c = (unsigned)(col[p] - r0);
+                if (c < (unsigned)s) a[q * s + c] = v[p];
+            }
+        if (!seq_lu_factor(a, perm + r0, s)) atomicMin(err, (unsigned long long)lex_of_cm(g, (int)gid));
+    }
+}
+
+// Extract and factor one block of more than 16 members per CTA.
+__global__ void k_factor_big(const int* __restrict__ ids, const int* __restrict__ off,
                              const int* __restrict__ bptr, const int* __restrict__ rp, const int* __restrict__ col,
                              const double* __restrict__ v, Geo g, double* __restrict__ lu, int* __restrict__ perm,
                              unsigned long long* err) {
     const int gid = ids[blockIdx.x];
     const int r0 = bptr[gid], s = bptr[gid + 1] - r0;
-    double* a = lu + off[blockIdx.x];
+    double* a = lu + off[gid];
     for (long e = threadIdx.x; e < (long)s * s; e += blockDim.x) a[e] = 0.0;
     __syncthreads();
     for (int q = threadIdx.x; q < s; q += blockDim.x)
@@ -470,8 +473,8 @@ __global__ void k_inverse(const double* __restrict__ lu, const int* __restrict__
 }
 __global__ void k_inverse_scatter(const double* __restrict__ work, const int* __restrict__ lex_of_storage, int n,
                                   double* __restrict__ inv) {
-    GSTRIDE(e, (long)n * n) {
-        const int is = (int)(e / n), js = (int)(e % n);
+    GSTRIDE(e, (long)n * n) {   // column-major: inv[js*n + is] = M(is, js)
+        const int js = (int)(e / n), is = (int)(e % n);
         inv[e] = work[(size_t)js * n + lex_of_storage[is]];
     }
 }
@@ -668,6 +671,9 @@ void setup_device(aux_hierarchy* h, const aux_csr_view* A, const double* xy, lon
         F.bptr.alloc(nL + 1);
         exclusive_scan(cnt.p, F.bptr.p, nL, s);
     }
+    for (int c = 0; c <= 4; ++c)
+        AUX_CUDA(cudaMemcpyAsync(&F.color_row[c], F.bptr.p + (c < 4 ? (c << gL.lq) : nL), sizeof(int),
+                                 cudaMemcpyDeviceToHost, s));
     F.iperm.alloc(n);
     F.cell.alloc(n);
     F.lex_of_row.alloc(n);
@@ -692,9 +698,26 @@ void setup_device(aux_hierarchy* h, const aux_csr_view* A, const double* xy, lon
         DBuf<int> flag(nL), mb(1);
         AUX_CUDA(cudaMemsetAsync(err.p, 0xff, sizeof(unsigned long long), s));
         AUX_CUDA(cudaMemsetAsync(mb.p, 0, sizeof(int), s));
-        k_block_check<<<grid_for(nL), kT, 0, s>>>(F.bptr.p, F.rp.p, F.col.p, F.v.p, gL, err.p, flag.p, mb.p);
+        k_block_check<<<grid_for(nL), kT, 0, s>>>(F.bptr.p, gL, flag.p, mb.p);
         AUX_LAUNCHED(1);
         F.max_block = read1(mb.p, s);
+        // stored LU factors of every block with s >= 2 (factor_blocks, smoother.hpp:129-156)
+        if ((long long)n * F.max_block >= (1ll << 31))
+            throw_aux(AUX_CAPACITY_ERROR, "block factor pool exceeds 2^31 entries");
+        {
+            DBuf<int> cnt(nL);
+            F.cell_lu_off.alloc(nL + 1);
+            k_lu_sizes<<<grid_for(nL), kT, 0, s>>>(F.bptr.p, nL, cnt.p);
+            AUX_LAUNCHED(1);
+            exclusive_scan(cnt.p, F.cell_lu_off.p, nL, s);
+            const int pool = read1(F.cell_lu_off.p + nL, s);
+            F.big_lu.alloc(std::max(pool, 1));
+            F.big_perm.alloc(n);
+            k_factor_cells<<<grid_for(nL), kT, 0, s>>>(F.bptr.p, F.rp.p, F.col.p, F.v.p, gL, F.cell_lu_off.p,
+                                                       F.big_lu.p, F.big_perm.p, err.p);
+            AUX_LAUNCHED(1);
+            F.scratch.alloc(2 * (size_t)n);   // colour-pass residuals + big-block solutions
+        }
         DBuf<int> pos(nL + 1);
         exclusive_scan(flag.p, pos.p, nL, s);
         int nbig = 0;
@@ -713,7 +736,7 @@ void setup_device(aux_hierarchy* h, const aux_csr_view* A, const double* xy, lon
             AUX_CUDA(cudaStreamSynchronize(s));
             // order: per colour, the warp class (<= 32 members) then the CTA class
             auto bsize = [&](int g) { return bptr_h[g + 1] - bptr_h[g]; };
-            std::vector<int> ord;
+            std::vector<int> ord, huge;
             ord.reserve(nbig);
             for (int c = 0; c < 4; ++c) {
                 F.big_color_begin[c] = (int)ord.size();
@@ -725,20 +748,17 @@ void setup_device(aux_hierarchy* h, const aux_csr_view* A, const double* xy, lon
             }
             F.big_color_begin[4] = (int)ord.size();
             ids.swap(ord);
+            for (int g : ids)
+                if (bsize(g) > 16) huge.push_back(g);
             AUX_CUDA(cudaMemcpyAsync(F.big_ids.p, ids.data(), sizeof(int) * nbig, cudaMemcpyHostToDevice, s));
-            std::vector<long long> off(nbig + 1, 0);
-            for (int j = 0; j < nbig; ++j) {
-                const long long sz = bsize(ids[j]);
-                off[j + 1] = off[j] + sz * sz;
+            if (!huge.empty()) {   // blocks the thread-per-block factorisation skipped
+                DBuf<int> hid(huge.size());
+                AUX_CUDA(cudaMemcpyAsync(hid.p, huge.data(), sizeof(int) * huge.size(), cudaMemcpyHostToDevice, s));
+                k_factor_big<<<(unsigned)huge.size(), 128, 0, s>>>(hid.p, F.cell_lu_off.p, F.bptr.p, F.rp.p, F.col.p,
+                                                                    F.v.p, gL, F.big_lu.p, F.big_perm.p, err.p);
+                AUX_LAUNCHED(1);
+                AUX_CUDA(cudaStreamSynchronize(s));
             }
-            F.big_off.alloc(nbig + 1);
-            AUX_CUDA(cudaMemcpyAsync(F.big_off.p, off.data(), sizeof(long long) * (nbig + 1), cudaMemcpyHostToDevice, s));
-            F.big_lu.alloc(off[nbig]);
-            F.big_perm.alloc(n);
-            k_factor_big<<<nbig, 128, 0, s>>>(F.big_ids.p, F.big_off.p, F.bptr.p, F.rp.p, F.col.p, F.v.p, gL,
-                                               F.big_lu.p, F.big_perm.p, err.p);
-            AUX_LAUNCHED(1);
-            F.scratch.alloc(2 * (size_t)n);   // residuals + solutions of the big-block solves
         }
         const unsigned long long e = read1(err.p, s);
         if (e != ~0ull) throw_aux(AUX_DEFINITENESS_ERROR, "aggregate " + std::to_string(e) + " has a singular block");

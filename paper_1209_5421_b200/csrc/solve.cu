@@ -223,16 +223,21 @@ __global__ void __launch_bounds__(kRedThreads) k_dot(long n, const double* __res
 // ------------------------------------------------------------ coarsest solve
 
 // u = A_c^{-1} f with the explicit inverse (one warp per row, fixed order).
+// The inverse is column-major (inv[j*n + i] = M_ij); each row is summed as four
+// sequential quarter sums combined in order — the same order as the fused
+// kernel's coarse solve, so both paths give identical bits.
 __global__ void k_coarse_inv(int n, const double* __restrict__ inv, const double* __restrict__ f,
                              double* __restrict__ u) {
-    const int lane = threadIdx.x & 31;
-    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int nw = (gridDim.x * blockDim.x) >> 5;
-    for (int i = warp; i < n; i += nw) {
-        double s = 0.0;
-        for (int j = lane; j < n; j += 32) s = fma(inv[(size_t)i * n + j], f[j], s);
-        s = warp_sum(s);
-        if (lane == 0) u[i] = s;
+    const int cs = (n + 3) / 4;
+    GSTRIDE(i, n) {
+        double part[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            double s = 0.0;
+            for (int j = k * cs; j < min(n, (k + 1) * cs); ++j) s = fma(inv[(size_t)j * n + i], f[j], s);
+            part[k] = s;
+        }
+        u[i] = ((part[0] + part[1]) + part[2]) + part[3];
     }
 }
 
@@ -249,60 +254,86 @@ __global__ void k_coarse_lu(int n, const double* __restrict__ lu, const int* __r
 }
 
 // ------------------------------------------------------------ finest level (CSR)
+//
+// One colour pass of block_gs_sweep (smoother.hpp:162-205) is split in two
+// row-parallel kernels:
+//   k_rows      thread per row, residual b_i - sum_p a_p x_p in CSR storage
+//               order (smoother.hpp:196-199) into a scratch vector — the
+//               bandwidth part, shaped like a CSR SpMV;
+//   k_bgs_solve thread per block (<= kTileBlock members): LuFactors::solve
+//               (dense.hpp:52-67) with the factors stored at setup, exactly as
+//               the reference stores them; singletons take the point update
+//               (smoother.hpp:178-191).
+// Blocks above kTileBlock are solved by k_bgs_warp / k_bgs_cta from the same
+// residuals.  With zero = true (first pass from u = 0) the residual is b.
 
-template <int S>
-__device__ __forceinline__ void bgs_block(const int* __restrict__ rp, const int* __restrict__ col,
-                                          const double* __restrict__ v, const double* __restrict__ b,
-                                          const double* __restrict__ xin, double* __restrict__ xout, int r0,
-                                          bool zero) {
-    double a[S][S];
-    double res[S], d[S];
-    int perm[S];
-#pragma unroll
-    for (int q = 0; q < S; ++q) {
-#pragma unroll
-        for (int c = 0; c < S; ++c) a[q][c] = 0.0;
-        const int i = r0 + q;
-        double sum = b[i];
-        for (int p = rp[i]; p < rp[i + 1]; ++p) {
-            const int c = col[p];
-            const double val = v[p];
-            const unsigned off = (unsigned)(c - r0);
-#pragma unroll
-            for (int cc = 0; cc < S; ++cc)
-                if (off == (unsigned)cc) a[q][cc] = val;
-            if (!zero) sum = __dsub_rn(sum, __dmul_rn(val, xin[c]));
+// r_i = b_i - sum a x (mode 0, smoother) or r_i = b_i - (0 + sum a x)
+// (mode 1, residual before restriction, cycle.hpp:173-176).
+__global__ void __launch_bounds__(256) k_rows(const int* __restrict__ rp, const int* __restrict__ col,
+                                             const double* __restrict__ v, const double* __restrict__ b,
+                                             const double* __restrict__ x, double* __restrict__ r, int r0, int r1,
+                                             int mode) {
+    GSTRIDE(ii, (long)(r1 - r0)) {
+        const int i = r0 + (int)ii;
+        const int p0 = rp[i], p1 = rp[i + 1];
+        if (mode == 0) {
+            double s = b[i];
+            for (int p = p0; p < p1; ++p) s = __dsub_rn(s, __dmul_rn(v[p], x[col[p]]));
+            r[i] = s;
+        } else {
+            double s = 0.0;
+            for (int p = p0; p < p1; ++p) s = __dadd_rn(s, __dmul_rn(v[p], x[col[p]]));
+            r[i] = __dsub_rn(b[i], s);
         }
-        res[q] = sum;
     }
-    reg_lu_factor<S>(a, perm);
-    reg_lu_solve<S>(a, perm, res, d);
-#pragma unroll
-    for (int q = 0; q < S; ++q) xout[r0 + q] = __dadd_rn(zero ? 0.0 : xin[r0 + q], d[q]);
 }
 
-// One colour pass of block_gs_sweep (smoother.hpp:162-205) over the cells
-// [g0, g1) of one colour, for the blocks with LO <= size <= HI: size 1 uses the
-// point update (smoother.hpp:178-191), sizes up to kSmallBlock re-factor in
-// registers (one thread per block).  The <1,4> instance also clears the
-// sibling rows on the first pass from zero.
-template <int LO, int HI>
-__global__ void __launch_bounds__(128) k_bgs(const int* __restrict__ bptr, const int* __restrict__ rp,
-                                            const int* __restrict__ col, const double* __restrict__ v,
-                                            const double* __restrict__ b, const double* __restrict__ xin,
-                                            double* __restrict__ xout, int g0, int g1, int zero) {
+template <int S>
+__device__ __forceinline__ void block_solve_stored(const double* __restrict__ lu, const int* __restrict__ perm,
+                                                   const double* __restrict__ res, int r0,
+                                                   const double* __restrict__ xin, double* __restrict__ xout,
+                                                   bool zero) {
+    double x[S];
+#pragma unroll
+    for (int i = 0; i < S; ++i) x[i] = res[r0 + perm[r0 + i]];
+#pragma unroll
+    for (int i = 1; i < S; ++i) {
+        double s = x[i];
+#pragma unroll
+        for (int j = 0; j < i; ++j) s = __dsub_rn(s, __dmul_rn(lu[i * S + j], x[j]));
+        x[i] = s;
+    }
+#pragma unroll
+    for (int i = S - 1; i >= 0; --i) {
+        double s = x[i];
+#pragma unroll
+        for (int j = i + 1; j < S; ++j) s = __dsub_rn(s, __dmul_rn(lu[i * S + j], x[j]));
+        x[i] = __ddiv_rn(s, lu[i * S + i]);
+    }
+#pragma unroll
+    for (int q = 0; q < S; ++q) xout[r0 + q] = __dadd_rn(zero ? 0.0 : xin[r0 + q], x[q]);
+}
+
+// Blocks of one colour [g0, g1) with at most kTileBlock members.  res holds the
+// residual rows (or is b on the zero pass).  On the zero pass the rows of the
+// sibling cells of the other colours are cleared (u = 0, cycle.hpp:170).
+__global__ void __launch_bounds__(128) k_bgs_solve(const int* __restrict__ bptr, const int* __restrict__ rp,
+                                                  const int* __restrict__ col, const double* __restrict__ v,
+                                                  const double* __restrict__ b, const double* __restrict__ res,
+                                                  const int* __restrict__ lu_off, const double* __restrict__ lu,
+                                                  const int* __restrict__ perm, const double* __restrict__ xin,
+                                                  double* __restrict__ xout, int g0, int g1, int zero) {
     GSTRIDE(gg, (long)(g1 - g0)) {
         const int g = g0 + (int)gg;
         const int r0 = bptr[g], s = bptr[g + 1] - r0;
-        if (LO == 1 && zero) {   // u = 0 on the rows of the sibling cells of the other colours
+        if (zero) {
             const int nq = g1 - g0;
             for (int cc = 1; cc < 4; ++cc) {
                 const int gs = g + cc * nq;
                 for (int i = bptr[gs]; i < bptr[gs + 1]; ++i) xout[i] = 0.0;
             }
         }
-        if (s < LO || s > HI) continue;
-        if (s == 1) {
+        if (s == 1) {   // point update with the diagonal split off (smoother.hpp:178-191)
             double diag = 0.0, sum = b[r0];
             for (int p = rp[r0]; p < rp[r0 + 1]; ++p) {
                 const int c = col[p];
@@ -310,46 +341,32 @@ __global__ void __launch_bounds__(128) k_bgs(const int* __restrict__ bptr, const
                 else if (!zero) sum = __dsub_rn(sum, __dmul_rn(v[p], xin[c]));
             }
             xout[r0] = __ddiv_rn(sum, diag);
-        } else if (s == 2) {
-            bgs_block<2>(rp, col, v, b, xin, xout, r0, zero);
-        } else if (s == 3) {
-            bgs_block<3>(rp, col, v, b, xin, xout, r0, zero);
-        } else if (HI >= 4 && s == 4) {
-            bgs_block<(HI >= 4 ? 4 : 1)>(rp, col, v, b, xin, xout, r0, zero);
-        } else if (HI >= 5 && s == 5) {
-            bgs_block<(HI >= 5 ? 5 : 1)>(rp, col, v, b, xin, xout, r0, zero);
-        } else if (HI >= 6 && s == 6) {
-            bgs_block<(HI >= 6 ? 6 : 1)>(rp, col, v, b, xin, xout, r0, zero);
-        } else if (HI >= 7 && s == 7) {
-            bgs_block<(HI >= 7 ? 7 : 1)>(rp, col, v, b, xin, xout, r0, zero);
-        } else if (HI >= 8 && s == 8) {
-            bgs_block<(HI >= 8 ? 8 : 1)>(rp, col, v, b, xin, xout, r0, zero);
+            continue;
+        }
+        const double* f = lu + lu_off[g];
+        switch (s) {
+            case 2: block_solve_stored<2>(f, perm, res, r0, xin, xout, zero); break;
+            case 3: block_solve_stored<3>(f, perm, res, r0, xin, xout, zero); break;
+            case 4: block_solve_stored<4>(f, perm, res, r0, xin, xout, zero); break;
+            case 5: block_solve_stored<5>(f, perm, res, r0, xin, xout, zero); break;
+            case 6: block_solve_stored<6>(f, perm, res, r0, xin, xout, zero); break;
+            case 7: block_solve_stored<7>(f, perm, res, r0, xin, xout, zero); break;
+            case 8: block_solve_stored<8>(f, perm, res, r0, xin, xout, zero); break;
+            default: break;   // larger blocks: k_bgs_warp / k_bgs_cta
         }
     }
 }
 
-// Residual row b_i - sum_p a_p x_p over the whole row in storage order
-// (smoother.hpp:196-199).
-__device__ __forceinline__ double block_res_row(const int* __restrict__ rp, const int* __restrict__ col,
-                                                const double* __restrict__ v, const double* __restrict__ b,
-                                                const double* __restrict__ xin, int i, bool zero) {
-    double sum = b[i];
-    if (!zero)
-        for (int p = rp[i]; p < rp[i + 1]; ++p) sum = __dsub_rn(sum, __dmul_rn(v[p], xin[col[p]]));
-    return sum;
-}
-
-// Blocks of kSmallBlock+1 .. 32 members: one warp per block, lane q owns row q.
-// The stored LU factors (setup, factor_blocks) are staged in shared memory;
-// the forward substitution runs column by column across lanes (every row
-// still subtracts in ascending column order, dense.hpp:57-61); the backward
-// substitution is the reference's row loop (dense.hpp:62-66) on one lane.
-__global__ void __launch_bounds__(128) k_bgs_warp(const int* __restrict__ ids, const long long* __restrict__ off,
+// Blocks of kTileBlock+1 .. 32 members: one warp per block, lane q owns row q.
+// The stored factors are staged in shared memory; the forward substitution
+// runs column by column across lanes (every row still subtracts in ascending
+// column order, dense.hpp:57-61); the backward substitution is the reference's
+// row loop (dense.hpp:62-66) on one lane, unrolled so loads run ahead.
+__global__ void __launch_bounds__(128) k_bgs_warp(const int* __restrict__ ids, const int* __restrict__ lu_off,
                                                  const double* __restrict__ lu, const int* __restrict__ lperm,
-                                                 const int* __restrict__ bptr, const int* __restrict__ rp,
-                                                 const int* __restrict__ col, const double* __restrict__ v,
-                                                 const double* __restrict__ b, const double* __restrict__ xin,
-                                                 double* __restrict__ xout, int j0, int j1, int zero) {
+                                                 const int* __restrict__ bptr, const double* __restrict__ res,
+                                                 const double* __restrict__ xin, double* __restrict__ xout, int j0,
+                                                 int j1, int zero) {
     __shared__ double sLU[4][32 * 32];
     __shared__ double sx[4][32];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -360,12 +377,11 @@ __global__ void __launch_bounds__(128) k_bgs_warp(const int* __restrict__ ids, c
     for (int j = j0 + warp; j < j1; j += nw) {
         const int g = ids[j];
         const int r0 = bptr[g], s = bptr[g + 1] - r0;
-        const double* F = lu + off[j];
+        const double* F = lu + lu_off[g];
         for (int e = lane; e < s * s; e += 32) U[e] = F[e];
-        const double res = lane < s ? block_res_row(rp, col, v, b, xin, r0 + lane, zero) : 0.0;
         const int pm = lane < s ? lperm[r0 + lane] : 0;
+        double x = lane < s ? res[r0 + pm] : 0.0;
         __syncwarp();
-        double x = __shfl_sync(0xffffffffu, res, pm);
         for (int c = 0; c + 1 < s; ++c) {
             const double xc = __shfl_sync(0xffffffffu, x, c);
             if (lane > c && lane < s) x = __dsub_rn(x, __dmul_rn(U[lane * s + c], xc));
@@ -375,8 +391,10 @@ __global__ void __launch_bounds__(128) k_bgs_warp(const int* __restrict__ ids, c
         if (lane == 0) {
             for (int i = s - 1; i >= 0; --i) {
                 double t = X[i];
-                for (int c = i + 1; c < s; ++c) t = __dsub_rn(t, __dmul_rn(U[i * s + c], X[c]));
-                X[i] = __ddiv_rn(t, U[i * s + i]);
+                const double* Ui = U + i * s;
+#pragma unroll 8
+                for (int c = i + 1; c < s; ++c) t = __dsub_rn(t, __dmul_rn(Ui[c], X[c]));
+                X[i] = __ddiv_rn(t, Ui[i]);
             }
         }
         __syncwarp();
@@ -385,61 +403,57 @@ __global__ void __launch_bounds__(128) k_bgs_warp(const int* __restrict__ ids, c
     }
 }
 
-// Blocks of more than 32 members: one CTA per block, factors in dynamic
-// shared memory when they fit (smem_lu), otherwise read from global memory.
-__global__ void __launch_bounds__(128) k_bgs_cta(const int* __restrict__ ids, const long long* __restrict__ off,
+// Blocks of more than 32 members: one CTA per block.  SMEM: factors and the
+// solution live in dynamic shared memory (blocks up to ~160 members), so the
+// backward substitution chain runs on shared-memory loads issued ahead of the
+// dependent subtractions; otherwise they are read from global memory.
+template <bool SMEM>
+__global__ void __launch_bounds__(128) k_bgs_cta(const int* __restrict__ ids, const int* __restrict__ lu_off,
                                                 const double* __restrict__ lu, const int* __restrict__ lperm,
-                                                const int* __restrict__ bptr, const int* __restrict__ rp,
-                                                const int* __restrict__ col, const double* __restrict__ v,
-                                                const double* __restrict__ b, const double* __restrict__ xin,
-                                                double* __restrict__ xout, double* __restrict__ scratch, int j0,
-                                                int zero, int smem_lu) {
+                                                const int* __restrict__ bptr, const double* __restrict__ res,
+                                                const double* __restrict__ xin, double* __restrict__ xout,
+                                                double* __restrict__ solbuf, int j0, int zero) {
     extern __shared__ double dyn[];
-    const int j = j0 + blockIdx.x;
-    const int g = ids[j];
+    const int g = ids[j0 + blockIdx.x];
     const int r0 = bptr[g], s = bptr[g + 1] - r0;
-    const double* F = lu + off[j];
-    double* X = smem_lu ? dyn + (size_t)s * s : scratch + r0;   // solution vector
+    const double* F = lu + lu_off[g];
+    double* X = SMEM ? dyn + (size_t)s * s : solbuf + r0;
     const double* U = F;
-    if (smem_lu) {
+    if (SMEM) {
         double* d = dyn;
         for (int e = threadIdx.x; e < s * s; e += blockDim.x) d[e] = F[e];
         U = d;
     }
-    double* R = scratch + r0;   // residuals (global scratch, row r0..)
-    for (int q = threadIdx.x; q < s; q += blockDim.x) R[q] = block_res_row(rp, col, v, b, xin, r0 + q, zero);
-    __syncthreads();
-    for (int q = threadIdx.x; q < s; q += blockDim.x) X[q] = R[lperm[r0 + q]];
+    for (int q = threadIdx.x; q < s; q += blockDim.x) X[q] = res[r0 + lperm[r0 + q]];
     __syncthreads();
     for (int c = 0; c + 1 < s; ++c) {   // column-oriented forward substitution
         const double xc = X[c];
-        for (int q = c + 1 + threadIdx.x; q < s; q += blockDim.x) X[q] = __dsub_rn(X[q], __dmul_rn(U[(size_t)q * s + c], xc));
+        for (int q = c + 1 + threadIdx.x; q < s; q += blockDim.x)
+            X[q] = __dsub_rn(X[q], __dmul_rn(U[(size_t)q * s + c], xc));
         __syncthreads();
     }
     if (threadIdx.x == 0) {
         for (int i = s - 1; i >= 0; --i) {
             double t = X[i];
-            for (int c = i + 1; c < s; ++c) t = __dsub_rn(t, __dmul_rn(U[(size_t)i * s + c], X[c]));
-            X[i] = __ddiv_rn(t, U[(size_t)i * s + i]);
+            const double* Ui = U + (size_t)i * s;
+#pragma unroll 8
+            for (int c = i + 1; c < s; ++c) t = __dsub_rn(t, __dmul_rn(Ui[c], X[c]));
+            X[i] = __ddiv_rn(t, Ui[i]);
         }
     }
     __syncthreads();
     for (int q = threadIdx.x; q < s; q += blockDim.x) xout[r0 + q] = __dadd_rn(zero ? 0.0 : xin[r0 + q], X[q]);
 }
 
-// r = f - A u on the finest level, restricted to level L (member order).
-__global__ void __launch_bounds__(256) k_csr_resid_restrict(const int* __restrict__ bptr, const int* __restrict__ rp,
-                                                           const int* __restrict__ col, const double* __restrict__ v,
-                                                           const double* __restrict__ f, const double* __restrict__ u,
-                                                           int nL, double* __restrict__ rc, double* sc_c) {
+// Restriction of finest residual rows to level L: member rows in order,
+// sum from 0.0 (hierarchy.hpp:272-276).  Block 0 clears the level-1 PCG
+// breakdown flag.
+__global__ void k_restrict_cells(const int* __restrict__ bptr, int nL, const double* __restrict__ r,
+                                 double* __restrict__ rc, double* sc_c) {
     if (blockIdx.x == 0 && threadIdx.x == 0) sc_c[2] = 0.0;
     GSTRIDE(g, nL) {
         double sum = 0.0;
-        for (int i = bptr[g]; i < bptr[g + 1]; ++i) {
-            double au = 0.0;
-            for (int p = rp[i]; p < rp[i + 1]; ++p) au = __dadd_rn(au, __dmul_rn(v[p], u[col[p]]));
-            sum = __dadd_rn(sum, __dsub_rn(f[i], au));
-        }
+        for (int i = bptr[g]; i < bptr[g + 1]; ++i) sum = __dadd_rn(sum, r[i]);
         rc[g] = sum;
     }
 }
@@ -562,9 +576,7 @@ void coarse_solve(Ctx& c, const double* f, double* u) {
     if (h->gpu.coarse_solve == 1) {
         k_coarse_lu<<<1, 32, 0, c.s>>>(h->nc, h->c_lu.p, h->c_perm.p, h->c_lex.p, f, u, h->c_work.p);
     } else {
-        const int warps = h->nc;
-        const unsigned blocks = (unsigned)std::min(1184, (warps * 32 + 255) / 256);
-        k_coarse_inv<<<blocks, 256, 0, c.s>>>(h->nc, h->c_inv.p, f, u);
+        k_coarse_inv<<<blocks_for(h->nc, 128), 128, 0, c.s>>>(h->nc, h->c_inv.p, f, u);
     }
     AUX_LAUNCHED(1);
 }
@@ -657,32 +669,39 @@ void finest_bgs_pass(Ctx& c, int color, const double* f, double* u, bool zero, d
     }
     prof_begin(c, 0);
     const int z = zero ? 1 : 0;
-    k_bgs<1, 4><<<blocks_for(g1 - g0, 128), 128, 0, c.s>>>(F.bptr.p, F.rp.p, F.col.p, F.v.p, f, xin, u, g0, g1, z);
-    AUX_LAUNCHED(1);
-    if (F.max_block >= 5) {
-        k_bgs<5, kSmallBlock><<<blocks_for(g1 - g0, 128), 128, 0, c.s>>>(F.bptr.p, F.rp.p, F.col.p, F.v.p, f, xin,
-                                                                          u, g0, g1, z);
+    const int r0 = F.color_row[color], r1 = F.color_row[color + 1];
+    // residual rows of this colour (from u = 0 the residual is b itself)
+    const double* res = f;
+    if (!zero && r1 > r0) {
+        k_rows<<<blocks_for(r1 - r0), 256, 0, c.s>>>(F.rp.p, F.col.p, F.v.p, f, xin, F.scratch.p, r0, r1, 0);
         AUX_LAUNCHED(1);
+        res = F.scratch.p;
     }
+    k_bgs_solve<<<blocks_for(g1 - g0, 128), 128, 0, c.s>>>(F.bptr.p, F.rp.p, F.col.p, F.v.p, f, res, F.cell_lu_off.p,
+                                                         F.big_lu.p, F.big_perm.p, xin, u, g0, g1, z);
+    AUX_LAUNCHED(1);
     const int j0 = F.big_color_begin[color], jc = F.big_cta_begin[color], j1 = F.big_color_begin[color + 1];
     if (jc > j0) {   // 9..32 members: warp per block
         const int warps = jc - j0;
         k_bgs_warp<<<(unsigned)std::min(4736, (warps + 3) / 4), 128, 0, c.s>>>(
-            F.big_ids.p, F.big_off.p, F.big_lu.p, F.big_perm.p, F.bptr.p, F.rp.p, F.col.p, F.v.p, f, xin, u, j0, jc,
-            z);
+            F.big_ids.p, F.cell_lu_off.p, F.big_lu.p, F.big_perm.p, F.bptr.p, res, xin, u, j0, jc, z);
         AUX_LAUNCHED(1);
     }
     if (j1 > jc) {   // more than 32 members: CTA per block
         const size_t need = ((size_t)F.max_block * F.max_block + F.max_block) * sizeof(double);
-        const int smem_lu = need <= (size_t)200 * 1024 ? 1 : 0;
         static bool attr = false;
         if (!attr) {
-            AUX_CUDA(cudaFuncSetAttribute(k_bgs_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+            AUX_CUDA(cudaFuncSetAttribute(k_bgs_cta<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
             attr = true;
         }
-        k_bgs_cta<<<(unsigned)(j1 - jc), 128, smem_lu ? need : 0, c.s>>>(F.big_ids.p, F.big_off.p, F.big_lu.p,
-                                                                         F.big_perm.p, F.bptr.p, F.rp.p, F.col.p,
-                                                                         F.v.p, f, xin, u, F.scratch.p, jc, z, smem_lu);
+        if (need <= (size_t)200 * 1024)
+            k_bgs_cta<true><<<(unsigned)(j1 - jc), 128, need, c.s>>>(F.big_ids.p, F.cell_lu_off.p, F.big_lu.p,
+                                                                     F.big_perm.p, F.bptr.p, res, xin, u,
+                                                                     F.scratch.p + F.n, jc, z);
+        else
+            k_bgs_cta<false><<<(unsigned)(j1 - jc), 128, 0, c.s>>>(F.big_ids.p, F.cell_lu_off.p, F.big_lu.p,
+                                                                   F.big_perm.p, F.bptr.p, res, xin, u,
+                                                                   F.scratch.p + F.n, jc, z);
         AUX_LAUNCHED(1);
     }
     prof_end(c, 0, g_color_bytes[color]);
@@ -699,9 +718,9 @@ void finest_cycle(Ctx& c, const double* f, double* u, double* snap) {
     for (int sw = 0; sw < c.o.pre_sweeps; ++sw)
         for (int col = 0; col < 4; ++col) finest_bgs_pass(c, col, f, u, sw == 0 && col == 0, snap);
     prof_begin(c, 2);
-    k_csr_resid_restrict<<<blocks_for(C.n), 256, 0, c.s>>>(F.bptr.p, F.rp.p, F.col.p, F.v.p, f, u, C.n, C.pcg.r.p,
-                                                          C.pcg.sc.p);
-    AUX_LAUNCHED(1);
+    k_rows<<<blocks_for(F.n), 256, 0, c.s>>>(F.rp.p, F.col.p, F.v.p, f, u, F.scratch.p, 0, F.n, 1);
+    k_restrict_cells<<<blocks_for(C.n), 256, 0, c.s>>>(F.bptr.p, C.n, F.scratch.p, C.pcg.r.p, C.pcg.sc.p);
+    AUX_LAUNCHED(2);
     prof_end(c, 2, 12.0 * F.nnz + 4.0 * (F.n + 1) + 16.0 * F.n + 4.0 * (C.n + 1) + 8.0 * C.n);
     g_trace.mark(c.s, 1);
     if (h->graph_valid) {
