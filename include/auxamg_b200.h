@@ -87,7 +87,11 @@ typedef struct aux_gpu_opts {
                                  inside the single-CTA coarse kernel; 0 = off,
                                  -1 = default */
     int32_t use_graphs;       /* capture the coarse K-cycle in a CUDA graph (1) */
-    int32_t reserved[4];
+    int32_t block_solve;      /* finest block smoother (block_gs_sweep, smoother.hpp:162-205):
+                                 0 = residual + explicit block inverse in one pass (default),
+                                 1 = stored LU factors, substitution in the reference order
+                                     (bitwise with the reference per element) */
+    int32_t reserved[3];
 } aux_gpu_opts;
 
 /* auxamg::LocalityReport, hierarchy.hpp:37-44. */

@@ -100,11 +100,13 @@ class GpuOptions:
     coarse_solve: int = 0        # 0 explicit inverse, 1 LU in reference order
     fused_max_cells: int = -1
     use_graphs: bool = True
+    block_solve: int = 0         # 0 explicit block inverses, 1 stored LU in reference order
 
     def c(self):
         o = _abi.GpuOpts()
         o.device, o.coarse_solve, o.fused_max_cells, o.use_graphs = (self.device, self.coarse_solve,
                                                                      self.fused_max_cells, int(self.use_graphs))
+        o.block_solve = self.block_solve
         return o
 
 

@@ -37,6 +37,8 @@ aux_status guarded(char* msg, size_t len, F&& f) {
 }
 
 aux_hierarchy* make_h(const aux_setup_opts* o, const aux_gpu_opts* g) {
+    if (g && (g->block_solve < 0 || g->block_solve > 1 || g->coarse_solve < 0 || g->coarse_solve > 1))
+        throw_aux(AUX_ARGUMENT_ERROR, "aux_gpu_opts: block_solve and coarse_solve must be 0 or 1");
     auto* h = new aux_hierarchy();
     aux_default_setup_opts(&h->opts);
     aux_default_gpu_opts(&h->gpu);

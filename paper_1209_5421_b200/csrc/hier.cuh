@@ -95,12 +95,19 @@ struct Finest {
     int big_cta_begin[4] = {0, 0, 0, 0};        // within a colour: first block with > 32 members
     DBuf<int> big_ids;        // cell ids (colour-major), sorted by colour
     DBuf<double> scratch;     // 2N: colour-pass residuals + big-block solutions
+    // block_solve = 0: explicit inverse of every block (s >= 1), column-major
+    // s*s at inv_off[g]; per row {inv_off of its cell, q | s << 16}
+    DBuf<double> inv;
+    DBuf<int> inv_off;        // n_L + 1
+    DBuf<int2> rmeta;         // N
+    int big_huge_begin[4] = {0, 0, 0, 0};       // within a colour: first block with > kWarpInvMax members
     int color_row[5] = {0, 0, 0, 0, 0};   // first finest row of each colour class (+ N)
     bool color_clean = true;  // check_color_locality (smoother.hpp:217-231) empty
     int max_block = 0;
 };
 
 constexpr int kTileBlock = 8;   // blocks up to this size: one thread per block
+constexpr int kWarpInvMax = 320;   // inverse mode: blocks up to this size are one CTA task of k_bgs_inv
 
 struct Profile {
     bool on = false;

@@ -332,6 +332,71 @@ __global__ void k_factor_big(const int* __restrict__ ids, const int* __restrict_
     if (zc >= 0 && threadIdx.x == 0) atomicMin(err, (unsigned long long)lex_of_cm(g, gid));
 }
 
+// ---- explicit block inverses (block_solve = 0).  The block smoother's
+// correction delta = A_gg^{-1} r_g (smoother.hpp:193-202) becomes one dense
+// mat-vec, so a colour pass is a single bandwidth-bound sweep instead of a
+// chain of s^2/2 dependent substitutions per block.  The inverse is formed
+// from the reference-order LU factors (columns = LU solves of unit vectors)
+// and stored column-major, so the lanes owning the rows of one block read
+// consecutive addresses.  Singletons store 1 / a_ii.
+__global__ void k_inv_sizes(const int* __restrict__ bptr, int nL, int* __restrict__ cnt) {
+    GSTRIDE(g, nL) {
+        const int s = bptr[g + 1] - bptr[g];
+        cnt[g] = s * s;
+    }
+}
+
+__global__ void k_rmeta(const int* __restrict__ bptr, const int* __restrict__ inv_off, int nL,
+                        int2* __restrict__ meta) {
+    GSTRIDE(g, nL) {
+        const int r0 = bptr[g], s = bptr[g + 1] - r0, off = inv_off[g];
+        for (int q = 0; q < s; ++q) meta[r0 + q] = make_int2(off, q | (s << 16));
+    }
+}
+
+// column j of LU^{-1}: forward/backward substitution of e_{j} (dense.hpp:52-67 order)
+__device__ inline void lu_solve_unit(const double* lu, const int* perm, int n, int j, double* x) {
+    for (int i = 0; i < n; ++i) x[i] = perm[i] == j ? 1.0 : 0.0;
+    for (int i = 1; i < n; ++i) {
+        double s = x[i];
+        for (int c = 0; c < i; ++c) s = __dsub_rn(s, __dmul_rn(lu[(size_t)i * n + c], x[c]));
+        x[i] = s;
+    }
+    for (int i = n - 1; i >= 0; --i) {
+        double s = x[i];
+        for (int c = i + 1; c < n; ++c) s = __dsub_rn(s, __dmul_rn(lu[(size_t)i * n + c], x[c]));
+        x[i] = s / lu[(size_t)i * n + i];
+    }
+}
+
+__global__ void k_inv_cells(const int* __restrict__ bptr, const int* __restrict__ rp, const int* __restrict__ col,
+                            const double* __restrict__ v, int nL, const int* __restrict__ lu_off,
+                            const double* __restrict__ lu, const int* __restrict__ perm,
+                            const int* __restrict__ inv_off, double* __restrict__ inv) {
+    GSTRIDE(g, nL) {
+        const int r0 = bptr[g], s = bptr[g + 1] - r0;
+        double* out = inv + inv_off[g];
+        if (s == 1) {
+            double d = 0.0;
+            for (int p = rp[r0]; p < rp[r0 + 1]; ++p)
+                if (col[p] == r0) d = v[p];
+            out[0] = 1.0 / d;
+        } else if (s >= 2 && s <= 16) {
+            for (int j = 0; j < s; ++j) lu_solve_unit(lu + lu_off[g], perm + r0, s, j, out + j * s);
+        }
+    }
+}
+
+// Blocks of more than 16 members: one CTA per block, one column per thread.
+__global__ void k_inv_big(const int* __restrict__ ids, const int* __restrict__ bptr, const int* __restrict__ lu_off,
+                          const double* __restrict__ lu, const int* __restrict__ perm,
+                          const int* __restrict__ inv_off, double* __restrict__ inv) {
+    const int g = ids[blockIdx.x];
+    const int r0 = bptr[g], s = bptr[g + 1] - r0;
+    for (int j = threadIdx.x; j < s; j += blockDim.x)
+        lu_solve_unit(lu + lu_off[g], perm + r0, s, j, inv + inv_off[g] + (size_t)j * s);
+}
+
 // check_color_locality (smoother.hpp:217-231): any nonzero coupling between
 // two distinct blocks of the same colour => keep per-colour snapshots.
 __global__ void k_color_check(const int* __restrict__ rp, const int* __restrict__ col, const double* __restrict__ v,
@@ -718,6 +783,20 @@ void setup_device(aux_hierarchy* h, const aux_csr_view* A, const double* xy, lon
             AUX_LAUNCHED(1);
             F.scratch.alloc(2 * (size_t)n);   // colour-pass residuals + big-block solutions
         }
+        if (h->gpu.block_solve == 0) {   // explicit inverses of all blocks (s <= 16 here, larger below)
+            DBuf<int> cnt(nL);
+            F.inv_off.alloc(nL + 1);
+            k_inv_sizes<<<grid_for(nL), kT, 0, s>>>(F.bptr.p, nL, cnt.p);
+            AUX_LAUNCHED(1);
+            exclusive_scan(cnt.p, F.inv_off.p, nL, s);
+            const int pool = read1(F.inv_off.p + nL, s);
+            F.inv.alloc(std::max(pool, 1));
+            F.rmeta.alloc(n);
+            k_rmeta<<<grid_for(nL), kT, 0, s>>>(F.bptr.p, F.inv_off.p, nL, F.rmeta.p);
+            k_inv_cells<<<grid_for(nL), kT, 0, s>>>(F.bptr.p, F.rp.p, F.col.p, F.v.p, nL, F.cell_lu_off.p,
+                                                    F.big_lu.p, F.big_perm.p, F.inv_off.p, F.inv.p);
+            AUX_LAUNCHED(2);
+        }
         DBuf<int> pos(nL + 1);
         exclusive_scan(flag.p, pos.p, nL, s);
         int nbig = 0;
@@ -734,7 +813,8 @@ void setup_device(aux_hierarchy* h, const aux_csr_view* A, const double* xy, lon
             std::vector<int> bptr_h(nL + 1);
             AUX_CUDA(cudaMemcpyAsync(bptr_h.data(), F.bptr.p, sizeof(int) * (nL + 1), cudaMemcpyDeviceToHost, s));
             AUX_CUDA(cudaStreamSynchronize(s));
-            // order: per colour, the warp class (<= 32 members) then the CTA class
+            // order: per colour, the warp class (<= 32 members) then the CTA
+            // class, the latter split at kWarpInvMax for the inverse mode
             auto bsize = [&](int g) { return bptr_h[g + 1] - bptr_h[g]; };
             std::vector<int> ord, huge;
             ord.reserve(nbig);
@@ -744,7 +824,10 @@ void setup_device(aux_hierarchy* h, const aux_csr_view* A, const double* xy, lon
                     if ((g >> gL.lq) == c && bsize(g) <= 32) ord.push_back(g);
                 F.big_cta_begin[c] = (int)ord.size();
                 for (int g : ids)
-                    if ((g >> gL.lq) == c && bsize(g) > 32) ord.push_back(g);
+                    if ((g >> gL.lq) == c && bsize(g) > 32 && bsize(g) <= kWarpInvMax) ord.push_back(g);
+                F.big_huge_begin[c] = (int)ord.size();
+                for (int g : ids)
+                    if ((g >> gL.lq) == c && bsize(g) > kWarpInvMax) ord.push_back(g);
             }
             F.big_color_begin[4] = (int)ord.size();
             ids.swap(ord);
@@ -757,6 +840,11 @@ void setup_device(aux_hierarchy* h, const aux_csr_view* A, const double* xy, lon
                 k_factor_big<<<(unsigned)huge.size(), 128, 0, s>>>(hid.p, F.cell_lu_off.p, F.bptr.p, F.rp.p, F.col.p,
                                                                     F.v.p, gL, F.big_lu.p, F.big_perm.p, err.p);
                 AUX_LAUNCHED(1);
+                if (h->gpu.block_solve == 0) {
+                    k_inv_big<<<(unsigned)huge.size(), 128, 0, s>>>(hid.p, F.bptr.p, F.cell_lu_off.p, F.big_lu.p,
+                                                                   F.big_perm.p, F.inv_off.p, F.inv.p);
+                    AUX_LAUNCHED(1);
+                }
                 AUX_CUDA(cudaStreamSynchronize(s));
             }
         }

