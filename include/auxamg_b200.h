@@ -91,7 +91,10 @@ typedef struct aux_gpu_opts {
                                  0 = residual + explicit block inverse in one pass (default),
                                  1 = stored LU factors, substitution in the reference order
                                      (bitwise with the reference per element) */
-    int32_t reserved[3];
+    int32_t tile_kernels;     /* structured levels above the single-CTA tier:
+                                 1 = two overlapped-tile kernels per K-cycle visit (default),
+                                 0 = one kernel per colour pass / phase */
+    int32_t reserved[2];
 } aux_gpu_opts;
 
 /* auxamg::LocalityReport, hierarchy.hpp:37-44. */

@@ -101,12 +101,14 @@ class GpuOptions:
     fused_max_cells: int = -1
     use_graphs: bool = True
     block_solve: int = 0         # 0 explicit block inverses, 1 stored LU in reference order
+    tile_kernels: bool = True    # overlapped-tile kernels for the structured levels
 
     def c(self):
         o = _abi.GpuOpts()
         o.device, o.coarse_solve, o.fused_max_cells, o.use_graphs = (self.device, self.coarse_solve,
                                                                      self.fused_max_cells, int(self.use_graphs))
         o.block_solve = self.block_solve
+        o.tile_kernels = int(self.tile_kernels)
         return o
 
 

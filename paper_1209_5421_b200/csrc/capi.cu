@@ -93,6 +93,8 @@ void aux_default_gpu_opts(aux_gpu_opts* o) {
     o->coarse_solve = 0;
     o->fused_max_cells = -1;
     o->use_graphs = 1;
+    o->block_solve = 0;
+    o->tile_kernels = 1;
 }
 
 const char* aux_version(void) { return "auxamg_b200 0.1 (sm_100a)"; }

@@ -195,4 +195,36 @@ __device__ bool grid_reduce(double (&v)[NV], const RedState& rs, double (&out)[N
     return true;
 }
 
+
+// Finaliser applied by the last block of a reduction kernel (device-resident
+// PCG scalars, so a whole coarse K-cycle needs no host round trip).
+constexpr double kBreakdown = 1e-300;   // breakdown_energy, cycle.hpp:78
+struct Fin {
+    int op;                    // 0 none, 1 alpha (e=s0, alpha=s1/e), 2 beta (-s0/e_in), 3 store s0
+    double* sc;                // [0]=alpha [1]=beta [2]=dead
+    const double* e_in;
+    double* e_out;             // op 1: energy slot; op 3: destination
+    double* a_slot = nullptr;  // op 1: also keep alpha of this step here ...
+    double* nval = nullptr;    // ... and count it as valid (step + 1) unless the PCG broke down
+    int step = 0;
+};
+
+__device__ __forceinline__ void finalize(const Fin& f, const double* s) {
+    if (f.op == 1) {
+        const double e = s[0];
+        const bool was_dead = f.sc[2] != 0.0;
+        *f.e_out = e;
+        if (!(e > kBreakdown)) f.sc[2] = 1.0;
+        f.sc[0] = s[1] / e;
+        if (f.a_slot && !was_dead && e > kBreakdown) {
+            *f.a_slot = s[1] / e;
+            *f.nval = (double)(f.step + 1);
+        }
+    } else if (f.op == 2) {
+        f.sc[1] = -s[0] / *f.e_in;
+    } else if (f.op == 3) {
+        *f.e_out = s[0];
+    }
+}
+
 }  // namespace auxb200

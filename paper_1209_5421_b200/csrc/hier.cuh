@@ -55,7 +55,11 @@ struct PcgBufs {
     DBuf<double> u;                 // PCG iterate (= ec of the finer level)
     std::vector<DBuf<double>> p;    // directions (z of step i is written into p[i])
     std::vector<DBuf<double>> ap;   // cached A p
-    // scalars: [0]=alpha [1]=beta [2]=dead flag [3..3+n_inner) energies
+    // tile path (tiles.cu): second residual buffer (the update r -= alpha A p
+    // is applied while tiles read their rings) and the pre-smoothed iterate
+    DBuf<double> r2, upre;
+    // scalars: [0]=alpha [1]=beta [2]=dead flag [3..3+n_inner) energies,
+    // [3+n_inner..3+2n_inner) alpha per step, [3+2n_inner] valid steps (tiles.cuh)
     DBuf<double> sc;
 };
 
@@ -157,6 +161,7 @@ struct aux_hierarchy {
     aux_cycle_opts graph_opts{};
     bool graph_valid = false;
     int fused_m0 = 1 << 30;          // first level run by the single-CTA kernel
+    bool tiles = false;              // levels [1, fused_m0) run the overlapped-tile kernels
     auxb200::DBuf<auxb200::FLevel> d_flv;
     auxb200::FusedArgs fused_args{};
     auxb200::Profile prof;

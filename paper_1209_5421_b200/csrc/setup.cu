@@ -25,6 +25,7 @@
 #include "lu.cuh"
 #include "scan_sort.cuh"
 #include "setup.cuh"
+#include "tiles.cuh"
 
 namespace auxb200 {
 
@@ -562,8 +563,10 @@ void alloc_pcg(aux_hierarchy* h, auxb200::Level& L, int n_inner) {
         P.p.emplace_back(L.n);
         P.ap.emplace_back(L.n);
     }
-    P.sc.alloc(3 + n_inner);
-    AUX_CUDA(cudaMemsetAsync(P.sc.p, 0, sizeof(double) * (3 + n_inner), h->stream));
+    P.r2.alloc(L.n);
+    P.upre.alloc(L.n);
+    P.sc.alloc(sc_size(n_inner));
+    AUX_CUDA(cudaMemsetAsync(P.sc.p, 0, sizeof(double) * sc_size(n_inner), h->stream));
 }
 
 // Coarsest-level dense factorization + explicit inverse from a dense

@@ -20,35 +20,14 @@
 #include "lu.cuh"
 #include "fused.cuh"
 #include "setup.cuh"
+#include "tiles.cuh"
 
 namespace auxb200 {
 
 namespace {
 
-constexpr double kBreakdown = 1e-300;   // cycle.hpp:78
 
 double g_color_bytes[4];   // algorithmic bytes of one finest colour pass
-
-// Finaliser applied by the last block of a reduction kernel.
-struct Fin {
-    int op;            // 0 none, 1 alpha (e=s0, alpha=s1/e), 2 beta (-s0/e_in), 3 store s0
-    double* sc;        // [0]=alpha [1]=beta [2]=dead
-    const double* e_in;
-    double* e_out;     // op 1: energy slot; op 3: destination
-};
-
-__device__ __forceinline__ void finalize(const Fin& f, const double* s) {
-    if (f.op == 1) {
-        const double e = s[0];
-        *f.e_out = e;
-        if (!(e > kBreakdown)) f.sc[2] = 1.0;
-        f.sc[0] = s[1] / e;
-    } else if (f.op == 2) {
-        f.sc[1] = -s[0] / *f.e_in;
-    } else if (f.op == 3) {
-        *f.e_out = s[0];
-    }
-}
 
 #define GSTRIDE(i, n) for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < (n); i += (long)gridDim.x * blockDim.x)
 
@@ -630,8 +609,11 @@ __global__ void __launch_bounds__(256) k_bgs_inv_cta(const int* __restrict__ rp,
 // sum from 0.0 (hierarchy.hpp:272-276).  Block 0 clears the level-1 PCG
 // breakdown flag.
 __global__ void k_restrict_cells(const int* __restrict__ bptr, int nL, const double* __restrict__ r,
-                                 double* __restrict__ rc, double* sc_c) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) sc_c[2] = 0.0;
+                                 double* __restrict__ rc, double* sc_c, int nval_idx) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        sc_c[2] = 0.0;
+        sc_c[nval_idx] = 0.0;
+    }
     GSTRIDE(g, nL) {
         double sum = 0.0;
         for (int i = bptr[g]; i < bptr[g + 1]; ++i) sum = __dadd_rn(sum, r[i]);
@@ -642,6 +624,20 @@ __global__ void k_restrict_cells(const int* __restrict__ bptr, int nL, const dou
 __global__ void k_csr_prolong(const int* __restrict__ cell, long n, double* __restrict__ u,
                               const double* __restrict__ ec) {
     GSTRIDE(i, n) u[i] = __dadd_rn(u[i], ec[cell[i]]);
+}
+
+// Explicit PCG iterate u = ((0 + alpha_0 p_0) + alpha_1 p_1) ... over the valid
+// steps (cycle.hpp:124); the tile path keeps only directions and alphas.
+struct PList {
+    const double* p[8];
+};
+__global__ void k_pcg_u(long n, PList pl, const double* __restrict__ sc, int ni, double* __restrict__ u) {
+    const int nval = (int)sc[3 + 2 * ni];
+    GSTRIDE(i, n) {
+        double e = 0.0;
+        for (int k = 0; k < nval; ++k) e = __dadd_rn(e, __dmul_rn(sc[3 + ni + k], pl.p[k][i]));
+        u[i] = e;
+    }
 }
 
 // csr_spmv (sparse.hpp:141-150) with the same fused inner products as k_spmv9.
@@ -751,6 +747,7 @@ struct Trace {
 Trace g_trace;
 
 void pcg_level(Ctx& c, int m);
+void coarse_root(Ctx& c);
 
 void coarse_solve(Ctx& c, const double* f, double* u) {
     aux_hierarchy* h = c.h;
@@ -829,6 +826,77 @@ void pcg_level(Ctx& c, int m) {
         k_update<<<red_blocks(n), kRedThreads, 0, c.s>>>(n, P.u.p, P.p[i].p, P.r.p, P.ap[i].p, i == 0 ? 1 : 0,
                                                         upd_r, 0, sc, c.rs, Fin{0, sc, nullptr, nullptr});
         AUX_LAUNCHED(1);
+    }
+}
+
+// nonlinear_pcg on level m >= 1 through the overlapped-tile kernels
+// (tiles.cu): per step one k_tile_down (pending residual update, pre-smoothing,
+// restriction), the child's PCG, one k_tile_up (prolongation, post-smoothing,
+// A z and the step's inner products), then the A-orthogonalisation.  The
+// iterate is never formed: the parent's k_tile_up sums alpha_k p_k on the fly.
+void pcg_tiles(Ctx& c, int m) {
+    aux_hierarchy* h = c.h;
+    if (m == h->fused_m0) {
+        launch_fused_pcg(h->fused_args, c.s);
+        return;
+    }
+    Level& L = h->lv[m];
+    Level& C = h->lv[m + 1];
+    PcgBufs& P = L.pcg;
+    const int ni = c.o.n_inner;
+    const long n = L.n;
+    double* sc = P.sc.p;
+    double* R[2] = {P.r.p, P.r2.p};
+    const int w = 1 << L.geo.k;
+    const int tx = w / tile_edge(w);
+    const bool child_fused = (m + 1 == h->fused_m0);
+    for (int i = 0; i < ni; ++i) {
+        TileDown d{};
+        d.g = L.geo;
+        d.gc = C.geo;
+        d.tiles_x = tx;
+        d.val = L.val.p;
+        d.r_in = i == 0 ? R[0] : R[(i - 1) & 1];
+        d.ap_prev = i == 0 ? nullptr : P.ap[i - 1].p;
+        d.sc = sc;
+        d.r_out = i == 0 ? nullptr : R[i & 1];
+        d.u_pre = P.upre.p;
+        d.rc = C.pcg.r.p;
+        d.sc_child = child_fused ? nullptr : C.pcg.sc.p;
+        d.child_nval = sc_nval(ni);
+        launch_tile_down(d, c.o.pre_sweeps, c.s);
+        pcg_tiles(c, m + 1);
+        TileUp u{};
+        u.g = L.geo;
+        u.gc = C.geo;
+        u.tiles_x = tx;
+        u.val = L.val.p;
+        u.act = L.active.p;
+        u.f = R[i & 1];
+        u.u_pre = P.upre.p;
+        u.ec = child_fused ? C.pcg.u.p : nullptr;
+        for (int k = 0; k < ni; ++k) u.cp[k] = C.pcg.p[k].p;
+        u.sc_c = C.pcg.sc.p;
+        u.c_ni = ni;
+        u.z = P.p[i].p;
+        u.az = P.ap[i].p;
+        u.ap0 = P.ap[0].p;
+        u.mode = i == 0 ? 0 : 1;
+        const Fin fin = i == 0 ? Fin{1, sc, nullptr, sc + 3, sc + sc_alpha(ni, 0), sc + sc_nval(ni), 0}
+                               : Fin{2, sc, sc + 3, nullptr};
+        launch_tile_up(u, c.o.post_sweeps, c.rs, fin, c.s);
+        if (i > 0) {
+            for (int j = 1; j < i; ++j) {
+                k_mgs<<<red_blocks(n), kRedThreads, 0, c.s>>>(n, P.p[i].p, P.ap[i].p, P.p[j - 1].p, P.ap[j - 1].p,
+                                                             P.ap[j].p, nullptr, 0, sc, c.rs,
+                                                             Fin{2, sc, sc + 3 + j, nullptr});
+                AUX_LAUNCHED(1);
+            }
+            k_mgs<<<red_blocks(n), kRedThreads, 0, c.s>>>(
+                n, P.p[i].p, P.ap[i].p, P.p[i - 1].p, P.ap[i - 1].p, nullptr, R[i & 1], 1, sc, c.rs,
+                Fin{1, sc, nullptr, sc + 3 + i, sc + sc_alpha(ni, i), sc + sc_nval(ni), i});
+            AUX_LAUNCHED(1);
+        }
     }
 }
 
@@ -927,7 +995,8 @@ void finest_cycle(Ctx& c, const double* f, double* u, double* snap) {
         for (int col = 0; col < 4; ++col) finest_bgs_pass(c, col, f, u, sw == 0 && col == 0, snap);
     prof_begin(c, 2);
     k_rows<<<blocks_for(F.n), 256, 0, c.s>>>(F.rp.p, F.col.p, F.v.p, f, u, F.scratch.p, 0, F.n, 1);
-    k_restrict_cells<<<blocks_for(C.n), 256, 0, c.s>>>(F.bptr.p, C.n, F.scratch.p, C.pcg.r.p, C.pcg.sc.p);
+    k_restrict_cells<<<blocks_for(C.n), 256, 0, c.s>>>(F.bptr.p, C.n, F.scratch.p, C.pcg.r.p, C.pcg.sc.p,
+                                                       sc_nval(c.o.n_inner));
     AUX_LAUNCHED(2);
     prof_end(c, 2, 12.0 * F.nnz + 4.0 * (F.n + 1) + 16.0 * F.n + 4.0 * (C.n + 1) + 8.0 * C.n);
     g_trace.mark(c.s, 1);
@@ -935,13 +1004,31 @@ void finest_cycle(Ctx& c, const double* f, double* u, double* snap) {
         AUX_CUDA(cudaGraphLaunch(h->graph, c.s));
         AUX_LAUNCHED(h->graph_kernels);
     } else {
-        pcg_level(c, 1);
+        coarse_root(c);
     }
     g_trace.mark(c.s, 2);
     k_csr_prolong<<<blocks_for(F.n), 256, 0, c.s>>>(F.cell.p, F.n, u, C.pcg.u.p);
     AUX_LAUNCHED(1);
     for (int sw = 0; sw < c.o.post_sweeps; ++sw)
         for (int col = 3; col >= 0; --col) finest_bgs_pass(c, col, f, u, false, snap);
+}
+
+// The coarse part of one finest visit: nonlinear_pcg on level 1; its iterate
+// lands in lv[1].pcg.u for the finest prolongation.
+void coarse_root(Ctx& c) {
+    aux_hierarchy* h = c.h;
+    if (!h->tiles) {
+        pcg_level(c, 1);
+        return;
+    }
+    pcg_tiles(c, 1);
+    if (h->fused_m0 != 1) {
+        Level& L = h->lv[1];
+        PList pl{};
+        for (int k = 0; k < c.o.n_inner; ++k) pl.p[k] = L.pcg.p[k].p;
+        k_pcg_u<<<blocks_for(L.n), 256, 0, c.s>>>(L.n, pl, L.pcg.sc.p, c.o.n_inner, L.pcg.u.p);
+        AUX_LAUNCHED(1);
+    }
 }
 
 void build_graph(aux_hierarchy* h, const aux_cycle_opts& o, RedState rs) {
@@ -956,7 +1043,7 @@ void build_graph(aux_hierarchy* h, const aux_cycle_opts& o, RedState rs) {
     const int64_t before = g_launches;
     cudaGraph_t g;
     AUX_CUDA(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
-    pcg_level(c, 1);
+    coarse_root(c);
     AUX_CUDA(cudaStreamEndCapture(h->stream, &g));
     h->graph_kernels = g_launches - before;
     g_launches = before;
@@ -980,6 +1067,21 @@ void setup_fused(aux_hierarchy* h, const aux_cycle_opts& o) {
     }
     if (m0 != h->fused_m0) h->graph_valid = false;
     h->fused_m0 = m0;
+    // overlapped-tile kernels for the levels above the single-CTA tier
+    bool tiles = h->gpu.tile_kernels != 0 && m0 < (int)h->lv.size() && o.n_inner <= kFusedMaxInner;
+    long max_tiles = 0;
+    for (int l = 1; tiles && l < m0; ++l) {
+        const int w = 1 << h->lv[l].geo.k;
+        if (!tiles_supported(w, o.pre_sweeps, o.post_sweeps)) tiles = false;
+        else max_tiles = std::max<long>(max_tiles, tile_count(w));
+    }
+    if (tiles != h->tiles) h->graph_valid = false;
+    h->tiles = tiles;
+    if (tiles && (size_t)(2 * max_tiles) > h->red_partials.n) {   // grid_reduce partials, 2 per tile
+        AUX_CUDA(cudaStreamSynchronize(h->stream));
+        h->red_partials.alloc((size_t)2 * max_tiles);
+        h->graph_valid = false;
+    }
     if (m0 < (int)h->lv.size()) {
         fa.m0 = m0;
         fa.last = (int)h->lv.size() - 1;
@@ -1031,7 +1133,6 @@ void solve_device(aux_hierarchy* h, const double* b, long n_b, const aux_cycle_o
     cudaStream_t s = h->stream;
     Finest& F = h->fine;
     const long n = h->n;
-    RedState rs{h->red_partials.p, h->red_ticket.p};
 
     // workspace
     const int slots = o->max_directions > 0 ? std::min(o->max_directions + 1, o->max_outer) : o->max_outer;
@@ -1047,6 +1148,7 @@ void solve_device(aux_hierarchy* h, const double* b, long n_b, const aux_cycle_o
         h->graph_valid = false;
     }
     setup_fused(h, *o);
+    RedState rs{h->red_partials.p, h->red_ticket.p};   // after setup_fused: it may grow the partials
     double* sc = h->w_sc.p;
     AUX_CUDA(cudaMemsetAsync(sc, 0, sizeof(double) * h->w_sc.n, s));
 

@@ -1,0 +1,61 @@
+// tiles.cuh — overlapped-tile kernels for the structured levels between the
+// finest level and the single-CTA tier (tiles.cu).
+#pragma once
+
+#include "common.cuh"
+
+namespace auxb200 {
+
+// Scalar block of a level's nonlinear PCG (cycle.hpp:106-128) on the device:
+//   [0] alpha of the last step  [1] beta  [2] breakdown flag
+//   [3 + i] energy e_i          [3 + ni + i] alpha_i      [3 + 2 ni] valid steps
+inline int sc_alpha(int ni, int i) { return 3 + ni + i; }
+inline int sc_nval(int ni) { return 3 + 2 * ni; }
+inline int sc_size(int ni) { return 4 + 2 * ni; }
+
+// Down half of a K-cycle visit of one level (cycle.hpp:169-178):
+// the pending PCG residual update r -= alpha A p (cycle.hpp:125), pre-smoothing
+// from zero, residual and restriction into the child's PCG right-hand side.
+struct TileDown {
+    Geo g, gc;
+    int tiles_x;
+    const double* val;
+    const double* r_in;      // PCG residual before this step's update
+    const double* ap_prev;   // A p of the previous step (nullptr: no update)
+    const double* sc;        // this level's scalars (alpha, breakdown)
+    double* r_out;           // updated residual (interior), nullptr when no update
+    double* u_pre;           // pre-smoothed iterate (interior)
+    double* rc;              // child's PCG right-hand side
+    double* sc_child;        // child's scalars to reset (nullptr: none)
+    int child_nval;          // index of the child's valid-step counter
+};
+
+// Up half (cycle.hpp:180-196) plus the PCG step's operator application:
+// prolongation of the child's correction, transposed post-smoothing,
+// A z and the fused inner products of the step (cycle.hpp:84-97, 119-123).
+struct TileUp {
+    Geo g, gc;
+    int tiles_x;
+    const double* val;
+    const uint8_t* act;
+    const double* f;         // right-hand side of this visit (the PCG residual)
+    const double* u_pre;
+    // child correction: explicit (ec) or sum_k alpha_k p_k of the child's PCG
+    const double* ec;
+    const double* cp[8];
+    const double* sc_c;      // child's scalars (alphas, valid steps)
+    int c_ni;
+    double* z;               // visit result = PCG direction p_i (interior)
+    double* az;              // A z (interior)
+    const double* ap0;       // mode 1: s0 = z . ap0
+    int mode;                // 0: s0 = z.Az, s1 = r.z   1: s0 = z.ap0
+};
+
+// Launch the tile kernels; T = tile edge, pre/post = sweeps (1 or 2).
+bool tiles_supported(int w, int pre, int post);
+int tile_edge(int w);
+int tile_count(int w);
+void launch_tile_down(const TileDown& a, int pre, cudaStream_t s);
+void launch_tile_up(const TileUp& a, int post, RedState rs, Fin fin, cudaStream_t s);
+
+}  // namespace auxb200

@@ -263,3 +263,31 @@ def test_block_solve_modes_agree_graded(gpu_api):
          for m in (0, 1)]
     assert r[0].iterations == r[1].iterations
     assert np.max(np.abs(r[0].u - r[1].u)) / np.max(np.abs(r[1].u)) <= U_TOL
+
+
+@pytest.mark.parametrize("name", list(PROBS))
+@pytest.mark.parametrize("tiles", [0, 1])
+def test_tile_kernels_parity(gpu_api, name, tiles):
+    """Structured levels through the overlapped-tile kernels (tiles.cu) or the
+    per-colour kernels, with the single-CTA tier cut down to 64 cells so the
+    tile path covers every level it can."""
+    s = PROBS[name]
+    g = gpu_api.GpuOptions(fused_max_cells=64, tile_kernels=bool(tiles))
+    h = gpu_api.setup_hierarchy(s.A, s.coords, gpu=g)
+    res = gpu_api.solve(s.A, s.b, h)
+    ref = ob.CpuHierarchy("oracle", s.A, s.coords).solve(s.b)
+    assert abs(res.iterations - ref["iterations"]) <= 1
+    err = np.max(np.abs(res.u - ref["u"])) / np.max(np.abs(ref["u"]))
+    assert err <= U_TOL, err
+
+
+@pytest.mark.parametrize("opts", [dict(n_inner=1), dict(n_inner=3), dict(pre_sweeps=2, post_sweeps=2),
+                                  dict(pre_sweeps=2, post_sweeps=1), dict(max_directions=2)])
+def test_tile_kernels_cycle_options(gpu_api, opts):
+    s = problems.jittered_p1(129)
+    h = gpu_api.setup_hierarchy(s.A, s.coords, gpu=gpu_api.GpuOptions(fused_max_cells=64))
+    res = gpu_api.solve(s.A, s.b, h, gpu_api.CycleOptions(**opts))
+    ref = ob.CpuHierarchy("oracle", s.A, s.coords).solve(s.b, ob.cycle_opts(**opts))
+    assert abs(res.iterations - ref["iterations"]) <= 1
+    err = np.max(np.abs(res.u - ref["u"])) / np.max(np.abs(ref["u"]))
+    assert err <= U_TOL, err
