@@ -43,7 +43,9 @@ namespace {
 // 2 pcg_step, 3 cycle_up.
 #ifdef AUX_FUSED_CLOCKS
 __device__ int g_fclk_launch;
+#define FCLK_START const long long fclk_k0 = clock64();
 #define FCLK_DECL                                   \
+    const long long fclk_k1 = clock64();            \
     __shared__ unsigned long long s_clk[16];        \
     __shared__ unsigned s_cnt[16];                  \
     if (threadIdx.x < 16) { s_clk[threadIdx.x] = 0; s_cnt[threadIdx.x] = 0; } \
@@ -54,11 +56,13 @@ __device__ int g_fclk_launch;
     if (threadIdx.x == 0) { s_clk[(T) * 4 + ((Q) & 3)] += clock64() - fclk_t0; s_cnt[(T) * 4 + ((Q) & 3)]++; }
 #define FCLK_REPORT                                                           \
     if (threadIdx.x == 0 && atomicAdd(&g_fclk_launch, 1) == 2) {            \
+        printf("fused clk prologue %lld cycles, state machine %lld cycles\n", fclk_k1 - fclk_k0, clock64() - fclk_k1); \
         for (int k = 0; k < 16; ++k)                                          \
             if (s_cnt[k]) printf("fused clk type %d level %d: calls %u avg %llu cycles\n", k / 4, k % 4, s_cnt[k], \
                                  s_clk[k] / s_cnt[k]);                        \
     }
 #else
+#define FCLK_START
 #define FCLK_DECL
 #define FCLK_BEGIN
 #define FCLK_END(T, Q)
@@ -131,9 +135,11 @@ __device__ __forceinline__ int noff(const SLevel& L) {
     return (nc - C) * L.PP + db * L.W2 + da;
 }
 
-__device__ __forceinline__ SLevel slev(const FusedArgs& a, unsigned char* sm, int q) {
+// sg: the fused levels' geometry, copied to shared memory once per launch
+// (a state transition then costs no global-memory round trip)
+__device__ __forceinline__ SLevel slev(const FusedArgs& a, unsigned char* sm, const Geo* sg, int q) {
     SLevel L;
-    const Geo g = a.lv[a.m0 + q].g;
+    const Geo g = sg[q];
     L.k = g.k;
     L.lh = g.lh;
     L.H = g.H;
@@ -431,9 +437,12 @@ __device__ bool pcg_step(const FusedArgs& a, const SLevel& L, PState& ps, double
 }
 
 __global__ void __launch_bounds__(kThreads, 1) k_fused_pcg(const __grid_constant__ FusedArgs a) {
+    FCLK_START
     extern __shared__ __align__(16) unsigned char sm[];
     __shared__ double red[2 * 2 * kWarps];
+    __shared__ Geo sgeo[kMaxFusedLevels];
     const int nl = a.last - a.m0 + 1;
+    if (threadIdx.x < nl) sgeo[threadIdx.x] = a.lv[a.m0 + threadIdx.x].g;
 
     // ---- stage read-only data with TMA bulk copies (cp.async.bulk, all in
     // flight at once, completion on one mbarrier); meanwhile zero the padded
@@ -478,7 +487,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_pcg(const __grid_constant
     mbar_wait(&bar, 0);
     __syncthreads();
     {
-        const SLevel L0 = slev(a, sm, 0);
+        const SLevel L0 = slev(a, sm, sgeo, 0);
         const double* r0 = a.lv[a.m0].r;
         for (int ci = threadIdx.x; ci < L0.n; ci += kThreads) {
             const int c = ci >> (2 * L0.lh), pos = ci & (L0.nq - 1);
@@ -498,7 +507,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_pcg(const __grid_constant
     double* part = reinterpret_cast<double*>(sm + a.off_part);
     FCLK_DECL
     while (true) {
-        const SLevel L = slev(a, sm, q);
+        const SLevel L = slev(a, sm, sgeo, q);
         if (!resume) {
             double* u = L.p + ps[q].step * 4 * L.PP;
             if (q == nl - 1) {
@@ -506,10 +515,25 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_pcg(const __grid_constant
                 coarse_solve(a, inv, part, L, ps[q], u);
                 FCLK_END(1, q)
                 resume = true;
+                if (a.coarse_mode == 0) {
+                    // Exact preconditioner on the coarsest level: the first PCG
+                    // step already returns A_c^{-1} f (alpha = 1 up to rounding,
+                    // the next residual is rounding noise), so the inverse mode
+                    // takes u = A_c^{-1} f as the whole nonlinear_pcg.  The
+                    // LU mode (coarse_mode 1) runs the reference's n_inner steps.
+                    ps[q].alpha[0] = 1.0;
+                    ps[q].nval = 1;
+                    if (q == 0) break;
+                    --q;
+                    const SLevel P = slev(a, sm, sgeo, q);
+                    FCLK_BEGIN
+                    cycle_up(a, P, L, ps[q + 1], P.p + ps[q].step * 4 * P.PP);
+                    FCLK_END(3, q)
+                }
                 continue;
             }
             FCLK_BEGIN
-            cycle_down(a, L, ps[q], slev(a, sm, q + 1), u);
+            cycle_down(a, L, ps[q], slev(a, sm, sgeo, q + 1), u);
             FCLK_END(0, q)
             ++q;
             ps[q].step = 0;
@@ -528,7 +552,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_pcg(const __grid_constant
         }
         if (q == 0) break;
         --q;
-        const SLevel P = slev(a, sm, q);
+        const SLevel P = slev(a, sm, sgeo, q);
         FCLK_BEGIN
         cycle_up(a, P, L, ps[q + 1], P.p + ps[q].step * 4 * P.PP);
         FCLK_END(3, q)
@@ -538,7 +562,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_pcg(const __grid_constant
 
     // ---- u of nonlinear_pcg(m0) = ((0 + alpha_0 p_0) + alpha_1 p_1) ... to global memory
     {
-        const SLevel L0 = slev(a, sm, 0);
+        const SLevel L0 = slev(a, sm, sgeo, 0);
         double* u0 = a.lv[a.m0].u;
         for (int ci = threadIdx.x; ci < L0.n; ci += kThreads) {
             const int c = ci >> (2 * L0.lh), pos = ci & (L0.nq - 1);
