@@ -198,6 +198,39 @@ aux_status aux_export_level(const aux_hierarchy* h, int32_t level, aux_level_exp
 aux_status aux_export_coarsest(const aux_hierarchy* h, int32_t* n, double* lu, int32_t* perm);
 void aux_destroy(aux_hierarchy* h);
 
+/* ---- multi-GPU; no reference analogue --------------------
+ * The fine grid is partitioned by quadtree subtree: part r of P (P = 2^j)
+ * owns one rectangle of level-L cells (2 halves, 4 quadrants, 8
+ * half-quadrants, ...) and the finest DoFs inside it.  Every part passes the
+ * same global A / coordinates (the drop-in input); setup extracts its rows,
+ * ghost DoFs and exchange lists.  Structured levels stay distributed while a
+ * part's rectangle is >= 16 cells per side (ring exchange of 10 cells per
+ * K-cycle kernel), the levels below are gathered on part 0.  aux_solve on a
+ * part writes the entries of the DoFs it owns into res->u; the residual
+ * history and iteration count are identical on every part. */
+typedef struct aux_dist_opts {
+    int32_t nparts;           /* P */
+    int32_t rank;             /* this part */
+    int32_t transport;        /* 0 = parts driven by threads of one process
+                                     (local_group, one device: the test path),
+                                 1 = NCCL, one process per GPU */
+    int32_t reserved;
+    void* local_group;        /* aux_local_group_create(P), transport 0 */
+    uint8_t nccl_id[128];     /* aux_nccl_unique_id on rank 0, broadcast by the caller */
+} aux_dist_opts;
+
+void* aux_local_group_create(int32_t parts);
+void aux_local_group_destroy(void* group);
+int32_t aux_nccl_unique_id(uint8_t id[128]);   /* 1 on success */
+/* setup_hierarchy for one part; A and xy are the global inputs (host / device). */
+aux_status aux_setup_dist(const aux_csr_view* A, const double* xy, int64_t n_points,
+                          const aux_setup_opts* opts, const aux_gpu_opts* gpu, const aux_dist_opts* d,
+                          aux_hierarchy** out, char* msg, size_t msg_len);
+aux_status aux_setup_dist_device(const aux_csr_view* A, const double* xy, int64_t n_points,
+                                 const aux_setup_opts* opts, const aux_gpu_opts* gpu,
+                                 const aux_dist_opts* d, aux_hierarchy** out, char* msg, size_t msg_len);
+int32_t aux_part_rows(const aux_hierarchy* h);   /* finest DoFs owned by this part */
+
 /* ---- measurement hooks (bench.py; not part of the reference API) ---- */
 /* Number of kernels this library launched (graph nodes count per replay). */
 int64_t aux_launch_count(void);

@@ -99,6 +99,12 @@ class GpuOpts(C.Structure):
                 ("tile_kernels", C.c_int32), ("reserved", C.c_int32 * 2)]
 
 
+class DistOpts(C.Structure):
+    """aux_dist_opts: one part of a multi-GPU hierarchy."""
+    _fields_ = [("nparts", C.c_int32), ("rank", C.c_int32), ("transport", C.c_int32), ("reserved", C.c_int32),
+                ("local_group", C.c_void_p), ("nccl_id", C.c_uint8 * 128)]
+
+
 class Locality(C.Structure):
     _fields_ = [("dropped", C.c_int64), ("dropped_mass", C.c_double),
                 ("lumped", C.c_int64), ("lumped_mass", C.c_double)]

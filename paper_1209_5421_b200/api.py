@@ -61,6 +61,17 @@ def lib():
     L.aux_last_timing.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(C.c_double)]
     L.aux_version.restype = C.c_char_p
     L.aux_set_num_threads.argtypes = [i32]
+    L.aux_local_group_create.argtypes = [i32]
+    L.aux_local_group_create.restype = vp
+    L.aux_local_group_destroy.argtypes = [vp]
+    L.aux_nccl_unique_id.argtypes = [vp]
+    L.aux_nccl_unique_id.restype = i32
+    L.aux_setup_dist.argtypes = [vp, vp, i64, vp, vp, vp, C.POINTER(vp), C.c_char_p, sz]
+    L.aux_setup_dist.restype = C.c_int
+    L.aux_setup_dist_device.argtypes = [vp, vp, i64, vp, vp, vp, C.POINTER(vp), C.c_char_p, sz]
+    L.aux_setup_dist_device.restype = C.c_int
+    L.aux_part_rows.argtypes = [vp]
+    L.aux_part_rows.restype = i32
     _lib = L
     return L
 
@@ -232,12 +243,20 @@ def setup_hierarchy_device(n: int, nnz: int, row_ptr: int, col_idx: int, values:
     return Hierarchy(h, None, n)
 
 
-def solve(A: CsrMatrix | None, b, h: Hierarchy, opts: CycleOptions | None = None) -> SolveResult:
-    """solve(A, b, h, opts).  A may be None or the matrix given to setup."""
+def solve(A: CsrMatrix | None, b, h: Hierarchy, opts: CycleOptions | None = None,
+          out: np.ndarray | None = None) -> SolveResult:
+    """solve(A, b, h, opts).  A may be None or the matrix given to setup.
+    out: optional caller-owned float64 array of length n (e.g. pinned) that
+    receives u; the result then references it instead of a fresh copy."""
     o = (opts or CycleOptions()).c()
     b = np.ascontiguousarray(b, dtype=np.float64)
     n = h.n
-    u = np.zeros(max(n, 1), np.float64)
+    if out is not None:
+        if out.dtype != np.float64 or not out.flags.c_contiguous or out.size < max(n, 1):
+            raise ValueError("out must be a contiguous float64 array of length n")
+        u = out
+    else:
+        u = np.zeros(max(n, 1), np.float64)
     hist = np.zeros(o.max_outer + 2, np.float64)
     res = _abi.SolveResultC(u.ctypes.data, hist.ctypes.data, hist.size, 0, 0, 0, 0.0, 0.0, 0.0)
     msg = C.create_string_buffer(512)
@@ -248,8 +267,8 @@ def solve(A: CsrMatrix | None, b, h: Hierarchy, opts: CycleOptions | None = None
         av = C.byref(_csr_view(A if A is h._A else _prep_csr(A)))
     s = lib().aux_solve(h.handle, av, b.ctypes.data, b.size, C.byref(o), C.byref(res), msg, 512)
     _abi.raise_for(s, msg.raw)
-    return SolveResult(u[:n].copy(), list(hist[: res.history_len]), res.iterations, bool(res.converged),
-                       res.setup_seconds, res.solve_seconds, res.total_seconds)
+    return SolveResult(u[:n] if out is not None else u[:n].copy(), list(hist[: res.history_len]), res.iterations,
+                       bool(res.converged), res.setup_seconds, res.solve_seconds, res.total_seconds)
 
 
 def solve_device(h: Hierarchy, b_ptr: int, u_ptr: int, n: int, opts: CycleOptions | None = None) -> SolveResult:
@@ -278,3 +297,94 @@ def stats(h: Hierarchy) -> HierarchyStats:
 
 def launch_count() -> int:
     return lib().aux_launch_count()
+
+
+# ---------------------------------------------------------------- multi-GPU
+
+class LocalGroup:
+    """P parts of one distributed hierarchy driven by P threads of this
+    process on one device (the CommLocal transport): the multi-GPU code path,
+    runnable on a single B200."""
+
+    def __init__(self, parts: int):
+        self.parts = parts
+        self._g = lib().aux_local_group_create(parts)
+        if not self._g:
+            raise _abi.ArgumentError(f"cannot create a local group of {parts} parts")
+
+    def __del__(self):
+        try:
+            if self._g:
+                lib().aux_local_group_destroy(self._g)
+                self._g = None
+        except Exception:
+            pass
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    if not lib().aux_nccl_unique_id(buf):
+        raise _abi.DeviceError("NCCL unavailable (libnccl.so.2 not found)")
+    return bytes(buf)
+
+
+def setup_hierarchy_dist(A: CsrMatrix, coords, nparts: int, rank: int, group: LocalGroup | None = None,
+                         nccl_id: bytes | None = None, opts: SetupOptions | None = None,
+                         gpu: GpuOptions | None = None) -> Hierarchy:
+    """setup_hierarchy for part `rank` of `nparts` (A and coords are the global
+    inputs).  group: local transport (threads, one device); nccl_id: NCCL, one
+    process per GPU."""
+    A = _prep_csr(A)
+    xy = np.ascontiguousarray(coords, dtype=np.float64)
+    npts = xy.shape[0] if xy.ndim == 2 else xy.size // 2
+    d = _abi.DistOpts()
+    d.nparts, d.rank = nparts, rank
+    if group is not None:
+        d.transport, d.local_group = 0, group._g
+    else:
+        if nccl_id is None or len(nccl_id) != 128:
+            raise _abi.ArgumentError("setup_hierarchy_dist: need a LocalGroup or a 128-byte NCCL id")
+        d.transport = 1
+        C.memmove(d.nccl_id, nccl_id, 128)
+    o = (opts or SetupOptions()).c()
+    g = (gpu or GpuOptions()).c()
+    h = C.c_void_p()
+    msg = C.create_string_buffer(512)
+    s = lib().aux_setup_dist(C.byref(_csr_view(A)), xy.ctypes.data, npts, C.byref(o), C.byref(g), C.byref(d),
+                             C.byref(h), msg, 512)
+    _abi.raise_for(s, msg.raw)
+    return Hierarchy(h, A, A.n_rows)
+
+
+def part_rows(h: Hierarchy) -> int:
+    return lib().aux_part_rows(h.handle)
+
+
+def solve_parts(A: CsrMatrix, coords, b, parts: int, opts: SetupOptions | None = None,
+                cycle: CycleOptions | None = None, gpu: GpuOptions | None = None):
+    """Set up and solve with `parts` parts on this process's device (local
+    transport, one thread per part).  Returns (u assembled from the parts'
+    owned entries, list of per-part SolveResult, list of per-part stats)."""
+    import threading
+    grp = LocalGroup(parts)
+    u = np.zeros(A.n_rows)
+    results, stats_, errors = [None] * parts, [None] * parts, [None] * parts
+
+    def run(r):
+        try:
+            h = setup_hierarchy_dist(A, coords, parts, r, group=grp, opts=opts, gpu=gpu)
+            stats_[r] = h.stats()
+            results[r] = solve(A, b, h, cycle, out=u)
+            del h
+        except Exception as e:   # noqa: BLE001 - re-raised below
+            errors[r] = e
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(parts)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for e in errors:
+        if e is not None:
+            raise e
+    return u, results, stats_

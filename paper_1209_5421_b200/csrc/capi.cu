@@ -6,10 +6,11 @@
 #include <new>
 #include <string>
 
+#include "comm.cuh"
 #include "setup.cuh"
 
 namespace auxb200 {
-int64_t g_launches = 0;
+std::atomic<int64_t> g_launches{0};
 }
 
 using namespace auxb200;
@@ -61,6 +62,8 @@ aux_hierarchy::~aux_hierarchy() {
         for (auto e : prof.ev_end[k]) cudaEventDestroy(e);
     }
     if (stream) cudaStreamSynchronize(stream);
+    delete dist.comm;
+    dist.comm = nullptr;
     // DBufs free themselves; the stream goes last
     fine = Finest();
     lv.clear();
@@ -156,6 +159,80 @@ aux_status aux_setup(const aux_csr_view* A, const double* xy, int64_t n_points, 
     return AUX_OK;
 }
 
+// ---- multi-GPU
+void* aux_local_group_create(int32_t parts) {
+    try {
+        return local_group_create(parts);
+    } catch (...) {
+        return nullptr;
+    }
+}
+void aux_local_group_destroy(void* g) { local_group_destroy(static_cast<LocalGroup*>(g)); }
+int32_t aux_nccl_unique_id(uint8_t id[128]) { return nccl_unique_id(id) ? 1 : 0; }
+
+static aux_status setup_dist_impl(const aux_csr_view* A, const double* xy, int64_t n_points,
+                                  const aux_setup_opts* opts, const aux_gpu_opts* gpu, const aux_dist_opts* d,
+                                  aux_hierarchy** out, char* msg, size_t msg_len, bool host) {
+    *out = nullptr;
+    aux_hierarchy* h = nullptr;
+    const aux_status st = guarded(msg, msg_len, [&] {
+        if (!d || d->nparts < 1 || d->rank < 0 || d->rank >= d->nparts)
+            throw_aux(AUX_ARGUMENT_ERROR, "aux_dist_opts: bad part count or rank");
+        h = make_h(opts, gpu);
+        const auto t0 = std::chrono::steady_clock::now();
+        if (d->transport == 0) {
+            if (!d->local_group) throw_aux(AUX_ARGUMENT_ERROR, "aux_dist_opts: local transport needs a group");
+            h->dist.comm = make_local_comm(static_cast<LocalGroup*>(d->local_group), d->rank);
+        } else {
+            h->dist.comm = make_nccl_comm(d->nccl_id, d->nparts, d->rank);
+        }
+        h->dist.dsum.alloc(8);
+        if (A->n_rows < 0 || A->nnz < 0) throw_aux(AUX_SIZE_ERROR, "setup_hierarchy: negative size");
+        if (host) {
+            const long n = A->n_rows;
+            DBuf<int> rp(n + 1), col(std::max<long>(A->nnz, 1));
+            DBuf<double> v(std::max<long>(A->nnz, 1)), xy_d(2 * std::max<long>(n_points, 1));
+            AUX_CUDA(cudaMemcpyAsync(rp.p, A->row_ptr, sizeof(int) * (n + 1), cudaMemcpyHostToDevice, h->stream));
+            if (A->nnz) {
+                AUX_CUDA(cudaMemcpyAsync(col.p, A->col_idx, sizeof(int) * A->nnz, cudaMemcpyHostToDevice, h->stream));
+                AUX_CUDA(cudaMemcpyAsync(v.p, A->values, sizeof(double) * A->nnz, cudaMemcpyHostToDevice, h->stream));
+            }
+            if (n_points > 0)
+                AUX_CUDA(cudaMemcpyAsync(xy_d.p, xy, sizeof(double) * 2 * n_points, cudaMemcpyHostToDevice, h->stream));
+            aux_csr_view dv = *A;
+            dv.row_ptr = rp.p;
+            dv.col_idx = col.p;
+            dv.values = v.p;
+            setup_device_dist(h, &dv, xy_d.p, (long)n_points);
+            h->host_rp = A->row_ptr;
+            h->host_col = A->col_idx;
+            h->host_val = A->values;
+            h->host_nnz = A->nnz;
+        } else {
+            setup_device_dist(h, A, xy, (long)n_points);
+        }
+        h->last_setup_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    });
+    if (st != AUX_OK) {
+        delete h;
+        return st;
+    }
+    *out = h;
+    return AUX_OK;
+}
+
+aux_status aux_setup_dist(const aux_csr_view* A, const double* xy, int64_t n_points, const aux_setup_opts* opts,
+                          const aux_gpu_opts* gpu, const aux_dist_opts* d, aux_hierarchy** out, char* msg,
+                          size_t msg_len) {
+    return setup_dist_impl(A, xy, n_points, opts, gpu, d, out, msg, msg_len, true);
+}
+aux_status aux_setup_dist_device(const aux_csr_view* A, const double* xy, int64_t n_points,
+                                 const aux_setup_opts* opts, const aux_gpu_opts* gpu, const aux_dist_opts* d,
+                                 aux_hierarchy** out, char* msg, size_t msg_len) {
+    return setup_dist_impl(A, xy, n_points, opts, gpu, d, out, msg, msg_len, false);
+}
+int32_t aux_part_rows(const aux_hierarchy* h) { return h->fine.n; }
+
 aux_status aux_solve(aux_hierarchy* h, const aux_csr_view* A, const double* b, int64_t n_b,
                      const aux_cycle_opts* opts, aux_solve_result* res, char* msg, size_t msg_len) {
     return guarded(msg, msg_len, [&] {
@@ -180,7 +257,17 @@ aux_status aux_solve(aux_hierarchy* h, const aux_csr_view* A, const double* b, i
         if (n_b > 0)
             AUX_CUDA(cudaMemcpyAsync(bd.p, b, sizeof(double) * n_b, cudaMemcpyHostToDevice, h->stream));
         solve_device(h, bd.p, (long)n_b, &o, res, ud.p);
-        if (res->u && n > 0) {
+        if (res->u && n > 0 && h->dist.comm) {   // a part writes the entries of the DoFs it owns
+            const long m = h->fine.n;
+            std::vector<double> uv(m);
+            std::vector<int> gv(m);
+            DBuf<double> ul(m);
+            gather_owned(h, ud.p, ul.p);
+            AUX_CUDA(cudaMemcpyAsync(uv.data(), ul.p, sizeof(double) * m, cudaMemcpyDeviceToHost, h->stream));
+            AUX_CUDA(cudaMemcpyAsync(gv.data(), h->dist.gid.p, sizeof(int) * m, cudaMemcpyDeviceToHost, h->stream));
+            AUX_CUDA(cudaStreamSynchronize(h->stream));
+            for (long i = 0; i < m; ++i) res->u[gv[i]] = uv[i];
+        } else if (res->u && n > 0) {
             AUX_CUDA(cudaMemcpyAsync(res->u, ud.p, sizeof(double) * n, cudaMemcpyDeviceToHost, h->stream));
             AUX_CUDA(cudaStreamSynchronize(h->stream));
         }
@@ -232,7 +319,7 @@ aux_status aux_level_info_get(const aux_hierarchy* h, int32_t level, aux_level_i
 }
 
 aux_status aux_export_level(const aux_hierarchy* h, int32_t level, aux_level_export* out) {
-    if (level < 0 || level >= (int)h->lv.size()) return AUX_ARGUMENT_ERROR;
+    if (level < 0 || level >= (int)h->lv.size() || h->dist.comm) return AUX_ARGUMENT_ERROR;
     return guarded(nullptr, 0, [&] { export_level(h, level, out); });
 }
 

@@ -23,6 +23,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <cstdio>
 #include <stdexcept>
 #include <string>
@@ -48,7 +49,7 @@ struct AuxError : std::runtime_error {
     } while (0)
 
 // Host-side kernel launch counter (bench.py's gpu_launches).
-extern int64_t g_launches;
+extern std::atomic<int64_t> g_launches;
 #define AUX_LAUNCHED(n) (::auxb200::g_launches += (n))
 
 // --------------------------------------------------------------- layout
@@ -200,7 +201,8 @@ __device__ bool grid_reduce(double (&v)[NV], const RedState& rs, double (&out)[N
 // PCG scalars, so a whole coarse K-cycle needs no host round trip).
 constexpr double kBreakdown = 1e-300;   // breakdown_energy, cycle.hpp:78
 struct Fin {
-    int op;                    // 0 none, 1 alpha (e=s0, alpha=s1/e), 2 beta (-s0/e_in), 3 store s0
+    int op;                    // 0 none, 1 alpha (e=s0, alpha=s1/e), 2 beta (-s0/e_in), 3 store s0,
+                               // 5/6 raw s0 / (s0, s1) into e_out
     double* sc;                // [0]=alpha [1]=beta [2]=dead
     const double* e_in;
     double* e_out;             // op 1: energy slot; op 3: destination
@@ -224,6 +226,11 @@ __device__ __forceinline__ void finalize(const Fin& f, const double* s) {
         f.sc[1] = -s[0] / *f.e_in;
     } else if (f.op == 3) {
         *f.e_out = s[0];
+    } else if (f.op == 5) {        // raw sums for a cross-GPU all-reduce (solve.cu routed())
+        f.e_out[0] = s[0];
+    } else if (f.op == 6) {
+        f.e_out[0] = s[0];
+        f.e_out[1] = s[1];
     }
 }
 

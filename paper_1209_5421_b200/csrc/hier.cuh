@@ -48,6 +48,21 @@ struct DBuf {
     T* get() const { return p; }
 };
 
+// Rectangle of cells [x0, x1) x [y0, y1) on one structured level (global
+// coordinates): the cells a part owns (multi-GPU path).
+struct Rect {
+    int x0 = 0, y0 = 0, x1 = 0, y1 = 0;
+    int w() const { return x1 - x0; }
+    int h() const { return y1 - y0; }
+    long cells() const { return (long)w() * h(); }
+    bool empty() const { return x1 <= x0 || y1 <= y0; }
+};
+inline Rect intersect(const Rect& a, const Rect& b) {
+    Rect r{a.x0 > b.x0 ? a.x0 : b.x0, a.y0 > b.y0 ? a.y0 : b.y0, a.x1 < b.x1 ? a.x1 : b.x1, a.y1 < b.y1 ? a.y1 : b.y1};
+    return r;
+}
+inline Rect dilate(const Rect& a, int d) { return Rect{a.x0 - d, a.y0 - d, a.x1 + d, a.y1 + d}; }
+
 // Per-level PCG state (nonlinear_pcg, cycle.hpp:106-128) for a level that is
 // the target of a coarse-grid correction.
 struct PcgBufs {
@@ -74,7 +89,15 @@ struct Level {
     DBuf<uint8_t> active;
     int zero_diag_lex = -1;        // first active row (colour, then index) with a_ii == 0
     PcgBufs pcg;                   // used when this level is a PCG target (index >= 1)
+    // multi-GPU: the owned rectangle (the whole grid on one GPU); on a
+    // distributed level every part keeps global-layout arrays, computes its
+    // rectangle and receives a ring of kRing cells from its neighbours
+    Rect own;
+    bool dist = false;
+    DBuf<double> xbuf;             // ring-exchange staging (send | receive)
 };
+
+constexpr int kRing = 10;          // ring width: tile halos up to 4*2+1 cells
 
 // Finest level (CSR, rows permuted into level-L cell order).
 struct Finest {
@@ -108,6 +131,22 @@ struct Finest {
     int color_row[5] = {0, 0, 0, 0, 0};   // first finest row of each colour class (+ N)
     bool color_clean = true;  // check_color_locality (smoother.hpp:217-231) empty
     int max_block = 0;
+    // multi-GPU: local rows = the DoFs of the owned level-L cells; columns
+    // n..n+n_ghost-1 are ghost DoFs, grouped by owner part
+    int n_ghost = 0;
+    std::vector<int> g_peer, g_recv_off, g_send_off;   // per neighbour part
+    DBuf<int> g_send_idx;     // local rows each neighbour needs, by peer
+    DBuf<double> g_send_buf;
+};
+
+// Multi-GPU bookkeeping of one part.
+struct Comm;
+struct DistInfo {
+    Comm* comm = nullptr;
+    int PX = 1, PY = 1, px = 0, py = 0;
+    int agg = 1 << 30;        // first level index gathered on part 0 (levels below are distributed)
+    DBuf<double> dsum;        // raw inner products before the all-reduce
+    DBuf<int> gid;            // local finest row -> caller DoF id
 };
 
 constexpr int kTileBlock = 8;   // blocks up to this size: one thread per block
@@ -165,6 +204,7 @@ struct aux_hierarchy {
     auxb200::DBuf<auxb200::FLevel> d_flv;
     auxb200::FusedArgs fused_args{};
     auxb200::Profile prof;
+    auxb200::DistInfo dist;          // comm == nullptr: one GPU
     double last_setup_ms = 0.0, last_solve_ms = 0.0;
     ~aux_hierarchy();
 };

@@ -26,6 +26,7 @@
 #include "scan_sort.cuh"
 #include "setup.cuh"
 #include "tiles.cuh"
+#include "comm.cuh"
 
 namespace auxb200 {
 
@@ -545,6 +546,135 @@ __global__ void k_inverse_scatter(const double* __restrict__ work, const int* __
     }
 }
 
+// ---------------------------------------------------------------- multi-GPU setup kernels
+// (SURVEY 8(e)): a part owns the finest DoFs of one rectangle of level-L cells.
+
+__device__ __forceinline__ bool cm_in_rect(const Geo& g, int cm, int x0, int y0, int x1, int y1) {
+    int t1, t2;
+    xy_of_cm(g, cm, t1, t2);
+    return t1 >= x0 && t1 < x1 && t2 >= y0 && t2 < y1;
+}
+__global__ void k_own_flag(const unsigned* __restrict__ key, long n, Geo g, int x0, int y0, int x1, int y1,
+                           int* __restrict__ flag) {
+    GSTRIDE(i, n) flag[i] = cm_in_rect(g, (int)key[i], x0, y0, x1, y1) ? 1 : 0;
+}
+__global__ void k_mark_local(const int* __restrict__ l2s, int n_own, int* __restrict__ s2l) {
+    GSTRIDE(l, n_own) s2l[l2s[l]] = (int)l;
+}
+// non-owned entries of each local row (sorted-order column index)
+__global__ void k_ghost_count(const int* __restrict__ l2s, int n_own, const int* __restrict__ perm,
+                              const int* __restrict__ rp, const int* __restrict__ col, const int* __restrict__ iperm,
+                              const int* __restrict__ s2l, int* __restrict__ cnt) {
+    GSTRIDE(l, n_own) {
+        const int c = perm[l2s[l]];
+        int k = 0;
+        for (int p = rp[c]; p < rp[c + 1]; ++p) k += s2l[iperm[col[p]]] < 0 ? 1 : 0;
+        cnt[l] = k;
+    }
+}
+__global__ void k_ghost_emit(const int* __restrict__ l2s, int n_own, const int* __restrict__ perm,
+                             const int* __restrict__ rp, const int* __restrict__ col, const int* __restrict__ iperm,
+                             const int* __restrict__ s2l, const int* __restrict__ off, unsigned* __restrict__ out) {
+    GSTRIDE(l, n_own) {
+        const int c = perm[l2s[l]];
+        int k = off[l];
+        for (int p = rp[c]; p < rp[c + 1]; ++p) {
+            const int j = iperm[col[p]];
+            if (s2l[j] < 0) out[k++] = (unsigned)j;
+        }
+    }
+}
+__global__ void k_owner_key(const int* __restrict__ idx, long m, const unsigned* __restrict__ key, Geo g, int PX,
+                            int PY, unsigned* __restrict__ okey) {
+    const int w = 1 << g.k;
+    GSTRIDE(i, m) {
+        int t1, t2;
+        xy_of_cm(g, (int)key[idx[i]], t1, t2);
+        okey[i] = (unsigned)((t2 / (w / PY)) * PX + t1 / (w / PX));
+    }
+}
+__global__ void k_first_of_run(const unsigned* __restrict__ v, long m, int* __restrict__ flag) {
+    GSTRIDE(i, m) flag[i] = (i == 0 || v[i] != v[i - 1]) ? 1 : 0;
+}
+__global__ void k_compact_u(const int* __restrict__ flag, const int* __restrict__ pos, const unsigned* __restrict__ v,
+                            long m, int* __restrict__ out) {
+    GSTRIDE(i, m) if (flag[i]) out[pos[i]] = (int)v[i];
+}
+__global__ void k_ghost_map(const int* __restrict__ ghosts, int ng, int n_own, int* __restrict__ s2l) {
+    GSTRIDE(i, ng) s2l[ghosts[i]] = n_own + (int)i;
+}
+__global__ void k_local_len(const int* __restrict__ l2s, int n_own, const int* __restrict__ perm,
+                            const int* __restrict__ rp, int* __restrict__ len, int* __restrict__ gid) {
+    GSTRIDE(l, n_own) {
+        const int c = perm[l2s[l]];
+        len[l] = rp[c + 1] - rp[c];
+        gid[l] = c;
+    }
+}
+// local rows (entries in the caller's storage order, columns relabelled to
+// local / ghost indices), one warp per row
+__global__ void k_local_csr(const int* __restrict__ gid, int n_own, const int* __restrict__ rp,
+                            const int* __restrict__ col, const double* __restrict__ v, const int* __restrict__ iperm,
+                            const int* __restrict__ s2l, const int* __restrict__ rpl, int* __restrict__ coll,
+                            double* __restrict__ vl) {
+    const int lane = threadIdx.x & 31;
+    const long warp = (blockIdx.x * (long)blockDim.x + threadIdx.x) >> 5;
+    const long nw = ((long)gridDim.x * blockDim.x) >> 5;
+    for (long l = warp; l < n_own; l += nw) {
+        const int c = gid[l];
+        const int a = rp[c], b = rp[c + 1], o = rpl[l];
+        for (int p = a + lane; p < b; p += 32) {
+            coll[o + (p - a)] = s2l[iperm[col[p]]];
+            vl[o + (p - a)] = v[p];
+        }
+    }
+}
+__global__ void k_local_cell(const int* __restrict__ l2s, int n_own, const int* __restrict__ ghosts, int ng,
+                             const unsigned* __restrict__ key, int* __restrict__ cell) {
+    GSTRIDE(i, (long)n_own + ng) cell[i] = (int)key[i < n_own ? l2s[i] : ghosts[i - n_own]];
+}
+__global__ void k_count_i(const int* __restrict__ key, long n, int* cnt) {
+    GSTRIDE(i, n) atomicAdd(&cnt[key[i]], 1);
+}
+// per-level nnz / zero diagonal over the owned rectangle only
+__global__ void k_level_nnz_rect(Geo g, const uint8_t* __restrict__ act, int x0, int y0, int rw, long cells,
+                                 unsigned long long* out) {
+    unsigned long long s = 0;
+    GSTRIDE(j, cells) {
+        const int t1 = x0 + (int)(j % rw), t2 = y0 + (int)(j / rw);
+        const int i = cm_of_xy(g, t1, t2);
+        s += 1;
+        if (!act[i]) continue;
+        const int c = i >> g.lq, pos = i & (g.nq - 1);
+        const int a = pos & (g.H - 1), b = pos >> g.lh;
+        for (int t = 1; t < 9; ++t) s += cm_neighbor(g, c, a, b, t) >= 0 ? 1 : 0;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) atomicAdd(out, s);
+}
+__global__ void k_zero_diag_rect(Geo g, const double* __restrict__ val, const uint8_t* __restrict__ act, int x0,
+                                 int y0, int rw, long cells, unsigned long long* err) {
+    GSTRIDE(j, cells) {
+        const int t1 = x0 + (int)(j % rw), t2 = y0 + (int)(j / rw);
+        const int i = cm_of_xy(g, t1, t2);
+        if (!act[i] || val[i] != 0.0) continue;
+        atomicMin(err, (unsigned long long)(i >> g.lq) * g.n + lex_of_cm(g, i));
+    }
+}
+__global__ void k_inv_perm(const int* __restrict__ perm, long n, int* __restrict__ iperm) {
+    GSTRIDE(i, n) iperm[perm[i]] = (int)i;
+}
+__global__ void k_gather_int(const int* __restrict__ idx, long n, const int* __restrict__ map, int* __restrict__ out) {
+    GSTRIDE(i, n) out[i] = map[idx[i]];
+}
+__global__ void k_u8_to_d(const uint8_t* __restrict__ a, long n, double* __restrict__ d) {
+    GSTRIDE(i, n) d[i] = a[i];
+}
+__global__ void k_d_to_u8(const double* __restrict__ d, long n, uint8_t* __restrict__ a) {
+    GSTRIDE(i, n) a[i] = d[i] != 0.0 ? 1 : 0;
+}
+
 template <class T>
 T read1(const T* d, cudaStream_t s) {
     T v;
@@ -597,170 +727,15 @@ void alloc_solve_levels(aux_hierarchy* h, int n_inner) {
 }
 
 // A: device CSR view (arrays not retained); xy: device coordinates.
-void setup_device(aux_hierarchy* h, const aux_csr_view* A, const double* xy, long n_points) {
+// factor_blocks (smoother.hpp:129-156) on the finest level: block census,
+// stored LU factors, explicit inverses (block_solve = 0), big-block lists and
+// check_color_locality.  Returns the lowest singular aggregate (~0: none) and
+// the colour-locality flag through the out-parameters.
+void finest_blocks(aux_hierarchy* h, const Geo& gL, unsigned long long& sing, int& color_flag) {
     cudaStream_t s = h->stream;
-    const aux_setup_opts& o = h->opts;
-    if (A->n_rows != A->n_cols) throw_aux(AUX_SIZE_ERROR, "setup_hierarchy: matrix not square");
-    if (n_points != A->n_rows)
-        throw_aux(AUX_SIZE_ERROR, "setup_hierarchy: coordinate count does not match matrix order");
-    const int n = A->n_rows;
-    const long nnz = A->nnz;
-    h->n = n;
-
-    // ---- validate_csr (sparse.hpp:101-116)
-    {
-        int ends[2] = {0, 0};
-        if (n >= 0) {
-            AUX_CUDA(cudaMemcpyAsync(&ends[0], A->row_ptr, sizeof(int), cudaMemcpyDeviceToHost, s));
-            AUX_CUDA(cudaMemcpyAsync(&ends[1], A->row_ptr + n, sizeof(int), cudaMemcpyDeviceToHost, s));
-            AUX_CUDA(cudaStreamSynchronize(s));
-        }
-        if (ends[0] != 0 || (long)ends[1] != nnz)
-            throw_aux(AUX_STRUCTURE_ERROR, "CSR row_ptr endpoints inconsistent with nnz");
-        DBuf<unsigned long long> err(3);
-        AUX_CUDA(cudaMemsetAsync(err.p, 0xff, 2 * sizeof(unsigned long long), s));
-        if (n > 0) {
-            k_validate<<<grid_for(n), kT, 0, s>>>(A->row_ptr, A->col_idx, n, nnz, A->n_cols, err.p);
-            AUX_LAUNCHED(1);
-        }
-        const unsigned long long e = read1(err.p, s);
-        if (e != ~0ull) {
-            const long r = (long)(e / 4);
-            const int kind = (int)(e % 4);
-            if (kind == 1) throw_aux(AUX_STRUCTURE_ERROR, "CSR row_ptr not nondecreasing at row " + std::to_string(r));
-            if (kind == 2) throw_aux(AUX_STRUCTURE_ERROR, "CSR column index out of range in row " + std::to_string(r));
-            throw_aux(AUX_STRUCTURE_ERROR, "CSR row " + std::to_string(r) + " not sorted by column");
-        }
-        // diagonal > 0 (hierarchy.hpp:321-323)
-        if (n > 0) {
-            k_diag<<<grid_for(n), kT, 0, s>>>(A->row_ptr, A->col_idx, A->values, n, err.p + 1);
-            AUX_LAUNCHED(1);
-        }
-        const unsigned long long d = read1(err.p + 1, s);
-        if (d != ~0ull) throw_aux(AUX_DEFINITENESS_ERROR, "nonpositive diagonal at row " + std::to_string(d));
-        // symmetry (hierarchy.hpp:324-325)
-        DBuf<unsigned long long> sy(2);
-        AUX_CUDA(cudaMemsetAsync(sy.p, 0, 2 * sizeof(unsigned long long), s));
-        if (n > 0) {
-            k_symm<<<grid_for(n), kT, 0, s>>>(A->row_ptr, A->col_idx, A->values, n, sy.p);
-            AUX_LAUNCHED(1);
-        }
-        unsigned long long syh[2];
-        AUX_CUDA(cudaMemcpyAsync(syh, sy.p, sizeof syh, cudaMemcpyDeviceToHost, s));
-        AUX_CUDA(cudaStreamSynchronize(s));
-        double defect, scale;
-        std::memcpy(&defect, &syh[0], 8);
-        std::memcpy(&scale, &syh[1], 8);
-        scale = (1.0 < scale) ? scale : 1.0;
-        if (defect / scale > o.symmetry_tol) throw_aux(AUX_STRUCTURE_ERROR, "matrix is not symmetric to tolerance");
-    }
-    h->opts.coarsest_size = std::max(o.coarsest_size, 4);
-    const int coarsest_size = h->opts.coarsest_size;
-
     Finest& F = h->fine;
-    F.n = n;
-    F.nnz = nnz;
-    h->lv.clear();
-    h->lv.emplace_back();
-    h->lv[0].k = 0;
-    h->lv[0].structured = false;
-    h->lv[0].n = n;
-    h->lv[0].nnz = nnz;
-
-    if (n <= coarsest_size) {   // direct-only hierarchy (hierarchy.hpp:339-344)
-        h->direct_only = true;
-        F.rp.alloc(n + 1);
-        F.col.alloc(nnz);
-        F.v.alloc(nnz);
-        AUX_CUDA(cudaMemcpyAsync(F.rp.p, A->row_ptr, sizeof(int) * (n + 1), cudaMemcpyDeviceToDevice, s));
-        AUX_CUDA(cudaMemcpyAsync(F.col.p, A->col_idx, sizeof(int) * nnz, cudaMemcpyDeviceToDevice, s));
-        AUX_CUDA(cudaMemcpyAsync(F.v.p, A->values, sizeof(double) * nnz, cudaMemcpyDeviceToDevice, s));
-        h->nc = n;
-        h->c_lu.alloc((size_t)n * n);
-        h->c_perm.alloc(n);
-        h->c_lex.alloc(n);
-        AUX_CUDA(cudaMemsetAsync(h->c_lu.p, 0, sizeof(double) * n * n, s));
-        k_dense_from_csr<<<grid_for(n), kT, 0, s>>>(F.rp.p, F.col.p, F.v.p, n, h->c_lu.p, h->c_lex.p);
-        AUX_LAUNCHED(1);
-        factor_coarsest(h);
-        return;
-    }
-
-    // ---- bounding box + depth (auxgrid.hpp:75-104)
-    {
-        DBuf<unsigned long long> bb(4);
-        DBuf<int> bad(1);
-        unsigned long long init[4] = {~0ull, 0ull, ~0ull, 0ull};
-        AUX_CUDA(cudaMemcpyAsync(bb.p, init, sizeof init, cudaMemcpyHostToDevice, s));
-        AUX_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), s));
-        k_bbox<<<grid_for(n, 4), kT, 0, s>>>(xy, n, bb.p, bad.p);
-        AUX_LAUNCHED(1);
-        unsigned long long r[4];
-        int badh = 0;
-        AUX_CUDA(cudaMemcpyAsync(r, bb.p, sizeof r, cudaMemcpyDeviceToHost, s));
-        AUX_CUDA(cudaMemcpyAsync(&badh, bad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
-        AUX_CUDA(cudaStreamSynchronize(s));
-        if (badh) throw_aux(AUX_ARGUMENT_ERROR, "bounding_box: non-finite coordinate");
-        auto val = [](unsigned long long k) {
-            const unsigned long long b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
-            double d;
-            std::memcpy(&d, &b, 8);
-            return d;
-        };
-        h->box[0] = val(r[0]);
-        h->box[1] = val(r[1]);
-        h->box[2] = val(r[2]);
-        h->box[3] = val(r[3]);
-        if (!(h->box[1] > h->box[0]) || !(h->box[3] > h->box[2]))
-            throw_aux(AUX_GEOMETRY_ERROR, "bounding_box: degenerate point set");
-    }
-    int depth = 0;
-    {
-        long cells = 1;
-        while (cells * 4 < n) { cells *= 4; ++depth; }
-        if (depth == 0) depth = 1;
-    }
-    h->depth = depth;
-    h->lv[0].k = depth + 1;
-    const Geo gL = make_geo(depth);
+    const int n = F.n;
     const int nL = gL.n;
-
-    // ---- aggregate_finest: keys, stable sort, member pointers
-    DBuf<unsigned> key(n);
-    F.perm.alloc(n);
-    k_cellkey<<<grid_for(n), kT, 0, s>>>(xy, n, h->box[0], h->box[1], h->box[2], h->box[3], gL, key.p);
-    AUX_LAUNCHED(1);
-    radix_sort_pairs(key.p, F.perm.p, n, 2 * depth, s, true);
-    {
-        DBuf<int> cnt(nL);
-        AUX_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(int) * nL, s));
-        k_count<<<grid_for(n), kT, 0, s>>>(key.p, n, cnt.p);
-        AUX_LAUNCHED(1);
-        F.bptr.alloc(nL + 1);
-        exclusive_scan(cnt.p, F.bptr.p, nL, s);
-    }
-    for (int c = 0; c <= 4; ++c)
-        AUX_CUDA(cudaMemcpyAsync(&F.color_row[c], F.bptr.p + (c < 4 ? (c << gL.lq) : nL), sizeof(int),
-                                 cudaMemcpyDeviceToHost, s));
-    F.iperm.alloc(n);
-    F.cell.alloc(n);
-    F.lex_of_row.alloc(n);
-    {
-        DBuf<int> len(n);
-        k_after_sort<<<grid_for(n), kT, 0, s>>>(key.p, F.perm.p, n, gL, F.iperm.p, F.cell.p, F.lex_of_row.p, len.p,
-                                                 A->row_ptr);
-        AUX_LAUNCHED(1);
-        F.rp.alloc(n + 1);
-        exclusive_scan(len.p, F.rp.p, n, s);
-    }
-    key.release();
-    F.col.alloc(nnz);
-    F.v.alloc(nnz);
-    k_permute_csr<<<grid_for((long)n * 32), kT, 0, s>>>(A->row_ptr, A->col_idx, A->values, F.perm.p, F.iperm.p, n,
-                                                        F.rp.p, F.col.p, F.v.p);
-    AUX_LAUNCHED(1);
-
-    // ---- finest blocks: singularity check, big-block factors (factor_blocks)
     {
         DBuf<unsigned long long> err(1);
         DBuf<int> flag(nL), mb(1);
@@ -851,13 +826,201 @@ void setup_device(aux_hierarchy* h, const aux_csr_view* A, const double* xy, lon
                 AUX_CUDA(cudaStreamSynchronize(s));
             }
         }
-        const unsigned long long e = read1(err.p, s);
-        if (e != ~0ull) throw_aux(AUX_DEFINITENESS_ERROR, "aggregate " + std::to_string(e) + " has a singular block");
+        sing = read1(err.p, s);
         DBuf<int> cflag(1);
         AUX_CUDA(cudaMemsetAsync(cflag.p, 0, sizeof(int), s));
         k_color_check<<<grid_for(n), kT, 0, s>>>(F.rp.p, F.col.p, F.v.p, F.cell.p, n, gL.lq, cflag.p);
         AUX_LAUNCHED(1);
-        F.color_clean = read1(cflag.p, s) == 0;
+        color_flag = read1(cflag.p, s);
+    }
+
+}
+
+// validate_csr (sparse.hpp:101-116), diagonal > 0 and symmetry
+// (hierarchy.hpp:321-325), in the reference's precedence.
+void validate_input(aux_hierarchy* h, const aux_csr_view* A) {
+    cudaStream_t s = h->stream;
+    const aux_setup_opts& o = h->opts;
+    const int n = A->n_rows;
+    const long nnz = A->nnz;
+    {
+        int ends[2] = {0, 0};
+        if (n >= 0) {
+            AUX_CUDA(cudaMemcpyAsync(&ends[0], A->row_ptr, sizeof(int), cudaMemcpyDeviceToHost, s));
+            AUX_CUDA(cudaMemcpyAsync(&ends[1], A->row_ptr + n, sizeof(int), cudaMemcpyDeviceToHost, s));
+            AUX_CUDA(cudaStreamSynchronize(s));
+        }
+        if (ends[0] != 0 || (long)ends[1] != nnz)
+            throw_aux(AUX_STRUCTURE_ERROR, "CSR row_ptr endpoints inconsistent with nnz");
+        DBuf<unsigned long long> err(3);
+        AUX_CUDA(cudaMemsetAsync(err.p, 0xff, 2 * sizeof(unsigned long long), s));
+        if (n > 0) {
+            k_validate<<<grid_for(n), kT, 0, s>>>(A->row_ptr, A->col_idx, n, nnz, A->n_cols, err.p);
+            AUX_LAUNCHED(1);
+        }
+        const unsigned long long e = read1(err.p, s);
+        if (e != ~0ull) {
+            const long r = (long)(e / 4);
+            const int kind = (int)(e % 4);
+            if (kind == 1) throw_aux(AUX_STRUCTURE_ERROR, "CSR row_ptr not nondecreasing at row " + std::to_string(r));
+            if (kind == 2) throw_aux(AUX_STRUCTURE_ERROR, "CSR column index out of range in row " + std::to_string(r));
+            throw_aux(AUX_STRUCTURE_ERROR, "CSR row " + std::to_string(r) + " not sorted by column");
+        }
+        // diagonal > 0 (hierarchy.hpp:321-323)
+        if (n > 0) {
+            k_diag<<<grid_for(n), kT, 0, s>>>(A->row_ptr, A->col_idx, A->values, n, err.p + 1);
+            AUX_LAUNCHED(1);
+        }
+        const unsigned long long d = read1(err.p + 1, s);
+        if (d != ~0ull) throw_aux(AUX_DEFINITENESS_ERROR, "nonpositive diagonal at row " + std::to_string(d));
+        // symmetry (hierarchy.hpp:324-325)
+        DBuf<unsigned long long> sy(2);
+        AUX_CUDA(cudaMemsetAsync(sy.p, 0, 2 * sizeof(unsigned long long), s));
+        if (n > 0) {
+            k_symm<<<grid_for(n), kT, 0, s>>>(A->row_ptr, A->col_idx, A->values, n, sy.p);
+            AUX_LAUNCHED(1);
+        }
+        unsigned long long syh[2];
+        AUX_CUDA(cudaMemcpyAsync(syh, sy.p, sizeof syh, cudaMemcpyDeviceToHost, s));
+        AUX_CUDA(cudaStreamSynchronize(s));
+        double defect, scale;
+        std::memcpy(&defect, &syh[0], 8);
+        std::memcpy(&scale, &syh[1], 8);
+        scale = (1.0 < scale) ? scale : 1.0;
+        if (defect / scale > o.symmetry_tol) throw_aux(AUX_STRUCTURE_ERROR, "matrix is not symmetric to tolerance");
+    }
+}
+
+// bounding_box (auxgrid.hpp:75-91) into h->box; non-finite -> argument_error,
+// degenerate -> geometry_error.
+void bounding_box(aux_hierarchy* h, const double* xy, long n) {
+    cudaStream_t s = h->stream;
+    {
+        DBuf<unsigned long long> bb(4);
+        DBuf<int> bad(1);
+        unsigned long long init[4] = {~0ull, 0ull, ~0ull, 0ull};
+        AUX_CUDA(cudaMemcpyAsync(bb.p, init, sizeof init, cudaMemcpyHostToDevice, s));
+        AUX_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), s));
+        k_bbox<<<grid_for(n, 4), kT, 0, s>>>(xy, n, bb.p, bad.p);
+        AUX_LAUNCHED(1);
+        unsigned long long r[4];
+        int badh = 0;
+        AUX_CUDA(cudaMemcpyAsync(r, bb.p, sizeof r, cudaMemcpyDeviceToHost, s));
+        AUX_CUDA(cudaMemcpyAsync(&badh, bad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+        AUX_CUDA(cudaStreamSynchronize(s));
+        if (badh) throw_aux(AUX_ARGUMENT_ERROR, "bounding_box: non-finite coordinate");
+        auto val = [](unsigned long long k) {
+            const unsigned long long b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+            double d;
+            std::memcpy(&d, &b, 8);
+            return d;
+        };
+        h->box[0] = val(r[0]);
+        h->box[1] = val(r[1]);
+        h->box[2] = val(r[2]);
+        h->box[3] = val(r[3]);
+        if (!(h->box[1] > h->box[0]) || !(h->box[3] > h->box[2]))
+            throw_aux(AUX_GEOMETRY_ERROR, "bounding_box: degenerate point set");
+    }
+}
+
+void setup_device(aux_hierarchy* h, const aux_csr_view* A, const double* xy, long n_points) {
+    cudaStream_t s = h->stream;
+    const aux_setup_opts& o = h->opts;
+    if (A->n_rows != A->n_cols) throw_aux(AUX_SIZE_ERROR, "setup_hierarchy: matrix not square");
+    if (n_points != A->n_rows)
+        throw_aux(AUX_SIZE_ERROR, "setup_hierarchy: coordinate count does not match matrix order");
+    const int n = A->n_rows;
+    const long nnz = A->nnz;
+    h->n = n;
+
+    validate_input(h, A);
+    h->opts.coarsest_size = std::max(o.coarsest_size, 4);
+    const int coarsest_size = h->opts.coarsest_size;
+
+    Finest& F = h->fine;
+    F.n = n;
+    F.nnz = nnz;
+    h->lv.clear();
+    h->lv.emplace_back();
+    h->lv[0].k = 0;
+    h->lv[0].structured = false;
+    h->lv[0].n = n;
+    h->lv[0].nnz = nnz;
+
+    if (n <= coarsest_size) {   // direct-only hierarchy (hierarchy.hpp:339-344)
+        h->direct_only = true;
+        F.rp.alloc(n + 1);
+        F.col.alloc(nnz);
+        F.v.alloc(nnz);
+        AUX_CUDA(cudaMemcpyAsync(F.rp.p, A->row_ptr, sizeof(int) * (n + 1), cudaMemcpyDeviceToDevice, s));
+        AUX_CUDA(cudaMemcpyAsync(F.col.p, A->col_idx, sizeof(int) * nnz, cudaMemcpyDeviceToDevice, s));
+        AUX_CUDA(cudaMemcpyAsync(F.v.p, A->values, sizeof(double) * nnz, cudaMemcpyDeviceToDevice, s));
+        h->nc = n;
+        h->c_lu.alloc((size_t)n * n);
+        h->c_perm.alloc(n);
+        h->c_lex.alloc(n);
+        AUX_CUDA(cudaMemsetAsync(h->c_lu.p, 0, sizeof(double) * n * n, s));
+        k_dense_from_csr<<<grid_for(n), kT, 0, s>>>(F.rp.p, F.col.p, F.v.p, n, h->c_lu.p, h->c_lex.p);
+        AUX_LAUNCHED(1);
+        factor_coarsest(h);
+        return;
+    }
+
+    bounding_box(h, xy, n);
+    int depth = 0;
+    {
+        long cells = 1;
+        while (cells * 4 < n) { cells *= 4; ++depth; }
+        if (depth == 0) depth = 1;
+    }
+    h->depth = depth;
+    h->lv[0].k = depth + 1;
+    const Geo gL = make_geo(depth);
+    const int nL = gL.n;
+
+    // ---- aggregate_finest: keys, stable sort, member pointers
+    DBuf<unsigned> key(n);
+    F.perm.alloc(n);
+    k_cellkey<<<grid_for(n), kT, 0, s>>>(xy, n, h->box[0], h->box[1], h->box[2], h->box[3], gL, key.p);
+    AUX_LAUNCHED(1);
+    radix_sort_pairs(key.p, F.perm.p, n, 2 * depth, s, true);
+    {
+        DBuf<int> cnt(nL);
+        AUX_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(int) * nL, s));
+        k_count<<<grid_for(n), kT, 0, s>>>(key.p, n, cnt.p);
+        AUX_LAUNCHED(1);
+        F.bptr.alloc(nL + 1);
+        exclusive_scan(cnt.p, F.bptr.p, nL, s);
+    }
+    for (int c = 0; c <= 4; ++c)
+        AUX_CUDA(cudaMemcpyAsync(&F.color_row[c], F.bptr.p + (c < 4 ? (c << gL.lq) : nL), sizeof(int),
+                                 cudaMemcpyDeviceToHost, s));
+    F.iperm.alloc(n);
+    F.cell.alloc(n);
+    F.lex_of_row.alloc(n);
+    {
+        DBuf<int> len(n);
+        k_after_sort<<<grid_for(n), kT, 0, s>>>(key.p, F.perm.p, n, gL, F.iperm.p, F.cell.p, F.lex_of_row.p, len.p,
+                                                 A->row_ptr);
+        AUX_LAUNCHED(1);
+        F.rp.alloc(n + 1);
+        exclusive_scan(len.p, F.rp.p, n, s);
+    }
+    key.release();
+    F.col.alloc(nnz);
+    F.v.alloc(nnz);
+    k_permute_csr<<<grid_for((long)n * 32), kT, 0, s>>>(A->row_ptr, A->col_idx, A->values, F.perm.p, F.iperm.p, n,
+                                                        F.rp.p, F.col.p, F.v.p);
+    AUX_LAUNCHED(1);
+
+    {
+        unsigned long long sing = ~0ull;
+        int color_flag = 0;
+        finest_blocks(h, gL, sing, color_flag);
+        if (sing != ~0ull)
+            throw_aux(AUX_DEFINITENESS_ERROR, "aggregate " + std::to_string(sing) + " has a singular block");
+        F.color_clean = color_flag == 0;
     }
 
     // ---- level L operator (assemble_coarse_finest)
@@ -931,6 +1094,11 @@ void setup_device(aux_hierarchy* h, const aux_csr_view* A, const double* xy, lon
         }
     }
 
+    for (size_t l = 1; l < h->lv.size(); ++l) {   // one GPU: every level owns its whole grid
+        const int w = 1 << h->lv[l].k;
+        h->lv[l].own = Rect{0, 0, w, w};
+    }
+
     // ---- coarsest dense LU (hierarchy.hpp:383)
     {
         auxb200::Level& C = h->lv.back();
@@ -945,6 +1113,391 @@ void setup_device(aux_hierarchy* h, const aux_csr_view* A, const double* xy, lon
         factor_coarsest(h);
     }
     AUX_CUDA(cudaStreamSynchronize(s));
+}
+
+
+// ================================================================= multi-GPU setup
+//
+// One part of a distributed hierarchy.  Every part receives the
+// global (replicated) CSR and coordinates, runs the same validation and
+// bounding box, and owns one rectangle of level-L cells (quadtree subtree:
+// P = 2 halves, 4 quadrants, 8 half-quadrants, ...).
+//   finest   the DoFs of its cells as local rows (global aggregation order),
+//            ghost DoFs as extra columns grouped by owner, exchange lists from
+//            a setup-time request/reply; blocks, inverses, Galerkin rows local
+//   levels   global-layout arrays per part; the owned rectangle is computed,
+//            a ring of kRing cells is refreshed from the neighbours; a level
+//            stays distributed while the rectangle is >= 16 cells on each side
+//   agg      the first level below that is gathered on part 0, which builds
+//            the rest of the hierarchy exactly as on one GPU.
+namespace {
+
+void part_grid(int P, int& PX, int& PY) {
+    PX = PY = 1;
+    bool x = true;
+    for (int p = P; p > 1; p >>= 1) {
+        if (p & 1) throw_aux(AUX_ARGUMENT_ERROR, "part count must be a power of two");
+        (x ? PX : PY) *= 2;
+        x = !x;
+    }
+}
+
+double allsum(aux_hierarchy* h, double v) {
+    DBuf<double> d(1);
+    AUX_CUDA(cudaMemcpyAsync(d.p, &v, sizeof v, cudaMemcpyHostToDevice, h->stream));
+    h->dist.comm->allreduce_sum(d.p, 1, h->stream);
+    return read1(d.p, h->stream);
+}
+unsigned long long allmax(aux_hierarchy* h, unsigned long long v) {
+    DBuf<unsigned long long> d(1);
+    AUX_CUDA(cudaMemcpyAsync(d.p, &v, sizeof v, cudaMemcpyHostToDevice, h->stream));
+    h->dist.comm->allreduce_max(d.p, 1, h->stream);
+    return read1(d.p, h->stream);
+}
+
+int bits_for(long v) {
+    int b = 1;
+    while ((1l << b) <= v) ++b;
+    return b;
+}
+
+void exchange_level_values(aux_hierarchy* h, int l, bool gather) {
+    Level& L = h->lv[l];
+    DBuf<double> actd(L.n);
+    k_u8_to_d<<<grid_for(L.n), kT, 0, h->stream>>>(L.active.p, L.n, actd.p);
+    std::vector<double*> v;
+    for (int t = 0; t < 9; ++t) v.push_back(L.val.p + (size_t)t * L.n);
+    v.push_back(actd.p);
+    if (gather) gather_level_to_root(h, l, v, h->stream);
+    else ring_exchange_level(h, l, v, h->stream);
+    k_d_to_u8<<<grid_for(L.n), kT, 0, h->stream>>>(actd.p, L.n, L.active.p);
+    AUX_LAUNCHED(2);
+    AUX_CUDA(cudaStreamSynchronize(h->stream));
+}
+
+}  // namespace
+
+void setup_device_dist(aux_hierarchy* h, const aux_csr_view* A, const double* xy, long n_points) {
+    cudaStream_t s = h->stream;
+    Comm* cm = h->dist.comm;
+    const int P = cm->size, rank = cm->rank;
+    if (A->n_rows != A->n_cols) throw_aux(AUX_SIZE_ERROR, "setup_hierarchy: matrix not square");
+    if (n_points != A->n_rows)
+        throw_aux(AUX_SIZE_ERROR, "setup_hierarchy: coordinate count does not match matrix order");
+    validate_input(h, A);
+    h->opts.coarsest_size = std::max(h->opts.coarsest_size, 4);
+    const int coarsest_size = h->opts.coarsest_size;
+    const int n = A->n_rows;
+    h->n = n;
+    if (n <= coarsest_size) throw_aux(AUX_ARGUMENT_ERROR, "distributed setup needs more DoFs than coarsest_size");
+    bounding_box(h, xy, n);
+    int depth = 0;
+    {
+        long cells = 1;
+        while (cells * 4 < n) { cells *= 4; ++depth; }
+        if (depth == 0) depth = 1;
+    }
+    h->depth = depth;
+    int PX, PY;
+    part_grid(P, PX, PY);
+    h->dist.PX = PX;
+    h->dist.PY = PY;
+    h->dist.px = rank % PX;
+    h->dist.py = rank / PX;
+    const Geo gL = make_geo(depth);
+    const int w = 1 << depth, nL = gL.n;
+    if (w / PX < 16 || w / PY < 16)
+        throw_aux(AUX_ARGUMENT_ERROR, "problem too small for " + std::to_string(P) + " parts (level-L rectangle < 16)");
+    const Rect ownL{h->dist.px * w / PX, h->dist.py * w / PY, (h->dist.px + 1) * w / PX, (h->dist.py + 1) * w / PY};
+
+    // ---- global aggregation (the same keys and stable sort as one GPU)
+    DBuf<unsigned> key(n);
+    DBuf<int> perm(n), iperm(n);
+    k_cellkey<<<grid_for(n), kT, 0, s>>>(xy, n, h->box[0], h->box[1], h->box[2], h->box[3], gL, key.p);
+    AUX_LAUNCHED(1);
+    radix_sort_pairs(key.p, perm.p, n, 2 * depth, s, true);
+    k_inv_perm<<<grid_for(n), kT, 0, s>>>(perm.p, n, iperm.p);
+    AUX_LAUNCHED(1);
+
+    // ---- owned rows (sorted order restricted to the rectangle)
+    int n_own = 0;
+    DBuf<int> l2s, s2l(n);
+    {
+        DBuf<int> flag(n), pos(n + 1);
+        k_own_flag<<<grid_for(n), kT, 0, s>>>(key.p, n, gL, ownL.x0, ownL.y0, ownL.x1, ownL.y1, flag.p);
+        AUX_LAUNCHED(1);
+        exclusive_scan(flag.p, pos.p, n, s);
+        n_own = read1(pos.p + n, s);
+        l2s.alloc(std::max(n_own, 1));
+        k_compact<<<grid_for(n), kT, 0, s>>>(flag.p, pos.p, n, l2s.p);
+        AUX_CUDA(cudaMemsetAsync(s2l.p, 0xff, sizeof(int) * n, s));
+        k_mark_local<<<grid_for(n_own), kT, 0, s>>>(l2s.p, n_own, s2l.p);
+        AUX_LAUNCHED(2);
+    }
+    if (allmax(h, n_own == 0 ? 1ull : 0ull))   // decided together: a lone throw would strand the others
+        throw_aux(AUX_ARGUMENT_ERROR, "a part owns no DoFs (problem too small for the partition)");
+
+    // ---- ghost DoFs: sorted unique, grouped by owner part
+    int ng = 0;
+    DBuf<int> ghosts;
+    std::vector<int> gcount(P, 0);
+    {
+        DBuf<int> cnt(n_own), off(n_own + 1);
+        k_ghost_count<<<grid_for(n_own), kT, 0, s>>>(l2s.p, n_own, perm.p, A->row_ptr, A->col_idx, iperm.p, s2l.p,
+                                                     cnt.p);
+        AUX_LAUNCHED(1);
+        exclusive_scan(cnt.p, off.p, n_own, s);
+        const int m = read1(off.p + n_own, s);
+        if (m > 0) {
+            DBuf<unsigned> gl(m);
+            DBuf<int> dummy(m);
+            k_ghost_emit<<<grid_for(n_own), kT, 0, s>>>(l2s.p, n_own, perm.p, A->row_ptr, A->col_idx, iperm.p,
+                                                        s2l.p, off.p, gl.p);
+            AUX_LAUNCHED(1);
+            radix_sort_pairs(gl.p, dummy.p, m, bits_for(n), s, true);
+            DBuf<int> uf(m), up(m + 1);
+            k_first_of_run<<<grid_for(m), kT, 0, s>>>(gl.p, m, uf.p);
+            AUX_LAUNCHED(1);
+            exclusive_scan(uf.p, up.p, m, s);
+            ng = read1(up.p + m, s);
+            ghosts.alloc(ng);
+            k_compact_u<<<grid_for(m), kT, 0, s>>>(uf.p, up.p, gl.p, m, ghosts.p);
+            DBuf<unsigned> okey(ng);
+            k_owner_key<<<grid_for(ng), kT, 0, s>>>(ghosts.p, ng, key.p, gL, PX, PY, okey.p);
+            AUX_LAUNCHED(2);
+            radix_sort_pairs(okey.p, ghosts.p, ng, bits_for(P), s, false);
+            std::vector<unsigned> ok(ng);
+            AUX_CUDA(cudaMemcpyAsync(ok.data(), okey.p, sizeof(unsigned) * ng, cudaMemcpyDeviceToHost, s));
+            AUX_CUDA(cudaStreamSynchronize(s));
+            for (unsigned o : ok) gcount[o]++;
+            k_ghost_map<<<grid_for(ng), kT, 0, s>>>(ghosts.p, ng, n_own, s2l.p);
+            AUX_LAUNCHED(1);
+        }
+    }
+
+    // ---- local CSR: rows in aggregation order, entries in the caller's order
+    Finest& F = h->fine;
+    F.n = n_own;
+    F.n_ghost = ng;
+    h->dist.gid.alloc(n_own);
+    F.rp.alloc(n_own + 1);
+    {
+        DBuf<int> len(n_own);
+        k_local_len<<<grid_for(n_own), kT, 0, s>>>(l2s.p, n_own, perm.p, A->row_ptr, len.p, h->dist.gid.p);
+        AUX_LAUNCHED(1);
+        exclusive_scan(len.p, F.rp.p, n_own, s);
+    }
+    F.nnz = read1(F.rp.p + n_own, s);
+    F.col.alloc(std::max<long>(F.nnz, 1));
+    F.v.alloc(std::max<long>(F.nnz, 1));
+    k_local_csr<<<grid_for((long)n_own * 32), kT, 0, s>>>(h->dist.gid.p, n_own, A->row_ptr, A->col_idx, A->values,
+                                                          iperm.p, s2l.p, F.rp.p, F.col.p, F.v.p);
+    F.perm.alloc(n_own);
+    AUX_CUDA(cudaMemcpyAsync(F.perm.p, h->dist.gid.p, sizeof(int) * n_own, cudaMemcpyDeviceToDevice, s));
+    F.cell.alloc((size_t)n_own + ng);
+    k_local_cell<<<grid_for((long)n_own + ng), kT, 0, s>>>(l2s.p, n_own, ghosts.p, ng, key.p, F.cell.p);
+    AUX_LAUNCHED(2);
+    {
+        DBuf<int> cnt(nL);
+        AUX_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(int) * nL, s));
+        k_count_i<<<grid_for(n_own), kT, 0, s>>>(F.cell.p, n_own, cnt.p);
+        AUX_LAUNCHED(1);
+        F.bptr.alloc(nL + 1);
+        exclusive_scan(cnt.p, F.bptr.p, nL, s);
+    }
+    for (int c = 0; c <= 4; ++c)
+        AUX_CUDA(cudaMemcpyAsync(&F.color_row[c], F.bptr.p + (c < 4 ? (c << gL.lq) : nL), sizeof(int),
+                                 cudaMemcpyDeviceToHost, s));
+    AUX_CUDA(cudaStreamSynchronize(s));
+
+    // ---- ghost exchange lists: requests to the owners, replies = send lists
+    {
+        F.g_recv_off.assign(P + 1, 0);
+        for (int q = 0; q < P; ++q) F.g_recv_off[q + 1] = F.g_recv_off[q] + gcount[q];
+        DBuf<int> scnt(P), rcnt(P);
+        AUX_CUDA(cudaMemcpyAsync(scnt.p, gcount.data(), sizeof(int) * P, cudaMemcpyHostToDevice, s));
+        std::vector<Msg> sm, rm;
+        for (int q = 0; q < P; ++q) {
+            if (q == rank) continue;
+            sm.push_back({q, scnt.p + q, sizeof(int)});
+            rm.push_back({q, rcnt.p + q, sizeof(int)});
+        }
+        cm->exchange(sm, rm, s);
+        std::vector<int> rc(P, 0);
+        AUX_CUDA(cudaMemcpyAsync(rc.data(), rcnt.p, sizeof(int) * P, cudaMemcpyDeviceToHost, s));
+        AUX_CUDA(cudaStreamSynchronize(s));
+        rc[rank] = 0;
+        F.g_send_off.assign(P + 1, 0);
+        for (int q = 0; q < P; ++q) F.g_send_off[q + 1] = F.g_send_off[q] + rc[q];
+        const int ns = F.g_send_off[P];
+        DBuf<int> req(std::max(ns, 1));
+        sm.clear();
+        rm.clear();
+        for (int q = 0; q < P; ++q) {
+            if (q == rank) continue;
+            if (gcount[q]) sm.push_back({q, ghosts.p + F.g_recv_off[q], sizeof(int) * (size_t)gcount[q]});
+            if (rc[q]) rm.push_back({q, req.p + F.g_send_off[q], sizeof(int) * (size_t)rc[q]});
+        }
+        // parts with nothing to say still take part in the exchange
+        cm->exchange(sm, rm, s);
+        F.g_send_idx.alloc(std::max(ns, 1));
+        F.g_send_buf.alloc(std::max(ns, 1));
+        if (ns) {
+            k_gather_int<<<grid_for(ns), kT, 0, s>>>(req.p, ns, s2l.p, F.g_send_idx.p);
+            AUX_LAUNCHED(1);
+        }
+        F.g_peer.clear();
+        for (int q = 0; q < P; ++q)
+            if (q != rank && (gcount[q] || rc[q])) F.g_peer.push_back(q);
+    }
+
+    // ---- blocks (owned cells only; others have no rows)
+    {
+        unsigned long long sing = ~0ull;
+        int color_flag = 0;
+        finest_blocks(h, gL, sing, color_flag);
+        sing = ~allmax(h, ~sing);
+        if (sing != ~0ull)
+            throw_aux(AUX_DEFINITENESS_ERROR, "aggregate " + std::to_string(sing) + " has a singular block");
+        F.color_clean = allmax(h, (unsigned long long)color_flag) == 0;
+    }
+
+    // ---- level L operator for the owned cells
+    h->lv.clear();
+    h->lv.emplace_back();
+    h->lv[0].k = depth + 1;
+    h->lv[0].structured = false;
+    h->lv[0].n = n;
+    h->lv[0].nnz = A->nnz;
+    h->lv.emplace_back();
+    {
+        Level& L1 = h->lv[1];
+        L1.k = depth;
+        L1.structured = true;
+        L1.n = nL;
+        L1.geo = gL;
+        L1.own = ownL;
+        L1.dist = P > 1;
+        L1.val.alloc((size_t)9 * nL);
+        L1.active.alloc(nL);
+        k_active_from_count<<<grid_for(nL), kT, 0, s>>>(F.bptr.p, nL, L1.active.p);
+        DBuf<int> dcnt(nL);
+        DBuf<double> dmass(nL);
+        DBuf<unsigned long long> tot(1);
+        AUX_CUDA(cudaMemsetAsync(dcnt.p, 0, sizeof(int) * nL, s));
+        AUX_CUDA(cudaMemsetAsync(dmass.p, 0, sizeof(double) * nL, s));
+        AUX_CUDA(cudaMemsetAsync(tot.p, 0, sizeof(unsigned long long), s));
+        const int lump = (h->opts.lump_locality && !h->opts.strict_locality) ? 1 : 0;
+        k_galerkin_L<<<grid_for(nL), kT, 0, s>>>(F.bptr.p, F.rp.p, F.col.p, F.v.p, F.cell.p, gL, lump, L1.val.p,
+                                                   dcnt.p, dmass.p, tot.p);
+        AUX_LAUNCHED(2);
+        const double dropped = allsum(h, (double)read1(tot.p, s));
+        std::memset(&h->loc, 0, sizeof h->loc);
+        if (dropped > 0) {
+            DBuf<double> m(1);
+            k_locality_sum<<<1, 32, 0, s>>>(dcnt.p, dmass.p, gL, m.p);
+            AUX_LAUNCHED(1);
+            const double mass = allsum(h, read1(m.p, s));
+            if (lump) { h->loc.lumped = (int64_t)dropped; h->loc.lumped_mass = mass; }
+            else { h->loc.dropped = (int64_t)dropped; h->loc.dropped_mass = mass; }
+        }
+        if (h->opts.strict_locality && h->loc.dropped > 0)
+            throw_aux(AUX_STRUCTURE_ERROR, "strict locality: " + std::to_string(h->loc.dropped) +
+                                               " couplings fall outside the 9-point stencil");
+    }
+    if (h->lv[1].dist) exchange_level_values(h, 1, false);
+    h->dist.agg = P > 1 ? 1 << 30 : 1;   // one part: every level is "on part 0"
+
+    // ---- structured coarsening: distributed while the rectangle allows tiles
+    DBuf<int> ovf(1);
+    AUX_CUDA(cudaMemsetAsync(ovf.p, 0, sizeof(int), s));
+    while (h->lv.back().k > 0 && h->lv.back().n > coarsest_size) {
+        if ((int)h->lv.size() >= AUX_MAX_LEVELS) throw_aux(AUX_INTERNAL_ERROR, "too many levels");
+        const int k = h->lv.back().k;
+        h->lv.emplace_back();
+        Level& cur = h->lv[h->lv.size() - 2];
+        Level& nx = h->lv.back();
+        const int li = (int)h->lv.size() - 1;
+        nx.k = k - 1;
+        nx.structured = true;
+        nx.n = 1 << (2 * (k - 1));
+        nx.geo = make_geo(k - 1);
+        const int wn = 1 << (k - 1);
+        if (cur.dist) {
+            nx.own = Rect{cur.own.x0 / 2, cur.own.y0 / 2, cur.own.x1 / 2, cur.own.y1 / 2};
+            nx.dist = nx.own.w() >= 16 && nx.own.h() >= 16;
+        } else {
+            nx.own = Rect{0, 0, wn, wn};
+            nx.dist = false;
+        }
+        const bool compute = cur.dist || rank == 0;
+        if (compute) {
+            nx.val.alloc((size_t)9 * nx.n);
+            nx.active.alloc(nx.n);
+            k_coarsen<<<grid_for(nx.n), kT, 0, s>>>(cur.geo, cur.val.p, cur.active.p, nx.geo, nx.val.p, nx.active.p,
+                                                   ovf.p);
+            AUX_LAUNCHED(1);
+        }
+        if (nx.dist) {
+            exchange_level_values(h, li, false);
+        } else if (cur.dist) {   // agglomeration level: gather on part 0
+            h->dist.agg = li;
+            nx.own = Rect{0, 0, wn, wn};
+            exchange_level_values(h, li, true);
+        }
+    }
+    if (h->lv.back().dist) {   // still distributed at the coarsest level: gather it
+        Level& C = h->lv.back();
+        const int wc = 1 << C.k;
+        h->dist.agg = (int)h->lv.size() - 1;
+        C.dist = false;
+        C.own = Rect{0, 0, wc, wc};
+        exchange_level_values(h, h->dist.agg, true);
+    }
+    if (allmax(h, (unsigned long long)read1(ovf.p, s)))
+        throw_aux(AUX_STRUCTURE_ERROR, "4-child coarsening escaped the 9-point stencil");
+
+    // ---- per-level nnz and zero-diagonal records (global values)
+    {
+        DBuf<unsigned long long> cnt(1), zd(1);
+        for (size_t l = 1; l < h->lv.size(); ++l) {
+            Level& L = h->lv[l];
+            unsigned long long c = 0, z = ~0ull;
+            if (L.dist || rank == 0) {
+                const Rect r = L.dist ? L.own : Rect{0, 0, 1 << L.k, 1 << L.k};
+                AUX_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long), s));
+                AUX_CUDA(cudaMemsetAsync(zd.p, 0xff, sizeof(unsigned long long), s));
+                k_level_nnz_rect<<<grid_for(r.cells(), 4), kT, 0, s>>>(L.geo, L.active.p, r.x0, r.y0, r.w(),
+                                                                      r.cells(), cnt.p);
+                k_zero_diag_rect<<<grid_for(r.cells(), 4), kT, 0, s>>>(L.geo, L.val.p, L.active.p, r.x0, r.y0,
+                                                                      r.w(), r.cells(), zd.p);
+                AUX_LAUNCHED(2);
+                c = read1(cnt.p, s);
+                z = read1(zd.p, s);
+            }
+            L.nnz = (long)allsum(h, (double)c);
+            z = ~allmax(h, ~z);
+            L.zero_diag_lex = z == ~0ull ? -1 : (int)(z % (unsigned long long)L.n);
+        }
+    }
+
+    // ---- coarsest dense LU on part 0
+    {
+        Level& C = h->lv.back();
+        const int nc = C.n;
+        h->nc = nc;
+        if (rank == 0) {
+            h->c_lu.alloc((size_t)nc * nc);
+            h->c_perm.alloc(nc);
+            h->c_lex.alloc(nc);
+            AUX_CUDA(cudaMemsetAsync(h->c_lu.p, 0, sizeof(double) * nc * nc, s));
+            k_dense_from_level<<<grid_for(nc), kT, 0, s>>>(C.geo, C.val.p, C.active.p, h->c_lu.p, h->c_lex.p);
+            AUX_LAUNCHED(1);
+            factor_coarsest(h);
+        }
+    }
+    AUX_CUDA(cudaStreamSynchronize(s));
+    cm->barrier(s);
 }
 
 }  // namespace auxb200

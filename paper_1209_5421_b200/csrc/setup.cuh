@@ -10,6 +10,14 @@ void alloc_solve_levels(aux_hierarchy* h, int n_inner);
 // Device solve; b and u are device pointers in the caller's DoF order.
 void solve_device(aux_hierarchy* h, const double* b, long n_b, const aux_cycle_opts* o, aux_solve_result* res,
                   double* u_dev);
+// Multi-GPU setup of one part (h->dist.comm set): A and xy are the global
+// (replicated) inputs in device memory.
+void setup_device_dist(aux_hierarchy* h, const aux_csr_view* A, const double* xy, long n_points);
+// Ring exchange of a distributed level / gather of part rectangles on part 0.
+void ring_exchange_level(aux_hierarchy* h, int m, const std::vector<double*>& vecs, cudaStream_t s);
+void gather_level_to_root(aux_hierarchy* h, int t, const std::vector<double*>& vecs, cudaStream_t s);
+// u_local[i] = u_global[gid[i]] for the part's rows.
+void gather_owned(aux_hierarchy* h, const double* u_global, double* u_local);
 // Exports (reference layout, host arrays).
 void export_level(const aux_hierarchy* h, int level, aux_level_export* x);
 void level_info(const aux_hierarchy* h, int level, aux_level_info* o);

@@ -21,6 +21,7 @@
 #include "fused.cuh"
 #include "setup.cuh"
 #include "tiles.cuh"
+#include "comm.cuh"
 
 namespace auxb200 {
 
@@ -140,13 +141,32 @@ __global__ void __launch_bounds__(kRedThreads) k_spmv9(Geo g, const double* __re
 //   mode 0: s0 = p.w          (next MGS projection)
 //   mode 1: s0 = p.ap, s1 = r.p (energy and alpha numerator)
 // beta is read before the loop; the finaliser may overwrite it.
-__global__ void __launch_bounds__(kRedThreads) k_mgs(long n, double* __restrict__ p, double* __restrict__ ap,
+// The cells a vector kernel visits: [0, n) flat, or (w > 0) the owned
+// rectangle of a distributed structured level in its global layout.
+struct Span {
+    long n;
+    Geo g;
+    int x0, y0, w;
+};
+__device__ __forceinline__ long span_idx(const Span& sp, long j) {
+    if (sp.w == 0) return j;
+    const int t1 = sp.x0 + (int)(j % sp.w), t2 = sp.y0 + (int)(j / sp.w);
+    return ((((t2 & 1) << 1) | (t1 & 1)) << sp.g.lq) + ((t2 >> 1) << sp.g.lh) + (t1 >> 1);
+}
+inline Span flat_span(long n) {
+    Span sp{};
+    sp.n = n;
+    return sp;
+}
+
+__global__ void __launch_bounds__(kRedThreads) k_mgs(Span sp, double* __restrict__ p, double* __restrict__ ap,
                                                     const double* __restrict__ pj, const double* __restrict__ apj,
                                                     const double* __restrict__ w, const double* __restrict__ r,
                                                     int mode, const double* sc, RedState rs, Fin fin) {
     const double beta = sc[1];
     double v[2] = {0.0, 0.0};
-    GSTRIDE(i, n) {
+    GSTRIDE(j, sp.n) {
+        const long i = span_idx(sp, j);
         const double pi = __dadd_rn(p[i], __dmul_rn(beta, pj[i]));
         const double api = __dadd_rn(ap[i], __dmul_rn(beta, apj[i]));
         p[i] = pi;
@@ -631,9 +651,10 @@ __global__ void k_csr_prolong(const int* __restrict__ cell, long n, double* __re
 struct PList {
     const double* p[8];
 };
-__global__ void k_pcg_u(long n, PList pl, const double* __restrict__ sc, int ni, double* __restrict__ u) {
+__global__ void k_pcg_u(Span sp, PList pl, const double* __restrict__ sc, int ni, double* __restrict__ u) {
     const int nval = (int)sc[3 + 2 * ni];
-    GSTRIDE(i, n) {
+    GSTRIDE(j, sp.n) {
+        const long i = span_idx(sp, j);
         double e = 0.0;
         for (int k = 0; k < nval; ++k) e = __dadd_rn(e, __dmul_rn(sc[3 + ni + k], pl.p[k][i]));
         u[i] = e;
@@ -813,12 +834,12 @@ void pcg_level(Ctx& c, int m) {
         } else {
             apply_spmv(c, m, P.p[i].p, P.ap[i].p, 1, nullptr, P.ap[0].p, Fin{2, sc, sc + 3, nullptr});
             for (int j = 1; j < i; ++j) {
-                k_mgs<<<red_blocks(n), kRedThreads, 0, c.s>>>(n, P.p[i].p, P.ap[i].p, P.p[j - 1].p, P.ap[j - 1].p,
+                k_mgs<<<red_blocks(n), kRedThreads, 0, c.s>>>(flat_span(n), P.p[i].p, P.ap[i].p, P.p[j - 1].p, P.ap[j - 1].p,
                                                              P.ap[j].p, nullptr, 0, sc, c.rs,
                                                              Fin{2, sc, sc + 3 + j, nullptr});
                 AUX_LAUNCHED(1);
             }
-            k_mgs<<<red_blocks(n), kRedThreads, 0, c.s>>>(n, P.p[i].p, P.ap[i].p, P.p[i - 1].p, P.ap[i - 1].p,
+            k_mgs<<<red_blocks(n), kRedThreads, 0, c.s>>>(flat_span(n), P.p[i].p, P.ap[i].p, P.p[i - 1].p, P.ap[i - 1].p,
                                                          nullptr, P.r.p, 1, sc, c.rs, Fin{1, sc, nullptr, sc + 3 + i});
             AUX_LAUNCHED(1);
         }
@@ -829,11 +850,178 @@ void pcg_level(Ctx& c, int m) {
     }
 }
 
+// ---- multi-GPU plumbing; no-ops on one GPU -------------------
+
+// Inner products on a distributed level: the kernel stores its raw block-tree
+// sums (Fin op 5/6), the parts all-reduce them (NCCL / in part order) and a
+// one-thread kernel applies the real finaliser, so every part holds the same
+// alpha, beta and breakdown state.
+__global__ void k_fin(const double* sum, Fin fin) { finalize(fin, sum); }
+
+struct Route {
+    Fin launch, real;
+    int nv;
+    bool dist;
+};
+Route route(Ctx& c, bool dist_level, Fin real) {
+    const int nv = real.op == 1 ? 2 : 1;
+    if (!dist_level) return Route{real, real, nv, false};
+    Fin f{nv == 2 ? 6 : 5, real.sc, nullptr, c.h->dist.dsum.p};
+    return Route{f, real, nv, true};
+}
+void routed(Ctx& c, const Route& r) {
+    if (!r.dist) return;
+    c.h->dist.comm->allreduce_sum(c.h->dist.dsum.p, r.nv, c.s);
+    k_fin<<<1, 1, 0, c.s>>>(c.h->dist.dsum.p, r.real);
+    AUX_LAUNCHED(1);
+}
+
+struct VecList {
+    double* p[12];
+};
+// copy a box of cells of nv vectors between a level's global-layout arrays and
+// a packed buffer (dir 0: pack, 1: unpack)
+__global__ void k_box(Geo g, int x0, int y0, int bw, int bh, VecList v, int nv, double* buf, int dir) {
+    const long cells = (long)bw * bh;
+    GSTRIDE(i, cells * nv) {
+        const int k = (int)(i / cells);
+        const long j = i - (long)k * cells;
+        const int t1 = x0 + (int)(j % bw), t2 = y0 + (int)(j / bw);
+        const long gi = ((((t2 & 1) << 1) | (t1 & 1)) << g.lq) + ((t2 >> 1) << g.lh) + (t1 >> 1);
+        if (dir == 0) buf[i] = v.p[k][gi];
+        else v.p[k][gi] = buf[i];
+    }
+}
+
+Rect part_rect_of(const aux_hierarchy* h, int level, int part) {
+    const int w = 1 << h->lv[level].geo.k;
+    const int qx = part % h->dist.PX, qy = part / h->dist.PX;
+    return Rect{qx * w / h->dist.PX, qy * w / h->dist.PY, (qx + 1) * w / h->dist.PX, (qy + 1) * w / h->dist.PY};
+}
+
+// Refresh the kRing-cell ring of a distributed level m from the neighbours'
+// owned cells, for the listed vectors.
+void ring_exchange_v(aux_hierarchy* h, int m, const std::vector<double*>& vecs, cudaStream_t stream) {
+    Level& L = h->lv[m];
+    if (!L.dist) return;
+    Comm* cm = h->dist.comm;
+    VecList vl{};
+    int nv = 0;
+    for (double* v : vecs) vl.p[nv++] = v;
+    struct { cudaStream_t s; } c{stream};
+    const Rect me = L.own;
+    struct Box { int peer; Rect r; size_t off; };
+    std::vector<Box> snd, rcv;
+    size_t off = 0;
+    for (int q = 0; q < cm->size; ++q) {
+        if (q == cm->rank) continue;
+        const Rect o = part_rect_of(h, m, q);
+        const Rect sb = intersect(me, dilate(o, kRing));
+        if (!sb.empty()) { snd.push_back({q, sb, off}); off += (size_t)sb.cells() * nv; }
+    }
+    for (int q = 0; q < cm->size; ++q) {
+        if (q == cm->rank) continue;
+        const Rect o = part_rect_of(h, m, q);
+        const Rect rb = intersect(o, dilate(me, kRing));
+        if (!rb.empty()) { rcv.push_back({q, rb, off}); off += (size_t)rb.cells() * nv; }
+    }
+    if (L.xbuf.n < off) {
+        AUX_CUDA(cudaStreamSynchronize(c.s));
+        L.xbuf.alloc(off);
+    }
+    std::vector<Msg> sm, rm;
+    for (const Box& b : snd) {
+        k_box<<<blocks_for(b.r.cells() * nv), 256, 0, c.s>>>(L.geo, b.r.x0, b.r.y0, b.r.w(), b.r.h(), vl, nv,
+                                                            L.xbuf.p + b.off, 0);
+        AUX_LAUNCHED(1);
+        sm.push_back({b.peer, L.xbuf.p + b.off, sizeof(double) * (size_t)b.r.cells() * nv});
+    }
+    for (const Box& b : rcv) rm.push_back({b.peer, L.xbuf.p + b.off, sizeof(double) * (size_t)b.r.cells() * nv});
+    cm->exchange(sm, rm, c.s);
+    for (const Box& b : rcv) {
+        k_box<<<blocks_for(b.r.cells() * nv), 256, 0, c.s>>>(L.geo, b.r.x0, b.r.y0, b.r.w(), b.r.h(), vl, nv,
+                                                            L.xbuf.p + b.off, 1);
+        AUX_LAUNCHED(1);
+    }
+}
+void ring_exchange(Ctx& c, int m, std::initializer_list<double*> vecs) {
+    if (c.h->lv[m].dist) ring_exchange_v(c.h, m, std::vector<double*>(vecs), c.s);
+}
+
+// Gather every part's rectangle of level t (listed vectors) into part 0's arrays.
+void gather_root_v(aux_hierarchy* h, int t, const std::vector<double*>& vecs, cudaStream_t s) {
+    Comm* cm = h->dist.comm;
+    Level& T = h->lv[t];
+    VecList vl{};
+    int nv = 0;
+    for (double* v : vecs) vl.p[nv++] = v;
+    const size_t need = (size_t)nv * T.n;
+    if (T.xbuf.n < need) {
+        AUX_CUDA(cudaStreamSynchronize(s));
+        T.xbuf.alloc(need);
+    }
+    std::vector<Msg> sm, rm;
+    std::vector<std::pair<size_t, Rect>> boxes;
+    size_t off = 0;
+    if (cm->rank == 0) {
+        for (int q = 1; q < cm->size; ++q) {
+            const Rect r = part_rect_of(h, t, q);
+            rm.push_back({q, T.xbuf.p + off, sizeof(double) * (size_t)r.cells() * nv});
+            boxes.push_back({off, r});
+            off += (size_t)r.cells() * nv;
+        }
+    } else {
+        const Rect r = part_rect_of(h, t, cm->rank);
+        k_box<<<blocks_for(r.cells() * nv), 256, 0, s>>>(T.geo, r.x0, r.y0, r.w(), r.h(), vl, nv, T.xbuf.p, 0);
+        AUX_LAUNCHED(1);
+        sm.push_back({0, T.xbuf.p, sizeof(double) * (size_t)r.cells() * nv});
+    }
+    cm->exchange(sm, rm, s);
+    for (auto& b : boxes) {
+        k_box<<<blocks_for(b.second.cells() * nv), 256, 0, s>>>(T.geo, b.second.x0, b.second.y0, b.second.w(),
+                                                                b.second.h(), vl, nv, T.xbuf.p + b.first, 1);
+        AUX_LAUNCHED(1);
+    }
+}
+
+void pcg_tiles(Ctx& c, int m);
+
+// Agglomeration: the child level t = dist.agg and everything
+// below live on part 0.  Gather the restricted residual of every part's
+// rectangle, run nonlinear_pcg(t) there, broadcast its iterate.
+void agglomerated_pcg(Ctx& c, int t) {
+    aux_hierarchy* h = c.h;
+    Comm* cm = h->dist.comm;
+    Level& T = h->lv[t];
+    const int ni = c.o.n_inner;
+    gather_root_v(h, t, {T.pcg.r.p}, c.s);
+    std::vector<Msg> sm, rm;
+    if (cm->rank == 0) {
+        pcg_tiles(c, t);   // levels >= t are not distributed: plain single-GPU path on part 0
+        if (t != h->fused_m0) {
+            PList pl{};
+            for (int k = 0; k < ni; ++k) pl.p[k] = T.pcg.p[k].p;
+            k_pcg_u<<<blocks_for(T.n), 256, 0, c.s>>>(flat_span(T.n), pl, T.pcg.sc.p, ni, T.pcg.u.p);
+            AUX_LAUNCHED(1);
+        }
+    }
+    sm.clear();
+    rm.clear();
+    if (cm->rank == 0) {
+        for (int q = 1; q < cm->size; ++q) sm.push_back({q, T.pcg.u.p, sizeof(double) * (size_t)T.n});
+    } else {
+        rm.push_back({0, T.pcg.u.p, sizeof(double) * (size_t)T.n});
+    }
+    cm->exchange(sm, rm, c.s);
+}
+
 // nonlinear_pcg on level m >= 1 through the overlapped-tile kernels
 // (tiles.cu): per step one k_tile_down (pending residual update, pre-smoothing,
 // restriction), the child's PCG, one k_tile_up (prolongation, post-smoothing,
 // A z and the step's inner products), then the A-orthogonalisation.  The
 // iterate is never formed: the parent's k_tile_up sums alpha_k p_k on the fly.
+// On a distributed level the tiles cover the part's rectangle and the rings
+// are refreshed after every kernel that writes a vector a neighbour reads.
 void pcg_tiles(Ctx& c, int m) {
     aux_hierarchy* h = c.h;
     if (m == h->fused_m0) {
@@ -844,17 +1032,24 @@ void pcg_tiles(Ctx& c, int m) {
     Level& C = h->lv[m + 1];
     PcgBufs& P = L.pcg;
     const int ni = c.o.n_inner;
-    const long n = L.n;
     double* sc = P.sc.p;
     double* R[2] = {P.r.p, P.r2.p};
-    const int w = 1 << L.geo.k;
-    const int tx = w / tile_edge(w);
-    const bool child_fused = (m + 1 == h->fused_m0);
+    const Rect own = L.own;
+    const int T = tile_edge(std::min(own.w(), own.h()));
+    const int tx = own.w() / T, ntiles = tx * (own.h() / T);
+    const bool child_agg = L.dist && (m + 1 == h->dist.agg);
+    const bool child_explicit = (m + 1 == h->fused_m0) || child_agg;
+    Span sp = flat_span(L.n);
+    if (L.dist) sp = Span{own.cells(), L.geo, own.x0, own.y0, own.w()};
+    const int nb = red_blocks(sp.n);
     for (int i = 0; i < ni; ++i) {
         TileDown d{};
         d.g = L.geo;
         d.gc = C.geo;
+        d.ox = own.x0;
+        d.oy = own.y0;
         d.tiles_x = tx;
+        d.tiles_x_edge = T;
         d.val = L.val.p;
         d.r_in = i == 0 ? R[0] : R[(i - 1) & 1];
         d.ap_prev = i == 0 ? nullptr : P.ap[i - 1].p;
@@ -862,19 +1057,31 @@ void pcg_tiles(Ctx& c, int m) {
         d.r_out = i == 0 ? nullptr : R[i & 1];
         d.u_pre = P.upre.p;
         d.rc = C.pcg.r.p;
-        d.sc_child = child_fused ? nullptr : C.pcg.sc.p;
+        d.sc_child = (m + 1 == h->fused_m0) ? nullptr : C.pcg.sc.p;
         d.child_nval = sc_nval(ni);
-        launch_tile_down(d, c.o.pre_sweeps, c.s);
-        pcg_tiles(c, m + 1);
+        launch_tile_down(d, ntiles, c.o.pre_sweeps, c.s);
+        if (L.dist) {
+            if (i == 0) ring_exchange(c, m, {P.upre.p});
+            else ring_exchange(c, m, {P.upre.p, R[i & 1]});
+        }
+        if (child_agg) {
+            agglomerated_pcg(c, m + 1);
+        } else {
+            ring_exchange(c, m + 1, {C.pcg.r.p});
+            pcg_tiles(c, m + 1);
+        }
         TileUp u{};
         u.g = L.geo;
         u.gc = C.geo;
+        u.ox = own.x0;
+        u.oy = own.y0;
         u.tiles_x = tx;
+        u.tiles_x_edge = T;
         u.val = L.val.p;
         u.act = L.active.p;
         u.f = R[i & 1];
         u.u_pre = P.upre.p;
-        u.ec = child_fused ? C.pcg.u.p : nullptr;
+        u.ec = child_explicit ? C.pcg.u.p : nullptr;
         for (int k = 0; k < ni; ++k) u.cp[k] = C.pcg.p[k].p;
         u.sc_c = C.pcg.sc.p;
         u.c_ni = ni;
@@ -882,21 +1089,25 @@ void pcg_tiles(Ctx& c, int m) {
         u.az = P.ap[i].p;
         u.ap0 = P.ap[0].p;
         u.mode = i == 0 ? 0 : 1;
-        const Fin fin = i == 0 ? Fin{1, sc, nullptr, sc + 3, sc + sc_alpha(ni, 0), sc + sc_nval(ni), 0}
-                               : Fin{2, sc, sc + 3, nullptr};
-        launch_tile_up(u, c.o.post_sweeps, c.rs, fin, c.s);
+        const Route ru = route(c, L.dist, i == 0 ? Fin{1, sc, nullptr, sc + 3, sc + sc_alpha(ni, 0), sc + sc_nval(ni), 0}
+                                                 : Fin{2, sc, sc + 3, nullptr});
+        launch_tile_up(u, ntiles, c.o.post_sweeps, c.rs, ru.launch, c.s);
+        routed(c, ru);
         if (i > 0) {
             for (int j = 1; j < i; ++j) {
-                k_mgs<<<red_blocks(n), kRedThreads, 0, c.s>>>(n, P.p[i].p, P.ap[i].p, P.p[j - 1].p, P.ap[j - 1].p,
-                                                             P.ap[j].p, nullptr, 0, sc, c.rs,
-                                                             Fin{2, sc, sc + 3 + j, nullptr});
+                const Route rj = route(c, L.dist, Fin{2, sc, sc + 3 + j, nullptr});
+                k_mgs<<<nb, kRedThreads, 0, c.s>>>(sp, P.p[i].p, P.ap[i].p, P.p[j - 1].p, P.ap[j - 1].p, P.ap[j].p,
+                                                   nullptr, 0, sc, c.rs, rj.launch);
                 AUX_LAUNCHED(1);
+                routed(c, rj);
             }
-            k_mgs<<<red_blocks(n), kRedThreads, 0, c.s>>>(
-                n, P.p[i].p, P.ap[i].p, P.p[i - 1].p, P.ap[i - 1].p, nullptr, R[i & 1], 1, sc, c.rs,
-                Fin{1, sc, nullptr, sc + 3 + i, sc + sc_alpha(ni, i), sc + sc_nval(ni), i});
+            const Route rf = route(c, L.dist, Fin{1, sc, nullptr, sc + 3 + i, sc + sc_alpha(ni, i), sc + sc_nval(ni), i});
+            k_mgs<<<nb, kRedThreads, 0, c.s>>>(sp, P.p[i].p, P.ap[i].p, P.p[i - 1].p, P.ap[i - 1].p, nullptr,
+                                               R[i & 1], 1, sc, c.rs, rf.launch);
             AUX_LAUNCHED(1);
+            routed(c, rf);
         }
+        ring_exchange(c, m, {P.p[i].p, P.ap[i].p});
     }
 }
 
@@ -906,14 +1117,38 @@ struct ColorBytes {
     double b[4];
 };
 
+// Multi-GPU: refresh the ghost DoFs x[n .. n+n_ghost) of a finest vector from
+// their owners (grouped by owner, so each message lands contiguously).
+bool finest_dist(const aux_hierarchy* h) { return h->dist.comm && h->dist.comm->size > 1; }
+void ghost_exchange(Ctx& c, double* x) {
+    aux_hierarchy* h = c.h;
+    if (!finest_dist(h)) return;
+    Finest& F = h->fine;
+    const int P = h->dist.comm->size;
+    const int ns = F.g_send_off[P];
+    if (ns) {
+        k_gather<<<blocks_for(ns), 256, 0, c.s>>>(ns, F.g_send_idx.p, x, F.g_send_buf.p);
+        AUX_LAUNCHED(1);
+    }
+    std::vector<Msg> sm, rm;
+    for (int q : F.g_peer) {
+        const int so = F.g_send_off[q], sn = F.g_send_off[q + 1] - so;
+        const int ro = F.g_recv_off[q], rn = F.g_recv_off[q + 1] - ro;
+        if (sn) sm.push_back({q, F.g_send_buf.p + so, sizeof(double) * (size_t)sn});
+        if (rn) rm.push_back({q, x + F.n + ro, sizeof(double) * (size_t)rn});
+    }
+    h->dist.comm->exchange(sm, rm, c.s);
+}
+
 void finest_bgs_pass(Ctx& c, int color, const double* f, double* u, bool zero, double* snap) {
     aux_hierarchy* h = c.h;
     Finest& F = h->fine;
     const Geo& gL = h->lv[1].geo;
     const int g0 = color << gL.lq, g1 = (color + 1) << gL.lq;
     const double* xin = u;
+    if (!zero) ghost_exchange(c, u);
     if (!F.color_clean && !zero) {
-        AUX_CUDA(cudaMemcpyAsync(snap, u, sizeof(double) * F.n, cudaMemcpyDeviceToDevice, c.s));
+        AUX_CUDA(cudaMemcpyAsync(snap, u, sizeof(double) * ((size_t)F.n + F.n_ghost), cudaMemcpyDeviceToDevice, c.s));
         xin = snap;
     }
     prof_begin(c, 0);
@@ -993,6 +1228,7 @@ void finest_cycle(Ctx& c, const double* f, double* u, double* snap) {
     Level& C = h->lv[1];
     for (int sw = 0; sw < c.o.pre_sweeps; ++sw)
         for (int col = 0; col < 4; ++col) finest_bgs_pass(c, col, f, u, sw == 0 && col == 0, snap);
+    ghost_exchange(c, u);
     prof_begin(c, 2);
     k_rows<<<blocks_for(F.n), 256, 0, c.s>>>(F.rp.p, F.col.p, F.v.p, f, u, F.scratch.p, 0, F.n, 1);
     k_restrict_cells<<<blocks_for(C.n), 256, 0, c.s>>>(F.bptr.p, C.n, F.scratch.p, C.pcg.r.p, C.pcg.sc.p,
@@ -1021,17 +1257,28 @@ void coarse_root(Ctx& c) {
         pcg_level(c, 1);
         return;
     }
+    Level& L = h->lv[1];
+    if (L.dist && h->dist.agg == 1) {   // level 1 itself gathered (tiny distributed problems)
+        agglomerated_pcg(c, 1);
+        return;
+    }
+    ring_exchange(c, 1, {L.pcg.r.p});
     pcg_tiles(c, 1);
     if (h->fused_m0 != 1) {
-        Level& L = h->lv[1];
         PList pl{};
         for (int k = 0; k < c.o.n_inner; ++k) pl.p[k] = L.pcg.p[k].p;
-        k_pcg_u<<<blocks_for(L.n), 256, 0, c.s>>>(L.n, pl, L.pcg.sc.p, c.o.n_inner, L.pcg.u.p);
+        Span sp = flat_span(L.n);
+        if (L.dist) sp = Span{L.own.cells(), L.geo, L.own.x0, L.own.y0, L.own.w()};
+        k_pcg_u<<<blocks_for(sp.n), 256, 0, c.s>>>(sp, pl, L.pcg.sc.p, c.o.n_inner, L.pcg.u.p);
         AUX_LAUNCHED(1);
     }
 }
 
 void build_graph(aux_hierarchy* h, const aux_cycle_opts& o, RedState rs) {
+    if (h->dist.comm) {   // multi-GPU: exchanges synchronise the parts from the host; no capture
+        h->graph_valid = false;
+        return;
+    }
     if (h->graph_valid && std::memcmp(&h->graph_opts, &o, sizeof o) == 0) return;
     if (h->graph) {
         cudaGraphExecDestroy(h->graph);
@@ -1062,7 +1309,8 @@ void setup_fused(aux_hierarchy* h, const aux_cycle_opts& o) {
     std::memset(&fa, 0, sizeof fa);
     if (!h->direct_only && cap > 0 && o.n_inner <= kFusedMaxInner) {
         // the largest tail of levels whose data fits in one CTA's shared memory
-        for (int l = 1; l < (int)h->lv.size(); ++l)
+        // (multi-GPU: only among the levels gathered on part 0)
+        for (int l = h->dist.comm ? std::max(1, h->dist.agg) : 1; l < (int)h->lv.size(); ++l)
             if (h->lv[l].n <= cap && fused_layout(h, l, o.n_inner, &fa) > 0) { m0 = l; break; }
     }
     if (m0 != h->fused_m0) h->graph_valid = false;
@@ -1071,10 +1319,14 @@ void setup_fused(aux_hierarchy* h, const aux_cycle_opts& o) {
     bool tiles = h->gpu.tile_kernels != 0 && m0 < (int)h->lv.size() && o.n_inner <= kFusedMaxInner;
     long max_tiles = 0;
     for (int l = 1; tiles && l < m0; ++l) {
-        const int w = 1 << h->lv[l].geo.k;
+        const Rect& r = h->lv[l].own;
+        const int w = std::min(r.w(), r.h());
         if (!tiles_supported(w, o.pre_sweeps, o.post_sweeps)) tiles = false;
-        else max_tiles = std::max<long>(max_tiles, tile_count(w));
+        else max_tiles = std::max<long>(max_tiles, (long)(r.w() / tile_edge(w)) * (r.h() / tile_edge(w)));
     }
+    if (h->dist.comm && !tiles)
+        throw_aux(AUX_ARGUMENT_ERROR, "distributed solve needs the tile kernels (1 or 2 sweeps, tile_kernels=1) "
+                                      "and a single-CTA tier on part 0");
     if (tiles != h->tiles) h->graph_valid = false;
     h->tiles = tiles;
     if (tiles && (size_t)(2 * max_tiles) > h->red_partials.n) {   // grid_reduce partials, 2 per tile
@@ -1121,6 +1373,19 @@ void setup_fused(aux_hierarchy* h, const aux_cycle_opts& o) {
 
 }  // namespace
 
+void gather_owned(aux_hierarchy* h, const double* u_global, double* u_local) {
+    const long m = h->fine.n;
+    k_gather<<<blocks_for(m), 256, 0, h->stream>>>(m, h->dist.gid.p, u_global, u_local);
+    AUX_LAUNCHED(1);
+}
+
+void ring_exchange_level(aux_hierarchy* h, int m, const std::vector<double*>& vecs, cudaStream_t s) {
+    ring_exchange_v(h, m, vecs, s);
+}
+void gather_level_to_root(aux_hierarchy* h, int t, const std::vector<double*>& vecs, cudaStream_t s) {
+    gather_root_v(h, t, vecs, s);
+}
+
 void solve_device(aux_hierarchy* h, const double* b, long n_b, const aux_cycle_opts* o, aux_solve_result* res,
                   double* u_out) {
     if (o->n_inner < 1 || o->pre_sweeps < 1 || o->post_sweeps < 1 || o->max_outer < 1)
@@ -1132,7 +1397,10 @@ void solve_device(aux_hierarchy* h, const double* b, long n_b, const aux_cycle_o
     const auto t0 = std::chrono::steady_clock::now();
     cudaStream_t s = h->stream;
     Finest& F = h->fine;
-    const long n = h->n;
+    const long N = h->n;                       // global order (the caller's vectors)
+    const long n = F.n;                        // rows of this part (all rows on one GPU)
+    const long nx = (long)F.n + F.n_ghost;     // + ghost DoFs (multi-GPU)
+    const bool fd = finest_dist(h);
 
     // workspace
     const int slots = o->max_directions > 0 ? std::min(o->max_directions + 1, o->max_outer) : o->max_outer;
@@ -1140,7 +1408,7 @@ void solve_device(aux_hierarchy* h, const double* b, long n_b, const aux_cycle_o
         h->w_r.alloc(n);
         h->w_u.alloc(n);
         h->w_b.alloc(n);
-        h->w_tmp.alloc(n);
+        h->w_tmp.alloc(nx);
     }
     if (h->w_sc.n < (size_t)(8 + o->max_outer + 1)) h->w_sc.alloc(8 + o->max_outer + 1);
     if (!h->direct_only && h->lv.size() > 1 && (int)h->lv[1].pcg.p.size() != o->n_inner) {
@@ -1154,7 +1422,7 @@ void solve_device(aux_hierarchy* h, const double* b, long n_b, const aux_cycle_o
 
     // norm of b (caller order) and b in storage order
     Fin fnorm{3, sc, nullptr, sc + 4};
-    k_dot<<<red_blocks(n), kRedThreads, 0, s>>>(n, b, b, rs, fnorm);
+    k_dot<<<red_blocks(N), kRedThreads, 0, s>>>(N, b, b, rs, fnorm);   // b is global on every part
     AUX_LAUNCHED(1);
     if (h->direct_only) {
         AUX_CUDA(cudaMemcpyAsync(h->w_r.p, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
@@ -1208,7 +1476,7 @@ void solve_device(aux_hierarchy* h, const double* b, long n_b, const aux_cycle_o
             int slot = 0;
             while (in_use[slot]) ++slot;
             while ((int)h->w_p.size() <= slot) {   // direction storage grows on demand
-                h->w_p.emplace_back(n);
+                h->w_p.emplace_back(nx);            // (+ ghost DoFs: the outer A z reads them)
                 h->w_ap.emplace_back(n);
             }
             double* p = h->w_p[slot].p;
@@ -1217,33 +1485,39 @@ void solve_device(aux_hierarchy* h, const double* b, long n_b, const aux_cycle_o
             g_trace.mark(s, 5);
             finest_cycle(c, r, p, h->w_tmp.p);
             g_trace.mark(s, 3);
+            ghost_exchange(c, p);
             prof_begin(c, 1);
-            if (h->direct_only) {
+            {
+                const Route rs0 = route(c, fd, kept.empty() ? Fin{1, sc, nullptr, e_slot}
+                                                             : Fin{2, sc, sc + 8 + kept[0], nullptr});
                 k_csr_spmv<<<red_blocks(n), kRedThreads, 0, s>>>(n, F.rp.p, F.col.p, F.v.p, p, ap, kept.empty() ? 0 : 1,
                                                                 r, kept.empty() ? nullptr : h->w_ap[kept[0]].p, rs,
-                                                                kept.empty() ? Fin{1, sc, nullptr, e_slot}
-                                                                             : Fin{2, sc, sc + 8 + kept[0], nullptr});
-            } else {
-                k_csr_spmv<<<red_blocks(n), kRedThreads, 0, s>>>(n, F.rp.p, F.col.p, F.v.p, p, ap, kept.empty() ? 0 : 1,
-                                                                r, kept.empty() ? nullptr : h->w_ap[kept[0]].p, rs,
-                                                                kept.empty() ? Fin{1, sc, nullptr, e_slot}
-                                                                             : Fin{2, sc, sc + 8 + kept[0], nullptr});
+                                                                rs0.launch);
+                AUX_LAUNCHED(1);
+                routed(c, rs0);
             }
-            AUX_LAUNCHED(1);
             prof_end(c, 1, spmv_bytes + (kept.empty() ? 16.0 : 8.0) * n);
             if (!kept.empty()) {
                 for (size_t j = 1; j < kept.size(); ++j) {
-                    k_mgs<<<red_blocks(n), kRedThreads, 0, s>>>(n, p, ap, h->w_p[kept[j - 1]].p, h->w_ap[kept[j - 1]].p,
-                                                               h->w_ap[kept[j]].p, nullptr, 0, sc, rs,
-                                                               Fin{2, sc, sc + 8 + kept[j], nullptr});
+                    const Route rj = route(c, fd, Fin{2, sc, sc + 8 + kept[j], nullptr});
+                    k_mgs<<<red_blocks(n), kRedThreads, 0, s>>>(flat_span(n), p, ap, h->w_p[kept[j - 1]].p,
+                                                               h->w_ap[kept[j - 1]].p, h->w_ap[kept[j]].p, nullptr, 0,
+                                                               sc, rs, rj.launch);
                     AUX_LAUNCHED(1);
+                    routed(c, rj);
                 }
-                k_mgs<<<red_blocks(n), kRedThreads, 0, s>>>(n, p, ap, h->w_p[kept.back()].p, h->w_ap[kept.back()].p,
-                                                           nullptr, r, 1, sc, rs, Fin{1, sc, nullptr, e_slot});
+                const Route rf = route(c, fd, Fin{1, sc, nullptr, e_slot});
+                k_mgs<<<red_blocks(n), kRedThreads, 0, s>>>(flat_span(n), p, ap, h->w_p[kept.back()].p,
+                                                           h->w_ap[kept.back()].p, nullptr, r, 1, sc, rs, rf.launch);
                 AUX_LAUNCHED(1);
+                routed(c, rf);
             }
-            k_update<<<red_blocks(n), kRedThreads, 0, s>>>(n, u, p, r, ap, 0, 1, 1, sc, rs, Fin{3, sc, nullptr, sc + 3});
-            AUX_LAUNCHED(1);
+            {
+                const Route ru = route(c, fd, Fin{3, sc, nullptr, sc + 3});
+                k_update<<<red_blocks(n), kRedThreads, 0, s>>>(n, u, p, r, ap, 0, 1, 1, sc, rs, ru.launch);
+                AUX_LAUNCHED(1);
+                routed(c, ru);
+            }
             g_trace.mark(s, 4);
             double st[2];
             AUX_CUDA(cudaMemcpyAsync(st, sc + 2, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));

@@ -88,10 +88,10 @@ __device__ __forceinline__ double row9s(const double* __restrict__ val, const do
 }
 
 template <int T, int H>
-__device__ __forceinline__ void tile_origin(int tiles_x, int& x0, int& y0) {
+__device__ __forceinline__ void tile_origin(int ox, int oy, int tiles_x, int& x0, int& y0) {
     const int tx = blockIdx.x % tiles_x, ty = blockIdx.x / tiles_x;
-    x0 = tx * T - H;
-    y0 = ty * T - H;
+    x0 = ox + tx * T - H;
+    y0 = oy + ty * T - H;
 }
 
 // ---------------------------------------------------------------- down
@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(kTT) k_tile_down(const __grid_constant__ TileD
     double* u = val + 9 * N;
     double* f = u + N;
     int x0, y0;
-    tile_origin<T, H>(a.tiles_x, x0, y0);
+    tile_origin<T, H>(a.ox, a.oy, a.tiles_x, x0, y0);
     const int w = 1 << a.g.k;
     const bool upd = a.ap_prev != nullptr;
     const double na = upd ? -a.sc[0] : 0.0;
@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(kTT) k_tile_up(const __grid_constant__ TileUp 
     double* u = val + 9 * N;
     double* f = u + N;
     int x0, y0;
-    tile_origin<T, H>(a.tiles_x, x0, y0);
+    tile_origin<T, H>(a.ox, a.oy, a.tiles_x, x0, y0);
     const int w = 1 << a.g.k;
     // child correction: explicit, or ((0 + alpha_0 p_0) + alpha_1 p_1) ... over
     // the child's valid PCG steps (axpy order, cycle.hpp:124)
@@ -251,49 +251,45 @@ void set_smem(K kernel, size_t bytes) {
 }  // namespace
 
 int tile_edge(int w) { return w >= 256 ? 16 : 8; }
-int tile_count(int w) {
-    const int T = tile_edge(w);
-    return (w / T) * (w / T);
-}
 bool tiles_supported(int w, int pre, int post) { return w >= 16 && pre >= 1 && pre <= 2 && post >= 1 && post <= 2; }
 
 template <int T, int H>
-static void down_t(const TileDown& a, cudaStream_t s) {
+static void down_t(const TileDown& a, int ntiles, cudaStream_t s) {
     static bool init = false;
     if (!init) {
         set_smem(k_tile_down<T, H>, Tile<T, H>::bytes);
         init = true;
     }
-    k_tile_down<T, H><<<(unsigned)(a.tiles_x * a.tiles_x), kTT, Tile<T, H>::bytes, s>>>(a);
+    k_tile_down<T, H><<<(unsigned)ntiles, kTT, Tile<T, H>::bytes, s>>>(a);
     AUX_LAUNCHED(1);
 }
 
 template <int T, int H>
-static void up_t(const TileUp& a, RedState rs, Fin fin, cudaStream_t s) {
+static void up_t(const TileUp& a, int ntiles, RedState rs, Fin fin, cudaStream_t s) {
     static bool init = false;
     if (!init) {
         set_smem(k_tile_up<T, H>, Tile<T, H>::bytes);
         init = true;
     }
-    k_tile_up<T, H><<<(unsigned)(a.tiles_x * a.tiles_x), kTT, Tile<T, H>::bytes, s>>>(a, rs, fin);
+    k_tile_up<T, H><<<(unsigned)ntiles, kTT, Tile<T, H>::bytes, s>>>(a, rs, fin);
     AUX_LAUNCHED(1);
 }
 
-void launch_tile_down(const TileDown& a, int pre, cudaStream_t s) {
-    const int T = tile_edge(1 << a.g.k);
+void launch_tile_down(const TileDown& a, int ntiles, int pre, cudaStream_t s) {
+    const int T = a.tiles_x_edge;
     if (T == 16) {
-        if (pre == 1) down_t<16, 4>(a, s); else down_t<16, 8>(a, s);
+        if (pre == 1) down_t<16, 4>(a, ntiles, s); else down_t<16, 8>(a, ntiles, s);
     } else {
-        if (pre == 1) down_t<8, 4>(a, s); else down_t<8, 8>(a, s);
+        if (pre == 1) down_t<8, 4>(a, ntiles, s); else down_t<8, 8>(a, ntiles, s);
     }
 }
 
-void launch_tile_up(const TileUp& a, int post, RedState rs, Fin fin, cudaStream_t s) {
-    const int T = tile_edge(1 << a.g.k);
+void launch_tile_up(const TileUp& a, int ntiles, int post, RedState rs, Fin fin, cudaStream_t s) {
+    const int T = a.tiles_x_edge;
     if (T == 16) {
-        if (post == 1) up_t<16, 5>(a, rs, fin, s); else up_t<16, 9>(a, rs, fin, s);
+        if (post == 1) up_t<16, 5>(a, ntiles, rs, fin, s); else up_t<16, 9>(a, ntiles, rs, fin, s);
     } else {
-        if (post == 1) up_t<8, 5>(a, rs, fin, s); else up_t<8, 9>(a, rs, fin, s);
+        if (post == 1) up_t<8, 5>(a, ntiles, rs, fin, s); else up_t<8, 9>(a, ntiles, rs, fin, s);
     }
 }
 

@@ -18,7 +18,9 @@ inline int sc_size(int ni) { return 4 + 2 * ni; }
 // from zero, residual and restriction into the child's PCG right-hand side.
 struct TileDown {
     Geo g, gc;
+    int ox, oy;              // owned rectangle origin (global cells); tiles cover it
     int tiles_x;
+    int tiles_x_edge;        // tile edge T (tile_edge of the owned rectangle)
     const double* val;
     const double* r_in;      // PCG residual before this step's update
     const double* ap_prev;   // A p of the previous step (nullptr: no update)
@@ -35,7 +37,9 @@ struct TileDown {
 // A z and the fused inner products of the step (cycle.hpp:84-97, 119-123).
 struct TileUp {
     Geo g, gc;
+    int ox, oy;
     int tiles_x;
+    int tiles_x_edge;
     const double* val;
     const uint8_t* act;
     const double* f;         // right-hand side of this visit (the PCG residual)
@@ -52,10 +56,10 @@ struct TileUp {
 };
 
 // Launch the tile kernels; T = tile edge, pre/post = sweeps (1 or 2).
-bool tiles_supported(int w, int pre, int post);
+bool tiles_supported(int w, int pre, int post);   // w: smaller edge of the owned rectangle
 int tile_edge(int w);
-int tile_count(int w);
-void launch_tile_down(const TileDown& a, int pre, cudaStream_t s);
-void launch_tile_up(const TileUp& a, int post, RedState rs, Fin fin, cudaStream_t s);
+// ntiles = tiles of the owned rectangle (tiles_x per row)
+void launch_tile_down(const TileDown& a, int ntiles, int pre, cudaStream_t s);
+void launch_tile_up(const TileUp& a, int ntiles, int post, RedState rs, Fin fin, cudaStream_t s);
 
 }  // namespace auxb200
