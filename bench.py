@@ -191,6 +191,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dist", action="store_true",
+                    help="use the multi-GPU (NCCL) path even on one GPU (it is always used for --gpus > 1)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     world, rank, local, dist = dist_setup(args)
@@ -207,10 +209,35 @@ def main():
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     api.lib()
+    use_dist = world > 1 or args.dist
+    if world > 1:   # weak scaling: the global problem grows with the GPU count (same DoFs per GPU)
+        cfg = dict(cfg)
+        cfg["n"] = int(round((cfg["n"] - 1) * world ** 0.5)) + 1
+        cfg["name"] = f"{cfg['name']} x{world} GPUs weak scaling (global n={cfg['n']})"
     s = make_problem(cfg)
     N, nnz = s.A.n_rows, s.A.nnz
     mdof = N / 1e6
     gpu = api.GpuOptions(device=local)
+    comm = None
+    if use_dist:   # one NCCL communicator for every hierarchy of the run
+        nid = api.nccl_unique_id() if rank == 0 else bytes(128)
+        if dist is not None:
+            obj = [nid]
+            dist.broadcast_object_list(obj, src=0)
+            nid = obj[0]
+        comm = api.NcclComm(nid, world, rank, local)
+
+    def setup_dev():
+        if use_dist:
+            return api.setup_hierarchy_dist_device(N, nnz, d_rp.data_ptr(), d_col.data_ptr(), d_val.data_ptr(),
+                                                   d_xy.data_ptr(), N, world, rank, comm=comm, gpu=gpu)
+        return api.setup_hierarchy_device(N, nnz, d_rp.data_ptr(), d_col.data_ptr(), d_val.data_ptr(),
+                                          d_xy.data_ptr(), N, gpu=gpu)
+
+    def setup_host(A_h, xy_h):
+        if use_dist:
+            return api.setup_hierarchy_dist(A_h, xy_h, world, rank, comm=comm, gpu=gpu)
+        return api.setup_hierarchy(A_h, xy_h, gpu=gpu)
 
     # ---- inputs resident in HBM (value)
     d_rp = torch.from_numpy(s.A.row_ptr).to(dev)
@@ -221,8 +248,7 @@ def main():
     d_u = torch.empty(N, dtype=torch.float64, device=dev)
 
     def device_step():
-        h = api.setup_hierarchy_device(N, nnz, d_rp.data_ptr(), d_col.data_ptr(), d_val.data_ptr(),
-                                       d_xy.data_ptr(), N, gpu=gpu)
+        h = setup_dev()
         r = api.solve_device(h, d_b.data_ptr(), d_u.data_ptr(), N)
         return h, r
 
@@ -244,8 +270,7 @@ def main():
         barrier()
         ev0.record()
         for k in range(args.steps):
-            h = api.setup_hierarchy_device(N, nnz, d_rp.data_ptr(), d_col.data_ptr(), d_val.data_ptr(),
-                                           d_xy.data_ptr(), N, gpu=gpu)
+            h = setup_dev()
             if k == args.steps - 1:
                 h.profile(True)   # events around the finest-level kernels of this step
             r = api.solve_device(h, d_b.data_ptr(), d_u.data_ptr(), N)
@@ -266,8 +291,8 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         elapsed = float(t.item())
     ms_step = elapsed / args.steps
-    # whole-job throughput: `world` replicas of mdof each finish in ms_step
-    value = ms_step / (world * mdof)
+    # whole-job throughput: the global problem (all GPUs' DoFs) per step
+    value = ms_step / mdof
     u_dev = d_u.cpu().numpy()
 
     # ---- e2e through the host-buffer C ABI, pinned memory
@@ -278,14 +303,14 @@ def main():
     h2d = A_h.row_ptr.nbytes + A_h.col_idx.nbytes + A_h.values.nbytes + xy_h.nbytes + b_h.nbytes
     d2h = N * 8
     for _ in range(max(1, args.warmup // 2)):
-        h = api.setup_hierarchy(A_h, xy_h, gpu=gpu)
+        h = setup_host(A_h, xy_h)
         api.solve(A_h, b_h, h, out=u_h)
         del h
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(args.steps):
-        h = api.setup_hierarchy(A_h, xy_h, gpu=gpu)
+        h = setup_host(A_h, xy_h)
         res = api.solve(A_h, b_h, h, out=u_h)
         del h
     e1.record()
@@ -295,7 +320,13 @@ def main():
         t = torch.tensor([e2e_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
-    assert np.array_equal(res.u, u_dev), "host-API and device-API solutions differ"
+    if use_dist:   # each part wrote the entries of the DoFs it owns
+        hq = setup_dev()
+        ids = api.part_dofs(hq)
+        del hq
+        assert np.array_equal(res.u[ids], u_dev[ids]), "host-API and device-API solutions differ"
+    else:
+        assert np.array_equal(res.u, u_dev), "host-API and device-API solutions differ"
 
     # ---- roofline of the dominant finest-level kernel (live CUDA events)
     peak, peak_src = peaks()
@@ -316,10 +347,11 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": False, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": cfg["name"], "N": N, "nnz": nnz, "iterations": iters, "rtol": 1e-6,
-                       "parallelism": "replicas" if world > 1 else "1 GPU",
+                       "parallelism": (f"quadtree-subtree partition over {world} GPUs, NCCL halo/ghost exchange "
+                                       "+ all-reduce, coarse levels agglomerated on rank 0") if use_dist else "1 GPU",
                        "setup_ms": statistics.median(setup_ms), "solve_ms": statistics.median(solve_ms),
                        "l2": f"inputs {(s.A.values.nbytes + s.A.col_idx.nbytes + 24 * N) / 1e6:.0f} MB > 126 MB L2"},
-            "e2e": {"value": e2e_ms / (world * mdof), "unit": "ms/MDOF", "h2d_bytes_per_step": int(h2d),
+            "e2e": {"value": e2e_ms / mdof, "unit": "ms/MDOF", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h)},
             "roofline": {"bound": "hbm", "kernel": PROFILE_KINDS[kind], "achieved": achieved, "peak": peak,
                          "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,

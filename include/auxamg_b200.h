@@ -213,15 +213,19 @@ typedef struct aux_dist_opts {
     int32_t rank;             /* this part */
     int32_t transport;        /* 0 = parts driven by threads of one process
                                      (local_group, one device: the test path),
-                                 1 = NCCL, one process per GPU */
+                                 1 = NCCL, one process per GPU (a communicator per hierarchy),
+                                 2 = a communicator from aux_comm_create_nccl (in local_group),
+                                     shared by successive hierarchies, not owned */
     int32_t reserved;
-    void* local_group;        /* aux_local_group_create(P), transport 0 */
+    void* local_group;        /* aux_local_group_create(P) (0) / aux_comm_create_nccl (2) */
     uint8_t nccl_id[128];     /* aux_nccl_unique_id on rank 0, broadcast by the caller */
 } aux_dist_opts;
 
 void* aux_local_group_create(int32_t parts);
 void aux_local_group_destroy(void* group);
 int32_t aux_nccl_unique_id(uint8_t id[128]);   /* 1 on success */
+void* aux_comm_create_nccl(const uint8_t id[128], int32_t nranks, int32_t rank, int32_t device);
+void aux_comm_destroy(void* comm);
 /* setup_hierarchy for one part; A and xy are the global inputs (host / device). */
 aux_status aux_setup_dist(const aux_csr_view* A, const double* xy, int64_t n_points,
                           const aux_setup_opts* opts, const aux_gpu_opts* gpu, const aux_dist_opts* d,
@@ -230,6 +234,7 @@ aux_status aux_setup_dist_device(const aux_csr_view* A, const double* xy, int64_
                                  const aux_setup_opts* opts, const aux_gpu_opts* gpu,
                                  const aux_dist_opts* d, aux_hierarchy** out, char* msg, size_t msg_len);
 int32_t aux_part_rows(const aux_hierarchy* h);   /* finest DoFs owned by this part */
+aux_status aux_part_dofs(const aux_hierarchy* h, int32_t* ids);   /* their caller ids (aux_part_rows of them) */
 
 /* ---- measurement hooks (bench.py; not part of the reference API) ---- */
 /* Number of kernels this library launched (graph nodes count per replay). */

@@ -70,6 +70,11 @@ def lib():
     L.aux_setup_dist.restype = C.c_int
     L.aux_setup_dist_device.argtypes = [vp, vp, i64, vp, vp, vp, C.POINTER(vp), C.c_char_p, sz]
     L.aux_setup_dist_device.restype = C.c_int
+    L.aux_comm_create_nccl.argtypes = [vp, i32, i32, i32]
+    L.aux_comm_create_nccl.restype = vp
+    L.aux_comm_destroy.argtypes = [vp]
+    L.aux_part_dofs.argtypes = [vp, vp]
+    L.aux_part_dofs.restype = C.c_int
     L.aux_part_rows.argtypes = [vp]
     L.aux_part_rows.restype = i32
     _lib = L
@@ -321,6 +326,26 @@ class LocalGroup:
             pass
 
 
+class NcclComm:
+    """An NCCL communicator (one process per GPU) shared by successive
+    distributed hierarchies (transport 2), so setup does not re-initialise NCCL."""
+
+    def __init__(self, nccl_id: bytes, nranks: int, rank: int, device: int = 0):
+        buf = (C.c_uint8 * 128).from_buffer_copy(nccl_id)
+        self.nranks, self.rank = nranks, rank
+        self._c = lib().aux_comm_create_nccl(buf, nranks, rank, device)
+        if not self._c:
+            raise _abi.DeviceError("NCCL communicator creation failed")
+
+    def __del__(self):
+        try:
+            if self._c:
+                lib().aux_comm_destroy(self._c)
+                self._c = None
+        except Exception:
+            pass
+
+
 def nccl_unique_id() -> bytes:
     buf = (C.c_uint8 * 128)()
     if not lib().aux_nccl_unique_id(buf):
@@ -330,7 +355,7 @@ def nccl_unique_id() -> bytes:
 
 def setup_hierarchy_dist(A: CsrMatrix, coords, nparts: int, rank: int, group: LocalGroup | None = None,
                          nccl_id: bytes | None = None, opts: SetupOptions | None = None,
-                         gpu: GpuOptions | None = None) -> Hierarchy:
+                         gpu: GpuOptions | None = None, comm: NcclComm | None = None) -> Hierarchy:
     """setup_hierarchy for part `rank` of `nparts` (A and coords are the global
     inputs).  group: local transport (threads, one device); nccl_id: NCCL, one
     process per GPU."""
@@ -339,7 +364,9 @@ def setup_hierarchy_dist(A: CsrMatrix, coords, nparts: int, rank: int, group: Lo
     npts = xy.shape[0] if xy.ndim == 2 else xy.size // 2
     d = _abi.DistOpts()
     d.nparts, d.rank = nparts, rank
-    if group is not None:
+    if comm is not None:
+        d.transport, d.local_group = 2, comm._c
+    elif group is not None:
         d.transport, d.local_group = 0, group._g
     else:
         if nccl_id is None or len(nccl_id) != 128:
@@ -353,11 +380,49 @@ def setup_hierarchy_dist(A: CsrMatrix, coords, nparts: int, rank: int, group: Lo
     s = lib().aux_setup_dist(C.byref(_csr_view(A)), xy.ctypes.data, npts, C.byref(o), C.byref(g), C.byref(d),
                              C.byref(h), msg, 512)
     _abi.raise_for(s, msg.raw)
-    return Hierarchy(h, A, A.n_rows)
+    hh = Hierarchy(h, A, A.n_rows)
+    hh._transport = comm if comm is not None else group   # outlives the hierarchy
+    return hh
+
+
+def setup_hierarchy_dist_device(n: int, nnz: int, row_ptr: int, col_idx: int, values: int, xy: int, n_points: int,
+                                nparts: int, rank: int, group: LocalGroup | None = None,
+                                nccl_id: bytes | None = None, opts: SetupOptions | None = None,
+                                gpu: GpuOptions | None = None, comm: NcclComm | None = None) -> Hierarchy:
+    """setup_hierarchy_dist with the global inputs already in device memory."""
+    v = _abi.CsrView(n, n, nnz, row_ptr, col_idx, values)
+    d = _abi.DistOpts()
+    d.nparts, d.rank = nparts, rank
+    if comm is not None:
+        d.transport, d.local_group = 2, comm._c
+    elif group is not None:
+        d.transport, d.local_group = 0, group._g
+    else:
+        if nccl_id is None or len(nccl_id) != 128:
+            raise _abi.ArgumentError("setup_hierarchy_dist_device: need a LocalGroup or a 128-byte NCCL id")
+        d.transport = 1
+        C.memmove(d.nccl_id, nccl_id, 128)
+    o = (opts or SetupOptions()).c()
+    g = (gpu or GpuOptions()).c()
+    h = C.c_void_p()
+    msg = C.create_string_buffer(512)
+    s = lib().aux_setup_dist_device(C.byref(v), xy, n_points, C.byref(o), C.byref(g), C.byref(d), C.byref(h), msg,
+                                    512)
+    _abi.raise_for(s, msg.raw)
+    hh = Hierarchy(h, None, n)
+    hh._transport = comm if comm is not None else group
+    return hh
 
 
 def part_rows(h: Hierarchy) -> int:
     return lib().aux_part_rows(h.handle)
+
+
+def part_dofs(h: Hierarchy) -> np.ndarray:
+    """Caller ids of the finest DoFs this part owns."""
+    ids = np.empty(max(part_rows(h), 1), np.int32)
+    _abi.raise_for(lib().aux_part_dofs(h.handle, ids.ctypes.data), b"aux_part_dofs")
+    return ids[: part_rows(h)]
 
 
 def solve_parts(A: CsrMatrix, coords, b, parts: int, opts: SetupOptions | None = None,

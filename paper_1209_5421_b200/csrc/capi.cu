@@ -62,7 +62,7 @@ aux_hierarchy::~aux_hierarchy() {
         for (auto e : prof.ev_end[k]) cudaEventDestroy(e);
     }
     if (stream) cudaStreamSynchronize(stream);
-    delete dist.comm;
+    if (dist.owns_comm) delete dist.comm;
     dist.comm = nullptr;
     // DBufs free themselves; the stream goes last
     fine = Finest();
@@ -169,6 +169,15 @@ void* aux_local_group_create(int32_t parts) {
 }
 void aux_local_group_destroy(void* g) { local_group_destroy(static_cast<LocalGroup*>(g)); }
 int32_t aux_nccl_unique_id(uint8_t id[128]) { return nccl_unique_id(id) ? 1 : 0; }
+void* aux_comm_create_nccl(const uint8_t id[128], int32_t nranks, int32_t rank, int32_t device) {
+    try {
+        AUX_CUDA(cudaSetDevice(device));
+        return make_nccl_comm(id, nranks, rank);
+    } catch (...) {
+        return nullptr;
+    }
+}
+void aux_comm_destroy(void* comm) { delete static_cast<Comm*>(comm); }
 
 static aux_status setup_dist_impl(const aux_csr_view* A, const double* xy, int64_t n_points,
                                   const aux_setup_opts* opts, const aux_gpu_opts* gpu, const aux_dist_opts* d,
@@ -183,6 +192,12 @@ static aux_status setup_dist_impl(const aux_csr_view* A, const double* xy, int64
         if (d->transport == 0) {
             if (!d->local_group) throw_aux(AUX_ARGUMENT_ERROR, "aux_dist_opts: local transport needs a group");
             h->dist.comm = make_local_comm(static_cast<LocalGroup*>(d->local_group), d->rank);
+        } else if (d->transport == 2) {
+            if (!d->local_group) throw_aux(AUX_ARGUMENT_ERROR, "aux_dist_opts: transport 2 needs a communicator");
+            h->dist.comm = static_cast<Comm*>(d->local_group);
+            h->dist.owns_comm = false;
+            if (h->dist.comm->size != d->nparts || h->dist.comm->rank != d->rank)
+                throw_aux(AUX_ARGUMENT_ERROR, "aux_dist_opts: communicator does not match nparts / rank");
         } else {
             h->dist.comm = make_nccl_comm(d->nccl_id, d->nparts, d->rank);
         }
@@ -232,6 +247,12 @@ aux_status aux_setup_dist_device(const aux_csr_view* A, const double* xy, int64_
     return setup_dist_impl(A, xy, n_points, opts, gpu, d, out, msg, msg_len, false);
 }
 int32_t aux_part_rows(const aux_hierarchy* h) { return h->fine.n; }
+aux_status aux_part_dofs(const aux_hierarchy* h, int32_t* ids) {
+    return guarded(nullptr, 0, [&] {
+        const int32_t* src = h->dist.comm ? h->dist.gid.p : h->fine.perm.p;
+        AUX_CUDA(cudaMemcpy(ids, src, sizeof(int32_t) * h->fine.n, cudaMemcpyDeviceToHost));
+    });
+}
 
 aux_status aux_solve(aux_hierarchy* h, const aux_csr_view* A, const double* b, int64_t n_b,
                      const aux_cycle_opts* opts, aux_solve_result* res, char* msg, size_t msg_len) {

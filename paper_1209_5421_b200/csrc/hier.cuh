@@ -143,6 +143,7 @@ struct Finest {
 struct Comm;
 struct DistInfo {
     Comm* comm = nullptr;
+    bool owns_comm = true;    // false: a communicator shared across hierarchies (aux_comm_create_nccl)
     int PX = 1, PY = 1, px = 0, py = 0;
     int agg = 1 << 30;        // first level index gathered on part 0 (levels below are distributed)
     DBuf<double> dsum;        // raw inner products before the all-reduce

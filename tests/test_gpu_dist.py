@@ -51,3 +51,37 @@ def test_parts_errors_consistent(gpu_api):
     s = problems.poisson5(20)   # level-L grid too small for 8 parts
     with pytest.raises(gpu_api.ArgumentError):
         gpu_api.solve_parts(s.A, s.coords, s.b, 8)
+
+
+def test_nccl_transport_single_rank(gpu_api):
+    """The NCCL transport (dlopen'ed libnccl, shared communicator) with one rank:
+    the code path a torchrun launch takes on every rank."""
+    s = problems.jittered_p1(129)
+    comm = gpu_api.NcclComm(gpu_api.nccl_unique_id(), 1, 0, 0)
+    h = gpu_api.setup_hierarchy_dist(s.A, s.coords, 1, 0, comm=comm)
+    r = gpu_api.solve(s.A, s.b, h)
+    ref = ob.CpuHierarchy("oracle", s.A, s.coords).solve(s.b)
+    assert abs(r.iterations - ref["iterations"]) <= 1
+    assert np.max(np.abs(r.u - ref["u"])) / np.max(np.abs(ref["u"])) <= U_TOL
+    assert sorted(gpu_api.part_dofs(h).tolist()) == list(range(s.A.n_rows))
+
+
+@pytest.mark.parametrize("parts", [2, 4, 8])
+def test_parts_partition_dofs(gpu_api, parts):
+    """Every DoF is owned by exactly one part; parts own their rectangles' DoFs."""
+    import threading
+    s = problems.jittered_p1(257)
+    grp = gpu_api.LocalGroup(parts)
+    ids = [None] * parts
+
+    def run(r):
+        h = gpu_api.setup_hierarchy_dist(s.A, s.coords, parts, r, group=grp)
+        ids[r] = gpu_api.part_dofs(h)
+        del h
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(parts)]
+    [t.start() for t in th]
+    [t.join() for t in th]
+    allids = np.concatenate(ids)
+    assert np.array_equal(np.sort(allids), np.arange(s.A.n_rows))
+    assert max(len(i) for i in ids) < s.A.n_rows
