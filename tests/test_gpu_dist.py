@@ -85,3 +85,8 @@ def test_parts_partition_dofs(gpu_api, parts):
     allids = np.concatenate(ids)
     assert np.array_equal(np.sort(allids), np.arange(s.A.n_rows))
     assert max(len(i) for i in ids) < s.A.n_rows
+    # the library's rows are exactly the host-side statement of the partition
+    from paper_1209_5421_b200 import partition as pt
+    P = pt.Partition(s.A, s.coords, parts)
+    for r in range(parts):
+        assert np.array_equal(ids[r], P.owned_dofs(r))
