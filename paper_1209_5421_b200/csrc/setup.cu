@@ -295,14 +295,72 @@ __global__ void k_lu_sizes(const int* __restrict__ bptr, int nL, int* __restrict
     }
 }
 
+// Blocks of S <= 6 members: extract, factor (reg_lu_factor: lu_factor's
+// operation order) and, for block_solve = 0, invert in registers.
+template <int S>
+__device__ __forceinline__ bool factor_small(const int* __restrict__ rp, const int* __restrict__ col,
+                                             const double* __restrict__ v, int r0, double* __restrict__ lu,
+                                             int* __restrict__ perm, double* __restrict__ inv) {
+    double a[S][S];
+#pragma unroll
+    for (int i = 0; i < S; ++i)
+#pragma unroll
+        for (int j = 0; j < S; ++j) a[i][j] = 0.0;
+#pragma unroll
+    for (int q = 0; q < S; ++q)
+        for (int p = rp[r0 + q]; p < rp[r0 + q + 1]; ++p) {
+            const int c = col[p] - r0;
+            const double x = v[p];
+#pragma unroll
+            for (int j = 0; j < S; ++j)
+                if (c == j) a[q][j] = x;
+        }
+    int pm[S];
+    if (!reg_lu_factor<S>(a, pm)) return false;
+#pragma unroll
+    for (int i = 0; i < S; ++i) {
+        perm[r0 + i] = pm[i];
+#pragma unroll
+        for (int j = 0; j < S; ++j) lu[i * S + j] = a[i][j];
+    }
+    if (inv) {   // column j of A^-1 = LU solve of e_j, column-major
+#pragma unroll
+        for (int j = 0; j < S; ++j) {
+            double e[S], x[S];
+#pragma unroll
+            for (int i = 0; i < S; ++i) e[i] = i == j ? 1.0 : 0.0;
+            reg_lu_solve<S>(a, pm, e, x);
+#pragma unroll
+            for (int i = 0; i < S; ++i) inv[j * S + i] = x[i];
+        }
+    }
+    return true;
+}
+
 // factor_blocks (smoother.hpp:129-156) for 2 <= s <= 16: one thread extracts the
-// principal block into the pool and factors it in place (lu_factor order).
+// principal block and factors it (lu_factor order): s <= 6 in registers (and
+// inverted there when inv_off is given), otherwise in place in the pool.
 __global__ void k_factor_cells(const int* __restrict__ bptr, const int* __restrict__ rp, const int* __restrict__ col,
                                const double* __restrict__ v, Geo g, const int* __restrict__ off,
-                               double* __restrict__ lu, int* __restrict__ perm, unsigned long long* err) {
+                               double* __restrict__ lu, int* __restrict__ perm, unsigned long long* err,
+                               const int* __restrict__ inv_off, double* __restrict__ inv) {
     GSTRIDE(gid, g.n) {
         const int r0 = bptr[gid], s = bptr[gid + 1] - r0;
         if (s < 2 || s > 16) continue;
+        if (s <= 6) {
+            double* iv = inv_off ? inv + inv_off[gid] : nullptr;
+            double* f = lu + off[gid];
+            bool ok = true;
+            switch (s) {
+                case 2: ok = factor_small<2>(rp, col, v, r0, f, perm, iv); break;
+                case 3: ok = factor_small<3>(rp, col, v, r0, f, perm, iv); break;
+                case 4: ok = factor_small<4>(rp, col, v, r0, f, perm, iv); break;
+                case 5: ok = factor_small<5>(rp, col, v, r0, f, perm, iv); break;
+                default: ok = factor_small<6>(rp, col, v, r0, f, perm, iv); break;
+            }
+            if (!ok) atomicMin(err, (unsigned long long)lex_of_cm(g, (int)gid));
+            continue;
+        }
         double* a = lu + off[gid];
         for (int e = 0; e < s * s; ++e) a[e] = 0.0;
         for (int q = 0; q < s; ++q)
@@ -383,7 +441,7 @@ __global__ void k_inv_cells(const int* __restrict__ bptr, const int* __restrict_
             for (int p = rp[r0]; p < rp[r0 + 1]; ++p)
                 if (col[p] == r0) d = v[p];
             out[0] = 1.0 / d;
-        } else if (s >= 2 && s <= 16) {
+        } else if (s >= 7 && s <= 16) {   // s <= 6: inverted by k_factor_cells
             for (int j = 0; j < s; ++j) lu_solve_unit(lu + lu_off[g], perm + r0, s, j, out + j * s);
         }
     }
@@ -756,12 +814,9 @@ void finest_blocks(aux_hierarchy* h, const Geo& gL, unsigned long long& sing, in
             const int pool = read1(F.cell_lu_off.p + nL, s);
             F.big_lu.alloc(std::max(pool, 1));
             F.big_perm.alloc(n);
-            k_factor_cells<<<grid_for(nL), kT, 0, s>>>(F.bptr.p, F.rp.p, F.col.p, F.v.p, gL, F.cell_lu_off.p,
-                                                       F.big_lu.p, F.big_perm.p, err.p);
-            AUX_LAUNCHED(1);
             F.scratch.alloc(2 * (size_t)n);   // colour-pass residuals + big-block solutions
         }
-        if (h->gpu.block_solve == 0) {   // explicit inverses of all blocks (s <= 16 here, larger below)
+        if (h->gpu.block_solve == 0) {   // explicit inverses of all blocks (pool offsets first)
             DBuf<int> cnt(nL);
             F.inv_off.alloc(nL + 1);
             k_inv_sizes<<<grid_for(nL), kT, 0, s>>>(F.bptr.p, nL, cnt.p);
@@ -771,9 +826,17 @@ void finest_blocks(aux_hierarchy* h, const Geo& gL, unsigned long long& sing, in
             F.inv.alloc(std::max(pool, 1));
             F.rmeta.alloc(n);
             k_rmeta<<<grid_for(nL), kT, 0, s>>>(F.bptr.p, F.inv_off.p, nL, F.rmeta.p);
+            AUX_LAUNCHED(1);
+        }
+        const bool inv_mode = h->gpu.block_solve == 0;
+        k_factor_cells<<<grid_for(nL), kT, 0, s>>>(F.bptr.p, F.rp.p, F.col.p, F.v.p, gL, F.cell_lu_off.p, F.big_lu.p,
+                                                   F.big_perm.p, err.p, inv_mode ? F.inv_off.p : nullptr,
+                                                   inv_mode ? F.inv.p : nullptr);
+        AUX_LAUNCHED(1);
+        if (inv_mode) {   // singletons (1 / a_ii) and 7..16-member blocks
             k_inv_cells<<<grid_for(nL), kT, 0, s>>>(F.bptr.p, F.rp.p, F.col.p, F.v.p, nL, F.cell_lu_off.p,
                                                     F.big_lu.p, F.big_perm.p, F.inv_off.p, F.inv.p);
-            AUX_LAUNCHED(2);
+            AUX_LAUNCHED(1);
         }
         DBuf<int> pos(nL + 1);
         exclusive_scan(flag.p, pos.p, nL, s);

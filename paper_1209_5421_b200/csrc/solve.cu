@@ -165,14 +165,16 @@ __global__ void __launch_bounds__(kRedThreads) k_mgs(Span sp, double* __restrict
                                                     int mode, const double* sc, RedState rs, Fin fin) {
     const double beta = sc[1];
     double v[2] = {0.0, 0.0};
+    // p and ap are re-read by every step of the chain: keep them in L2 and
+    // stream the kept directions through with evict-first loads (ld.global.cs)
     GSTRIDE(j, sp.n) {
         const long i = span_idx(sp, j);
-        const double pi = __dadd_rn(p[i], __dmul_rn(beta, pj[i]));
-        const double api = __dadd_rn(ap[i], __dmul_rn(beta, apj[i]));
+        const double pi = __dadd_rn(p[i], __dmul_rn(beta, __ldcs(pj + i)));
+        const double api = __dadd_rn(ap[i], __dmul_rn(beta, __ldcs(apj + i)));
         p[i] = pi;
         ap[i] = api;
         if (mode == 0) {
-            v[0] = __dadd_rn(v[0], __dmul_rn(pi, w[i]));
+            v[0] = __dadd_rn(v[0], __dmul_rn(pi, __ldcs(w + i)));
         } else {
             v[0] = __dadd_rn(v[0], __dmul_rn(pi, api));
             v[1] = __dadd_rn(v[1], __dmul_rn(r[i], pi));
