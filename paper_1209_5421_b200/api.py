@@ -289,8 +289,15 @@ def solve_device(h: Hierarchy, b_ptr: int, u_ptr: int, n: int, opts: CycleOption
 
 
 def _same_arrays(a: CsrMatrix, b: CsrMatrix) -> bool:
-    return (a.n_rows == b.n_rows and a.values.size == b.values.size and np.array_equal(a.row_ptr, b.row_ptr)
-            and np.array_equal(a.col_idx, b.col_idx) and np.array_equal(a.values, b.values))
+    if a.n_rows != b.n_rows or a.values.size != b.values.size:
+        return False
+    def same_buf(x, y):
+        return (x.__array_interface__["data"][0] == y.__array_interface__["data"][0] and x.size == y.size
+                and x.dtype == y.dtype)
+    if same_buf(a.row_ptr, b.row_ptr) and same_buf(a.col_idx, b.col_idx) and same_buf(a.values, b.values):
+        return True   # the setup matrix itself (no O(nnz) host compare)
+    return (np.array_equal(a.row_ptr, b.row_ptr) and np.array_equal(a.col_idx, b.col_idx)
+            and np.array_equal(a.values, b.values))
 
 
 def stats(h: Hierarchy) -> HierarchyStats:
