@@ -295,7 +295,7 @@ __global__ void k_lu_sizes(const int* __restrict__ bptr, int nL, int* __restrict
     }
 }
 
-// Blocks of S <= 6 members: extract, factor (reg_lu_factor: lu_factor's
+// Blocks of S <= 4 members: extract, factor (reg_lu_factor: lu_factor's
 // operation order) and, for block_solve = 0, invert in registers.
 template <int S>
 __device__ __forceinline__ bool factor_small(const int* __restrict__ rp, const int* __restrict__ col,
@@ -346,29 +346,19 @@ __global__ void k_factor_cells(const int* __restrict__ bptr, const int* __restri
                                const int* __restrict__ inv_off, double* __restrict__ inv) {
     GSTRIDE(gid, g.n) {
         const int r0 = bptr[gid], s = bptr[gid + 1] - r0;
-        if (s < 2 || s > 16) continue;
-        if (s <= 6) {
+        if (s < 2 || s > 4) continue;   // 5+ members: k_factor_warp / k_factor_cta_smem / k_factor_big
+        {
             double* iv = inv_off ? inv + inv_off[gid] : nullptr;
             double* f = lu + off[gid];
             bool ok = true;
             switch (s) {
                 case 2: ok = factor_small<2>(rp, col, v, r0, f, perm, iv); break;
                 case 3: ok = factor_small<3>(rp, col, v, r0, f, perm, iv); break;
-                case 4: ok = factor_small<4>(rp, col, v, r0, f, perm, iv); break;
-                case 5: ok = factor_small<5>(rp, col, v, r0, f, perm, iv); break;
-                default: ok = factor_small<6>(rp, col, v, r0, f, perm, iv); break;
+                default: ok = factor_small<4>(rp, col, v, r0, f, perm, iv); break;
             }
             if (!ok) atomicMin(err, (unsigned long long)lex_of_cm(g, (int)gid));
             continue;
         }
-        double* a = lu + off[gid];
-        for (int e = 0; e < s * s; ++e) a[e] = 0.0;
-        for (int q = 0; q < s; ++q)
-            for (int p = rp[r0 + q]; p < rp[r0 + q + 1]; ++p) {
-                const unsigned c = (unsigned)(col[p] - r0);
-                if (c < (unsigned)s) a[q * s + c] = v[p];
-            }
-        if (!seq_lu_factor(a, perm + r0, s)) atomicMin(err, (unsigned long long)lex_of_cm(g, (int)gid));
     }
 }
 
@@ -429,6 +419,10 @@ __device__ inline void lu_solve_unit(const double* lu, const int* perm, int n, i
     }
 }
 
+__device__ inline void lu_solve_unit_smem(const double* lu, const int* perm, int n, int j, double* x) {
+    lu_solve_unit(lu, perm, n, j, x);
+}
+
 __global__ void k_inv_cells(const int* __restrict__ bptr, const int* __restrict__ rp, const int* __restrict__ col,
                             const double* __restrict__ v, int nL, const int* __restrict__ lu_off,
                             const double* __restrict__ lu, const int* __restrict__ perm,
@@ -441,9 +435,7 @@ __global__ void k_inv_cells(const int* __restrict__ bptr, const int* __restrict_
             for (int p = rp[r0]; p < rp[r0 + 1]; ++p)
                 if (col[p] == r0) d = v[p];
             out[0] = 1.0 / d;
-        } else if (s >= 7 && s <= 16) {   // s <= 6: inverted by k_factor_cells
-            for (int j = 0; j < s; ++j) lu_solve_unit(lu + lu_off[g], perm + r0, s, j, out + j * s);
-        }
+        }   // s >= 2: inverted where it is factored (k_factor_cells / k_factor_warp / k_factor_cta_smem)
     }
 }
 
@@ -455,6 +447,146 @@ __global__ void k_inv_big(const int* __restrict__ ids, const int* __restrict__ b
     const int r0 = bptr[g], s = bptr[g + 1] - r0;
     for (int j = threadIdx.x; j < s; j += blockDim.x)
         lu_solve_unit(lu + lu_off[g], perm + r0, s, j, inv + inv_off[g] + (size_t)j * s);
+}
+
+// Blocks of 5..32 members: one warp per block, the block in shared memory,
+// lane r owning row r.  lu_factor (dense.hpp:76-102) step k: the pivot is the
+// first row of the strict maximum |a(r,k)| (warp arg-max, ties -> lower row),
+// full-row swap, then every row r > k forms m = a(r,k)/a(k,k) and updates its
+// own entries c > k in ascending order -- each element sees exactly the
+// reference's operations, so the factors are bitwise those of lu_factor.
+// With inv != nullptr lane j then forms column j of the inverse (LU solve of
+// e_j in the dense.hpp:52-67 order) from the shared factors.
+constexpr int kWarpLU = 32;
+constexpr int kSmemLU = 160;   // 160^2 doubles = 200 KB of shared memory
+__global__ void k_size_flag(const int* __restrict__ bptr, int nL, int lo, int hi, int* __restrict__ flag) {
+    GSTRIDE(g, nL) {
+        const int s = bptr[g + 1] - bptr[g];
+        flag[g] = (s >= lo && s <= hi) ? 1 : 0;
+    }
+}
+__global__ void __launch_bounds__(64) k_factor_warp(const int* __restrict__ ids, int nids, const int* __restrict__ bptr,
+                                                    const int* __restrict__ rp, const int* __restrict__ col,
+                                                    const double* __restrict__ v, Geo g, const int* __restrict__ off,
+                                                    double* __restrict__ lu, int* __restrict__ perm,
+                                                    unsigned long long* err, const int* __restrict__ inv_off,
+                                                    double* __restrict__ inv) {
+    __shared__ double sa[2][kWarpLU * kWarpLU];
+    __shared__ double sx[2][kWarpLU * kWarpLU];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int task = blockIdx.x * 2 + w;
+    if (task >= nids) return;
+    const int gid = ids[task];
+    const int r0 = bptr[gid], n = bptr[gid + 1] - r0;
+    double* a = sa[w];
+    for (int e = lane; e < n * n; e += 32) a[e] = 0.0;
+    __syncwarp();
+    if (lane < n)
+        for (int p = rp[r0 + lane]; p < rp[r0 + lane + 1]; ++p) {
+            const unsigned c = (unsigned)(col[p] - r0);
+            if (c < (unsigned)n) a[lane * n + c] = v[p];
+        }
+    int pm = lane;   // perm[lane]
+    __syncwarp();
+    for (int k = 0; k < n; ++k) {
+        double best = (lane >= k && lane < n) ? fabs(a[lane * n + k]) : -1.0;
+        int br = lane;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+            const int orow = __shfl_xor_sync(0xffffffffu, br, o);
+            if (ob > best || (ob == best && orow < br)) { best = ob; br = orow; }
+        }
+        if (best == 0.0) {
+            if (lane == 0) atomicMin(err, (unsigned long long)lex_of_cm(g, gid));
+            return;
+        }
+        if (br != k) {
+            for (int c = lane; c < n; c += 32) {
+                const double t = a[k * n + c];
+                a[k * n + c] = a[br * n + c];
+                a[br * n + c] = t;
+            }
+            const int pk = __shfl_sync(0xffffffffu, pm, k), pb = __shfl_sync(0xffffffffu, pm, br);
+            if (lane == k) pm = pb;
+            if (lane == br) pm = pk;
+        }
+        __syncwarp();
+        if (lane > k && lane < n) {
+            double* ar = a + lane * n;
+            const double* ak = a + k * n;
+            const double m = ar[k] / ak[k];
+            ar[k] = m;
+            for (int c = k + 1; c < n; ++c) ar[c] = __dsub_rn(ar[c], __dmul_rn(m, ak[c]));
+        }
+        __syncwarp();
+    }
+    double* out = lu + off[gid];
+    for (int e = lane; e < n * n; e += 32) out[e] = a[e];
+    if (lane < n) perm[r0 + lane] = pm;
+    if (!inv) return;
+    // column j = lane of A^-1: x = P e_j, forward, backward (reference order)
+    double* x = sx[w];   // column-major scratch: x[c * n + j] holds entry c of column j
+    __syncwarp();
+    if (lane < n) {
+        const int j = lane;
+        for (int i = 0; i < n; ++i) x[i * n + j] = (__shfl_sync(0xffffffffu, pm, i) == j) ? 1.0 : 0.0;
+    } else {
+        for (int i = 0; i < n; ++i) (void)__shfl_sync(0xffffffffu, pm, i);
+    }
+    __syncwarp();
+    if (lane < n) {
+        const int j = lane;
+        for (int i = 1; i < n; ++i) {
+            double sm = x[i * n + j];
+            for (int c = 0; c < i; ++c) sm = __dsub_rn(sm, __dmul_rn(a[i * n + c], x[c * n + j]));
+            x[i * n + j] = sm;
+        }
+        for (int i = n - 1; i >= 0; --i) {
+            double sm = x[i * n + j];
+            for (int c = i + 1; c < n; ++c) sm = __dsub_rn(sm, __dmul_rn(a[i * n + c], x[c * n + j]));
+            x[i * n + j] = sm / a[i * n + i];
+        }
+    }
+    __syncwarp();
+    double* iv = inv + inv_off[gid];   // column-major: iv[j * n + i] = (A^-1)(i, j)
+    for (int e = lane; e < n * n; e += 32) {
+        const int j = e / n, i = e - j * n;
+        iv[e] = x[i * n + j];
+    }
+}
+
+// Blocks of more than 32 members: one CTA per block, the block in shared
+// memory (cta_lu_factor: the reference's operation order), then one inverse
+// column per thread from the shared factors.
+__global__ void __launch_bounds__(256) k_factor_cta_smem(const int* __restrict__ ids, const int* __restrict__ bptr,
+                                                        const int* __restrict__ rp, const int* __restrict__ col,
+                                                        const double* __restrict__ v, Geo g,
+                                                        const int* __restrict__ off, double* __restrict__ lu,
+                                                        int* __restrict__ perm, unsigned long long* err,
+                                                        const int* __restrict__ inv_off, double* __restrict__ inv) {
+    extern __shared__ double da[];
+    const int gid = ids[blockIdx.x];
+    const int r0 = bptr[gid], n = bptr[gid + 1] - r0;
+    for (long e = threadIdx.x; e < (long)n * n; e += blockDim.x) da[e] = 0.0;
+    __syncthreads();
+    for (int q = threadIdx.x; q < n; q += blockDim.x)
+        for (int p = rp[r0 + q]; p < rp[r0 + q + 1]; ++p) {
+            const unsigned c = (unsigned)(col[p] - r0);
+            if (c < (unsigned)n) da[(size_t)q * n + c] = v[p];
+        }
+    __syncthreads();
+    const int zc = cta_lu_factor(da, perm + r0, n);
+    if (zc >= 0) {
+        if (threadIdx.x == 0) atomicMin(err, (unsigned long long)lex_of_cm(g, gid));
+        return;
+    }
+    double* out = lu + off[gid];
+    for (long e = threadIdx.x; e < (long)n * n; e += blockDim.x) out[e] = da[e];
+    if (!inv) return;
+    __syncthreads();
+    for (int j = threadIdx.x; j < n; j += blockDim.x)
+        lu_solve_unit_smem(da, perm + r0, n, j, inv + inv_off[gid] + (size_t)j * n);
 }
 
 // check_color_locality (smoother.hpp:217-231): any nonzero coupling between
@@ -565,6 +697,37 @@ __global__ void k_dense_from_csr(const int* __restrict__ rp, const int* __restri
     GSTRIDE(r, n) {
         lex_of_storage[r] = (int)r;
         for (int p = rp[r]; p < rp[r + 1]; ++p) d[(size_t)r * n + col[p]] = v[p];
+    }
+}
+
+// Coarsest level, n <= 128: factor (cta_lu_factor, reference order) with the
+// matrix in shared memory, then the explicit inverse's columns from the
+// shared factors (same operations as k_inverse).
+__global__ void __launch_bounds__(256) k_coarse_lu_inv_smem(double* a, int* perm, int n, int* zero_col,
+                                                           const int* __restrict__ lex_of_storage,
+                                                           double* __restrict__ work) {
+    extern __shared__ double sl[];
+    for (int e = threadIdx.x; e < n * n; e += blockDim.x) sl[e] = a[e];
+    __syncthreads();
+    const int zc = cta_lu_factor(sl, perm, n);
+    if (threadIdx.x == 0) *zero_col = zc;
+    if (zc >= 0) return;
+    for (int e = threadIdx.x; e < n * n; e += blockDim.x) a[e] = sl[e];
+    __syncthreads();
+    for (int js = threadIdx.x; js < n; js += blockDim.x) {
+        const int j = lex_of_storage[js];
+        double* x = work + (size_t)js * n;
+        for (int i = 0; i < n; ++i) x[i] = perm[i] == j ? 1.0 : 0.0;
+        for (int i = 1; i < n; ++i) {
+            double sm = x[i];
+            for (int q = 0; q < i; ++q) sm = __dsub_rn(sm, __dmul_rn(sl[i * n + q], x[q]));
+            x[i] = sm;
+        }
+        for (int i = n - 1; i >= 0; --i) {
+            double sm = x[i];
+            for (int q = i + 1; q < n; ++q) sm = __dsub_rn(sm, __dmul_rn(sl[i * n + q], x[q]));
+            x[i] = sm / sl[i * n + i];
+        }
     }
 }
 
@@ -763,16 +926,31 @@ void factor_coarsest(aux_hierarchy* h) {
     cudaStream_t s = h->stream;
     const int nc = h->nc;
     DBuf<int> zc(1);
-    k_cta_lu<<<1, 256, 0, s>>>(h->c_lu.p, h->c_perm.p, nc, zc.p);
-    AUX_LAUNCHED(1);
-    const int z = read1(zc.p, s);
-    if (z >= 0) throw_aux(AUX_SINGULAR_ERROR, "lu_factor: zero pivot at column " + std::to_string(z));
     DBuf<double> work((size_t)nc * nc);
     h->c_work.alloc((size_t)2 * nc);
     h->c_inv.alloc((size_t)nc * nc);
-    k_inverse<<<grid_for(nc), kT, 0, s>>>(h->c_lu.p, h->c_perm.p, nc, h->c_lex.p, work.p, h->c_inv.p);
+    if (nc <= 128) {
+        const size_t sm = (size_t)nc * nc * sizeof(double);
+        static bool attr = false;
+        if (!attr) {
+            AUX_CUDA(cudaFuncSetAttribute(k_coarse_lu_inv_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          128 * 128 * (int)sizeof(double)));
+            attr = true;
+        }
+        k_coarse_lu_inv_smem<<<1, 256, sm, s>>>(h->c_lu.p, h->c_perm.p, nc, zc.p, h->c_lex.p, work.p);
+        AUX_LAUNCHED(1);
+    } else {
+        k_cta_lu<<<1, 256, 0, s>>>(h->c_lu.p, h->c_perm.p, nc, zc.p);
+        AUX_LAUNCHED(1);
+    }
+    const int z = read1(zc.p, s);
+    if (z >= 0) throw_aux(AUX_SINGULAR_ERROR, "lu_factor: zero pivot at column " + std::to_string(z));
+    if (nc > 128) {
+        k_inverse<<<grid_for(nc), kT, 0, s>>>(h->c_lu.p, h->c_perm.p, nc, h->c_lex.p, work.p, h->c_inv.p);
+        AUX_LAUNCHED(1);
+    }
     k_inverse_scatter<<<grid_for((long)nc * nc), kT, 0, s>>>(work.p, h->c_lex.p, nc, h->c_inv.p);
-    AUX_LAUNCHED(2);
+    AUX_LAUNCHED(1);
     AUX_CUDA(cudaGetLastError());
     AUX_CUDA(cudaStreamSynchronize(s));
 }
@@ -833,10 +1011,27 @@ void finest_blocks(aux_hierarchy* h, const Geo& gL, unsigned long long& sing, in
                                                    F.big_perm.p, err.p, inv_mode ? F.inv_off.p : nullptr,
                                                    inv_mode ? F.inv.p : nullptr);
         AUX_LAUNCHED(1);
-        if (inv_mode) {   // singletons (1 / a_ii) and 7..16-member blocks
+        if (inv_mode) {   // singletons: 1 / a_ii
             k_inv_cells<<<grid_for(nL), kT, 0, s>>>(F.bptr.p, F.rp.p, F.col.p, F.v.p, nL, F.cell_lu_off.p,
                                                     F.big_lu.p, F.big_perm.p, F.inv_off.p, F.inv.p);
             AUX_LAUNCHED(1);
+        }
+        {   // 5..32 members: a warp per block
+            DBuf<int> f7(nL), p7(nL + 1);
+            k_size_flag<<<grid_for(nL), kT, 0, s>>>(F.bptr.p, nL, 5, kWarpLU, f7.p);
+            AUX_LAUNCHED(1);
+            exclusive_scan(f7.p, p7.p, nL, s);
+            const int n7 = read1(p7.p + nL, s);
+            if (n7 > 0) {
+                DBuf<int> l7(n7);
+                k_compact<<<grid_for(nL), kT, 0, s>>>(f7.p, p7.p, nL, l7.p);
+                k_factor_warp<<<(unsigned)((n7 + 1) / 2), 64, 0, s>>>(l7.p, n7, F.bptr.p, F.rp.p, F.col.p, F.v.p, gL,
+                                                                     F.cell_lu_off.p, F.big_lu.p, F.big_perm.p, err.p,
+                                                                     inv_mode ? F.inv_off.p : nullptr,
+                                                                     inv_mode ? F.inv.p : nullptr);
+                AUX_LAUNCHED(2);
+                AUX_CUDA(cudaStreamSynchronize(s));
+            }
         }
         DBuf<int> pos(nL + 1);
         exclusive_scan(flag.p, pos.p, nL, s);
@@ -872,10 +1067,31 @@ void finest_blocks(aux_hierarchy* h, const Geo& gL, unsigned long long& sing, in
             }
             F.big_color_begin[4] = (int)ord.size();
             ids.swap(ord);
-            for (int g : ids)
-                if (bsize(g) > 16) huge.push_back(g);
+            std::vector<int> mid;   // 33..kSmemLU members: CTA with the block in shared memory
+            int mid_max = 0;
+            for (int g : ids) {
+                const int b = bsize(g);
+                if (b > kWarpLU && b <= kSmemLU) { mid.push_back(g); mid_max = std::max(mid_max, b); }
+                else if (b > kSmemLU) huge.push_back(g);
+            }
             AUX_CUDA(cudaMemcpyAsync(F.big_ids.p, ids.data(), sizeof(int) * nbig, cudaMemcpyHostToDevice, s));
-            if (!huge.empty()) {   // blocks the thread-per-block factorisation skipped
+            if (!mid.empty()) {
+                DBuf<int> mid_d(mid.size());
+                AUX_CUDA(cudaMemcpyAsync(mid_d.p, mid.data(), sizeof(int) * mid.size(), cudaMemcpyHostToDevice, s));
+                const size_t sm = (size_t)mid_max * mid_max * sizeof(double);
+                static bool attr = false;
+                if (!attr) {
+                    AUX_CUDA(cudaFuncSetAttribute(k_factor_cta_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  (int)((size_t)kSmemLU * kSmemLU * sizeof(double))));
+                    attr = true;
+                }
+                k_factor_cta_smem<<<(unsigned)mid.size(), 256, sm, s>>>(
+                    mid_d.p, F.bptr.p, F.rp.p, F.col.p, F.v.p, gL, F.cell_lu_off.p, F.big_lu.p, F.big_perm.p, err.p,
+                    h->gpu.block_solve == 0 ? F.inv_off.p : nullptr, h->gpu.block_solve == 0 ? F.inv.p : nullptr);
+                AUX_LAUNCHED(1);
+                AUX_CUDA(cudaStreamSynchronize(s));
+            }
+            if (!huge.empty()) {   // beyond shared memory: factors in place in global memory
                 DBuf<int> hid(huge.size());
                 AUX_CUDA(cudaMemcpyAsync(hid.p, huge.data(), sizeof(int) * huge.size(), cudaMemcpyHostToDevice, s));
                 k_factor_big<<<(unsigned)huge.size(), 128, 0, s>>>(hid.p, F.cell_lu_off.p, F.bptr.p, F.rp.p, F.col.p,
