@@ -43,6 +43,15 @@ __device__ __forceinline__ int cmi(const Geo& g, int t1, int t2) {
     return ((((t2 & 1) << 1) | (t1 & 1)) << g.lq) + ((t2 >> 1) << g.lh) + (t1 >> 1);
 }
 
+// 8-byte asynchronous global -> shared copies (LDGSTS): every stencil value a
+// tile stages is in flight at once, without passing through registers.
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(smem)),
+                 "l"(gmem)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 template <int T, int H>
 struct Tile {
     static constexpr int RW = T + 2 * H;
@@ -119,7 +128,7 @@ __global__ void __launch_bounds__(kTT) k_tile_down(const __grid_constant__ TileD
         if ((unsigned)t1 < (unsigned)w && (unsigned)t2 < (unsigned)w) {
             const int gi = cmi(a.g, t1, t2);
 #pragma unroll
-            for (int t = 0; t < 9; ++t) val[t * N + idx] = a.val[(size_t)t * a.g.n + gi];
+            for (int t = 0; t < 9; ++t) cp_async8(&val[t * N + idx], &a.val[(size_t)t * a.g.n + gi]);
             double fi = a.r_in[gi];
             if (upd) fi = __dadd_rn(fi, __dmul_rn(na, a.ap_prev[gi]));   // axpy(-alpha, ap, r)
             f[idx] = fi;
@@ -130,6 +139,7 @@ __global__ void __launch_bounds__(kTT) k_tile_down(const __grid_constant__ TileD
             f[idx] = 0.0;
         }
     }
+    cp_async_wait_all();
     __syncthreads();
     const int cx = x0 & 1, cy = y0 & 1;
     constexpr int P = H / 4;   // pre sweeps
@@ -189,7 +199,7 @@ __global__ void __launch_bounds__(kTT) k_tile_up(const __grid_constant__ TileUp 
         if ((unsigned)t1 < (unsigned)w && (unsigned)t2 < (unsigned)w) {
             const int gi = cmi(a.g, t1, t2);
 #pragma unroll
-            for (int t = 0; t < 9; ++t) val[t * N + idx] = a.val[(size_t)t * a.g.n + gi];
+            for (int t = 0; t < 9; ++t) cp_async8(&val[t * N + idx], &a.val[(size_t)t * a.g.n + gi]);
             f[idx] = a.f[gi];
             double ui = a.u_pre[gi];
             if (a.act[gi]) {
@@ -214,6 +224,7 @@ __global__ void __launch_bounds__(kTT) k_tile_up(const __grid_constant__ TileUp 
             u[idx] = 0.0;
         }
     }
+    cp_async_wait_all();
     __syncthreads();
     const int cx = x0 & 1, cy = y0 & 1;
     constexpr int P = (H - 1) / 4;   // post sweeps
