@@ -27,6 +27,7 @@
 #include <cstdio>
 #include <stdexcept>
 #include <string>
+#include <utility>
 
 #include "../../include/auxamg_b200.h"
 
@@ -48,9 +49,36 @@ struct AuxError : std::runtime_error {
             ::auxb200::throw_aux(AUX_CUDA_ERROR, std::string(#call) + ": " + cudaGetErrorString(e_)); \
     } while (0)
 
+// Programmatic dependent launch (PDL).  A kernel launched with
+// launch_pdl may start while its predecessor in the stream is still running:
+// it announces early launch of its own successor (pdl_trigger), does the work
+// that only reads data that is constant during the solve (stencil values,
+// inverses, layouts), then pdl_wait()s for the predecessor's completion and
+// memory before touching anything the predecessor wrote.  Every PDL kernel
+// calls pdl_wait, so completion stays transitively ordered along the chain.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // Host-side kernel launch counter (bench.py's gpu_launches).
 extern std::atomic<int64_t> g_launches;
 #define AUX_LAUNCHED(n) (::auxb200::g_launches += (n))
+
+template <class... KArgs, class... Args>
+inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    AUX_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+    AUX_LAUNCHED(1);
+}
 
 // --------------------------------------------------------------- layout
 

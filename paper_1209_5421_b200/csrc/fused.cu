@@ -438,6 +438,7 @@ __device__ bool pcg_step(const FusedArgs& a, const SLevel& L, PState& ps, double
 
 __global__ void __launch_bounds__(kThreads, 1) k_fused_pcg(const __grid_constant__ FusedArgs a) {
     FCLK_START
+    pdl_trigger();
     extern __shared__ __align__(16) unsigned char sm[];
     __shared__ double red[2 * 2 * kWarps];
     __shared__ Geo sgeo[kMaxFusedLevels];
@@ -485,6 +486,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_pcg(const __grid_constant
         for (int i = threadIdx.x; i < nv2; i += kThreads) v[i] = make_double2(0.0, 0.0);
     }
     mbar_wait(&bar, 0);
+    pdl_wait();   // everything above reads data that is constant during the solve
     __syncthreads();
     {
         const SLevel L0 = slev(a, sm, sgeo, 0);
@@ -613,8 +615,7 @@ void launch_fused_pcg(const FusedArgs& a, cudaStream_t s) {
         AUX_CUDA(cudaFuncSetAttribute(k_fused_pcg, cudaFuncAttributeMaxDynamicSharedMemorySize, kFusedSmemMax));
         attr_set = true;
     }
-    k_fused_pcg<<<1, kThreads, a.smem_bytes, s>>>(a);
-    AUX_LAUNCHED(1);
+    launch_pdl(k_fused_pcg, dim3(1), dim3(kThreads), a.smem_bytes, s, a);
 }
 
 }  // namespace auxb200

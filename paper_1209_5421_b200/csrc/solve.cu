@@ -163,6 +163,8 @@ __global__ void __launch_bounds__(kRedThreads) k_mgs(Span sp, double* __restrict
                                                     const double* __restrict__ pj, const double* __restrict__ apj,
                                                     const double* __restrict__ w, const double* __restrict__ r,
                                                     int mode, const double* sc, RedState rs, Fin fin) {
+    pdl_trigger();
+    pdl_wait();
     const double beta = sc[1];
     double v[2] = {0.0, 0.0};
     // p and ap are re-read by every step of the chain: keep them in L2 and
@@ -654,6 +656,8 @@ struct PList {
     const double* p[8];
 };
 __global__ void k_pcg_u(Span sp, PList pl, const double* __restrict__ sc, int ni, double* __restrict__ u) {
+    pdl_trigger();
+    pdl_wait();
     const int nval = (int)sc[3 + 2 * ni];
     GSTRIDE(j, sp.n) {
         const long i = span_idx(sp, j);
@@ -1098,15 +1102,15 @@ void pcg_tiles(Ctx& c, int m) {
         if (i > 0) {
             for (int j = 1; j < i; ++j) {
                 const Route rj = route(c, L.dist, Fin{2, sc, sc + 3 + j, nullptr});
-                k_mgs<<<nb, kRedThreads, 0, c.s>>>(sp, P.p[i].p, P.ap[i].p, P.p[j - 1].p, P.ap[j - 1].p, P.ap[j].p,
-                                                   nullptr, 0, sc, c.rs, rj.launch);
-                AUX_LAUNCHED(1);
+                launch_pdl(k_mgs, dim3(nb), dim3(kRedThreads), 0, c.s, sp, P.p[i].p, P.ap[i].p, P.p[j - 1].p,
+                           P.ap[j - 1].p, (const double*)P.ap[j].p, (const double*)nullptr, 0, (const double*)sc,
+                           c.rs, rj.launch);
                 routed(c, rj);
             }
             const Route rf = route(c, L.dist, Fin{1, sc, nullptr, sc + 3 + i, sc + sc_alpha(ni, i), sc + sc_nval(ni), i});
-            k_mgs<<<nb, kRedThreads, 0, c.s>>>(sp, P.p[i].p, P.ap[i].p, P.p[i - 1].p, P.ap[i - 1].p, nullptr,
-                                               R[i & 1], 1, sc, c.rs, rf.launch);
-            AUX_LAUNCHED(1);
+            launch_pdl(k_mgs, dim3(nb), dim3(kRedThreads), 0, c.s, sp, P.p[i].p, P.ap[i].p, P.p[i - 1].p,
+                       P.ap[i - 1].p, (const double*)nullptr, (const double*)R[i & 1], 1, (const double*)sc, c.rs,
+                       rf.launch);
             routed(c, rf);
         }
         ring_exchange(c, m, {P.p[i].p, P.ap[i].p});
@@ -1271,8 +1275,8 @@ void coarse_root(Ctx& c) {
         for (int k = 0; k < c.o.n_inner; ++k) pl.p[k] = L.pcg.p[k].p;
         Span sp = flat_span(L.n);
         if (L.dist) sp = Span{L.own.cells(), L.geo, L.own.x0, L.own.y0, L.own.w()};
-        k_pcg_u<<<blocks_for(sp.n), 256, 0, c.s>>>(sp, pl, L.pcg.sc.p, c.o.n_inner, L.pcg.u.p);
-        AUX_LAUNCHED(1);
+        launch_pdl(k_pcg_u, dim3(blocks_for(sp.n)), dim3(256), 0, c.s, sp, pl, (const double*)L.pcg.sc.p,
+                   c.o.n_inner, L.pcg.u.p);
     }
 }
 

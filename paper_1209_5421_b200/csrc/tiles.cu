@@ -115,6 +115,24 @@ __global__ void __launch_bounds__(kTT) k_tile_down(const __grid_constant__ TileD
     int x0, y0;
     tile_origin<T, H>(a.ox, a.oy, a.tiles_x, x0, y0);
     const int w = 1 << a.g.k;
+    pdl_trigger();
+    // stencil values are constant during the solve: staged before the wait
+    for (int idx = threadIdx.x; idx < N; idx += kTT) {
+        const int br = idx / RW, ar = idx - br * RW;
+        const int t1 = x0 + ar, t2 = y0 + br;
+        u[idx] = 0.0;
+        if ((unsigned)t1 < (unsigned)w && (unsigned)t2 < (unsigned)w) {
+            const int gi = cmi(a.g, t1, t2);
+#pragma unroll
+            for (int t = 0; t < 9; ++t) cp_async8(&val[t * N + idx], &a.val[(size_t)t * a.g.n + gi]);
+        } else {
+            val[idx] = 1.0;
+#pragma unroll
+            for (int t = 1; t < 9; ++t) val[t * N + idx] = 0.0;
+            f[idx] = 0.0;
+        }
+    }
+    pdl_wait();
     const bool upd = a.ap_prev != nullptr;
     const double na = upd ? -a.sc[0] : 0.0;
     if (a.sc_child && blockIdx.x == 0 && threadIdx.x == 0) {   // child's PCG starts afresh
@@ -124,19 +142,11 @@ __global__ void __launch_bounds__(kTT) k_tile_down(const __grid_constant__ TileD
     for (int idx = threadIdx.x; idx < N; idx += kTT) {
         const int br = idx / RW, ar = idx - br * RW;
         const int t1 = x0 + ar, t2 = y0 + br;
-        u[idx] = 0.0;
         if ((unsigned)t1 < (unsigned)w && (unsigned)t2 < (unsigned)w) {
             const int gi = cmi(a.g, t1, t2);
-#pragma unroll
-            for (int t = 0; t < 9; ++t) cp_async8(&val[t * N + idx], &a.val[(size_t)t * a.g.n + gi]);
             double fi = a.r_in[gi];
             if (upd) fi = __dadd_rn(fi, __dmul_rn(na, a.ap_prev[gi]));   // axpy(-alpha, ap, r)
             f[idx] = fi;
-        } else {
-            val[idx] = 1.0;
-#pragma unroll
-            for (int t = 1; t < 9; ++t) val[t * N + idx] = 0.0;
-            f[idx] = 0.0;
         }
     }
     cp_async_wait_all();
@@ -184,6 +194,23 @@ __global__ void __launch_bounds__(kTT) k_tile_up(const __grid_constant__ TileUp 
     int x0, y0;
     tile_origin<T, H>(a.ox, a.oy, a.tiles_x, x0, y0);
     const int w = 1 << a.g.k;
+    pdl_trigger();
+    for (int idx = threadIdx.x; idx < N; idx += kTT) {   // constant data first (before the wait)
+        const int br = idx / RW, ar = idx - br * RW;
+        const int t1 = x0 + ar, t2 = y0 + br;
+        if ((unsigned)t1 < (unsigned)w && (unsigned)t2 < (unsigned)w) {
+            const int gi = cmi(a.g, t1, t2);
+#pragma unroll
+            for (int t = 0; t < 9; ++t) cp_async8(&val[t * N + idx], &a.val[(size_t)t * a.g.n + gi]);
+        } else {
+            val[idx] = 1.0;
+#pragma unroll
+            for (int t = 1; t < 9; ++t) val[t * N + idx] = 0.0;
+            f[idx] = 0.0;
+            u[idx] = 0.0;
+        }
+    }
+    pdl_wait();
     // child correction: explicit, or ((0 + alpha_0 p_0) + alpha_1 p_1) ... over
     // the child's valid PCG steps (axpy order, cycle.hpp:124)
     int nval = 0;
@@ -198,8 +225,6 @@ __global__ void __launch_bounds__(kTT) k_tile_up(const __grid_constant__ TileUp 
         const int t1 = x0 + ar, t2 = y0 + br;
         if ((unsigned)t1 < (unsigned)w && (unsigned)t2 < (unsigned)w) {
             const int gi = cmi(a.g, t1, t2);
-#pragma unroll
-            for (int t = 0; t < 9; ++t) cp_async8(&val[t * N + idx], &a.val[(size_t)t * a.g.n + gi]);
             f[idx] = a.f[gi];
             double ui = a.u_pre[gi];
             if (a.act[gi]) {
@@ -216,12 +241,6 @@ __global__ void __launch_bounds__(kTT) k_tile_up(const __grid_constant__ TileUp 
                 ui = __dadd_rn(ui, e);
             }
             u[idx] = ui;
-        } else {
-            val[idx] = 1.0;
-#pragma unroll
-            for (int t = 1; t < 9; ++t) val[t * N + idx] = 0.0;
-            f[idx] = 0.0;
-            u[idx] = 0.0;
         }
     }
     cp_async_wait_all();
@@ -271,8 +290,7 @@ static void down_t(const TileDown& a, int ntiles, cudaStream_t s) {
         set_smem(k_tile_down<T, H>, Tile<T, H>::bytes);
         init = true;
     }
-    k_tile_down<T, H><<<(unsigned)ntiles, kTT, Tile<T, H>::bytes, s>>>(a);
-    AUX_LAUNCHED(1);
+    launch_pdl(k_tile_down<T, H>, dim3((unsigned)ntiles), dim3(kTT), Tile<T, H>::bytes, s, a);
 }
 
 template <int T, int H>
@@ -282,8 +300,7 @@ static void up_t(const TileUp& a, int ntiles, RedState rs, Fin fin, cudaStream_t
         set_smem(k_tile_up<T, H>, Tile<T, H>::bytes);
         init = true;
     }
-    k_tile_up<T, H><<<(unsigned)ntiles, kTT, Tile<T, H>::bytes, s>>>(a, rs, fin);
-    AUX_LAUNCHED(1);
+    launch_pdl(k_tile_up<T, H>, dim3((unsigned)ntiles), dim3(kTT), Tile<T, H>::bytes, s, a, rs, fin);
 }
 
 void launch_tile_down(const TileDown& a, int ntiles, int pre, cudaStream_t s) {
