@@ -1,0 +1,57 @@
+"""BASELINE.json full-size configurations on the GPU, checked through
+size-independent properties (the oracle takes minutes at these sizes):
+the true residual ||b - A u|| / ||b|| recomputed on the host in float64
+meets rtol, the iteration counts match the reference's (SURVEY 8(c) goldens,
+measured with the reference itself), setup statistics match the survey's,
+and the two finest-smoother modes agree."""
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+from paper_1209_5421_b200 import problems
+
+pytestmark = [pytest.mark.gpu, pytest.mark.timeout(900)]
+
+
+def _true_rel_residual(s, u):
+    A = sp.csr_matrix((s.A.values, s.A.col_idx, s.A.row_ptr), shape=(s.A.n_rows, s.A.n_rows))
+    return np.linalg.norm(s.b - A @ u) / np.linalg.norm(s.b)
+
+
+@pytest.mark.parametrize("name,make,iters,opcx", [
+    # graded(2049,1.3) -> 25 iterations, opcx 1.4280; jittered n=1025 -> 12, 1.4274
+    ("C2_graded_2049", lambda: problems.graded_p1(2049, 1.3), 25, 1.4280),
+    ("C1_jitter_1025", lambda: problems.jittered_p1(1025), 12, 1.4274),
+])
+def test_full_size_solve(gpu_api, name, make, iters, opcx):
+    s = make()
+    h = gpu_api.setup_hierarchy(s.A, s.coords)
+    st = h.stats()
+    assert round(st.operator_complexity, 4) == opcx
+    r = gpu_api.solve(s.A, s.b, h)
+    assert r.converged and abs(r.iterations - iters) <= 1, r.iterations
+    assert _true_rel_residual(s, r.u) <= 1.0e-6 * (1 + 1e-9)
+    hist = np.array(r.residual_history)
+    assert hist[-1] <= 1e-6 * hist[0]
+
+
+def test_full_size_modes_agree():
+    from paper_1209_5421_b200 import api
+    s = problems.jittered_p1(1025)
+    us = []
+    for bs in (0, 1):
+        h = api.setup_hierarchy(s.A, s.coords, gpu=api.GpuOptions(block_solve=bs, coarse_solve=bs))
+        r = api.solve(s.A, s.b, h)
+        us.append((r.iterations, r.u))
+    assert us[0][0] == us[1][0]
+    assert np.max(np.abs(us[0][1] - us[1][1])) / np.max(np.abs(us[1][1])) <= 1e-12
+
+
+def test_c3_16m(gpu_api):
+    """C3: jittered P1, N = 16,777,216 (13 iterations, opcx 1.4283)."""
+    s = problems.jittered_p1(4097)
+    h = gpu_api.setup_hierarchy(s.A, s.coords)
+    assert round(h.stats().operator_complexity, 4) == 1.4283
+    r = gpu_api.solve(s.A, s.b, h)
+    assert r.converged and abs(r.iterations - 13) <= 1, r.iterations
+    assert _true_rel_residual(s, r.u) <= 1.0e-6 * (1 + 1e-9)
