@@ -236,6 +236,24 @@ aux_status aux_setup_dist_device(const aux_csr_view* A, const double* xy, int64_
 int32_t aux_part_rows(const aux_hierarchy* h);   /* finest DoFs owned by this part */
 aux_status aux_part_dofs(const aux_hierarchy* h, int32_t* ids);   /* their caller ids (aux_part_rows of them) */
 
+/* ---- device P1 FEM assembly ----------------------
+ * assemble_fem_triangle (problems.hpp:152-193) + csr_from_triplets
+ * (sparse.hpp:193-215) on the GPU: mesh in (nodes x,y interleaved, triangles
+ * as 3 node ids, boundary node ids), the Dirichlet-eliminated system out
+ * (DoFs = interior nodes in node order).  jump > 0 multiplies the element
+ * matrix on the odd cells of an 8x8 checkerboard (the C4 configuration).
+ * The system stays in device memory: aux_system_device hands its CSR / b /
+ * coordinates to aux_setup_device / aux_solve_device. */
+typedef struct aux_system aux_system;
+aux_status aux_assemble_p1(const double* nodes_xy, int32_t n_nodes, const int32_t* tris, int64_t n_tris,
+                           const int32_t* boundary, int32_t n_boundary, double f, double jump, int32_t device,
+                           aux_system** out, char* msg, size_t msg_len);
+aux_status aux_system_info(const aux_system* s, int32_t* n, int64_t* nnz);
+aux_status aux_system_device(const aux_system* s, aux_csr_view* A, const double** b, const double** xy);
+aux_status aux_system_copy(const aux_system* s, int32_t* row_ptr, int32_t* col_idx, double* values, double* b,
+                           double* xy);
+void aux_system_destroy(aux_system* s);
+
 /* ---- measurement hooks (bench.py; not part of the reference API) ---- */
 /* Number of kernels this library launched (graph nodes count per replay). */
 int64_t aux_launch_count(void);

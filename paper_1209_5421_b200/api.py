@@ -75,6 +75,16 @@ def lib():
     L.aux_comm_destroy.argtypes = [vp]
     L.aux_part_dofs.argtypes = [vp, vp]
     L.aux_part_dofs.restype = C.c_int
+    L.aux_assemble_p1.argtypes = [vp, i32, vp, i64, vp, i32, C.c_double, C.c_double, i32, C.POINTER(vp),
+                                  C.c_char_p, sz]
+    L.aux_assemble_p1.restype = C.c_int
+    L.aux_system_info.argtypes = [vp, C.POINTER(i32), C.POINTER(i64)]
+    L.aux_system_info.restype = C.c_int
+    L.aux_system_device.argtypes = [vp, vp, C.POINTER(vp), C.POINTER(vp)]
+    L.aux_system_device.restype = C.c_int
+    L.aux_system_copy.argtypes = [vp, vp, vp, vp, vp, vp]
+    L.aux_system_copy.restype = C.c_int
+    L.aux_system_destroy.argtypes = [vp]
     L.aux_part_rows.argtypes = [vp]
     L.aux_part_rows.restype = i32
     _lib = L
@@ -460,3 +470,62 @@ def solve_parts(A: CsrMatrix, coords, b, parts: int, opts: SetupOptions | None =
         if e is not None:
             raise e
     return u, results, stats_
+
+
+# ---------------------------------------------------------------- device assembly
+
+class DeviceSystem:
+    """A P1 system assembled on the GPU (aux_assemble_p1), resident in device memory."""
+
+    def __init__(self, nodes, triangles, boundary, f: float = 1.0, jump: float = 0.0, device: int = 0):
+        nd = np.ascontiguousarray(nodes, dtype=np.float64)
+        tr = np.ascontiguousarray(triangles, dtype=np.int32)
+        bd = np.ascontiguousarray(boundary, dtype=np.int32)
+        h = C.c_void_p()
+        msg = C.create_string_buffer(512)
+        s = lib().aux_assemble_p1(nd.ctypes.data, nd.shape[0], tr.ctypes.data, tr.shape[0], bd.ctypes.data,
+                                  bd.size, f, jump, device, C.byref(h), msg, 512)
+        _abi.raise_for(s, msg.raw)
+        self._s = h
+        n, nnz = C.c_int32(), C.c_int64()
+        lib().aux_system_info(h, C.byref(n), C.byref(nnz))
+        self.n, self.nnz = n.value, nnz.value
+
+    def device_view(self):
+        """(aux_csr_view with device pointers, b pointer, coordinates pointer)."""
+        v = _abi.CsrView()
+        b, xy = C.c_void_p(), C.c_void_p()
+        lib().aux_system_device(self._s, C.byref(v), C.byref(b), C.byref(xy))
+        return v, b.value, xy.value
+
+    def to_host(self):
+        """(CsrMatrix, b, coords) copied to the host."""
+        rp = np.empty(self.n + 1, np.int32)
+        col = np.empty(max(self.nnz, 1), np.int32)
+        val = np.empty(max(self.nnz, 1), np.float64)
+        b = np.empty(max(self.n, 1), np.float64)
+        xy = np.empty((max(self.n, 1), 2), np.float64)
+        _abi.raise_for(lib().aux_system_copy(self._s, rp.ctypes.data, col.ctypes.data, val.ctypes.data,
+                                             b.ctypes.data, xy.ctypes.data), b"aux_system_copy")
+        return CsrMatrix(self.n, self.n, rp, col[: self.nnz], val[: self.nnz]), b[: self.n], xy[: self.n]
+
+    def setup(self, opts: SetupOptions | None = None, gpu: GpuOptions | None = None) -> Hierarchy:
+        """setup_hierarchy straight from the device-resident system."""
+        v, _, xy = self.device_view()
+        o = (opts or SetupOptions()).c()
+        g = (gpu or GpuOptions()).c()
+        h = C.c_void_p()
+        msg = C.create_string_buffer(512)
+        s = lib().aux_setup_device(C.byref(v), xy, self.n, C.byref(o), C.byref(g), C.byref(h), msg, 512)
+        _abi.raise_for(s, msg.raw)
+        hh = Hierarchy(h, None, self.n)
+        hh._system = self   # the device arrays outlive nothing they are needed for, but keep them
+        return hh
+
+    def __del__(self):
+        try:
+            if self._s:
+                lib().aux_system_destroy(self._s)
+                self._s = None
+        except Exception:
+            pass

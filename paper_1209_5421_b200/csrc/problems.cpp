@@ -35,6 +35,7 @@ struct Mesh {
 };
 
 struct System {
+    Mesh mesh;   // kinds 1-4: the mesh the system was assembled from
     int n = 0;
     std::vector<int> row_ptr, col_idx;
     std::vector<double> values, b, xy;
@@ -248,6 +249,7 @@ auxgen_system* auxgen_make(int kind, int n, double param, unsigned seed, double 
             throw std::invalid_argument("unknown kind");
         }
         assemble(*s, mesh, 1.0, jump);
+        s->mesh = std::move(mesh);
     } catch (...) {
         delete s;
         return nullptr;
@@ -332,6 +334,27 @@ const double* auxgen_b(const auxgen_system* p) { return reinterpret_cast<const S
 const double* auxgen_xy(const auxgen_system* p) { return reinterpret_cast<const System*>(p)->xy.data(); }
 const int* auxgen_ell_col(const auxgen_system* p) { return reinterpret_cast<const System*>(p)->ell_col.data(); }
 const double* auxgen_ell_val(const auxgen_system* p) { return reinterpret_cast<const System*>(p)->ell_val.data(); }
+// the mesh of kinds 1-4 (node coordinates, triangles, boundary node list)
+int auxgen_mesh_nodes(const auxgen_system* p) {
+    return static_cast<int>(reinterpret_cast<const System*>(p)->mesh.nodes.size());
+}
+int auxgen_mesh_tris(const auxgen_system* p) {
+    return static_cast<int>(reinterpret_cast<const System*>(p)->mesh.tris.size());
+}
+int auxgen_mesh_nboundary(const auxgen_system* p) {
+    return static_cast<int>(reinterpret_cast<const System*>(p)->mesh.boundary.size());
+}
+void auxgen_mesh_copy(const auxgen_system* p, double* xy, int* tris, int* boundary) {
+    const Mesh& m = reinterpret_cast<const System*>(p)->mesh;
+    for (size_t i = 0; i < m.nodes.size(); ++i) {
+        xy[2 * i] = m.nodes[i].x;
+        xy[2 * i + 1] = m.nodes[i].y;
+    }
+    for (size_t e = 0; e < m.tris.size(); ++e)
+        for (int a = 0; a < 3; ++a) tris[3 * e + a] = m.tris[e][a];
+    for (size_t i = 0; i < m.boundary.size(); ++i) boundary[i] = m.boundary[i];
+}
+
 void auxgen_free(auxgen_system* p) { delete reinterpret_cast<System*>(p); }
 
 }  // extern "C"

@@ -30,9 +30,10 @@ def _load():
         lib.auxgen_random_stencil.restype = C.c_void_p
         lib.auxgen_random_stencil.argtypes = [C.c_int, C.c_uint]
         lib.auxgen_random_vector.argtypes = [C.c_int64, C.c_uint, C.c_double, C.c_double, C.c_void_p]
-        for f in ("auxgen_n",):
+        for f in ("auxgen_n", "auxgen_mesh_nodes", "auxgen_mesh_tris", "auxgen_mesh_nboundary"):
             getattr(lib, f).argtypes = [C.c_void_p]
             getattr(lib, f).restype = C.c_int
+        lib.auxgen_mesh_copy.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         lib.auxgen_nnz.argtypes = [C.c_void_p]
         lib.auxgen_nnz.restype = C.c_int64
         for f in ("auxgen_row_ptr", "auxgen_col_idx", "auxgen_ell_col"):
@@ -145,3 +146,35 @@ def random_vector(n: int, seed: int, lo: float = -1.0, hi: float = 1.0) -> np.nd
     out = np.zeros(n, np.float64)
     lib.auxgen_random_vector(n, seed, lo, hi, out.ctypes.data)
     return out
+
+
+@dataclass
+class TriMesh:
+    """auxamg::TriMesh (problems.hpp:41-47): nodes (M, 2), triangles (T, 3), boundary node ids."""
+    nodes: np.ndarray
+    triangles: np.ndarray
+    boundary: np.ndarray
+
+
+def make_with_mesh(kind: int, n: int, param: float = 0.0, seed: int = 1, jump: float = 0.0):
+    """(LinearSystem, TriMesh) of a P1 kind (1-4): the reference's assembly and its input mesh."""
+    lib = _load()
+    h = lib.auxgen_make(kind, n, param, seed, jump)
+    if not h:
+        raise ValueError("generator failed")
+    try:
+        N = lib.auxgen_n(h)
+        nnz = lib.auxgen_nnz(h)
+        A = CsrMatrix(N, N, _copy(lib.auxgen_row_ptr(h), N + 1, np.int32),
+                      _copy(lib.auxgen_col_idx(h), nnz, np.int32),
+                      _copy(lib.auxgen_values(h), nnz, np.float64))
+        b = _copy(lib.auxgen_b(h), N, np.float64)
+        xy = _copy(lib.auxgen_xy(h), 2 * N, np.float64).reshape(N, 2)
+        M, T, B = lib.auxgen_mesh_nodes(h), lib.auxgen_mesh_tris(h), lib.auxgen_mesh_nboundary(h)
+        nodes = np.zeros((M, 2))
+        tris = np.zeros((T, 3), np.int32)
+        bnd = np.zeros(max(B, 1), np.int32)
+        lib.auxgen_mesh_copy(h, nodes.ctypes.data, tris.ctypes.data, bnd.ctypes.data)
+    finally:
+        lib.auxgen_free(h)
+    return LinearSystem(A, b, xy), TriMesh(nodes, tris, bnd[:B])
