@@ -254,6 +254,13 @@ aux_status aux_system_copy(const aux_system* s, int32_t* row_ptr, int32_t* col_i
                            double* xy);
 void aux_system_destroy(aux_system* s);
 
+/* galerkin_dense (hierarchy.hpp:239-247): P^T A P for an
+ * arbitrary partition agg_of (n_rows entries, ids in [0, n_agg)) into the
+ * caller's n_agg x n_agg row-major C, every element summed in the reference's
+ * order (bitwise).  size_error if the map does not match the matrix. */
+aux_status aux_galerkin_dense(const aux_csr_view* A, const int32_t* agg_of, int64_t n_agg_of, int32_t n_agg,
+                              int32_t device, double* C, char* msg, size_t msg_len);
+
 /* ---- measurement hooks (bench.py; not part of the reference API) ---- */
 /* Number of kernels this library launched (graph nodes count per replay). */
 int64_t aux_launch_count(void);

@@ -937,3 +937,16 @@ int orc_point_gs_sweep_ell(int k, const int* col, const double* val, const doubl
 }
 
 double orc_dot(const double* a, const double* b, int64_t n) { return dot(a, b, (size_t)n); }
+
+/* galerkin_dense (hierarchy.hpp:239-247): C(agg(i), agg(j)) += a_ij over rows
+ * i ascending, then the row's entries in storage order, into a zeroed
+ * n_agg x n_agg row-major matrix.  Returns AUX_SIZE_ERROR when the map does
+ * not match the matrix (hierarchy.hpp:240-241). */
+int orc_galerkin_dense(const aux_csr_view* A, const int32_t* agg_of, int64_t n_agg_of, int32_t n_agg, double* C) {
+    if (n_agg_of != A->n_rows) return AUX_SIZE_ERROR;
+    memset(C, 0, sizeof(double) * (size_t)n_agg * (size_t)n_agg);
+    for (int i = 0; i < A->n_rows; ++i)
+        for (int p = A->row_ptr[i]; p < A->row_ptr[i + 1]; ++p)
+            C[(size_t)agg_of[i] * n_agg + agg_of[A->col_idx[p]]] += A->values[p];
+    return AUX_OK;
+}

@@ -166,3 +166,15 @@ def point_gs_sweep_ell(kind, k, col, val, b, x, dir_):
 def dot(kind, a, b):
     lib, p = _load(kind)
     return getattr(lib, p + "dot")(a.ctypes.data, b.ctypes.data, a.size)
+
+
+def galerkin_dense(kind, A, agg_of, n_agg):
+    """galerkin_dense (hierarchy.hpp:239-247) through the oracle or the reference."""
+    lib, p = _load(kind)
+    agg = np.ascontiguousarray(agg_of, dtype=np.int32)
+    C_ = np.zeros((n_agg, n_agg), np.float64)
+    v = csr_view(A)
+    s = getattr(lib, p + "galerkin_dense")(C.byref(v), C.c_void_p(agg.ctypes.data), C.c_int64(agg.size),
+                                            C.c_int32(n_agg), C.c_void_p(C_.ctypes.data))
+    _abi.raise_for(s, b"galerkin_dense")
+    return C_

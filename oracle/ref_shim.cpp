@@ -224,4 +224,17 @@ double ref_dot(const double* a, const double* b, int64_t n) {
     return auxamg::dot(std::span<const double>(a, n), std::span<const double>(b, n));
 }
 
+// auxamg::galerkin_dense (hierarchy.hpp:239-247) on an arbitrary partition
+int ref_galerkin_dense(const aux_csr_view* Av, const int32_t* agg_of, int64_t n_agg_of, int32_t n_agg, double* C) {
+    return guarded(nullptr, 0, [&] {
+        const auxamg::CsrMatrix A = to_csr(Av);
+        auxamg::AggregationMap agg;
+        agg.n_aggregates = n_agg;
+        agg.agg_of.assign(agg_of, agg_of + n_agg_of);
+        const auxamg::DenseMatrix D = auxamg::galerkin_dense(A, agg);
+        for (int r = 0; r < n_agg; ++r)
+            for (int c = 0; c < n_agg; ++c) C[(size_t)r * n_agg + c] = D(r, c);
+    });
+}
+
 }  // extern "C"

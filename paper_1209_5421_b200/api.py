@@ -85,6 +85,8 @@ def lib():
     L.aux_system_copy.argtypes = [vp, vp, vp, vp, vp, vp]
     L.aux_system_copy.restype = C.c_int
     L.aux_system_destroy.argtypes = [vp]
+    L.aux_galerkin_dense.argtypes = [vp, vp, i64, i32, i32, vp, C.c_char_p, sz]
+    L.aux_galerkin_dense.restype = C.c_int
     L.aux_part_rows.argtypes = [vp]
     L.aux_part_rows.restype = i32
     _lib = L
@@ -529,3 +531,15 @@ class DeviceSystem:
                 self._s = None
         except Exception:
             pass
+
+
+def galerkin_dense(A: CsrMatrix, agg_of, n_agg: int, device: int = 0) -> np.ndarray:
+    """galerkin_dense (hierarchy.hpp:239-247) on the GPU: dense P^T A P for an arbitrary partition."""
+    A = _prep_csr(A)
+    agg = np.ascontiguousarray(agg_of, dtype=np.int32)
+    out = np.zeros((n_agg, n_agg), np.float64)
+    msg = C.create_string_buffer(512)
+    s = lib().aux_galerkin_dense(C.byref(_csr_view(A)), agg.ctypes.data, agg.size, n_agg, device, out.ctypes.data,
+                                 msg, 512)
+    _abi.raise_for(s, msg.raw)
+    return out

@@ -200,6 +200,31 @@ __global__ void k_asm_load(const unsigned* __restrict__ brow, const double* __re
     }
 }
 
+// ---- galerkin_dense (hierarchy.hpp:239-247): one key
+// agg(i) * n_agg + agg(j) per stored entry, emitted in storage order (rows
+// ascending, entries in row order), a stable radix sort, then every run summed
+// sequentially from 0.0 -- the reference's accumulation order per element.
+__global__ void k_gd_keys(const int* __restrict__ rp, const int* __restrict__ col, const int* __restrict__ agg,
+                          int n, int n_agg, unsigned* __restrict__ key, unsigned long long* bad) {
+    GSTRIDE(i, n) {
+        const int ai = agg[i];
+        if (ai < 0 || ai >= n_agg) atomicMin(bad, (unsigned long long)i);
+        for (int p = rp[i]; p < rp[i + 1]; ++p) {
+            const int aj = agg[col[p]];
+            key[p] = (unsigned)ai * (unsigned)n_agg + (unsigned)aj;
+        }
+    }
+}
+__global__ void k_gd_sum(const unsigned* __restrict__ skey, const int* __restrict__ idx,
+                         const double* __restrict__ v, long m, double* __restrict__ C) {
+    GSTRIDE(i, m) {
+        if (i > 0 && skey[i - 1] == skey[i]) continue;
+        double sum = 0.0;
+        for (long j = i; j < m && skey[j] == skey[i]; ++j) sum += v[idx[j]];
+        C[skey[i]] = sum;
+    }
+}
+
 int bits_for(unsigned long v) {
     int b = 1;
     while ((1ul << b) <= v) ++b;
@@ -354,5 +379,48 @@ aux_status aux_system_copy(const aux_system* S, int32_t* row_ptr, int32_t* col_i
 }
 
 void aux_system_destroy(aux_system* S) { delete S; }
+
+aux_status aux_galerkin_dense(const aux_csr_view* A, const int32_t* agg_of, int64_t n_agg_of, int32_t n_agg,
+                              int32_t device, double* C, char* msg, size_t msg_len) {
+    cudaStream_t s = nullptr;
+    try {
+        if (n_agg_of != A->n_rows) throw_aux(AUX_SIZE_ERROR, "galerkin_dense: map does not match matrix");
+        if (n_agg < 1 || (long)n_agg * n_agg >= (1l << 32))
+            throw_aux(AUX_CAPACITY_ERROR, "galerkin_dense: aggregate count out of range for a dense result");
+        AUX_CUDA(cudaSetDevice(device));
+        AUX_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        const int n = A->n_rows;
+        const long m = A->nnz;
+        DBuf<int> rp(n + 1), col(std::max<long>(m, 1)), agg(std::max(n, 1)), idx(std::max<long>(m, 1));
+        DBuf<double> v(std::max<long>(m, 1)), Cd((size_t)n_agg * n_agg);
+        DBuf<unsigned> key(std::max<long>(m, 1));
+        DBuf<unsigned long long> bad(1);
+        AUX_CUDA(cudaMemcpyAsync(rp.p, A->row_ptr, sizeof(int) * (n + 1), cudaMemcpyHostToDevice, s));
+        if (m) {
+            AUX_CUDA(cudaMemcpyAsync(col.p, A->col_idx, sizeof(int) * m, cudaMemcpyHostToDevice, s));
+            AUX_CUDA(cudaMemcpyAsync(v.p, A->values, sizeof(double) * m, cudaMemcpyHostToDevice, s));
+        }
+        if (n) AUX_CUDA(cudaMemcpyAsync(agg.p, agg_of, sizeof(int) * n, cudaMemcpyHostToDevice, s));
+        AUX_CUDA(cudaMemsetAsync(Cd.p, 0, sizeof(double) * (size_t)n_agg * n_agg, s));
+        AUX_CUDA(cudaMemsetAsync(bad.p, 0xff, sizeof(unsigned long long), s));
+        k_gd_keys<<<grid_for(n), kT, 0, s>>>(rp.p, col.p, agg.p, n, n_agg, key.p, bad.p);
+        AUX_LAUNCHED(1);
+        if (read1(bad.p, s) != ~0ull) throw_aux(AUX_ARGUMENT_ERROR, "galerkin_dense: aggregate id out of range");
+        if (m) {
+            radix_sort_pairs(key.p, idx.p, m, bits_for((unsigned long)n_agg * n_agg), s, true);
+            k_gd_sum<<<grid_for(m), kT, 0, s>>>(key.p, idx.p, v.p, m, Cd.p);
+            AUX_LAUNCHED(1);
+        }
+        AUX_CUDA(cudaMemcpyAsync(C, Cd.p, sizeof(double) * (size_t)n_agg * n_agg, cudaMemcpyDeviceToHost, s));
+        AUX_CUDA(cudaStreamSynchronize(s));
+        cudaStreamDestroy(s);
+        if (msg && msg_len) msg[0] = 0;
+        return AUX_OK;
+    } catch (const AuxError& e) {
+        if (s) { cudaStreamSynchronize(s); cudaStreamDestroy(s); }
+        if (msg && msg_len) std::snprintf(msg, msg_len, "%s", e.what());
+        return e.code;
+    }
+}
 
 }  // extern "C"

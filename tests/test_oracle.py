@@ -185,3 +185,26 @@ def test_level_stack_n17_kat(kind):
     s16 = problems.poisson5(16)
     e16 = ob.CpuHierarchy(kind, s16.A, s16.coords).export()
     assert e16["stats"]["sizes"] == [225, 64] and e16["levels"][1]["k"] == 3
+
+
+def test_galerkin_dense_oracle_pinned_to_reference():
+    """galerkin_dense (hierarchy.hpp:239-247) on random SPD matrices with random
+    surjective partitions (acceptance.cpp:55-65) and on a level-L partition:
+    oracle == reference bitwise."""
+    from paper_1209_5421_b200 import problems
+    rng = np.random.default_rng(5)
+    cases = []
+    for trial in range(6):
+        n = 16 + 37 * trial
+        A = problems.random_spd(n, 1000 + trial)
+        n_agg = 4 + trial % 13
+        agg = rng.integers(0, n_agg, n).astype(np.int32)
+        agg[:n_agg] = np.arange(n_agg)   # surjective
+        cases.append((A, agg, n_agg))
+    s = problems.jittered_p1(33)
+    e = ob.CpuHierarchy("ref", s.A, s.coords).export()
+    cases.append((s.A, e["levels"][0]["agg_of"].astype(np.int32), int(e["levels"][1]["n"])))
+    for A, agg, n_agg in cases:
+        c_ref = ob.galerkin_dense("ref", A, agg, n_agg)
+        c_orc = ob.galerkin_dense("oracle", A, agg, n_agg)
+        assert np.array_equal(c_ref, c_orc)
