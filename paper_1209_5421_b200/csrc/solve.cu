@@ -186,6 +186,57 @@ __global__ void __launch_bounds__(kRedThreads) k_mgs(Span sp, double* __restrict
     if (grid_reduce<2>(v, rs, out) && threadIdx.x == 0) finalize(fin, out);
 }
 
+// The outer loop's MGS step (the same arithmetic as k_mgs) on whole vectors:
+// 16-byte loads, two pairs of elements in flight per thread, the kept
+// directions streamed with evict-first loads so p and ap stay in L2 across
+// the chain.  n even, 16-byte aligned vectors.
+__global__ void __launch_bounds__(kRedThreads) k_mgs_vec(long n, double* __restrict__ p, double* __restrict__ ap,
+                                                        const double* __restrict__ pj,
+                                                        const double* __restrict__ apj,
+                                                        const double* __restrict__ w, const double* __restrict__ r,
+                                                        int mode, const double* sc, RedState rs, Fin fin) {
+    pdl_trigger();
+    pdl_wait();
+    const double beta = sc[1];
+    double v[2] = {0.0, 0.0};
+    double2* p2 = reinterpret_cast<double2*>(p);
+    double2* a2 = reinterpret_cast<double2*>(ap);
+    const double2* pj2 = reinterpret_cast<const double2*>(pj);
+    const double2* aj2 = reinterpret_cast<const double2*>(apj);
+    const double2* w2 = reinterpret_cast<const double2*>(mode == 0 ? w : r);
+    const long n2 = n / 2, stride = (long)gridDim.x * blockDim.x;
+    auto step = [&](const double2 P, const double2 A, const double2 PJ, const double2 AJ, const double2 W, long k) {
+        double2 pn, an;
+        pn.x = __dadd_rn(P.x, __dmul_rn(beta, PJ.x));
+        pn.y = __dadd_rn(P.y, __dmul_rn(beta, PJ.y));
+        an.x = __dadd_rn(A.x, __dmul_rn(beta, AJ.x));
+        an.y = __dadd_rn(A.y, __dmul_rn(beta, AJ.y));
+        p2[k] = pn;
+        a2[k] = an;
+        if (mode == 0) {
+            v[0] = __dadd_rn(v[0], __dmul_rn(pn.x, W.x));
+            v[0] = __dadd_rn(v[0], __dmul_rn(pn.y, W.y));
+        } else {
+            v[0] = __dadd_rn(v[0], __dmul_rn(pn.x, an.x));
+            v[0] = __dadd_rn(v[0], __dmul_rn(pn.y, an.y));
+            v[1] = __dadd_rn(v[1], __dmul_rn(W.x, pn.x));
+            v[1] = __dadd_rn(v[1], __dmul_rn(W.y, pn.y));
+        }
+    };
+    long k = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    for (; k + stride < n2; k += 2 * stride) {
+        const long k2 = k + stride;
+        const double2 P0 = p2[k], P1 = p2[k2], A0 = a2[k], A1 = a2[k2];
+        const double2 J0 = __ldcs(pj2 + k), J1 = __ldcs(pj2 + k2), B0 = __ldcs(aj2 + k), B1 = __ldcs(aj2 + k2);
+        const double2 W0 = mode == 0 ? __ldcs(w2 + k) : w2[k], W1 = mode == 0 ? __ldcs(w2 + k2) : w2[k2];
+        step(P0, A0, J0, B0, W0, k);
+        step(P1, A1, J1, B1, W1, k2);
+    }
+    for (; k < n2; k += stride) step(p2[k], a2[k], __ldcs(pj2 + k), __ldcs(aj2 + k), w2[k], k);
+    double out[2];
+    if (grid_reduce<2>(v, rs, out) && threadIdx.x == 0) finalize(fin, out);
+}
+
 // u (+)= alpha p; r -= alpha ap (cycle.hpp:124-126, 233-235), skipped after a
 // breakdown.  assign: u starts at zero (first step).  norm: s0 = r.r.
 __global__ void __launch_bounds__(kRedThreads) k_update(long n, double* __restrict__ u, const double* __restrict__ p,
@@ -213,6 +264,39 @@ __global__ void __launch_bounds__(kRedThreads) k_update(long n, double* __restri
         double out[1];
         if (grid_reduce<1>(v, rs, out) && threadIdx.x == 0) finalize(fin, out);
     }
+}
+
+// The outer update u += alpha p; r -= alpha ap; s0 = r.r (same arithmetic as
+// k_update with assign = 0, upd_r = 1, norm = 1) with 16-byte accesses.
+__global__ void __launch_bounds__(kRedThreads) k_update_vec(long n, double* __restrict__ u,
+                                                           const double* __restrict__ p, double* __restrict__ r,
+                                                           const double* __restrict__ ap, const double* sc,
+                                                           RedState rs, Fin fin) {
+    const double alpha = sc[0];
+    const bool dead = sc[2] != 0.0;
+    const double nalpha = -alpha;
+    double v[1] = {0.0};
+    if (!dead) {
+        double2* u2 = reinterpret_cast<double2*>(u);
+        double2* r2 = reinterpret_cast<double2*>(r);
+        const double2* p2 = reinterpret_cast<const double2*>(p);
+        const double2* a2 = reinterpret_cast<const double2*>(ap);
+        const long n2 = n / 2, stride = (long)gridDim.x * blockDim.x;
+        for (long k = blockIdx.x * (long)blockDim.x + threadIdx.x; k < n2; k += stride) {
+            const double2 U = u2[k], P = p2[k], R = r2[k], A = a2[k];
+            double2 un, rn;
+            un.x = __dadd_rn(U.x, __dmul_rn(alpha, P.x));
+            un.y = __dadd_rn(U.y, __dmul_rn(alpha, P.y));
+            rn.x = __dadd_rn(R.x, __dmul_rn(nalpha, A.x));
+            rn.y = __dadd_rn(R.y, __dmul_rn(nalpha, A.y));
+            u2[k] = un;
+            r2[k] = rn;
+            v[0] = __dadd_rn(v[0], __dmul_rn(rn.x, rn.x));
+            v[0] = __dadd_rn(v[0], __dmul_rn(rn.y, rn.y));
+        }
+    }
+    double out[1];
+    if (grid_reduce<1>(v, rs, out) && threadIdx.x == 0) finalize(fin, out);
 }
 
 __global__ void __launch_bounds__(kRedThreads) k_dot(long n, const double* __restrict__ a, const double* __restrict__ b,
@@ -1102,15 +1186,26 @@ void pcg_tiles(Ctx& c, int m) {
         if (i > 0) {
             for (int j = 1; j < i; ++j) {
                 const Route rj = route(c, L.dist, Fin{2, sc, sc + 3 + j, nullptr});
-                launch_pdl(k_mgs, dim3(nb), dim3(kRedThreads), 0, c.s, sp, P.p[i].p, P.ap[i].p, P.p[j - 1].p,
-                           P.ap[j - 1].p, (const double*)P.ap[j].p, (const double*)nullptr, 0, (const double*)sc,
-                           c.rs, rj.launch);
+                if (!L.dist)
+                    launch_pdl(k_mgs_vec, dim3(red_blocks(sp.n / 2)), dim3(kRedThreads), 0, c.s, sp.n, P.p[i].p,
+                               P.ap[i].p, (const double*)P.p[j - 1].p, (const double*)P.ap[j - 1].p,
+                               (const double*)P.ap[j].p, (const double*)nullptr, 0, (const double*)sc, c.rs,
+                               rj.launch);
+                else
+                    launch_pdl(k_mgs, dim3(nb), dim3(kRedThreads), 0, c.s, sp, P.p[i].p, P.ap[i].p, P.p[j - 1].p,
+                               P.ap[j - 1].p, (const double*)P.ap[j].p, (const double*)nullptr, 0,
+                               (const double*)sc, c.rs, rj.launch);
                 routed(c, rj);
             }
             const Route rf = route(c, L.dist, Fin{1, sc, nullptr, sc + 3 + i, sc + sc_alpha(ni, i), sc + sc_nval(ni), i});
-            launch_pdl(k_mgs, dim3(nb), dim3(kRedThreads), 0, c.s, sp, P.p[i].p, P.ap[i].p, P.p[i - 1].p,
-                       P.ap[i - 1].p, (const double*)nullptr, (const double*)R[i & 1], 1, (const double*)sc, c.rs,
-                       rf.launch);
+            if (!L.dist)
+                launch_pdl(k_mgs_vec, dim3(red_blocks(sp.n / 2)), dim3(kRedThreads), 0, c.s, sp.n, P.p[i].p,
+                           P.ap[i].p, (const double*)P.p[i - 1].p, (const double*)P.ap[i - 1].p,
+                           (const double*)nullptr, (const double*)R[i & 1], 1, (const double*)sc, c.rs, rf.launch);
+            else
+                launch_pdl(k_mgs, dim3(nb), dim3(kRedThreads), 0, c.s, sp, P.p[i].p, P.ap[i].p, P.p[i - 1].p,
+                           P.ap[i - 1].p, (const double*)nullptr, (const double*)R[i & 1], 1, (const double*)sc,
+                           c.rs, rf.launch);
             routed(c, rf);
         }
         ring_exchange(c, m, {P.p[i].p, P.ap[i].p});
@@ -1473,6 +1568,7 @@ void solve_device(aux_hierarchy* h, const double* b, long n_b, const aux_cycle_o
         }
         std::deque<int> kept;
         std::vector<char> in_use(slots, 0);
+        const bool vec_ok = (n % 2) == 0;   // device vectors are 256-byte aligned allocations
         double* r = h->w_r.p;
         double* u = h->w_u.p;
         const double spmv_bytes = 12.0 * F.nnz + 4.0 * (n + 1) + 16.0 * n;
@@ -1506,21 +1602,34 @@ void solve_device(aux_hierarchy* h, const double* b, long n_b, const aux_cycle_o
             if (!kept.empty()) {
                 for (size_t j = 1; j < kept.size(); ++j) {
                     const Route rj = route(c, fd, Fin{2, sc, sc + 8 + kept[j], nullptr});
-                    k_mgs<<<red_blocks(n), kRedThreads, 0, s>>>(flat_span(n), p, ap, h->w_p[kept[j - 1]].p,
-                                                               h->w_ap[kept[j - 1]].p, h->w_ap[kept[j]].p, nullptr, 0,
-                                                               sc, rs, rj.launch);
+                    if (vec_ok)
+                        k_mgs_vec<<<red_blocks(n / 2), kRedThreads, 0, s>>>(n, p, ap, h->w_p[kept[j - 1]].p,
+                                                                           h->w_ap[kept[j - 1]].p, h->w_ap[kept[j]].p,
+                                                                           nullptr, 0, sc, rs, rj.launch);
+                    else
+                        k_mgs<<<red_blocks(n), kRedThreads, 0, s>>>(flat_span(n), p, ap, h->w_p[kept[j - 1]].p,
+                                                                   h->w_ap[kept[j - 1]].p, h->w_ap[kept[j]].p, nullptr,
+                                                                   0, sc, rs, rj.launch);
                     AUX_LAUNCHED(1);
                     routed(c, rj);
                 }
                 const Route rf = route(c, fd, Fin{1, sc, nullptr, e_slot});
-                k_mgs<<<red_blocks(n), kRedThreads, 0, s>>>(flat_span(n), p, ap, h->w_p[kept.back()].p,
-                                                           h->w_ap[kept.back()].p, nullptr, r, 1, sc, rs, rf.launch);
+                if (vec_ok)
+                    k_mgs_vec<<<red_blocks(n / 2), kRedThreads, 0, s>>>(n, p, ap, h->w_p[kept.back()].p,
+                                                                       h->w_ap[kept.back()].p, nullptr, r, 1, sc, rs,
+                                                                       rf.launch);
+                else
+                    k_mgs<<<red_blocks(n), kRedThreads, 0, s>>>(flat_span(n), p, ap, h->w_p[kept.back()].p,
+                                                               h->w_ap[kept.back()].p, nullptr, r, 1, sc, rs, rf.launch);
                 AUX_LAUNCHED(1);
                 routed(c, rf);
             }
             {
                 const Route ru = route(c, fd, Fin{3, sc, nullptr, sc + 3});
-                k_update<<<red_blocks(n), kRedThreads, 0, s>>>(n, u, p, r, ap, 0, 1, 1, sc, rs, ru.launch);
+                if (vec_ok)
+                    k_update_vec<<<red_blocks(n / 2), kRedThreads, 0, s>>>(n, u, p, r, ap, sc, rs, ru.launch);
+                else
+                    k_update<<<red_blocks(n), kRedThreads, 0, s>>>(n, u, p, r, ap, 0, 1, 1, sc, rs, ru.launch);
                 AUX_LAUNCHED(1);
                 routed(c, ru);
             }
