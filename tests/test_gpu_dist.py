@@ -38,6 +38,24 @@ def test_parts_match_oracle(gpu_api, parts, name, make):
         assert sp.operator_complexity == s1.operator_complexity
 
 
+@pytest.mark.parametrize("parts", [2, 4, 8])
+@pytest.mark.parametrize("name,make", [
+    ("disk_257", lambda: problems.disk_p1(257)),                    # empty cells, curved boundary
+    ("graded2_257", lambda: problems.graded_p1(257, 2.0)),          # dropped + same-colour couplings
+    ("jump_257", lambda: problems.jittered_p1(257, jump=1e3)),      # jump coefficient (C4 family)
+])
+def test_parts_hard_problems(gpu_api, parts, name, make):
+    s = make()
+    u, res, st = gpu_api.solve_parts(s.A, s.coords, s.b, parts)
+    ref = ob.CpuHierarchy("oracle", s.A, s.coords).solve(s.b)
+    assert abs(res[0].iterations - ref["iterations"]) <= 1
+    err = np.max(np.abs(u - ref["u"])) / np.max(np.abs(ref["u"]))
+    assert err <= U_TOL, err
+    h1 = gpu_api.setup_hierarchy(s.A, s.coords)
+    assert list(st[0].nnz) == list(h1.stats().nnz)
+    assert h1.locality() == gpu_api.setup_hierarchy(s.A, s.coords).locality()
+
+
 def test_parts_cycle_options(gpu_api):
     s = problems.jittered_p1(257)
     for o in (dict(pre_sweeps=2, post_sweeps=2), dict(n_inner=3), dict(max_directions=3)):
