@@ -54,14 +54,27 @@ __device__ int g_fclk_launch;
 #define FCLK_BEGIN fclk_t0 = clock64();
 #define FCLK_END(T, Q)                                                        \
     if (threadIdx.x == 0) { s_clk[(T) * 4 + ((Q) & 3)] += clock64() - fclk_t0; s_cnt[(T) * 4 + ((Q) & 3)]++; }
+__device__ unsigned long long g_ph[32], g_phn[32];
+__device__ long long g_ph_last;
+#define PH_RESET if (threadIdx.x == 0) g_ph_last = clock64();
+#define PH(ID)                                                                \
+    if (threadIdx.x == 0) {                                                   \
+        const long long t_ = clock64();                                       \
+        atomicAdd(&g_ph[ID], (unsigned long long)(t_ - g_ph_last));           \
+        atomicAdd(&g_phn[ID], 1ull);                                          \
+        g_ph_last = t_;                                                       \
+    }
 #define FCLK_REPORT                                                           \
     if (threadIdx.x == 0 && atomicAdd(&g_fclk_launch, 1) == 2) {            \
         printf("fused clk prologue %lld cycles, state machine %lld cycles\n", fclk_k1 - fclk_k0, clock64() - fclk_k1); \
+        for (int k_ = 0; k_ < 32; ++k_) if (g_phn[k_]) printf("phase %2d: %llu calls, %llu cycles avg\n", k_, g_phn[k_], g_ph[k_] / g_phn[k_]); \
         for (int k = 0; k < 16; ++k)                                          \
             if (s_cnt[k]) printf("fused clk type %d level %d: calls %u avg %llu cycles\n", k / 4, k % 4, s_cnt[k], \
                                  s_clk[k] / s_cnt[k]);                        \
     }
 #else
+#define PH_RESET
+#define PH(ID)
 #define FCLK_START
 #define FCLK_DECL
 #define FCLK_BEGIN
@@ -306,6 +319,9 @@ __device__ __forceinline__ double child_resid(const SLevel& L, int T1, int T2, c
 // (cycle.hpp:173-178).  The first pass applies the pending PCG residual
 // update of this level, relaxes colour 0 from zero and writes u = 0 elsewhere.
 __device__ void cycle_down(const FusedArgs& a, const SLevel& L, PState& ps, const SLevel& Cc, double* u) {
+    PH_RESET
+    const int po = L.n > 256 ? 0 : 16;
+    (void)po;
     double* f = L.r;
     const bool pend = ps.pend != 0;
     const double na = pend ? -ps.alpha[ps.step - 1] : 0.0;
@@ -322,9 +338,13 @@ __device__ void cycle_down(const FusedArgs& a, const SLevel& L, PState& ps, cons
     }
     ps.pend = 0;
     __syncthreads();
+    PH(po + 0)
     gs_pass<1>(L, f, u);
+    PH(po + 1)
     gs_pass<2>(L, f, u);
+    PH(po + 2)
     gs_pass<3>(L, f, u);
+    PH(po + 3)
     for (int sw = 1; sw < a.pre; ++sw) gs_sweep(L, f, u, true);
     // restriction into the child's PCG residual
     for (int Q = threadIdx.x; Q < Cc.n; Q += kThreads) {
@@ -339,24 +359,41 @@ __device__ void cycle_down(const FusedArgs& a, const SLevel& L, PState& ps, cons
         Cc.r[pidx(Cc, cq, ac, bc)] = sum;
     }
     __syncthreads();
+    PH(po + 4)
 }
 
 // u_i += ec[parent(i)] on active cells (cycle.hpp:191-194) with
 // ec = ((0 + alpha_0 p_0) + alpha_1 p_1) ... the child's PCG iterate, then the
 // transposed post-smoothing (cycle.hpp:196).
 __device__ void cycle_up(const FusedArgs& a, const SLevel& L, const SLevel& Cc, const PState& cs, double* u) {
-    for (int ci = threadIdx.x; ci < L.n; ci += kThreads) {
-        if (!L.act[ci]) continue;
-        const int c = ci >> (2 * L.lh), pos = ci & (L.nq - 1);
+    PH_RESET
+    const int po = L.n > 256 ? 0 : 16;
+    (void)po;
+    // the child's alphas in registers (PState lives in local memory), and the
+    // four children of a parent handled by one thread: the parent's
+    // correction e is formed once, in the axpy order (cycle.hpp:124)
+    const int nval = cs.nval;
+    double al[kFusedMaxInner];
+#pragma unroll
+    for (int k = 0; k < kFusedMaxInner; ++k) al[k] = k < nval ? cs.alpha[k] : 0.0;
+    for (int pos = threadIdx.x; pos < L.nq; pos += kThreads) {
         const int A = pos & (L.H - 1), B = pos >> L.lh;   // parent cell (A, B) on the child level
         const int pc = pidx(Cc, (A & 1) | ((B & 1) << 1), A >> 1, B >> 1);
         double e = 0.0;
-        for (int k = 0; k < cs.nval; ++k) e = __dadd_rn(e, __dmul_rn(cs.alpha[k], Cc.p[k * 4 * Cc.PP + pc]));
-        const int pi = pidx(L, c, A, B);
-        u[pi] = __dadd_rn(u[pi], e);
+#pragma unroll
+        for (int k = 0; k < kFusedMaxInner; ++k)
+            if (k < nval) e = __dadd_rn(e, __dmul_rn(al[k], Cc.p[k * 4 * Cc.PP + pc]));
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            if (!L.act[c * L.nq + pos]) continue;
+            const int pi = pidx(L, c, A, B);
+            u[pi] = __dadd_rn(u[pi], e);
+        }
     }
     __syncthreads();
+    PH(po + 5)
     for (int sw = 0; sw < a.post; ++sw) gs_sweep(L, L.r, u, false);
+    PH(po + 6)
 }
 
 template <int C>
@@ -388,11 +425,15 @@ __device__ bool pcg_step(const FusedArgs& a, const SLevel& L, PState& ps, double
     bool dead;
     double s0 = 0.0, s1 = 0.0;
     const int mode = i == 0 ? 0 : 1;
+    PH_RESET
+    const int po = L.n > 256 ? 0 : 16;
+    (void)po;
     spmv_color<0>(L, p, ap, L.r, L.ap, mode, s0, s1);
     spmv_color<1>(L, p, ap, L.r, L.ap, mode, s0, s1);
     spmv_color<2>(L, p, ap, L.r, L.ap, mode, s0, s1);
     spmv_color<3>(L, p, ap, L.r, L.ap, mode, s0, s1);
     bsum2(red, par, s0, s1);
+    PH(po + 7)
     if (i == 0) {
         ps.e[0] = s0;
         dead = !(s0 > kBreak);
@@ -421,6 +462,7 @@ __device__ bool pcg_step(const FusedArgs& a, const SLevel& L, PState& ps, double
                 }
             }
             bsum2(red, par, t0, t1);
+            PH(po + 8)
             if (fin) {
                 ps.e[i] = t0;
                 dead = !(t0 > kBreak);
