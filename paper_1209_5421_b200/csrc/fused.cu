@@ -252,6 +252,56 @@ __device__ __forceinline__ void gs_sweep(const SLevel& L, const double* f, doubl
     }
 }
 
+// ---- top fused level with nq == kThreads: thread t owns the four cells at
+// plane position t (one per colour) in every phase, so their 36 stencil
+// values live in registers for the whole kernel (RV) and each phase reads
+// only vectors from shared memory.  Same operations in the same order as the
+// shared-memory versions above (bitwise identical results).
+struct RV {
+    double v[4][9];
+};
+
+template <int C>
+__device__ __forceinline__ double row9_r(const SLevel& L, const RV& rv, int pi, const double* x) {
+    const double* v = rv.v[C];
+    double s = __dadd_rn(0.0, __dmul_rn(v[0], x[pi]));
+    s = __dadd_rn(s, __dmul_rn(v[1], x[pi + noff<C, 1>(L)]));
+    s = __dadd_rn(s, __dmul_rn(v[2], x[pi + noff<C, 2>(L)]));
+    s = __dadd_rn(s, __dmul_rn(v[3], x[pi + noff<C, 3>(L)]));
+    s = __dadd_rn(s, __dmul_rn(v[4], x[pi + noff<C, 4>(L)]));
+    s = __dadd_rn(s, __dmul_rn(v[5], x[pi + noff<C, 5>(L)]));
+    s = __dadd_rn(s, __dmul_rn(v[6], x[pi + noff<C, 6>(L)]));
+    s = __dadd_rn(s, __dmul_rn(v[7], x[pi + noff<C, 7>(L)]));
+    s = __dadd_rn(s, __dmul_rn(v[8], x[pi + noff<C, 8>(L)]));
+    return s;
+}
+
+template <int C>
+__device__ __forceinline__ void gs_pass_r(const SLevel& L, const RV& rv, const double* f, double* x) {
+    const int pos = threadIdx.x;
+    const int pi = pidx(L, C, pos & (L.H - 1), pos >> L.lh);
+    const double* v = rv.v[C];
+    double s = f[pi];
+    s = __dsub_rn(s, __dmul_rn(v[1], x[pi + noff<C, 1>(L)]));
+    s = __dsub_rn(s, __dmul_rn(v[2], x[pi + noff<C, 2>(L)]));
+    s = __dsub_rn(s, __dmul_rn(v[3], x[pi + noff<C, 3>(L)]));
+    s = __dsub_rn(s, __dmul_rn(v[4], x[pi + noff<C, 4>(L)]));
+    s = __dsub_rn(s, __dmul_rn(v[5], x[pi + noff<C, 5>(L)]));
+    s = __dsub_rn(s, __dmul_rn(v[6], x[pi + noff<C, 6>(L)]));
+    s = __dsub_rn(s, __dmul_rn(v[7], x[pi + noff<C, 7>(L)]));
+    s = __dsub_rn(s, __dmul_rn(v[8], x[pi + noff<C, 8>(L)]));
+    x[pi] = __ddiv_rn(s, v[0]);
+    __syncthreads();
+}
+
+__device__ __forceinline__ void gs_sweep_r(const SLevel& L, const RV& rv, const double* f, double* x, bool fwd) {
+    if (fwd) {
+        gs_pass_r<0>(L, rv, f, x); gs_pass_r<1>(L, rv, f, x); gs_pass_r<2>(L, rv, f, x); gs_pass_r<3>(L, rv, f, x);
+    } else {
+        gs_pass_r<3>(L, rv, f, x); gs_pass_r<2>(L, rv, f, x); gs_pass_r<1>(L, rv, f, x); gs_pass_r<0>(L, rv, f, x);
+    }
+}
+
 // Coarsest solve (cycle.hpp:152-155).  The coarsest level's vectors are padded
 // too; the inverse is stored in colour-major (compact) order.
 __device__ void coarse_solve(const FusedArgs& a, const double* inv, double* part, const SLevel& L, PState& ps,
@@ -318,7 +368,8 @@ __device__ __forceinline__ double child_resid(const SLevel& L, int T1, int T2, c
 // Pre-smoothing from u = 0 (cycle.hpp:170-171) and the restricted residual
 // (cycle.hpp:173-178).  The first pass applies the pending PCG residual
 // update of this level, relaxes colour 0 from zero and writes u = 0 elsewhere.
-__device__ void cycle_down(const FusedArgs& a, const SLevel& L, PState& ps, const SLevel& Cc, double* u) {
+__device__ void cycle_down(const FusedArgs& a, const SLevel& L, PState& ps, const SLevel& Cc, double* u,
+                           const RV* rv) {
     PH_RESET
     const int po = L.n > 256 ? 0 : 16;
     (void)po;
@@ -339,13 +390,35 @@ __device__ void cycle_down(const FusedArgs& a, const SLevel& L, PState& ps, cons
     ps.pend = 0;
     __syncthreads();
     PH(po + 0)
-    gs_pass<1>(L, f, u);
-    PH(po + 1)
-    gs_pass<2>(L, f, u);
-    PH(po + 2)
-    gs_pass<3>(L, f, u);
-    PH(po + 3)
-    for (int sw = 1; sw < a.pre; ++sw) gs_sweep(L, f, u, true);
+    if (rv) {
+        gs_pass_r<1>(L, *rv, f, u);
+        gs_pass_r<2>(L, *rv, f, u);
+        gs_pass_r<3>(L, *rv, f, u);
+        for (int sw = 1; sw < a.pre; ++sw) gs_sweep_r(L, *rv, f, u, true);
+    } else {
+        gs_pass<1>(L, f, u);
+        PH(po + 1)
+        gs_pass<2>(L, f, u);
+        PH(po + 2)
+        gs_pass<3>(L, f, u);
+        PH(po + 3)
+        for (int sw = 1; sw < a.pre; ++sw) gs_sweep(L, f, u, true);
+    }
+    if (rv) {   // thread t: the children at plane position t (all four colours)
+        const int t = threadIdx.x;
+        const int T1 = t & (L.H - 1), T2 = t >> L.lh;
+        const RV& r = *rv;
+        double sum = 0.0;
+        sum = __dadd_rn(sum, __dsub_rn(f[pidx(L, 0, T1, T2)], row9_r<0>(L, r, pidx(L, 0, T1, T2), u)));
+        sum = __dadd_rn(sum, __dsub_rn(f[pidx(L, 1, T1, T2)], row9_r<1>(L, r, pidx(L, 1, T1, T2), u)));
+        sum = __dadd_rn(sum, __dsub_rn(f[pidx(L, 2, T1, T2)], row9_r<2>(L, r, pidx(L, 2, T1, T2), u)));
+        sum = __dadd_rn(sum, __dsub_rn(f[pidx(L, 3, T1, T2)], row9_r<3>(L, r, pidx(L, 3, T1, T2), u)));
+        const int cq = (T1 & 1) | ((T2 & 1) << 1);
+        Cc.r[pidx(Cc, cq, T1 >> 1, T2 >> 1)] = sum;
+        __syncthreads();
+        PH(po + 4)
+        return;
+    }
     // restriction into the child's PCG residual
     for (int Q = threadIdx.x; Q < Cc.n; Q += kThreads) {
         const int cq = Q >> (2 * Cc.lh), pos = Q & (Cc.nq - 1);
@@ -365,7 +438,8 @@ __device__ void cycle_down(const FusedArgs& a, const SLevel& L, PState& ps, cons
 // u_i += ec[parent(i)] on active cells (cycle.hpp:191-194) with
 // ec = ((0 + alpha_0 p_0) + alpha_1 p_1) ... the child's PCG iterate, then the
 // transposed post-smoothing (cycle.hpp:196).
-__device__ void cycle_up(const FusedArgs& a, const SLevel& L, const SLevel& Cc, const PState& cs, double* u) {
+__device__ void cycle_up(const FusedArgs& a, const SLevel& L, const SLevel& Cc, const PState& cs, double* u,
+                         const RV* rv) {
     PH_RESET
     const int po = L.n > 256 ? 0 : 16;
     (void)po;
@@ -392,7 +466,10 @@ __device__ void cycle_up(const FusedArgs& a, const SLevel& L, const SLevel& Cc, 
     }
     __syncthreads();
     PH(po + 5)
-    for (int sw = 0; sw < a.post; ++sw) gs_sweep(L, L.r, u, false);
+    for (int sw = 0; sw < a.post; ++sw) {
+        if (rv) gs_sweep_r(L, *rv, L.r, u, false);
+        else gs_sweep(L, L.r, u, false);
+    }
     PH(po + 6)
 }
 
@@ -413,10 +490,27 @@ __device__ __forceinline__ void spmv_color(const SLevel& L, const double* x, dou
     }
 }
 
+template <int C>
+__device__ __forceinline__ void spmv_color_r(const SLevel& L, const RV& rv, const double* x, double* y, const double* r,
+                                           const double* w, int mode, double& s0, double& s1) {
+    for (int pos = threadIdx.x; pos < L.nq; pos += kThreads) {
+        const int pi = pidx(L, C, pos & (L.H - 1), pos >> L.lh);
+        const double yi = row9_r<C>(L, rv, pi, x);
+        y[pi] = yi;
+        const double xi = x[pi];
+        if (mode == 0) {
+            s0 = __dadd_rn(s0, __dmul_rn(xi, yi));
+            s1 = __dadd_rn(s1, __dmul_rn(r[pi], xi));
+        } else {
+            s0 = __dadd_rn(s0, __dmul_rn(xi, w[pi]));
+        }
+    }
+}
+
 // After the preconditioner application of step i: A z, the A-orthogonalisation
 // against the kept directions (cycle.hpp:84-97) and alpha (cycle.hpp:123).
 // Returns true when this PCG is finished (breakdown or last step).
-__device__ bool pcg_step(const FusedArgs& a, const SLevel& L, PState& ps, double* red, int& par) {
+__device__ bool pcg_step(const FusedArgs& a, const SLevel& L, PState& ps, double* red, int& par, const RV* rv) {
     const int vs = 4 * L.PP;
     const int i = ps.step;
     double* p = L.p + i * vs;
@@ -428,10 +522,17 @@ __device__ bool pcg_step(const FusedArgs& a, const SLevel& L, PState& ps, double
     PH_RESET
     const int po = L.n > 256 ? 0 : 16;
     (void)po;
-    spmv_color<0>(L, p, ap, L.r, L.ap, mode, s0, s1);
-    spmv_color<1>(L, p, ap, L.r, L.ap, mode, s0, s1);
-    spmv_color<2>(L, p, ap, L.r, L.ap, mode, s0, s1);
-    spmv_color<3>(L, p, ap, L.r, L.ap, mode, s0, s1);
+    if (rv) {
+        spmv_color_r<0>(L, *rv, p, ap, L.r, L.ap, mode, s0, s1);
+        spmv_color_r<1>(L, *rv, p, ap, L.r, L.ap, mode, s0, s1);
+        spmv_color_r<2>(L, *rv, p, ap, L.r, L.ap, mode, s0, s1);
+        spmv_color_r<3>(L, *rv, p, ap, L.r, L.ap, mode, s0, s1);
+    } else {
+        spmv_color<0>(L, p, ap, L.r, L.ap, mode, s0, s1);
+        spmv_color<1>(L, p, ap, L.r, L.ap, mode, s0, s1);
+        spmv_color<2>(L, p, ap, L.r, L.ap, mode, s0, s1);
+        spmv_color<3>(L, p, ap, L.r, L.ap, mode, s0, s1);
+    }
     bsum2(red, par, s0, s1);
     PH(po + 7)
     if (i == 0) {
@@ -540,6 +641,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_pcg(const __grid_constant
     }
     __syncthreads();
 
+    // stencil values of the top level in registers when its colour planes have
+    // exactly one cell per thread (the usual 1K-cell top level)
+    RV rv0;
+    const bool top_reg = sgeo[0].nq == kThreads && nl > 1;
+    if (top_reg) {
+        const SLevel L0 = slev(a, sm, sgeo, 0);
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+            for (int t = 0; t < 9; ++t) rv0.v[c][t] = L0.val[t * L0.n + c * L0.nq + threadIdx.x];
+    }
+
     // ---- the K-cycle as an explicit state machine over (level, PCG step)
     PState ps[kMaxFusedLevels];
     int par = 0;
@@ -571,13 +684,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_pcg(const __grid_constant
                     --q;
                     const SLevel P = slev(a, sm, sgeo, q);
                     FCLK_BEGIN
-                    cycle_up(a, P, L, ps[q + 1], P.p + ps[q].step * 4 * P.PP);
+                    cycle_up(a, P, L, ps[q + 1], P.p + ps[q].step * 4 * P.PP, (q == 0 && top_reg) ? &rv0 : nullptr);
                     FCLK_END(3, q)
                 }
                 continue;
             }
             FCLK_BEGIN
-            cycle_down(a, L, ps[q], slev(a, sm, sgeo, q + 1), u);
+            cycle_down(a, L, ps[q], slev(a, sm, sgeo, q + 1), u, (q == 0 && top_reg) ? &rv0 : nullptr);
             FCLK_END(0, q)
             ++q;
             ps[q].step = 0;
@@ -586,7 +699,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_pcg(const __grid_constant
             continue;
         }
         FCLK_BEGIN
-        const bool done = pcg_step(a, L, ps[q], red, par);
+        const bool done = pcg_step(a, L, ps[q], red, par, (q == 0 && top_reg) ? &rv0 : nullptr);
         FCLK_END(2, q)
         if (!done) {
             ps[q].pend = 1;
@@ -598,7 +711,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_pcg(const __grid_constant
         --q;
         const SLevel P = slev(a, sm, sgeo, q);
         FCLK_BEGIN
-        cycle_up(a, P, L, ps[q + 1], P.p + ps[q].step * 4 * P.PP);
+        cycle_up(a, P, L, ps[q + 1], P.p + ps[q].step * 4 * P.PP, (q == 0 && top_reg) ? &rv0 : nullptr);
         FCLK_END(3, q)
         resume = true;
     }
