@@ -189,6 +189,15 @@ __device__ bool grid_reduce(double (&v)[NV], const RedState& rs, double (&out)[N
         if (lane == 0) sm[i][wid] = s;
     }
     __syncthreads();
+    if (gridDim.x == 1) {   // one block: no partials, no ticket
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+            double s = 0.0;
+            for (int w = 0; w < kRedThreads / 32; ++w) s += sm[i][w];
+            out[i] = s;
+        }
+        return true;
+    }
     if (threadIdx.x == 0) {
 #pragma unroll
         for (int i = 0; i < NV; ++i) {

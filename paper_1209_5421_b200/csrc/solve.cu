@@ -1187,7 +1187,7 @@ void pcg_tiles(Ctx& c, int m) {
             for (int j = 1; j < i; ++j) {
                 const Route rj = route(c, L.dist, Fin{2, sc, sc + 3 + j, nullptr});
                 if (!L.dist)
-                    launch_pdl(k_mgs_vec, dim3(red_blocks(sp.n / 2)), dim3(kRedThreads), 0, c.s, sp.n, P.p[i].p,
+                    launch_pdl(k_mgs_vec, dim3(sp.n <= 4096 ? 1 : red_blocks(sp.n / 2)), dim3(kRedThreads), 0, c.s, sp.n, P.p[i].p,
                                P.ap[i].p, (const double*)P.p[j - 1].p, (const double*)P.ap[j - 1].p,
                                (const double*)P.ap[j].p, (const double*)nullptr, 0, (const double*)sc, c.rs,
                                rj.launch);
@@ -1199,7 +1199,7 @@ void pcg_tiles(Ctx& c, int m) {
             }
             const Route rf = route(c, L.dist, Fin{1, sc, nullptr, sc + 3 + i, sc + sc_alpha(ni, i), sc + sc_nval(ni), i});
             if (!L.dist)
-                launch_pdl(k_mgs_vec, dim3(red_blocks(sp.n / 2)), dim3(kRedThreads), 0, c.s, sp.n, P.p[i].p,
+                launch_pdl(k_mgs_vec, dim3(sp.n <= 4096 ? 1 : red_blocks(sp.n / 2)), dim3(kRedThreads), 0, c.s, sp.n, P.p[i].p,
                            P.ap[i].p, (const double*)P.p[i - 1].p, (const double*)P.ap[i - 1].p,
                            (const double*)nullptr, (const double*)R[i & 1], 1, (const double*)sc, c.rs, rf.launch);
             else
