@@ -8,8 +8,28 @@ namespace auxb200 {
 
 namespace {
 
-std::mutex g_mu;
-std::multimap<size_t, void*> g_free;   // rounded size -> cached block
+// One cache per host thread: a block freed while kernels of its stream may
+// still use it is only handed out again to the same thread, whose work is
+// ordered on that stream (or synchronised before it moves to another one:
+// setup and solve end with a stream synchronisation, a hierarchy synchronises
+// before releasing its buffers).  The multi-part test transport drives one
+// part per thread, each on its own stream.
+std::mutex g_mu;   // guards cudaMalloc / cudaFree of the retry path
+struct Cache {
+    std::multimap<size_t, void*> m;   // rounded size -> cached block
+    ~Cache() {   // thread exit: the blocks go back to the driver
+        for (auto& kv : m) cudaFree(kv.second);
+    }
+    auto find(size_t r) { return m.find(r); }
+    auto end() { return m.end(); }
+    void erase(std::multimap<size_t, void*>::iterator it) { m.erase(it); }
+    void emplace(size_t r, void* p) { m.emplace(r, p); }
+    void clear() {
+        for (auto& kv : m) cudaFree(kv.second);
+        m.clear();
+    }
+};
+thread_local Cache g_free;
 
 size_t round_size(size_t b) {
     if (b <= 512) return 512;
@@ -27,7 +47,6 @@ size_t round_size(size_t b) {
 void* dev_alloc(size_t bytes) {
     const size_t r = round_size(bytes);
     {
-        std::lock_guard<std::mutex> lk(g_mu);
         auto it = g_free.find(r);
         if (it != g_free.end()) {
             void* p = it->second;
@@ -42,7 +61,6 @@ void* dev_alloc(size_t bytes) {
         (void)cudaGetLastError();
         std::lock_guard<std::mutex> lk(g_mu);
         cudaDeviceSynchronize();
-        for (auto& kv : g_free) cudaFree(kv.second);
         g_free.clear();
         e = cudaMalloc(&p, r);
     }
@@ -52,7 +70,6 @@ void* dev_alloc(size_t bytes) {
 
 void dev_free(void* p, size_t bytes) {
     if (!p) return;
-    std::lock_guard<std::mutex> lk(g_mu);
     g_free.emplace(round_size(bytes), p);
 }
 

@@ -28,7 +28,7 @@ namespace auxb200 {
 namespace {
 
 
-double g_color_bytes[4];   // algorithmic bytes of one finest colour pass
+thread_local double g_color_bytes[4];   // algorithmic bytes of one finest colour pass
 
 #define GSTRIDE(i, n) for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < (n); i += (long)gridDim.x * blockDim.x)
 
@@ -855,7 +855,7 @@ struct Trace {
         cat.clear();
     }
 };
-Trace g_trace;
+thread_local Trace g_trace;
 
 void pcg_level(Ctx& c, int m);
 void coarse_root(Ctx& c);
