@@ -280,14 +280,17 @@ aux_status aux_solve(aux_hierarchy* h, const aux_csr_view* A, const double* b, i
         solve_device(h, bd.p, (long)n_b, &o, res, ud.p);
         if (res->u && n > 0 && h->dist.comm) {   // a part writes the entries of the DoFs it owns
             const long m = h->fine.n;
-            std::vector<double> uv(m);
-            std::vector<int> gv(m);
-            DBuf<double> ul(m);
-            gather_owned(h, ud.p, ul.p);
-            AUX_CUDA(cudaMemcpyAsync(uv.data(), ul.p, sizeof(double) * m, cudaMemcpyDeviceToHost, h->stream));
-            AUX_CUDA(cudaMemcpyAsync(gv.data(), h->dist.gid.p, sizeof(int) * m, cudaMemcpyDeviceToHost, h->stream));
-            AUX_CUDA(cudaStreamSynchronize(h->stream));
-            for (long i = 0; i < m; ++i) res->u[gv[i]] = uv[i];
+            if (m > 0) {
+                const int* gs = owned_ascending(h);
+                gather_owned_sorted(h, ud.p, h->dist.u_stage_h);
+                AUX_CUDA(cudaStreamSynchronize(h->stream));
+                const double* uv = h->dist.u_stage_h;
+                if (gs[m - 1] - gs[0] == m - 1) {   // one contiguous run of caller ids
+                    std::memcpy(res->u + gs[0], uv, sizeof(double) * m);
+                } else {
+                    for (long i = 0; i < m; ++i) res->u[gs[i]] = uv[i];   // ascending ids: streaming writes
+                }
+            }
         } else if (res->u && n > 0) {
             AUX_CUDA(cudaMemcpyAsync(res->u, ud.p, sizeof(double) * n, cudaMemcpyDeviceToHost, h->stream));
             AUX_CUDA(cudaStreamSynchronize(h->stream));

@@ -138,6 +138,7 @@ struct CommLocal : Comm {
         AUX_CUDA(cudaStreamSynchronize(s));
         g->bar.wait();
     }
+    bool graph_capturable() const override { return false; }   // host barriers between the parts
 };
 
 // ---- NCCL through dlopen (the process may already hold torch's libnccl)
@@ -214,6 +215,7 @@ struct CommNccl : Comm {
             if (m.bytes) AUX_NCCL(nccl().Recv(m.buf, m.bytes, ncclUint8, m.peer, comm, s));
         AUX_NCCL(nccl().GroupEnd());
     }
+    bool graph_capturable() const override { return true; }   // NCCL kernels capture into CUDA graphs
     void barrier(cudaStream_t s) override {
         DBuf<double> one(1);
         AUX_CUDA(cudaMemsetAsync(one.p, 0, sizeof(double), s));

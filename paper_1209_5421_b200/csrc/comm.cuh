@@ -35,6 +35,9 @@ struct Comm {
     // a batch of point-to-point messages; a part may appear in both lists
     virtual void exchange(const std::vector<Msg>& sends, const std::vector<Msg>& recvs, cudaStream_t s) = 0;
     virtual void barrier(cudaStream_t s) = 0;
+    // every operation is stream-ordered device work with no host round trip,
+    // so a sequence of them can be captured into a CUDA graph
+    virtual bool graph_capturable() const = 0;
 };
 
 // P parts in one process (opaque group shared by the P threads).

@@ -17,7 +17,11 @@ void setup_device_dist(aux_hierarchy* h, const aux_csr_view* A, const double* xy
 void ring_exchange_level(aux_hierarchy* h, int m, const std::vector<double*>& vecs, cudaStream_t s);
 void gather_level_to_root(aux_hierarchy* h, int t, const std::vector<double*>& vecs, cudaStream_t s);
 // u_local[i] = u_global[gid[i]] for the part's rows.
-void gather_owned(aux_hierarchy* h, const double* u_global, double* u_local);
+// Multi-GPU write-back: the part's local rows ordered by ascending caller id
+// (host array, cached), and its solution entries gathered in that order into a
+// pinned host buffer (asynchronous on h->stream).
+const int* owned_ascending(aux_hierarchy* h);
+void gather_owned_sorted(aux_hierarchy* h, const double* u_global, double* host_out);
 // Exports (reference layout, host arrays).
 void export_level(const aux_hierarchy* h, int level, aux_level_export* x);
 void level_info(const aux_hierarchy* h, int level, aux_level_info* o);

@@ -22,6 +22,7 @@
 #include "setup.cuh"
 #include "tiles.cuh"
 #include "comm.cuh"
+#include "scan_sort.cuh"
 
 namespace auxb200 {
 
@@ -991,6 +992,12 @@ Rect part_rect_of(const aux_hierarchy* h, int level, int part) {
 
 // Refresh the kRing-cell ring of a distributed level m from the neighbours'
 // owned cells, for the listed vectors.
+static void assert_not_capturing(cudaStream_t s) {
+    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+    AUX_CUDA(cudaStreamIsCapturing(s, &st));
+    if (st != cudaStreamCaptureStatusNone) throw_aux(AUX_INTERNAL_ERROR, "exchange buffer grows inside a graph capture");
+}
+
 void ring_exchange_v(aux_hierarchy* h, int m, const std::vector<double*>& vecs, cudaStream_t stream) {
     Level& L = h->lv[m];
     if (!L.dist) return;
@@ -1015,7 +1022,8 @@ void ring_exchange_v(aux_hierarchy* h, int m, const std::vector<double*>& vecs, 
         const Rect rb = intersect(o, dilate(me, kRing));
         if (!rb.empty()) { rcv.push_back({q, rb, off}); off += (size_t)rb.cells() * nv; }
     }
-    if (L.xbuf.n < off) {
+    if (L.xbuf.n < off) {   // sized by setup's 10-vector exchanges; never grows inside a graph capture
+        assert_not_capturing(c.s);
         AUX_CUDA(cudaStreamSynchronize(c.s));
         L.xbuf.alloc(off);
     }
@@ -1047,6 +1055,7 @@ void gather_root_v(aux_hierarchy* h, int t, const std::vector<double*>& vecs, cu
     for (double* v : vecs) vl.p[nv++] = v;
     const size_t need = (size_t)nv * T.n;
     if (T.xbuf.n < need) {
+        assert_not_capturing(s);
         AUX_CUDA(cudaStreamSynchronize(s));
         T.xbuf.alloc(need);
     }
@@ -1376,7 +1385,7 @@ void coarse_root(Ctx& c) {
 }
 
 void build_graph(aux_hierarchy* h, const aux_cycle_opts& o, RedState rs) {
-    if (h->dist.comm) {   // multi-GPU: exchanges synchronise the parts from the host; no capture
+    if (h->dist.comm && !h->dist.comm->graph_capturable()) {   // in-process parts: host barriers, no capture
         h->graph_valid = false;
         return;
     }
@@ -1474,10 +1483,34 @@ void setup_fused(aux_hierarchy* h, const aux_cycle_opts& o) {
 
 }  // namespace
 
-void gather_owned(aux_hierarchy* h, const double* u_global, double* u_local) {
+__global__ void k_gather_sorted(long m, const int* __restrict__ ord, const int* __restrict__ gid,
+                                const double* __restrict__ u_global, double* __restrict__ out) {
+    GSTRIDE(i, m) out[i] = u_global[gid[ord[i]]];
+}
+
+const int* owned_ascending(aux_hierarchy* h) {
+    DistInfo& d = h->dist;
     const long m = h->fine.n;
-    k_gather<<<blocks_for(m), 256, 0, h->stream>>>(m, h->dist.gid.p, u_global, u_local);
+    if (d.gid_sorted_h) return d.gid_sorted_h;
+    DBuf<unsigned> keys(m);
+    d.ord.alloc(m);
+    AUX_CUDA(cudaMemcpyAsync(keys.p, d.gid.p, sizeof(int) * m, cudaMemcpyDeviceToDevice, h->stream));
+    int bits = 1;
+    while (bits < 31 && (1L << bits) < (long)h->n) ++bits;
+    radix_sort_pairs(keys.p, d.ord.p, m, bits, h->stream, true);
+    AUX_CUDA(cudaHostAlloc(&d.gid_sorted_h, sizeof(int) * m, cudaHostAllocDefault));
+    AUX_CUDA(cudaHostAlloc(&d.u_stage_h, sizeof(double) * m, cudaHostAllocDefault));
+    AUX_CUDA(cudaMemcpyAsync(d.gid_sorted_h, keys.p, sizeof(int) * m, cudaMemcpyDeviceToHost, h->stream));
+    AUX_CUDA(cudaStreamSynchronize(h->stream));
+    return d.gid_sorted_h;
+}
+
+void gather_owned_sorted(aux_hierarchy* h, const double* u_global, double* host_out) {
+    const long m = h->fine.n;
+    DBuf<double> tmp(m);
+    k_gather_sorted<<<blocks_for(m), 256, 0, h->stream>>>(m, h->dist.ord.p, h->dist.gid.p, u_global, tmp.p);
     AUX_LAUNCHED(1);
+    AUX_CUDA(cudaMemcpyAsync(host_out, tmp.p, sizeof(double) * m, cudaMemcpyDeviceToHost, h->stream));
 }
 
 void ring_exchange_level(aux_hierarchy* h, int m, const std::vector<double*>& vecs, cudaStream_t s) {

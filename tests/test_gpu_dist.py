@@ -108,3 +108,16 @@ def test_parts_partition_dofs(gpu_api, parts):
     P = pt.Partition(s.A, s.coords, parts)
     for r in range(parts):
         assert np.array_equal(ids[r], P.owned_dofs(r))
+
+
+@pytest.mark.parametrize("parts", [4, 8])
+def test_parts_full_size_c1(gpu_api, parts):
+    """C1 (jittered P1, N = 1,048,576) split over 4 / 8 parts: SURVEY 8(c)
+    golden iteration count (12) and the true residual."""
+    import scipy.sparse as sp
+    s = problems.jittered_p1(1025)
+    u, res, st = gpu_api.solve_parts(s.A, s.coords, s.b, parts)
+    assert res[0].converged and abs(res[0].iterations - 12) <= 1
+    A = sp.csr_matrix((s.A.values, s.A.col_idx, s.A.row_ptr), shape=(s.A.n_rows, s.A.n_rows))
+    assert np.linalg.norm(s.b - A @ u) / np.linalg.norm(s.b) <= 1e-6 * (1 + 1e-9)
+    assert round(st[0].operator_complexity, 4) == 1.4274
