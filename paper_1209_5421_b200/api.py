@@ -25,7 +25,8 @@ from ._abi import (AuxamgError, SizeError, CapacityError, StructureError, Argume
 from .problems import CsrMatrix, LinearSystem  # noqa: F401
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libauxamg_b200.so")
+# AUX_B200_LIB: an alternative build of the same library (A/B timing experiments)
+LIB_PATH = os.environ.get("AUX_B200_LIB") or os.path.join(_HERE, "libauxamg_b200.so")
 _lib = None
 
 

@@ -527,6 +527,27 @@ __device__ bool pcg_step(const FusedArgs& a, const SLevel& L, PState& ps, double
         spmv_color_r<1>(L, *rv, p, ap, L.r, L.ap, mode, s0, s1);
         spmv_color_r<2>(L, *rv, p, ap, L.r, L.ap, mode, s0, s1);
         spmv_color_r<3>(L, *rv, p, ap, L.r, L.ap, mode, s0, s1);
+    } else if (L.n <= kThreads) {   // all four colours at once, one cell per thread
+        const int ci = threadIdx.x;
+        if (ci < L.n) {
+            const int c = ci >> (2 * L.lh), pos = ci & (L.nq - 1);
+            const int pi = pidx(L, c, pos & (L.H - 1), pos >> L.lh);
+            double yi;
+            switch (c) {
+                case 0: yi = row9<0>(L, ci, pi, p); break;
+                case 1: yi = row9<1>(L, ci, pi, p); break;
+                case 2: yi = row9<2>(L, ci, pi, p); break;
+                default: yi = row9<3>(L, ci, pi, p); break;
+            }
+            ap[pi] = yi;
+            const double xi = p[pi];
+            if (mode == 0) {
+                s0 = __dmul_rn(xi, yi);
+                s1 = __dmul_rn(L.r[pi], xi);
+            } else {
+                s0 = __dmul_rn(xi, L.ap[pi]);
+            }
+        }
     } else {
         spmv_color<0>(L, p, ap, L.r, L.ap, mode, s0, s1);
         spmv_color<1>(L, p, ap, L.r, L.ap, mode, s0, s1);
@@ -667,46 +688,41 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_pcg(const __grid_constant
         const SLevel L = slev(a, sm, sgeo, q);
         if (!resume) {
             double* u = L.p + ps[q].step * 4 * L.PP;
-            if (q == nl - 1) {
+            if (q < nl - 1) {
                 FCLK_BEGIN
-                coarse_solve(a, inv, part, L, ps[q], u);
-                FCLK_END(1, q)
-                resume = true;
-                if (a.coarse_mode == 0) {
-                    // Exact preconditioner on the coarsest level: the first PCG
-                    // step already returns A_c^{-1} f (alpha = 1 up to rounding,
-                    // the next residual is rounding noise), so the inverse mode
-                    // takes u = A_c^{-1} f as the whole nonlinear_pcg.  The
-                    // LU mode (coarse_mode 1) runs the reference's n_inner steps.
-                    ps[q].alpha[0] = 1.0;
-                    ps[q].nval = 1;
-                    if (q == 0) break;
-                    --q;
-                    const SLevel P = slev(a, sm, sgeo, q);
-                    FCLK_BEGIN
-                    cycle_up(a, P, L, ps[q + 1], P.p + ps[q].step * 4 * P.PP, (q == 0 && top_reg) ? &rv0 : nullptr);
-                    FCLK_END(3, q)
-                }
+                cycle_down(a, L, ps[q], slev(a, sm, sgeo, q + 1), u, (q == 0 && top_reg) ? &rv0 : nullptr);
+                FCLK_END(0, q)
+                ++q;
+                ps[q].step = 0;
+                ps[q].nval = 0;
+                ps[q].pend = 0;
                 continue;
             }
             FCLK_BEGIN
-            cycle_down(a, L, ps[q], slev(a, sm, sgeo, q + 1), u, (q == 0 && top_reg) ? &rv0 : nullptr);
-            FCLK_END(0, q)
-            ++q;
-            ps[q].step = 0;
-            ps[q].nval = 0;
-            ps[q].pend = 0;
-            continue;
+            coarse_solve(a, inv, part, L, ps[q], u);
+            FCLK_END(1, q)
+            resume = true;
+            if (a.coarse_mode != 0) continue;
+            // Exact preconditioner on the coarsest level: the first PCG step
+            // already returns A_c^{-1} f (alpha = 1 up to rounding, the next
+            // residual is rounding noise), so the inverse mode takes
+            // u = A_c^{-1} f as the whole nonlinear_pcg.  The LU mode
+            // (coarse_mode 1) runs the reference's n_inner steps.
+            ps[q].alpha[0] = 1.0;
+            ps[q].nval = 1;
+        } else {
+            FCLK_BEGIN
+            const bool done = pcg_step(a, L, ps[q], red, par, (q == 0 && top_reg) ? &rv0 : nullptr);
+            FCLK_END(2, q)
+            if (!done) {
+                ps[q].pend = 1;
+                ++ps[q].step;
+                resume = false;
+                continue;
+            }
         }
-        FCLK_BEGIN
-        const bool done = pcg_step(a, L, ps[q], red, par, (q == 0 && top_reg) ? &rv0 : nullptr);
-        FCLK_END(2, q)
-        if (!done) {
-            ps[q].pend = 1;
-            ++ps[q].step;
-            resume = false;
-            continue;
-        }
+        // nonlinear_pcg(q) finished: back to the parent (one call site keeps
+        // the kernel's code small — instruction fetch is a visible stall here)
         if (q == 0) break;
         --q;
         const SLevel P = slev(a, sm, sgeo, q);
