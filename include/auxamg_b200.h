@@ -94,7 +94,9 @@ typedef struct aux_gpu_opts {
     int32_t tile_kernels;     /* structured levels above the single-CTA tier:
                                  1 = two overlapped-tile kernels per K-cycle visit (default),
                                  0 = one kernel per colour pass / phase */
-    int32_t reserved[2];
+    int32_t cluster_tier;     /* the 64x64-cell level above a 32x32 single-CTA tier runs with
+                                 that tier in one 5-CTA thread-block cluster (1, default) */
+    int32_t reserved;
 } aux_gpu_opts;
 
 /* auxamg::LocalityReport, hierarchy.hpp:37-44. */

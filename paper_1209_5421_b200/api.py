@@ -131,6 +131,7 @@ class GpuOptions:
     use_graphs: bool = True
     block_solve: int = 0         # 0 explicit block inverses, 1 stored LU in reference order
     tile_kernels: bool = True    # overlapped-tile kernels for the structured levels
+    cluster_tier: bool = True    # 64x64 level + single-CTA tier in one thread-block cluster
 
     def c(self):
         o = _abi.GpuOpts()
@@ -138,6 +139,7 @@ class GpuOptions:
                                                                      self.fused_max_cells, int(self.use_graphs))
         o.block_solve = self.block_solve
         o.tile_kernels = int(self.tile_kernels)
+        o.cluster_tier = int(self.cluster_tier)
         return o
 
 

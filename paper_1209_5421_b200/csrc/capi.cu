@@ -98,6 +98,7 @@ void aux_default_gpu_opts(aux_gpu_opts* o) {
     o->use_graphs = 1;
     o->block_solve = 0;
     o->tile_kernels = 1;
+    o->cluster_tier = 1;
 }
 
 const char* aux_version(void) { return "auxamg_b200 0.1 (sm_100a)"; }

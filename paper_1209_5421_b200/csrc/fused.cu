@@ -600,23 +600,17 @@ __device__ bool pcg_step(const FusedArgs& a, const SLevel& L, PState& ps, double
     return i + 1 >= a.ni;
 }
 
-__global__ void __launch_bounds__(kThreads, 1) k_fused_pcg(const __grid_constant__ FusedArgs a) {
-    FCLK_START
-    pdl_trigger();
-    extern __shared__ __align__(16) unsigned char sm[];
-    __shared__ double red[2 * 2 * kWarps];
-    __shared__ Geo sgeo[kMaxFusedLevels];
+// ---- the single-CTA tier as building blocks: staging of its constant data,
+// and one nonlinear_pcg(m0) run of the state machine
+
+// Stage the tier's read-only data with TMA bulk copies (cp.async.bulk, all in
+// flight at once, completion on one mbarrier); meanwhile zero the padded
+// vectors (ghost rings) with 16-byte stores.  Returns after the data landed.
+__device__ void tier_stage(const FusedArgs& a, unsigned char* sm, Geo* sgeo, uint64_t* bar) {
     const int nl = a.last - a.m0 + 1;
     if (threadIdx.x < nl) sgeo[threadIdx.x] = a.lv[a.m0 + threadIdx.x].g;
-
-    // ---- stage read-only data with TMA bulk copies (cp.async.bulk, all in
-    // flight at once, completion on one mbarrier); meanwhile zero the padded
-    // vectors (ghost rings) with 16-byte stores.
-    __shared__ __align__(8) uint64_t bar;
-    const double* inv = a.inv;
-    if (a.inv_in_smem) inv = reinterpret_cast<const double*>(sm + a.off_inv);
     if (threadIdx.x == 0) {
-        mbar_init(&bar, 1);
+        mbar_init(bar, 1);
         fence_mbar_init();
     }
     __syncthreads();
@@ -628,14 +622,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_pcg(const __grid_constant
             if ((n & 15) == 0) bytes += (uint32_t)n;
         }
         if (a.inv_in_smem) bytes += (uint32_t)a.nc * a.nc * 8u;
-        mbar_arrive_expect_tx(&bar, bytes);
+        mbar_arrive_expect_tx(bar, bytes);
         for (int q = 0; q < nl; ++q) {
             const FLevel& G = a.lv[a.m0 + q];
             const int n = G.g.n;
-            bulk_g2s(sm + a.off_val[q], G.val, 9u * n * 8u, &bar);
-            if ((n & 15) == 0) bulk_g2s(sm + a.off_act[q], G.act, (uint32_t)n, &bar);
+            bulk_g2s(sm + a.off_val[q], G.val, 9u * n * 8u, bar);
+            if ((n & 15) == 0) bulk_g2s(sm + a.off_act[q], G.act, (uint32_t)n, bar);
         }
-        if (a.inv_in_smem) bulk_g2s(sm + a.off_inv, a.inv, (uint32_t)a.nc * a.nc * 8u, &bar);
+        if (a.inv_in_smem) bulk_g2s(sm + a.off_inv, a.inv, (uint32_t)a.nc * a.nc * 8u, bar);
     }
     for (int q = 0; q < nl; ++q) {
         const FLevel& G = a.lv[a.m0 + q];
@@ -649,31 +643,28 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_pcg(const __grid_constant
         const int nv2 = (1 + 2 * a.ni) * 2 * W2 * W2;   // doubles / 2 (4*W2*W2 is even)
         for (int i = threadIdx.x; i < nv2; i += kThreads) v[i] = make_double2(0.0, 0.0);
     }
-    mbar_wait(&bar, 0);
-    pdl_wait();   // everything above reads data that is constant during the solve
-    __syncthreads();
-    {
-        const SLevel L0 = slev(a, sm, sgeo, 0);
-        const double* r0 = a.lv[a.m0].r;
-        for (int ci = threadIdx.x; ci < L0.n; ci += kThreads) {
-            const int c = ci >> (2 * L0.lh), pos = ci & (L0.nq - 1);
-            L0.r[pidx(L0, c, pos & (L0.H - 1), pos >> L0.lh)] = r0[ci];
-        }
-    }
-    __syncthreads();
+    mbar_wait(bar, 0);
+}
 
-    // stencil values of the top level in registers when its colour planes have
-    // exactly one cell per thread (the usual 1K-cell top level)
-    RV rv0;
-    const bool top_reg = sgeo[0].nq == kThreads && nl > 1;
-    if (top_reg) {
-        const SLevel L0 = slev(a, sm, sgeo, 0);
-#pragma unroll
-        for (int c = 0; c < 4; ++c)
-#pragma unroll
-            for (int t = 0; t < 9; ++t) rv0.v[c][t] = L0.val[t * L0.n + c * L0.nq + threadIdx.x];
-    }
+// Stencil values of the top level in registers when its colour planes have
+// exactly one cell per thread (the usual 1K-cell top level).
+__device__ __forceinline__ bool tier_top_reg(const Geo* sgeo, int nl) { return sgeo[0].nq == kThreads && nl > 1; }
 
+__device__ __forceinline__ void tier_load_rv(const FusedArgs& a, unsigned char* sm, const Geo* sgeo, RV& rv) {
+    const SLevel L0 = slev(a, sm, sgeo, 0);
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int t = 0; t < 9; ++t) rv.v[c][t] = L0.val[t * L0.n + c * L0.nq + threadIdx.x];
+}
+
+// nonlinear_pcg(m0) with the K-cycle below it, right-hand side already in the
+// top level's padded r; returns the top level's PCG state (alphas, nval), the
+// directions stay in shared memory.
+__device__ void tier_run(const FusedArgs& a, unsigned char* sm, const Geo* sgeo, const double* inv, double* red,
+                         const RV& rv0, bool top_reg, PState& top) {
+    FCLK_START
+    const int nl = a.last - a.m0 + 1;
     // ---- the K-cycle as an explicit state machine over (level, PCG step)
     PState ps[kMaxFusedLevels];
     int par = 0;
@@ -732,19 +723,459 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_pcg(const __grid_constant
         resume = true;
     }
     FCLK_REPORT
+    top = ps[0];
+}
 
-    // ---- u of nonlinear_pcg(m0) = ((0 + alpha_0 p_0) + alpha_1 p_1) ... to global memory
+__global__ void __launch_bounds__(kThreads, 1) k_fused_pcg(const __grid_constant__ FusedArgs a) {
+    pdl_trigger();
+    extern __shared__ __align__(16) unsigned char sm[];
+    __shared__ double red[2 * 2 * kWarps];
+    __shared__ Geo sgeo[kMaxFusedLevels];
+    __shared__ __align__(8) uint64_t bar;
+    const int nl = a.last - a.m0 + 1;
+    const double* inv = a.inv_in_smem ? reinterpret_cast<const double*>(sm + a.off_inv) : a.inv;
+    tier_stage(a, sm, sgeo, &bar);
+    pdl_wait();   // everything above reads data that is constant during the solve
+    __syncthreads();
     {
         const SLevel L0 = slev(a, sm, sgeo, 0);
-        double* u0 = a.lv[a.m0].u;
+        const double* r0 = a.lv[a.m0].r;
         for (int ci = threadIdx.x; ci < L0.n; ci += kThreads) {
             const int c = ci >> (2 * L0.lh), pos = ci & (L0.nq - 1);
-            const int pi = pidx(L0, c, pos & (L0.H - 1), pos >> L0.lh);
-            double s = 0.0;
-            for (int k = 0; k < ps[0].nval; ++k) s = __dadd_rn(s, __dmul_rn(ps[0].alpha[k], L0.p[k * 4 * L0.PP + pi]));
-            u0[ci] = s;
+            L0.r[pidx(L0, c, pos & (L0.H - 1), pos >> L0.lh)] = r0[ci];
         }
     }
+    __syncthreads();
+    RV rv0;
+    const bool top_reg = tier_top_reg(sgeo, nl);
+    if (top_reg) tier_load_rv(a, sm, sgeo, rv0);
+    PState top;
+    tier_run(a, sm, sgeo, inv, red, rv0, top_reg, top);
+
+    // ---- u of nonlinear_pcg(m0) = ((0 + alpha_0 p_0) + alpha_1 p_1) ... to global memory
+    const SLevel L0 = slev(a, sm, sgeo, 0);
+    double* u0 = a.lv[a.m0].u;
+    for (int ci = threadIdx.x; ci < L0.n; ci += kThreads) {
+        const int c = ci >> (2 * L0.lh), pos = ci & (L0.nq - 1);
+        const int pi = pidx(L0, c, pos & (L0.H - 1), pos >> L0.lh);
+        double s = 0.0;
+        for (int k = 0; k < top.nval; ++k) s = __dadd_rn(s, __dmul_rn(top.alpha[k], L0.p[k * 4 * L0.PP + pi]));
+        u0[ci] = s;
+    }
+}
+
+// ============================================================================
+// Cluster tier: nonlinear_pcg on the 64x64-cell level above a 32x32-cell
+// single-CTA tier, and that tier, in ONE launch of a 5-CTA thread-block
+// cluster.  CTAs 0..3 own the four 32x32-cell quadrants of the 64x64 level
+// (thread t: plane position t of all four colours, the 36 stencil values in
+// registers); CTA 4 runs the single-CTA tier (tier_run) for every
+// preconditioner application.  The CTAs exchange through distributed shared
+// memory: after every colour pass a quadrant pushes the updated boundary of
+// that colour into its three neighbours' ghost rings (st.shared::cluster),
+// the restriction stores straight into CTA 4's right-hand side, the
+// prolongation loads CTA 4's directions (ld.shared::cluster), and inner
+// products are per-CTA block sums pushed to every CTA and added in CTA order.
+// One cluster barrier (barrier.cluster arrive.release / wait.acquire)
+// separates dependent phases — it replaces a kernel boundary.  Per-element
+// arithmetic is that of the tile kernels (bitwise colour-ordered GS).
+constexpr int kQuads = 4;
+constexpr int kTierRank = 4;
+constexpr int kClusterCtas = 5;
+constexpr int kQH = 16;              // quadrant colour-plane side
+constexpr int kQW2 = kQH + 2;
+constexpr int kQPP = kQW2 * kQW2;
+
+#ifdef AUX_CLUSTER_CLOCKS
+__device__ unsigned long long g_cph[32], g_cphn[32];
+__device__ int g_cph_launch;
+#define CPH_INIT long long cph_last = clock64();
+#define CPH(ID)                                                                              \
+    if (rank == 0 && threadIdx.x == 0) {                                                     \
+        const long long t_ = clock64();                                                      \
+        atomicAdd(&g_cph[ID], (unsigned long long)(t_ - cph_last));                          \
+        atomicAdd(&g_cphn[ID], 1ull);                                                        \
+        cph_last = t_;                                                                       \
+    }
+#define CPH_REPORT                                                                           \
+    if (rank == 0 && threadIdx.x == 0 && atomicAdd(&g_cph_launch, 1) == 40)                  \
+        for (int k_ = 0; k_ < 32; ++k_)                                                      \
+            if (g_cphn[k_]) printf("cluster phase %2d: %llu calls, %llu cycles avg\n", k_, g_cphn[k_], g_cph[k_] / g_cphn[k_]);
+#else
+#define CPH_INIT
+#define CPH(ID)
+#define CPH_REPORT
+#endif
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void csync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t mapa(const void* p, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void st_cluster(const void* p, uint32_t rank, double v) {
+    asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(mapa(p, rank)), "d"(v) : "memory");
+}
+// (not volatile, no memory clobber: the loads of one phase issue together;
+// ordering against the producer comes from the cluster barrier before them)
+__device__ __forceinline__ double ld_cluster(const void* p, uint32_t rank) {
+    uint32_t ra;
+    asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(p)), "r"(rank));
+    double v;
+    asm("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(ra));
+    return v;
+}
+
+// Push the quadrant boundary of colour C of x into the neighbours' ghost rings
+// (threads 0..32: 16 column cells, 16 row cells, the corner).
+template <int C>
+__device__ __forceinline__ void q_push(const SLevel& L, double* x, int qx, int qy) {
+    const int t = threadIdx.x;
+    if (t > 2 * kQH) return;
+    const int ea = qx == 0 ? kQH - 1 : 0, ga = qx == 0 ? -1 : kQH;   // my edge column, its ghost column
+    const int eb = qy == 0 ? kQH - 1 : 0, gb = qy == 0 ? -1 : kQH;
+    int sa, sb, da, db, nqx = qx, nqy = qy;
+    if (t < kQH) {
+        sa = ea; sb = t; da = ga; db = t; nqx = 1 - qx;
+    } else if (t < 2 * kQH) {
+        sa = t - kQH; sb = eb; da = sa; db = gb; nqy = 1 - qy;
+    } else {
+        sa = ea; sb = eb; da = ga; db = gb; nqx = 1 - qx; nqy = 1 - qy;
+    }
+    st_cluster(x + pidx(L, C, da, db), (uint32_t)(nqy * 2 + nqx), x[pidx(L, C, sa, sb)]);
+}
+
+template <int C>
+__device__ __forceinline__ void q_pass(const SLevel& L, const RV& rv, const double* f, double* x, int qx, int qy) {
+    gs_pass_r<C>(L, rv, f, x);   // ends with __syncthreads
+    q_push<C>(L, x, qx, qy);
+}
+
+// Block sum of (x, y) of the quadrant CTA, pushed to slot [par][rank] of every
+// CTA of the cluster.
+__device__ __forceinline__ void q_reduce_push(double* red, double (*cred)[kQuads][2], int par, int rank, double x,
+                                              double y) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    x = warp_sum(x);
+    y = warp_sum(y);
+    if (lane == 0) {
+        red[wid * 2] = x;
+        red[wid * 2 + 1] = y;
+    }
+    __syncthreads();
+    if (threadIdx.x < kClusterCtas) {
+        double tx = 0.0, ty = 0.0;
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) {
+            tx += red[w * 2];
+            ty += red[w * 2 + 1];
+        }
+        st_cluster(&cred[par][rank][0], threadIdx.x, tx);
+        st_cluster(&cred[par][rank][1], threadIdx.x, ty);
+    }
+}
+
+__device__ __forceinline__ void c_sum(const double (*cred)[kQuads][2], int par, double& x, double& y) {
+    x = ((cred[par][0][0] + cred[par][1][0]) + cred[par][2][0]) + cred[par][3][0];
+    y = ((cred[par][0][1] + cred[par][1][1]) + cred[par][2][1]) + cred[par][3][1];
+}
+
+__global__ void __launch_bounds__(kThreads, 1) k_cluster_pcg(const __grid_constant__ ClusterArgs ca) {
+    pdl_trigger();
+    extern __shared__ __align__(16) unsigned char sm[];
+    __shared__ double red[2 * 2 * kWarps];
+    __shared__ Geo sgeo[kMaxFusedLevels];
+    __shared__ __align__(8) uint64_t bar;
+    __shared__ double cred[2][kQuads][2];              // cluster inner products, double-buffered
+    __shared__ double cpub[kFusedMaxInner + 1];        // the tier's alphas and nval, pushed to the quadrants
+    const FusedArgs& a = ca.f;
+    const int rank = (int)cluster_rank();
+    const bool quad = rank < kQuads, tier = rank == kTierRank;
+    const int qx = rank & 1, qy = (rank >> 1) & 1;
+    const int ni = a.ni;
+    const int nl = a.last - a.m0 + 1;
+    const int t = threadIdx.x, ta = t & (kQH - 1), tb = t >> 4;
+    const int gN = ca.g.n, gq = ca.g.nq, gH = ca.g.H;   // 4096, 1024, 32
+
+    // quadrant view: padded colour-major vectors r, p[ni], ap[ni]; padded act
+    SLevel Q;
+    Q.k = ca.g.k;
+    Q.lh = 4;
+    Q.H = kQH;
+    Q.nq = kQH * kQH;
+    Q.n = 4 * Q.nq;
+    Q.W2 = kQW2;
+    Q.PP = kQPP;
+    Q.val = nullptr;
+    Q.act = nullptr;
+    double* qv = reinterpret_cast<double*>(sm);
+    Q.r = qv;
+    Q.p = qv + 4 * kQPP;
+    Q.ap = qv + (1 + ni) * 4 * kQPP;
+    uint8_t* qact = sm + (size_t)(1 + 2 * ni) * 4 * kQPP * sizeof(double);
+    // the tier's top level (32x32 cells) as seen from the quadrants
+    SLevel T0;
+    T0.k = 0; T0.lh = 4; T0.H = kQH; T0.nq = kQH * kQH; T0.n = 4 * T0.nq; T0.W2 = kQW2; T0.PP = kQPP;
+    T0.val = nullptr; T0.act = nullptr;
+    T0.r = reinterpret_cast<double*>(sm + a.off_vec[0]);
+    T0.p = T0.r + 4 * kQPP;
+    T0.ap = nullptr;
+
+    RV rv;
+    bool top_reg = false;
+    const double* inv = a.inv_in_smem ? reinterpret_cast<const double*>(sm + a.off_inv) : a.inv;
+    if (tier) {
+        tier_stage(a, sm, sgeo, &bar);
+        top_reg = tier_top_reg(sgeo, nl);
+        if (top_reg) tier_load_rv(a, sm, sgeo, rv);
+    } else if (quad) {
+        const int ga0 = kQH * qx, gb0 = kQH * qy;
+        const int gpos = (gb0 + tb) * gH + ga0 + ta;
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+            for (int s = 0; s < 9; ++s) rv.v[c][s] = __ldg(ca.val + (size_t)s * gN + c * gq + gpos);
+        const int nv2 = (1 + 2 * ni) * 2 * kQPP;
+        double2* v2 = reinterpret_cast<double2*>(qv);
+        for (int i = t; i < nv2; i += kThreads) v2[i] = make_double2(0.0, 0.0);
+        for (int i = t; i < 4 * kQPP; i += kThreads) {   // padded act, ghost ring from the neighbours' cells
+            const int c = i / kQPP, rem = i - c * kQPP, pb = rem / kQW2 - 1, pa = rem % kQW2 - 1;
+            const int A = ga0 + pa, B = gb0 + pb;
+            qact[i] = (A >= 0 && A < gH && B >= 0 && B < gH) ? ca.act[c * gq + B * gH + A] : 0;
+        }
+    }
+    pdl_wait();
+    if (quad) {
+        const int gpos = (kQH * qy + tb) * gH + kQH * qx + ta;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) Q.r[pidx(Q, c, ta, tb)] = ca.r[c * gq + gpos];
+    }
+    __syncthreads();
+    csync();
+    CPH_INIT
+    CPH(0)
+
+    // this thread's ghost-ring slot of colours 1..3 (3 x 68 slots), or -1
+    int zslot = -1;
+    if (t < 3 * 4 * (kQW2 - 1)) {
+        const int c = 1 + t / (4 * (kQW2 - 1)), k = t % (4 * (kQW2 - 1));
+        int pa, pb;
+        if (k < kQW2 - 1) { pa = k - 1; pb = -1; }
+        else if (k < 2 * (kQW2 - 1)) { pa = kQH; pb = k - (kQW2 - 1) - 1; }
+        else if (k < 3 * (kQW2 - 1)) { pa = kQH - (k - 2 * (kQW2 - 1)); pb = kQH; }
+        else { pa = -1; pb = kQH - (k - 3 * (kQW2 - 1)); }
+        zslot = pidx(Q, c, pa, pb);
+    }
+    double alpha[kFusedMaxInner], e[kFusedMaxInner];
+    int nval = 0, par = 0;
+    for (int i = 0; i < ni; ++i) {
+        double* u = Q.p + i * 4 * kQPP;
+        // ---- pre-smoothing from zero, pending PCG residual update (cycle.hpp:125)
+        if (quad) {
+            const double na = i > 0 ? -alpha[i - 1] : 0.0;
+            const double* apv = Q.ap + (i > 0 ? i - 1 : 0) * 4 * kQPP;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const int pi = pidx(Q, c, ta, tb);
+                double fi = Q.r[pi];
+                if (i > 0) {
+                    fi = __dadd_rn(fi, __dmul_rn(na, apv[pi]));
+                    Q.r[pi] = fi;
+                }
+                u[pi] = c == 0 ? __ddiv_rn(fi, rv.v[0][0]) : 0.0;
+            }
+            // ghost rings of colours 1..3 restart at zero (colour 0 is pushed)
+            if (zslot >= 0) u[zslot] = 0.0;
+            __syncthreads();
+            q_push<0>(Q, u, qx, qy);
+        }
+        csync();
+        CPH(1)
+        for (int sw = 0; sw < a.pre; ++sw) {
+            if (sw > 0) {
+                if (quad) q_pass<0>(Q, rv, Q.r, u, qx, qy);
+                csync();
+            }
+            if (quad) q_pass<1>(Q, rv, Q.r, u, qx, qy);
+            csync();
+            if (quad) q_pass<2>(Q, rv, Q.r, u, qx, qy);
+            csync();
+            if (quad) q_pass<3>(Q, rv, Q.r, u, qx, qy);
+            csync();
+        }
+        CPH(2)
+        // ---- restricted residual straight into the tier's right-hand side
+        if (quad) {
+            const double* f = Q.r;
+            double sum = 0.0;
+            sum = __dadd_rn(sum, __dsub_rn(f[pidx(Q, 0, ta, tb)], row9_r<0>(Q, rv, pidx(Q, 0, ta, tb), u)));
+            sum = __dadd_rn(sum, __dsub_rn(f[pidx(Q, 1, ta, tb)], row9_r<1>(Q, rv, pidx(Q, 1, ta, tb), u)));
+            sum = __dadd_rn(sum, __dsub_rn(f[pidx(Q, 2, ta, tb)], row9_r<2>(Q, rv, pidx(Q, 2, ta, tb), u)));
+            sum = __dadd_rn(sum, __dsub_rn(f[pidx(Q, 3, ta, tb)], row9_r<3>(Q, rv, pidx(Q, 3, ta, tb), u)));
+            const int T1 = kQH * qx + ta, T2 = kQH * qy + tb;   // coarse cell = fine plane coords
+            const int cq = (T1 & 1) | ((T2 & 1) << 1);
+            st_cluster(T0.r + pidx(T0, cq, T1 >> 1, T2 >> 1), kTierRank, sum);
+        }
+        csync();
+        CPH(3)
+        // ---- the child's nonlinear_pcg on the tier CTA
+        if (tier) {
+            PState top;
+            tier_run(a, sm, sgeo, inv, red, rv, top_reg, top);
+            if (t < kQuads) {
+                for (int k = 0; k < top.nval; ++k) st_cluster(&cpub[k], t, top.alpha[k]);
+                st_cluster(&cpub[kFusedMaxInner], t, (double)top.nval);
+            }
+        }
+        csync();
+        CPH(4)
+        // ---- prolongation of the child's iterate (cycle.hpp:191-194), own
+        // cells and the ghost ring (same arithmetic, so no exchange), then the
+        // transposed post-smoothing
+        if (quad) {
+            const int cn = (int)cpub[kFusedMaxInner];
+            double al[kFusedMaxInner];
+#pragma unroll
+            for (int k = 0; k < kFusedMaxInner; ++k) al[k] = k < cn ? cpub[k] : 0.0;
+            // own plane position, and for threads 0..32 one inner ghost position
+            // (my neighbours' edge cells)
+            const bool gh = t <= 2 * kQH;
+            int pa2 = ta, pb2 = tb;
+            if (gh) {
+                const int ga = qx == 0 ? kQH : -1, gb = qy == 0 ? kQH : -1;
+                if (t < kQH) { pa2 = ga; pb2 = t; }
+                else if (t < 2 * kQH) { pa2 = t - kQH; pb2 = gb; }
+                else { pa2 = ga; pb2 = gb; }
+            }
+            auto parent = [&](int pa, int pb) {
+                const int A = kQH * qx + pa, B = kQH * qy + pb;
+                return pidx(T0, (A & 1) | ((B & 1) << 1), A >> 1, B >> 1);
+            };
+            const int pc1 = parent(ta, tb), pc2 = parent(pa2, pb2);
+            double d1[kFusedMaxInner], d2[kFusedMaxInner];
+#pragma unroll
+            for (int k = 0; k < kFusedMaxInner; ++k) {
+                d1[k] = k < cn ? ld_cluster(T0.p + k * 4 * kQPP + pc1, kTierRank) : 0.0;
+                d2[k] = (k < cn && gh) ? ld_cluster(T0.p + k * 4 * kQPP + pc2, kTierRank) : 0.0;
+            }
+            double e1 = 0.0, e2 = 0.0;
+#pragma unroll
+            for (int k = 0; k < kFusedMaxInner; ++k)
+                if (k < cn) {
+                    e1 = __dadd_rn(e1, __dmul_rn(al[k], d1[k]));
+                    e2 = __dadd_rn(e2, __dmul_rn(al[k], d2[k]));
+                }
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const int pi = pidx(Q, c, ta, tb);
+                if (qact[pi]) u[pi] = __dadd_rn(u[pi], e1);
+                if (gh) {
+                    const int pj = pidx(Q, c, pa2, pb2);
+                    if (qact[pj]) u[pj] = __dadd_rn(u[pj], e2);
+                }
+            }
+            __syncthreads();
+        }
+        CPH(5)
+        for (int sw = 0; sw < a.post; ++sw) {
+            if (quad) q_pass<3>(Q, rv, Q.r, u, qx, qy);
+            csync();
+            if (quad) q_pass<2>(Q, rv, Q.r, u, qx, qy);
+            csync();
+            if (quad) q_pass<1>(Q, rv, Q.r, u, qx, qy);
+            csync();
+            if (quad) q_pass<0>(Q, rv, Q.r, u, qx, qy);
+            csync();
+        }
+        CPH(6)
+        // ---- A z and the step's inner products (cycle.hpp:84-97, 123)
+        double* ap = Q.ap + i * 4 * kQPP;
+        if (quad) {
+            double s0 = 0.0, s1 = 0.0;
+            spmv_color_r<0>(Q, rv, u, ap, Q.r, Q.ap, i == 0 ? 0 : 1, s0, s1);
+            spmv_color_r<1>(Q, rv, u, ap, Q.r, Q.ap, i == 0 ? 0 : 1, s0, s1);
+            spmv_color_r<2>(Q, rv, u, ap, Q.r, Q.ap, i == 0 ? 0 : 1, s0, s1);
+            spmv_color_r<3>(Q, rv, u, ap, Q.r, Q.ap, i == 0 ? 0 : 1, s0, s1);
+            q_reduce_push(red, cred, par, rank, s0, s1);
+        }
+        csync();
+        CPH(7)
+        double s0, s1;
+        c_sum(cred, par, s0, s1);
+        par ^= 1;
+        double al_i;
+        bool dead;
+        if (i == 0) {
+            e[0] = s0;
+            dead = !(s0 > kBreak);
+            al_i = s1 / s0;
+        } else {
+            double beta = -s0 / e[0];
+            dead = false;
+            al_i = 0.0;
+            for (int j = 1; j <= i; ++j) {
+                const bool fin = j == i;
+                if (quad) {
+                    const double* pj = Q.p + (j - 1) * 4 * kQPP;
+                    const double* apj = Q.ap + (j - 1) * 4 * kQPP;
+                    const double* wj = Q.ap + j * 4 * kQPP;
+                    double t0 = 0.0, t1 = 0.0;
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        const int pi = pidx(Q, c, ta, tb);
+                        const double pq = __dadd_rn(u[pi], __dmul_rn(beta, pj[pi]));
+                        const double aq = __dadd_rn(ap[pi], __dmul_rn(beta, apj[pi]));
+                        u[pi] = pq;
+                        ap[pi] = aq;
+                        if (fin) {
+                            t0 = __dadd_rn(t0, __dmul_rn(pq, aq));
+                            t1 = __dadd_rn(t1, __dmul_rn(Q.r[pi], pq));
+                        } else {
+                            t0 = __dadd_rn(t0, __dmul_rn(pq, wj[pi]));
+                        }
+                    }
+                    q_reduce_push(red, cred, par, rank, t0, t1);
+                }
+                csync();
+                CPH(8)
+                double t0, t1;
+                c_sum(cred, par, t0, t1);
+                par ^= 1;
+                if (fin) {
+                    e[i] = t0;
+                    dead = !(t0 > kBreak);
+                    al_i = t1 / t0;
+                } else {
+                    beta = -t0 / e[j];
+                }
+            }
+        }
+        if (dead) break;   // nonlinear_pcg returns the current iterate
+        alpha[i] = al_i;
+        nval = i + 1;
+    }
+    // ---- u = ((0 + alpha_0 p_0) + alpha_1 p_1) ... of the 64x64 level
+    if (quad) {
+        const int gpos = (kQH * qy + tb) * gH + kQH * qx + ta;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const int pi = pidx(Q, c, ta, tb);
+            double s = 0.0;
+            for (int k = 0; k < nval; ++k) s = __dadd_rn(s, __dmul_rn(alpha[k], Q.p[k * 4 * kQPP + pi]));
+            ca.u[c * gq + gpos] = s;
+        }
+    }
+    CPH(9)
+    // no final cluster barrier: the last remote access (the inner-product
+    // push) was followed by one, so no CTA can still touch another's memory
+    CPH_REPORT
 }
 
 }  // namespace
@@ -778,6 +1209,46 @@ unsigned fused_layout(const aux_hierarchy* h, int m0, int ni, FusedArgs* a) {
     }
     a->smem_bytes = off;
     return off;
+}
+
+bool cluster_layout(const aux_hierarchy* h, int m, const FusedArgs& fa, ClusterArgs* ca) {
+    if (!h->gpu.cluster_tier || m < 1 || fa.m0 != m + 1 || fa.ni > kFusedMaxInner) return false;
+    const Level& L = h->lv[m];
+    if (L.dist || L.geo.H != 2 * kQH || h->lv[m + 1].geo.nq != kThreads || fa.last - fa.m0 + 1 < 2) return false;
+    const size_t quad = (size_t)(1 + 2 * fa.ni) * 4 * kQPP * sizeof(double) + 4 * kQPP;
+    if (quad > (size_t)kFusedSmemMax) return false;
+    ca->f = fa;
+    ca->g = L.geo;
+    ca->val = L.val.p;
+    ca->act = L.active.p;
+    ca->r = L.pcg.r.p;
+    ca->u = L.pcg.u.p;
+    ca->smem_bytes = (unsigned)std::max<size_t>(fa.smem_bytes, (quad + 15) & ~size_t(15));
+    return true;
+}
+
+void launch_cluster_pcg(const ClusterArgs& a, cudaStream_t s) {
+    static bool attr_set = false;
+    if (!attr_set) {
+        AUX_CUDA(cudaFuncSetAttribute(k_cluster_pcg, cudaFuncAttributeMaxDynamicSharedMemorySize, kFusedSmemMax));
+        attr_set = true;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(kClusterCtas);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = a.smem_bytes;
+    cfg.stream = s;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = kClusterCtas;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    AUX_CUDA(cudaLaunchKernelEx(&cfg, k_cluster_pcg, a));
+    AUX_LAUNCHED(1);
 }
 
 void launch_fused_pcg(const FusedArgs& a, cudaStream_t s) {

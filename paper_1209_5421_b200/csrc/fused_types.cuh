@@ -40,4 +40,16 @@ struct FusedArgs {
     unsigned smem_bytes;
 };
 
+// The cluster tier (fused.cu): nonlinear_pcg on a 64x64-cell level whose child
+// is the single-CTA tier's 32x32-cell top level, in one 5-CTA cluster launch.
+struct ClusterArgs {
+    FusedArgs f;          // the single-CTA tier (levels m + 1 .. last), run by CTA 4
+    Geo g;                // level m
+    const double* val;    // its 9 stencil planes (global)
+    const uint8_t* act;
+    const double* r;      // right-hand side (restricted by the parent)
+    double* u;            // result: the PCG iterate
+    unsigned smem_bytes;
+};
+
 }  // namespace auxb200

@@ -213,6 +213,8 @@ struct aux_hierarchy {
     bool tiles = false;              // levels [1, fused_m0) run the overlapped-tile kernels
     auxb200::DBuf<auxb200::FLevel> d_flv;
     auxb200::FusedArgs fused_args{};
+    int cluster_m = -1;              // level run with the single-CTA tier in one cluster (-1: none)
+    auxb200::ClusterArgs cluster_args{};
     auxb200::Profile prof;
     auxb200::DistInfo dist;          // comm == nullptr: one GPU
     double last_setup_ms = 0.0, last_solve_ms = 0.0;

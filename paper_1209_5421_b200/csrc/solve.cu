@@ -1085,6 +1085,10 @@ void gather_root_v(aux_hierarchy* h, int t, const std::vector<double*>& vecs, cu
 
 void pcg_tiles(Ctx& c, int m);
 
+// Levels whose nonlinear_pcg runs as one kernel that writes the iterate u
+// itself (single-CTA tier, cluster tier); elsewhere the parent sums alpha_k p_k.
+bool explicit_iterate(const aux_hierarchy* h, int m) { return m == h->fused_m0 || m == h->cluster_m; }
+
 // Agglomeration: the child level t = dist.agg and everything
 // below live on part 0.  Gather the restricted residual of every part's
 // rectangle, run nonlinear_pcg(t) there, broadcast its iterate.
@@ -1097,7 +1101,7 @@ void agglomerated_pcg(Ctx& c, int t) {
     std::vector<Msg> sm, rm;
     if (cm->rank == 0) {
         pcg_tiles(c, t);   // levels >= t are not distributed: plain single-GPU path on part 0
-        if (t != h->fused_m0) {
+        if (!explicit_iterate(h, t)) {
             PList pl{};
             for (int k = 0; k < ni; ++k) pl.p[k] = T.pcg.p[k].p;
             k_pcg_u<<<blocks_for(T.n), 256, 0, c.s>>>(flat_span(T.n), pl, T.pcg.sc.p, ni, T.pcg.u.p);
@@ -1123,6 +1127,10 @@ void agglomerated_pcg(Ctx& c, int t) {
 // are refreshed after every kernel that writes a vector a neighbour reads.
 void pcg_tiles(Ctx& c, int m) {
     aux_hierarchy* h = c.h;
+    if (m == h->cluster_m) {
+        launch_cluster_pcg(h->cluster_args, c.s);
+        return;
+    }
     if (m == h->fused_m0) {
         launch_fused_pcg(h->fused_args, c.s);
         return;
@@ -1137,7 +1145,7 @@ void pcg_tiles(Ctx& c, int m) {
     const int T = tile_edge(std::min(own.w(), own.h()));
     const int tx = own.w() / T, ntiles = tx * (own.h() / T);
     const bool child_agg = L.dist && (m + 1 == h->dist.agg);
-    const bool child_explicit = (m + 1 == h->fused_m0) || child_agg;
+    const bool child_explicit = explicit_iterate(h, m + 1) || child_agg;
     Span sp = flat_span(L.n);
     if (L.dist) sp = Span{own.cells(), L.geo, own.x0, own.y0, own.w()};
     const int nb = red_blocks(sp.n);
@@ -1156,7 +1164,7 @@ void pcg_tiles(Ctx& c, int m) {
         d.r_out = i == 0 ? nullptr : R[i & 1];
         d.u_pre = P.upre.p;
         d.rc = C.pcg.r.p;
-        d.sc_child = (m + 1 == h->fused_m0) ? nullptr : C.pcg.sc.p;
+        d.sc_child = explicit_iterate(h, m + 1) ? nullptr : C.pcg.sc.p;
         d.child_nval = sc_nval(ni);
         launch_tile_down(d, ntiles, c.o.pre_sweeps, c.s);
         if (L.dist) {
@@ -1374,7 +1382,7 @@ void coarse_root(Ctx& c) {
     }
     ring_exchange(c, 1, {L.pcg.r.p});
     pcg_tiles(c, 1);
-    if (h->fused_m0 != 1) {
+    if (!explicit_iterate(h, 1)) {
         PList pl{};
         for (int k = 0; k < c.o.n_inner; ++k) pl.p[k] = L.pcg.p[k].p;
         Span sp = flat_span(L.n);
@@ -1425,25 +1433,6 @@ void setup_fused(aux_hierarchy* h, const aux_cycle_opts& o) {
     }
     if (m0 != h->fused_m0) h->graph_valid = false;
     h->fused_m0 = m0;
-    // overlapped-tile kernels for the levels above the single-CTA tier
-    bool tiles = h->gpu.tile_kernels != 0 && m0 < (int)h->lv.size() && o.n_inner <= kFusedMaxInner;
-    long max_tiles = 0;
-    for (int l = 1; tiles && l < m0; ++l) {
-        const Rect& r = h->lv[l].own;
-        const int w = std::min(r.w(), r.h());
-        if (!tiles_supported(w, o.pre_sweeps, o.post_sweeps)) tiles = false;
-        else max_tiles = std::max<long>(max_tiles, (long)(r.w() / tile_edge(w)) * (r.h() / tile_edge(w)));
-    }
-    if (h->dist.comm && !tiles)
-        throw_aux(AUX_ARGUMENT_ERROR, "distributed solve needs the tile kernels (1 or 2 sweeps, tile_kernels=1) "
-                                      "and a single-CTA tier on part 0");
-    if (tiles != h->tiles) h->graph_valid = false;
-    h->tiles = tiles;
-    if (tiles && (size_t)(2 * max_tiles) > h->red_partials.n) {   // grid_reduce partials, 2 per tile
-        AUX_CUDA(cudaStreamSynchronize(h->stream));
-        h->red_partials.alloc((size_t)2 * max_tiles);
-        h->graph_valid = false;
-    }
     if (m0 < (int)h->lv.size()) {
         fa.m0 = m0;
         fa.last = (int)h->lv.size() - 1;
@@ -1457,6 +1446,40 @@ void setup_fused(aux_hierarchy* h, const aux_cycle_opts& o) {
         fa.perm = h->c_perm.p;
         fa.lex = h->c_lex.p;
         fa.work = h->c_work.p;
+    }
+    // the level above the single-CTA tier joins it in one thread-block cluster
+    // when it is the 64x64-cell level (multi-GPU: a level gathered on part 0)
+    ClusterArgs ca;
+    std::memset(&ca, 0, sizeof ca);
+    int cm = -1;
+    if (m0 < (int)h->lv.size() && m0 - 1 >= (h->dist.comm ? std::max(1, h->dist.agg) : 1) &&
+        cluster_layout(h, m0 - 1, fa, &ca))
+        cm = m0 - 1;
+    if (cm != h->cluster_m) h->graph_valid = false;
+    h->cluster_m = cm;
+    const int top = cm > 0 ? cm : m0;   // first level not run by the tile kernels
+    // overlapped-tile kernels for the levels above the single-CTA / cluster tier
+    bool tiles = h->gpu.tile_kernels != 0 && m0 < (int)h->lv.size() && o.n_inner <= kFusedMaxInner;
+    long max_tiles = 0;
+    for (int l = 1; tiles && l < top; ++l) {
+        const Rect& r = h->lv[l].own;
+        const int w = std::min(r.w(), r.h());
+        if (!tiles_supported(w, o.pre_sweeps, o.post_sweeps)) tiles = false;
+        else max_tiles = std::max<long>(max_tiles, (long)(r.w() / tile_edge(w)) * (r.h() / tile_edge(w)));
+    }
+    if (h->dist.comm && !tiles)
+        throw_aux(AUX_ARGUMENT_ERROR, "distributed solve needs the tile kernels (1 or 2 sweeps, tile_kernels=1) "
+                                      "and a single-CTA tier on part 0");
+    if (!tiles && cm > 0) {   // the cluster tier is a member of the tile path
+        cm = -1;
+        h->cluster_m = -1;
+    }
+    if (tiles != h->tiles) h->graph_valid = false;
+    h->tiles = tiles;
+    if (tiles && (size_t)(2 * max_tiles) > h->red_partials.n) {   // grid_reduce partials, 2 per tile
+        AUX_CUDA(cudaStreamSynchronize(h->stream));
+        h->red_partials.alloc((size_t)2 * max_tiles);
+        h->graph_valid = false;
     }
     if (m0 >= (int)h->lv.size()) return;
     std::vector<FLevel> d(h->lv.size());
@@ -1479,6 +1502,8 @@ void setup_fused(aux_hierarchy* h, const aux_cycle_opts& o) {
     AUX_CUDA(cudaStreamSynchronize(h->stream));
     fa.lv = h->d_flv.p;
     h->fused_args = fa;
+    ca.f = fa;
+    h->cluster_args = ca;
 }
 
 }  // namespace

@@ -291,3 +291,46 @@ def test_tile_kernels_cycle_options(gpu_api, opts):
     assert abs(res.iterations - ref["iterations"]) <= 1
     err = np.max(np.abs(res.u - ref["u"])) / np.max(np.abs(ref["u"]))
     assert err <= U_TOL, err
+
+
+def _launches(gpu_api, s, g, opts=None):
+    h = gpu_api.setup_hierarchy(s.A, s.coords, gpu=g)
+    gpu_api.solve(s.A, s.b, h, opts)
+    n0 = gpu_api.launch_count()
+    r = gpu_api.solve(s.A, s.b, h, opts)
+    return r, gpu_api.launch_count() - n0
+
+
+CLUSTER_PROBS = {"jitter129": problems.jittered_p1(129), "jitter257": problems.jittered_p1(257),
+                 "graded257": problems.graded_p1(257, 1.3), "poisson257": problems.poisson5(257)}
+
+
+@pytest.mark.parametrize("name", list(CLUSTER_PROBS))
+@pytest.mark.parametrize("opts", [dict(), dict(n_inner=1), dict(n_inner=3), dict(pre_sweeps=2, post_sweeps=2),
+                                  dict(max_directions=2)])
+def test_cluster_tier_parity(gpu_api, name, opts):
+    """The 64x64-cell level and the single-CTA tier in one 5-CTA cluster
+    (fused.cu k_cluster_pcg): oracle parity, and fewer launches than the tile
+    path for the same level (so the cluster path is the one that ran)."""
+    s = CLUSTER_PROBS[name]
+    co = gpu_api.CycleOptions(**opts)
+    res, n_on = _launches(gpu_api, s, gpu_api.GpuOptions(cluster_tier=True), co)
+    off, n_off = _launches(gpu_api, s, gpu_api.GpuOptions(cluster_tier=False), co)
+    ref = ob.CpuHierarchy("oracle", s.A, s.coords).solve(s.b, ob.cycle_opts(**opts))
+    assert abs(res.iterations - ref["iterations"]) <= 1
+    assert np.max(np.abs(res.u - ref["u"])) / np.max(np.abs(ref["u"])) <= U_TOL
+    assert res.iterations == off.iterations
+    assert np.max(np.abs(res.u - off.u)) / np.max(np.abs(off.u)) <= U_TOL
+    assert n_on < n_off
+
+
+def test_cluster_tier_lu_coarse_and_determinism(gpu_api):
+    s = problems.jittered_p1(257)
+    g = gpu_api.GpuOptions(coarse_solve=1)
+    h = gpu_api.setup_hierarchy(s.A, s.coords, gpu=g)
+    r1 = gpu_api.solve(s.A, s.b, h)
+    r2 = gpu_api.solve(s.A, s.b, h)
+    ref = ob.CpuHierarchy("oracle", s.A, s.coords).solve(s.b)
+    assert abs(r1.iterations - ref["iterations"]) <= 1
+    assert np.max(np.abs(r1.u - ref["u"])) / np.max(np.abs(ref["u"])) <= U_TOL
+    assert np.array_equal(r1.u, r2.u)
