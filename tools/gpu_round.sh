@@ -13,6 +13,6 @@ timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > $out/bench_r
 AUX_TRACE=1 timeout 300 python tools/quick_perf.py graded2049 jitter1025 > $out/trace.log 2>&1
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 4000 --csv \
     --log-file $out/launches.csv python tools/prof_one.py graded2049 2 > $out/launches.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_bgs_inv|k_csr_spmv|k_tile_up|k_fused_pcg|k_mgs' -s 20 -c 10 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_bgs_inv|k_csr_spmv|k_tile_up|k_cluster_pcg|k_fused_pcg|k_mgs' -s 20 -c 10 \
     -o $out/prof python tools/prof_one.py graded2049 2 > $out/prof.log 2>&1
 echo done
