@@ -1393,8 +1393,9 @@ void coarse_root(Ctx& c) {
 }
 
 void build_graph(aux_hierarchy* h, const aux_cycle_opts& o, RedState rs) {
-    if (h->dist.comm && !h->dist.comm->graph_capturable()) {   // in-process parts: host barriers, no capture
-        h->graph_valid = false;
+    const char* dg = std::getenv("AUX_DIST_GRAPHS");   // 0: multi-GPU coarse cycle runs eagerly
+    if (h->dist.comm && (!h->dist.comm->graph_capturable() || (dg && std::atoi(dg) == 0))) {
+        h->graph_valid = false;   // in-process parts synchronise through host barriers: no capture
         return;
     }
     if (h->graph_valid && std::memcmp(&h->graph_opts, &o, sizeof o) == 0) return;
@@ -1405,6 +1406,15 @@ void build_graph(aux_hierarchy* h, const aux_cycle_opts& o, RedState rs) {
     h->graph_valid = false;
     if (!h->gpu.use_graphs || h->direct_only || h->lv.size() < 2) return;
     Ctx c{h, h->stream, o, rs, false};
+    if (h->dist.comm && h->dist.comm->size > 1) {
+        // one eager pass first, so every NCCL peer connection the coarse cycle
+        // uses exists before the capture (NCCL connects peers lazily); the
+        // solve overwrites whatever it computed
+        const int64_t b0 = g_launches;
+        coarse_root(c);
+        g_launches = b0;
+        AUX_CUDA(cudaStreamSynchronize(h->stream));
+    }
     const int64_t before = g_launches;
     cudaGraph_t g;
     AUX_CUDA(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
