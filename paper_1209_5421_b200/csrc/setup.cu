@@ -130,10 +130,22 @@ __device__ __forceinline__ double ord_val(unsigned long long k) {
 // bounding_box (auxgrid.hpp:75-91); out = {min x, max x, min y, max y} as
 // order-preserving keys, flag[0] = any non-finite coordinate.
 __global__ void k_bbox(const double* __restrict__ xy, long n, unsigned long long* out, int* flag) {
+    // few blocks, 16-byte loads, one set of atomics per block (per-warp
+    // atomics on the same four words serialised at L2)
     unsigned long long mnx = ~0ull, mxx = 0, mny = ~0ull, mxy = 0;
     int bad = 0;
+    const double2* p2 = reinterpret_cast<const double2*>(xy);
+    const bool a16 = (reinterpret_cast<uintptr_t>(xy) & 15) == 0;   // caller's device array may be 8-aligned
     GSTRIDE(i, n) {
-        const double x = xy[2 * i], y = xy[2 * i + 1];
+        double x, y;
+        if (a16) {
+            const double2 q = p2[i];
+            x = q.x;
+            y = q.y;
+        } else {
+            x = xy[2 * i];
+            y = xy[2 * i + 1];
+        }
         if (!isfinite(x) || !isfinite(y)) { bad = 1; continue; }
         const unsigned long long kx = ord_key(x), ky = ord_key(y);
         mnx = min(mnx, kx); mxx = max(mxx, kx);
@@ -147,7 +159,20 @@ __global__ void k_bbox(const double* __restrict__ xy, long n, unsigned long long
         mxy = max(mxy, __shfl_xor_sync(0xffffffffu, mxy, o));
         bad |= __shfl_xor_sync(0xffffffffu, bad, o);
     }
+    __shared__ unsigned long long sb[kT / 32][4];
+    __shared__ int sbad[kT / 32];
+    const int w = threadIdx.x >> 5;
     if ((threadIdx.x & 31) == 0) {
+        sb[w][0] = mnx; sb[w][1] = mxx; sb[w][2] = mny; sb[w][3] = mxy;
+        sbad[w] = bad;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int k = 1; k < kT / 32; ++k) {
+            mnx = min(mnx, sb[k][0]); mxx = max(mxx, sb[k][1]);
+            mny = min(mny, sb[k][2]); mxy = max(mxy, sb[k][3]);
+            bad |= sbad[k];
+        }
         atomicMin(&out[0], mnx); atomicMax(&out[1], mxx);
         atomicMin(&out[2], mny); atomicMax(&out[3], mxy);
         if (bad) atomicOr(flag, 1);
@@ -196,14 +221,15 @@ __global__ void k_active_from_count(const int* __restrict__ bptr, int nL, uint8_
 __global__ void k_permute_csr(const int* __restrict__ rp, const int* __restrict__ col, const double* __restrict__ v,
                               const int* __restrict__ perm, const int* __restrict__ iperm, long n,
                               const int* __restrict__ rpn, int* __restrict__ coln, double* __restrict__ vn) {
-    // one warp per row: coalesced copy of the row's entries
-    const int lane = threadIdx.x & 31;
-    const long warp = (blockIdx.x * (long)blockDim.x + threadIdx.x) >> 5;
-    const long nw = ((long)gridDim.x * blockDim.x) >> 5;
-    for (long i = warp; i < n; i += nw) {
+    // four lanes per row (rows hold ~7-9 entries): eight rows per warp keep
+    // eight dependent perm -> row_ptr -> col -> iperm chains in flight
+    const int sub = threadIdx.x & 3;
+    const long grp = (blockIdx.x * (long)blockDim.x + threadIdx.x) >> 2;
+    const long ng = ((long)gridDim.x * blockDim.x) >> 2;
+    for (long i = grp; i < n; i += ng) {
         const int old = perm[i];
         const int a = rp[old], b = rp[old + 1], o = rpn[i];
-        for (int p = a + lane; p < b; p += 32) {
+        for (int p = a + sub; p < b; p += 4) {
             coln[o + (p - a)] = iperm[col[p]];
             vn[o + (p - a)] = v[p];
         }
@@ -833,18 +859,18 @@ __global__ void k_local_len(const int* __restrict__ l2s, int n_own, const int* _
     }
 }
 // local rows (entries in the caller's storage order, columns relabelled to
-// local / ghost indices), one warp per row
+// local / ghost indices), four lanes per row (see k_permute_csr)
 __global__ void k_local_csr(const int* __restrict__ gid, int n_own, const int* __restrict__ rp,
                             const int* __restrict__ col, const double* __restrict__ v, const int* __restrict__ iperm,
                             const int* __restrict__ s2l, const int* __restrict__ rpl, int* __restrict__ coll,
                             double* __restrict__ vl) {
-    const int lane = threadIdx.x & 31;
-    const long warp = (blockIdx.x * (long)blockDim.x + threadIdx.x) >> 5;
-    const long nw = ((long)gridDim.x * blockDim.x) >> 5;
-    for (long l = warp; l < n_own; l += nw) {
+    const int sub = threadIdx.x & 3;
+    const long grp = (blockIdx.x * (long)blockDim.x + threadIdx.x) >> 2;
+    const long ng = ((long)gridDim.x * blockDim.x) >> 2;
+    for (long l = grp; l < n_own; l += ng) {
         const int c = gid[l];
         const int a = rp[c], b = rp[c + 1], o = rpl[l];
-        for (int p = a + lane; p < b; p += 32) {
+        for (int p = a + sub; p < b; p += 4) {
             coll[o + (p - a)] = s2l[iperm[col[p]]];
             vl[o + (p - a)] = v[p];
         }
@@ -1180,7 +1206,7 @@ void bounding_box(aux_hierarchy* h, const double* xy, long n) {
         unsigned long long init[4] = {~0ull, 0ull, ~0ull, 0ull};
         AUX_CUDA(cudaMemcpyAsync(bb.p, init, sizeof init, cudaMemcpyHostToDevice, s));
         AUX_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), s));
-        k_bbox<<<grid_for(n, 4), kT, 0, s>>>(xy, n, bb.p, bad.p);
+        k_bbox<<<(unsigned)std::min<long>(148L * 8, std::max<long>(1, (n + kT - 1) / kT)), kT, 0, s>>>(xy, n, bb.p, bad.p);
         AUX_LAUNCHED(1);
         unsigned long long r[4];
         int badh = 0;
@@ -1289,7 +1315,7 @@ void setup_device(aux_hierarchy* h, const aux_csr_view* A, const double* xy, lon
     key.release();
     F.col.alloc(nnz);
     F.v.alloc(nnz);
-    k_permute_csr<<<grid_for((long)n * 32), kT, 0, s>>>(A->row_ptr, A->col_idx, A->values, F.perm.p, F.iperm.p, n,
+    k_permute_csr<<<grid_for((long)n * 4), kT, 0, s>>>(A->row_ptr, A->col_idx, A->values, F.perm.p, F.iperm.p, n,
                                                         F.rp.p, F.col.p, F.v.p);
     AUX_LAUNCHED(1);
 
@@ -1569,7 +1595,7 @@ void setup_device_dist(aux_hierarchy* h, const aux_csr_view* A, const double* xy
     F.nnz = read1(F.rp.p + n_own, s);
     F.col.alloc(std::max<long>(F.nnz, 1));
     F.v.alloc(std::max<long>(F.nnz, 1));
-    k_local_csr<<<grid_for((long)n_own * 32), kT, 0, s>>>(h->dist.gid.p, n_own, A->row_ptr, A->col_idx, A->values,
+    k_local_csr<<<grid_for((long)n_own * 4), kT, 0, s>>>(h->dist.gid.p, n_own, A->row_ptr, A->col_idx, A->values,
                                                           iperm.p, s2l.p, F.rp.p, F.col.p, F.v.p);
     F.perm.alloc(n_own);
     AUX_CUDA(cudaMemcpyAsync(F.perm.p, h->dist.gid.p, sizeof(int) * n_own, cudaMemcpyDeviceToDevice, s));
