@@ -1,19 +1,19 @@
 // tiles.cu — overlapped-tile kernels for the structured levels between the
-// finest level and the single-CTA tier.
+// finest level and the single-CTA / cluster tiers.
 //
 // A K-cycle visit of a structured level (amli_cycle, cycle.hpp:161-197) is a
 // chain of colour passes: 4 per sweep before the coarse correction, 4 after,
 // plus residual, restriction, prolongation and the PCG step's A z.  With one
-// kernel per pass, a level of 4K..262K cells is pure launch latency (the
-// passes touch a few hundred KB each).  Here every visit is two kernels:
+// kernel per pass, a level of 4K..4M cells is pure launch latency.  Here every
+// visit is two kernels:
 //
 //   k_tile_down  per T x T tile: stage the tile plus a ring of h = 4*pre cells
-//                (stencil values, right-hand side) in shared memory, apply the
-//                pending PCG residual update r -= alpha A p (cycle.hpp:125),
-//                run the pre-smoothing colour passes from zero on shrinking
-//                rings (pass k on the tile dilated by h+1-k), then the
-//                residual and the restriction of the tile's parent cells
-//                (cycle.hpp:173-178, hierarchy.hpp:267-277);
+//                (stencil values, right-hand side), apply the pending PCG
+//                residual update r -= alpha A p (cycle.hpp:125), run the
+//                pre-smoothing colour passes from zero on shrinking rings
+//                (pass k on the tile dilated by h+1-k), then the residual and
+//                the restriction of the tile's parent cells (cycle.hpp:173-178,
+//                hierarchy.hpp:267-277);
 //   k_tile_up    stage the tile plus h = 4*post+1 rings of the pre-smoothed
 //                iterate, add the prolonged coarse correction on active cells
 //                (cycle.hpp:191-194), run the transposed post-smoothing passes
@@ -21,17 +21,28 @@
 //                (ell_spmv, sparse.hpp:120-132) and the step's inner products
 //                through the deterministic grid reduction.
 //
+// Staging is TMA: the levels are stored colour-major (plane c holds the cells
+// of parity c), so a staged region is one box of P x P plane positions in each
+// of the 4 colour planes and 9 stencil slots — ONE cp.async.bulk.tensor for
+// all stencil values of a tile, one per vector, out-of-level positions arriving
+// as zeros.  Shared memory keeps the same colour-major layout
+// [slot][colour][P][P], so every neighbour of a colour-C cell is a
+// compile-time offset and consecutive threads touch consecutive words.
+//
 // Redundant ring work is the price of removing 10+ dependent launches per
 // visit.  Every cell value a tile writes is computed with exactly the
 // operations, in exactly the order, of the sequential colour-ordered
 // Gauss-Seidel (smoother.hpp:81-86) — the ring argument: pass k on the ring-
 // (h+1-k) region only reads cells that passes < k completed on larger regions,
 // and cells of one colour never neighbour each other — so the smoothed values
-// are bitwise those of the per-colour kernels.  Off-grid cells are staged as
+// are bitwise those of the per-colour kernels.  Off-level cells are staged as
 // identity rows with zero right-hand side (their stencil slots in the owning
 // cells hold exact zeros, hierarchy.hpp:121-131), so no bounds checks remain
 // in the passes.
+#include <cudaTypedefs.h>
+
 #include "tiles.cuh"
+#include "tma.cuh"
 
 namespace auxb200 {
 
@@ -43,57 +54,103 @@ __device__ __forceinline__ int cmi(const Geo& g, int t1, int t2) {
     return ((((t2 & 1) << 1) | (t1 & 1)) << g.lq) + ((t2 >> 1) << g.lh) + (t1 >> 1);
 }
 
-// 8-byte asynchronous global -> shared copies (LDGSTS): every stencil value a
-// tile stages is in flight at once, without passing through registers.
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(smem)),
-                 "l"(gmem)
-                 : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
-
 template <int T, int H>
 struct Tile {
-    static constexpr int RW = T + 2 * H;
-    static constexpr int N = RW * RW;
-    // shared-memory layout (bytes): val[9][N], u[N], f[N], act[N]
-    static constexpr size_t bytes = (size_t)N * (9 * 8 + 8 + 8) + ((N + 15) & ~15);
+    static constexpr int RW = T + 2 * H;                   // staged cells per side
+    // plane positions per side: the box starts at an even plane column (a TMA
+    // box must start on a 16-byte boundary of its rows), so the a extent
+    // covers one more; both even so every plane group stays 128-byte aligned
+    static constexpr int PA = ((RW / 2 + 2) + 1) & ~1;
+    static constexpr int PB = ((RW / 2 + 1) + 1) & ~1;
+    static constexpr int PP = PA * PB;
+    // shared memory (bytes): val[9][4][PB][PA] | u[4][PB][PA] | f[4][PB][PA] | ep[PB][PA] | act[4][PB][PA] | mbarriers
+    static constexpr size_t o_u = (size_t)36 * PP * 8;     // PP a multiple of 4: 128-byte multiples
+    static constexpr size_t o_f = o_u + (size_t)4 * PP * 8;
+    static constexpr size_t o_ep = o_f + (size_t)4 * PP * 8;
+    static constexpr size_t o_act = o_ep + (size_t)PP * 8;
+    static constexpr size_t o_bar = (o_act + 4 * PP + 15) & ~size_t(15);
+    static constexpr size_t bytes = o_bar + 16 + 128;      // + alignment slack of the dynamic base
 };
 
-// slot offsets in the natural (row-major, width RW) staging layout
-template <int RW>
-__device__ __forceinline__ int soff(int t) {
-    return stencil_dx(t) + stencil_dy(t) * RW;
+__device__ __forceinline__ unsigned char* align128(unsigned char* p) {
+    return reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(p) + 127) & ~uintptr_t(127));
 }
 
-// One colour pass of point_gs_sweep on the square [lo, hi)^2 of the staged
-// region; cx, cy = parity of the region origin.
-template <int RW, int N>
+// Offset of the slot-S neighbour of a colour-C cell in the [colour][PB][PA] layout.
+template <int C, int S, int PA, int PB>
+__device__ __forceinline__ constexpr int noffp() {
+    constexpr int ux = (C & 1) + stencil_dx(S);
+    constexpr int uy = (C >> 1) + stencil_dy(S);
+    constexpr int nc = (ux & 1) | ((uy & 1) << 1);
+    constexpr int da = ux >> 1, db = uy >> 1;   // arithmetic shift: -1 >> 1 == -1
+    return (nc - C) * PA * PB + db * PA + da;
+}
+
+__device__ __forceinline__ int plane_a0(int x0) { return (x0 >> 1) & ~1; }   // even box start
+
+// One colour pass of point_gs_sweep (smoother.hpp:81-86) on the cells of
+// colour C in [x0 + lo, x0 + hi) x [y0 + lo, y0 + hi).
+template <int C, int PA, int PB>
 __device__ __forceinline__ void gs_pass(const double* __restrict__ val, const double* __restrict__ f, double* u,
-                                        int c, int lo, int hi, int cx, int cy, bool from_zero) {
-    const int ca = (c & 1) ^ cx, cb = (c >> 1) ^ cy;
-    const int a0 = lo + ((lo ^ ca) & 1), b0 = lo + ((lo ^ cb) & 1);
-    const int na = (hi - a0 + 1) >> 1, nb = (hi - b0 + 1) >> 1;
+                                        int lo, int hi, int x0, int y0, bool from_zero) {
+    constexpr int PP = PA * PB;
+    const int i0 = lo + (((x0 + lo) ^ C) & 1), j0 = lo + (((y0 + lo) ^ (C >> 1)) & 1);
+    const int na = (hi - i0 + 1) >> 1, nb = (hi - j0 + 1) >> 1;
+    const int a0 = ((x0 + i0) >> 1) - plane_a0(x0), b0 = ((y0 + j0) >> 1) - (y0 >> 1);
     for (int idx = threadIdx.x; idx < na * nb; idx += kTT) {
         const int j = idx / na;
-        const int s = (b0 + 2 * j) * RW + a0 + 2 * (idx - j * na);
+        const int s = C * PP + (b0 + j) * PA + a0 + (idx - j * na);
         double sum = f[s];
         if (!from_zero) {
-#pragma unroll
-            for (int t = 1; t < 9; ++t) sum = __dsub_rn(sum, __dmul_rn(val[t * N + s], u[s + soff<RW>(t)]));
+            sum = __dsub_rn(sum, __dmul_rn(val[1 * 4 * PP + s], u[s + noffp<C, 1, PA, PB>()]));
+            sum = __dsub_rn(sum, __dmul_rn(val[2 * 4 * PP + s], u[s + noffp<C, 2, PA, PB>()]));
+            sum = __dsub_rn(sum, __dmul_rn(val[3 * 4 * PP + s], u[s + noffp<C, 3, PA, PB>()]));
+            sum = __dsub_rn(sum, __dmul_rn(val[4 * 4 * PP + s], u[s + noffp<C, 4, PA, PB>()]));
+            sum = __dsub_rn(sum, __dmul_rn(val[5 * 4 * PP + s], u[s + noffp<C, 5, PA, PB>()]));
+            sum = __dsub_rn(sum, __dmul_rn(val[6 * 4 * PP + s], u[s + noffp<C, 6, PA, PB>()]));
+            sum = __dsub_rn(sum, __dmul_rn(val[7 * 4 * PP + s], u[s + noffp<C, 7, PA, PB>()]));
+            sum = __dsub_rn(sum, __dmul_rn(val[8 * 4 * PP + s], u[s + noffp<C, 8, PA, PB>()]));
         }
         u[s] = __ddiv_rn(sum, val[s]);
     }
     __syncthreads();
 }
 
-// (A x)_s in the ell_spmv order: from 0.0, slots 0..8
-template <int RW, int N>
+template <int PA, int PB>
+__device__ __forceinline__ void gs_pass_c(int c, const double* val, const double* f, double* u, int lo, int hi,
+                                          int x0, int y0, bool from_zero) {
+    switch (c) {   // c is a constant of the unrolled pass loop
+        case 0: gs_pass<0, PA, PB>(val, f, u, lo, hi, x0, y0, from_zero); break;
+        case 1: gs_pass<1, PA, PB>(val, f, u, lo, hi, x0, y0, from_zero); break;
+        case 2: gs_pass<2, PA, PB>(val, f, u, lo, hi, x0, y0, from_zero); break;
+        default: gs_pass<3, PA, PB>(val, f, u, lo, hi, x0, y0, from_zero); break;
+    }
+}
+
+// (A x)_s of a colour-C cell in the ell_spmv order: from 0.0, slots 0..8
+template <int C, int PA, int PB>
 __device__ __forceinline__ double row9s(const double* __restrict__ val, const double* x, int s) {
+    constexpr int PP = PA * PB;
     double y = __dadd_rn(0.0, __dmul_rn(val[s], x[s]));
-#pragma unroll
-    for (int t = 1; t < 9; ++t) y = __dadd_rn(y, __dmul_rn(val[t * N + s], x[s + soff<RW>(t)]));
+    y = __dadd_rn(y, __dmul_rn(val[1 * 4 * PP + s], x[s + noffp<C, 1, PA, PB>()]));
+    y = __dadd_rn(y, __dmul_rn(val[2 * 4 * PP + s], x[s + noffp<C, 2, PA, PB>()]));
+    y = __dadd_rn(y, __dmul_rn(val[3 * 4 * PP + s], x[s + noffp<C, 3, PA, PB>()]));
+    y = __dadd_rn(y, __dmul_rn(val[4 * 4 * PP + s], x[s + noffp<C, 4, PA, PB>()]));
+    y = __dadd_rn(y, __dmul_rn(val[5 * 4 * PP + s], x[s + noffp<C, 5, PA, PB>()]));
+    y = __dadd_rn(y, __dmul_rn(val[6 * 4 * PP + s], x[s + noffp<C, 6, PA, PB>()]));
+    y = __dadd_rn(y, __dmul_rn(val[7 * 4 * PP + s], x[s + noffp<C, 7, PA, PB>()]));
+    y = __dadd_rn(y, __dmul_rn(val[8 * 4 * PP + s], x[s + noffp<C, 8, PA, PB>()]));
     return y;
+}
+
+template <int PA, int PB>
+__device__ __forceinline__ double row9c(int c, const double* val, const double* x, int s) {
+    switch (c) {
+        case 0: return row9s<0, PA, PB>(val, x, s);
+        case 1: return row9s<1, PA, PB>(val, x, s);
+        case 2: return row9s<2, PA, PB>(val, x, s);
+        default: return row9s<3, PA, PB>(val, x, s);
+    }
 }
 
 template <int T, int H>
@@ -103,82 +160,92 @@ __device__ __forceinline__ void tile_origin(int ox, int oy, int tiles_x, int& x0
     y0 = oy + ty * T - H;
 }
 
+// Staged positions outside the level: identity rows, zero right-hand side.
+template <int PA, int PB>
+__device__ __forceinline__ void fix_off_level(double* val, double* f, int x0, int y0, int w) {
+    constexpr int PP = PA * PB;
+    const int ap0 = plane_a0(x0), bp0 = y0 >> 1;
+    for (int i = threadIdx.x; i < 4 * PP; i += kTT) {
+        const int c = i / PP, r = i - c * PP, b = r / PA, aa = r - b * PA;
+        const int t1 = 2 * (ap0 + aa) + (c & 1), t2 = 2 * (bp0 + b) + (c >> 1);
+        if ((unsigned)t1 >= (unsigned)w || (unsigned)t2 >= (unsigned)w) {
+            val[i] = 1.0;
+            f[i] = 0.0;
+        }
+    }
+}
+
 // ---------------------------------------------------------------- down
 template <int T, int H>
 __global__ void __launch_bounds__(kTT) k_tile_down(const __grid_constant__ TileDown a) {
     using L = Tile<T, H>;
-    constexpr int RW = L::RW, N = L::N;
-    extern __shared__ __align__(16) unsigned char smraw[];
-    double* val = reinterpret_cast<double*>(smraw);
-    double* u = val + 9 * N;
-    double* f = u + N;
+    constexpr int RW = L::RW, PA = L::PA, PB = L::PB, PP = L::PP, TP = T / 2;
+    extern __shared__ unsigned char smraw[];
+    unsigned char* sm = align128(smraw);
+    double* val = reinterpret_cast<double*>(sm);
+    double* u = reinterpret_cast<double*>(sm + L::o_u);
+    double* f = reinterpret_cast<double*>(sm + L::o_f);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::o_bar);
     int x0, y0;
     tile_origin<T, H>(a.ox, a.oy, a.tiles_x, x0, y0);
     const int w = 1 << a.g.k;
+    const int ap0 = plane_a0(x0), bp0 = y0 >> 1;
+    const bool upd = a.ap_prev != nullptr;
     pdl_trigger();
-    // stencil values are constant during the solve: staged before the wait
-    for (int idx = threadIdx.x; idx < N; idx += kTT) {
-        const int br = idx / RW, ar = idx - br * RW;
-        const int t1 = x0 + ar, t2 = y0 + br;
-        u[idx] = 0.0;
-        if ((unsigned)t1 < (unsigned)w && (unsigned)t2 < (unsigned)w) {
-            const int gi = cmi(a.g, t1, t2);
-#pragma unroll
-            for (int t = 0; t < 9; ++t) cp_async8(&val[t * N + idx], &a.val[(size_t)t * a.g.n + gi]);
-        } else {
-            val[idx] = 1.0;
-#pragma unroll
-            for (int t = 1; t < 9; ++t) val[t * N + idx] = 0.0;
-            f[idx] = 0.0;
-        }
+    if (threadIdx.x == 0) {   // stencil values are constant during the solve: requested before the wait
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        fence_mbar_init();
+        mbar_arrive_expect_tx(&bar[0], 36u * PP * 8u);
+        tma_load_4d(val, &a.m_val, ap0, bp0, 0, 0, &bar[0]);
     }
     pdl_wait();
-    const bool upd = a.ap_prev != nullptr;
-    const double na = upd ? -a.sc[0] : 0.0;
+    if (threadIdx.x == 0) {
+        mbar_arrive_expect_tx(&bar[1], (upd ? 8u : 4u) * PP * 8u);
+        tma_load_3d(f, &a.m_r, ap0, bp0, 0, &bar[1]);
+        if (upd) tma_load_3d(u, &a.m_ap, ap0, bp0, 0, &bar[1]);   // A p of the previous step, into u
+    }
     if (a.sc_child && blockIdx.x == 0 && threadIdx.x == 0) {   // child's PCG starts afresh
         a.sc_child[2] = 0.0;
         a.sc_child[a.child_nval] = 0.0;
     }
-    for (int idx = threadIdx.x; idx < N; idx += kTT) {
-        const int br = idx / RW, ar = idx - br * RW;
-        const int t1 = x0 + ar, t2 = y0 + br;
-        if ((unsigned)t1 < (unsigned)w && (unsigned)t2 < (unsigned)w) {
-            const int gi = cmi(a.g, t1, t2);
-            double fi = a.r_in[gi];
-            if (upd) fi = __dadd_rn(fi, __dmul_rn(na, a.ap_prev[gi]));   // axpy(-alpha, ap, r)
-            f[idx] = fi;
-        }
+    const double na = upd ? -a.sc[0] : 0.0;
+    __syncthreads();   // barrier init visible before anyone waits on it
+    mbar_wait(&bar[1], 0);
+    for (int i = threadIdx.x; i < 4 * PP; i += kTT) {
+        if (upd) f[i] = __dadd_rn(f[i], __dmul_rn(na, u[i]));   // axpy(-alpha, ap, r); zeros stay zero
+        u[i] = 0.0;
     }
-    cp_async_wait_all();
+    mbar_wait(&bar[0], 0);
+    if (x0 < 0 || y0 < 0 || x0 + RW > w || y0 + RW > w) fix_off_level<PA, PB>(val, f, x0, y0, w);
     __syncthreads();
-    const int cx = x0 & 1, cy = y0 & 1;
-    constexpr int P = H / 4;   // pre sweeps
+    constexpr int NP = H / 4;   // pre sweeps
 #pragma unroll
-    for (int k = 1; k <= 4 * P; ++k) {
+    for (int k = 1; k <= 4 * NP; ++k) {
         const int D = H + 1 - k;
-        gs_pass<RW, N>(val, f, u, (k - 1) & 3, H - D, H + T + D, cx, cy, k == 1);
+        gs_pass_c<PA, PB>((k - 1) & 3, val, f, u, H - D, H + T + D, x0, y0, k == 1);
     }
-    // interior outputs: pre-smoothed iterate, updated residual
-    for (int idx = threadIdx.x; idx < T * T; idx += kTT) {
-        const int bi = idx / T, ai = idx - bi * T;
-        const int s = (H + bi) * RW + H + ai;
-        const int gi = cmi(a.g, x0 + H + ai, y0 + H + bi);
+    // interior outputs: pre-smoothed iterate, updated residual (plane rows of
+    // T/2 consecutive words per colour)
+    const int ai = ((x0 + H) >> 1) - ap0, bi = ((y0 + H) >> 1) - bp0;
+    for (int idx = threadIdx.x; idx < 4 * TP * TP; idx += kTT) {
+        const int c = idx / (TP * TP), r = idx - c * TP * TP, pb = r / TP, pa = r - pb * TP;
+        const int s = c * PP + (bi + pb) * PA + ai + pa;
+        const int gi = (c << a.g.lq) + (((y0 + H) >> 1) + pb) * (1 << a.g.lh) + ((x0 + H) >> 1) + pa;
         a.u_pre[gi] = u[s];
         if (a.r_out) a.r_out[gi] = f[s];
     }
-    // residual r = f - A u of the four children, summed from 0.0 in member
-    // order SW, SE, NW, NE into the parent
-    constexpr int TP = T / 2;
+    // residual r = f - A u of the four children (colours 0..3 at one plane
+    // position), summed from 0.0 in member order SW, SE, NW, NE into the parent
     for (int idx = threadIdx.x; idx < TP * TP; idx += kTT) {
         const int pb = idx / TP, pa = idx - pb * TP;
-        const int s0 = (H + 2 * pb) * RW + H + 2 * pa;
+        const int s0 = (bi + pb) * PA + ai + pa;
         double sum = 0.0;
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            const int s = s0 + (c >> 1) * RW + (c & 1);
-            sum = __dadd_rn(sum, __dsub_rn(f[s], row9s<RW, N>(val, u, s)));
-        }
-        a.rc[cmi(a.gc, (x0 + H) / 2 + pa, (y0 + H) / 2 + pb)] = sum;
+        sum = __dadd_rn(sum, __dsub_rn(f[s0], row9s<0, PA, PB>(val, u, s0)));
+        sum = __dadd_rn(sum, __dsub_rn(f[PP + s0], row9s<1, PA, PB>(val, u, PP + s0)));
+        sum = __dadd_rn(sum, __dsub_rn(f[2 * PP + s0], row9s<2, PA, PB>(val, u, 2 * PP + s0)));
+        sum = __dadd_rn(sum, __dsub_rn(f[3 * PP + s0], row9s<3, PA, PB>(val, u, 3 * PP + s0)));
+        a.rc[cmi(a.gc, ((x0 + H) >> 1) + pa, ((y0 + H) >> 1) + pb)] = sum;
     }
 }
 
@@ -186,33 +253,41 @@ __global__ void __launch_bounds__(kTT) k_tile_down(const __grid_constant__ TileD
 template <int T, int H>
 __global__ void __launch_bounds__(kTT) k_tile_up(const __grid_constant__ TileUp a, RedState rs, Fin fin) {
     using L = Tile<T, H>;
-    constexpr int RW = L::RW, N = L::N;
-    extern __shared__ __align__(16) unsigned char smraw[];
-    double* val = reinterpret_cast<double*>(smraw);
-    double* u = val + 9 * N;
-    double* f = u + N;
+    constexpr int RW = L::RW, PA = L::PA, PB = L::PB, PP = L::PP, TP = T / 2;
+    extern __shared__ unsigned char smraw[];
+    unsigned char* sm = align128(smraw);
+    double* val = reinterpret_cast<double*>(sm);
+    double* u = reinterpret_cast<double*>(sm + L::o_u);
+    double* f = reinterpret_cast<double*>(sm + L::o_f);
+    double* ep = reinterpret_cast<double*>(sm + L::o_ep);
+    uint8_t* act = sm + L::o_act;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::o_bar);
     int x0, y0;
     tile_origin<T, H>(a.ox, a.oy, a.tiles_x, x0, y0);
     const int w = 1 << a.g.k;
+    const int ap0 = plane_a0(x0), bp0 = y0 >> 1;
     pdl_trigger();
-    for (int idx = threadIdx.x; idx < N; idx += kTT) {   // constant data first (before the wait)
-        const int br = idx / RW, ar = idx - br * RW;
-        const int t1 = x0 + ar, t2 = y0 + br;
-        if ((unsigned)t1 < (unsigned)w && (unsigned)t2 < (unsigned)w) {
-            const int gi = cmi(a.g, t1, t2);
-#pragma unroll
-            for (int t = 0; t < 9; ++t) cp_async8(&val[t * N + idx], &a.val[(size_t)t * a.g.n + gi]);
-        } else {
-            val[idx] = 1.0;
-#pragma unroll
-            for (int t = 1; t < 9; ++t) val[t * N + idx] = 0.0;
-            f[idx] = 0.0;
-            u[idx] = 0.0;
-        }
+    if (threadIdx.x == 0) {   // constant data first (before the wait)
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        fence_mbar_init();
+        mbar_arrive_expect_tx(&bar[0], 36u * PP * 8u);
+        tma_load_4d(val, &a.m_val, ap0, bp0, 0, 0, &bar[0]);
+    }
+    for (int i = threadIdx.x; i < 4 * PP; i += kTT) {
+        const int c = i / PP, r = i - c * PP, b = r / PA, aa = r - b * PA;
+        const int t1 = 2 * (ap0 + aa) + (c & 1), t2 = 2 * (bp0 + b) + (c >> 1);
+        act[i] = ((unsigned)t1 < (unsigned)w && (unsigned)t2 < (unsigned)w) ? a.act[cmi(a.g, t1, t2)] : 0;
     }
     pdl_wait();
-    // child correction: explicit, or ((0 + alpha_0 p_0) + alpha_1 p_1) ... over
-    // the child's valid PCG steps (axpy order, cycle.hpp:124)
+    if (threadIdx.x == 0) {
+        mbar_arrive_expect_tx(&bar[1], 8u * PP * 8u);
+        tma_load_3d(f, &a.m_f, ap0, bp0, 0, &bar[1]);
+        tma_load_3d(u, &a.m_u, ap0, bp0, 0, &bar[1]);
+    }
+    // child correction per parent cell (= plane position): explicit, or
+    // ((0 + alpha_0 p_0) + alpha_1 p_1) ... over the child's valid PCG steps
+    // (axpy order, cycle.hpp:124)
     int nval = 0;
     double al[8];
     if (!a.ec) {
@@ -220,46 +295,45 @@ __global__ void __launch_bounds__(kTT) k_tile_up(const __grid_constant__ TileUp 
 #pragma unroll
         for (int k = 0; k < 8; ++k) al[k] = k < nval ? a.sc_c[3 + a.c_ni + k] : 0.0;
     }
-    for (int idx = threadIdx.x; idx < N; idx += kTT) {
-        const int br = idx / RW, ar = idx - br * RW;
-        const int t1 = x0 + ar, t2 = y0 + br;
-        if ((unsigned)t1 < (unsigned)w && (unsigned)t2 < (unsigned)w) {
-            const int gi = cmi(a.g, t1, t2);
-            f[idx] = a.f[gi];
-            double ui = a.u_pre[gi];
-            if (a.act[gi]) {
-                const int pc = cmi(a.gc, t1 >> 1, t2 >> 1);
-                double e;
-                if (a.ec) {
-                    e = a.ec[pc];
-                } else {
-                    e = 0.0;
+    const int wc = w >> 1;
+    for (int i = threadIdx.x; i < PP; i += kTT) {
+        const int b = i / PA, aa = i - b * PA;
+        const int c1 = ap0 + aa, c2 = bp0 + b;
+        double e = 0.0;
+        if ((unsigned)c1 < (unsigned)wc && (unsigned)c2 < (unsigned)wc) {
+            const int pc = cmi(a.gc, c1, c2);
+            if (a.ec) {
+                e = a.ec[pc];
+            } else {
 #pragma unroll
-                    for (int k = 0; k < 8; ++k)
-                        if (k < nval) e = __dadd_rn(e, __dmul_rn(al[k], a.cp[k][pc]));
-                }
-                ui = __dadd_rn(ui, e);
+                for (int k = 0; k < 8; ++k)
+                    if (k < nval) e = __dadd_rn(e, __dmul_rn(al[k], a.cp[k][pc]));
             }
-            u[idx] = ui;
         }
+        ep[i] = e;
     }
-    cp_async_wait_all();
     __syncthreads();
-    const int cx = x0 & 1, cy = y0 & 1;
-    constexpr int P = (H - 1) / 4;   // post sweeps
+    mbar_wait(&bar[1], 0);
+    for (int i = threadIdx.x; i < 4 * PP; i += kTT)
+        if (act[i]) u[i] = __dadd_rn(u[i], ep[i % PP]);   // off-level positions are inactive
+    mbar_wait(&bar[0], 0);
+    if (x0 < 0 || y0 < 0 || x0 + RW > w || y0 + RW > w) fix_off_level<PA, PB>(val, f, x0, y0, w);
+    __syncthreads();
+    constexpr int NP = (H - 1) / 4;   // post sweeps
 #pragma unroll
-    for (int k = 1; k <= 4 * P; ++k) {
+    for (int k = 1; k <= 4 * NP; ++k) {
         const int D = H - k;
-        gs_pass<RW, N>(val, f, u, 3 - ((k - 1) & 3), H - D, H + T + D, cx, cy, false);
+        gs_pass_c<PA, PB>(3 - ((k - 1) & 3), val, f, u, H - D, H + T + D, x0, y0, false);
     }
     // A z on the tile, z and A z out, fused inner products
+    const int ai = ((x0 + H) >> 1) - ap0, bi = ((y0 + H) >> 1) - bp0;
     double v[2] = {0.0, 0.0};
-    for (int idx = threadIdx.x; idx < T * T; idx += kTT) {
-        const int bi = idx / T, ai = idx - bi * T;
-        const int s = (H + bi) * RW + H + ai;
-        const int gi = cmi(a.g, x0 + H + ai, y0 + H + bi);
+    for (int idx = threadIdx.x; idx < 4 * TP * TP; idx += kTT) {
+        const int c = idx / (TP * TP), r = idx - c * TP * TP, pb = r / TP, pa = r - pb * TP;
+        const int s = c * PP + (bi + pb) * PA + ai + pa;
+        const int gi = (c << a.g.lq) + (((y0 + H) >> 1) + pb) * (1 << a.g.lh) + ((x0 + H) >> 1) + pa;
         const double zi = u[s];
-        const double yi = row9s<RW, N>(val, u, s);
+        const double yi = row9c<PA, PB>(c, val, u, s);
         a.z[gi] = zi;
         a.az[gi] = yi;
         if (a.mode == 0) {
@@ -278,32 +352,65 @@ void set_smem(K kernel, size_t bytes) {
     AUX_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
 }
 
+// ---- host: tensor maps of the colour-major level arrays
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        AUX_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+        if (!p || q != cudaDriverEntryPointSuccess) throw_aux(AUX_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
+        fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+// dims (innermost first): plane a, plane b, colour [, slot]; box PA x PB x 4 [x 9]
+void encode_level_map(CUtensorMap* m, const double* base, const Geo& g, int PA, int PB, bool slots) {
+    const cuuint64_t dims[4] = {(cuuint64_t)g.H, (cuuint64_t)g.H, 4, 9};
+    const cuuint64_t strides[3] = {(cuuint64_t)g.H * 8, (cuuint64_t)g.nq * 8, (cuuint64_t)g.n * 8};
+    const cuuint32_t box[4] = {(cuuint32_t)PA, (cuuint32_t)PB, 4, 9};
+    const cuuint32_t es[4] = {1, 1, 1, 1};
+    const CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, slots ? 4 : 3, const_cast<double*>(base), dims,
+                                   strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw_aux(AUX_CUDA_ERROR, "cuTensorMapEncodeTiled failed for a tile level");
+}
+
 }  // namespace
 
 int tile_edge(int w) { return w >= 256 ? 16 : 8; }
 bool tiles_supported(int w, int pre, int post) { return w >= 16 && pre >= 1 && pre <= 2 && post >= 1 && post <= 2; }
 
 template <int T, int H>
-static void down_t(const TileDown& a, int ntiles, cudaStream_t s) {
+static void down_t(TileDown& a, int ntiles, cudaStream_t s) {
     static bool init = false;
     if (!init) {
         set_smem(k_tile_down<T, H>, Tile<T, H>::bytes);
         init = true;
     }
+    constexpr int PA = Tile<T, H>::PA, PB = Tile<T, H>::PB;
+    encode_level_map(&a.m_val, a.val, a.g, PA, PB, true);
+    encode_level_map(&a.m_r, a.r_in, a.g, PA, PB, false);
+    if (a.ap_prev) encode_level_map(&a.m_ap, a.ap_prev, a.g, PA, PB, false);
     launch_pdl(k_tile_down<T, H>, dim3((unsigned)ntiles), dim3(kTT), Tile<T, H>::bytes, s, a);
 }
 
 template <int T, int H>
-static void up_t(const TileUp& a, int ntiles, RedState rs, Fin fin, cudaStream_t s) {
+static void up_t(TileUp& a, int ntiles, RedState rs, Fin fin, cudaStream_t s) {
     static bool init = false;
     if (!init) {
         set_smem(k_tile_up<T, H>, Tile<T, H>::bytes);
         init = true;
     }
+    constexpr int PA = Tile<T, H>::PA, PB = Tile<T, H>::PB;
+    encode_level_map(&a.m_val, a.val, a.g, PA, PB, true);
+    encode_level_map(&a.m_f, a.f, a.g, PA, PB, false);
+    encode_level_map(&a.m_u, a.u_pre, a.g, PA, PB, false);
     launch_pdl(k_tile_up<T, H>, dim3((unsigned)ntiles), dim3(kTT), Tile<T, H>::bytes, s, a, rs, fin);
 }
 
-void launch_tile_down(const TileDown& a, int ntiles, int pre, cudaStream_t s) {
+void launch_tile_down(TileDown& a, int ntiles, int pre, cudaStream_t s) {
     const int T = a.tiles_x_edge;
     if (T == 16) {
         if (pre == 1) down_t<16, 4>(a, ntiles, s); else down_t<16, 8>(a, ntiles, s);
@@ -312,7 +419,7 @@ void launch_tile_down(const TileDown& a, int ntiles, int pre, cudaStream_t s) {
     }
 }
 
-void launch_tile_up(const TileUp& a, int ntiles, int post, RedState rs, Fin fin, cudaStream_t s) {
+void launch_tile_up(TileUp& a, int ntiles, int post, RedState rs, Fin fin, cudaStream_t s) {
     const int T = a.tiles_x_edge;
     if (T == 16) {
         if (post == 1) up_t<16, 5>(a, ntiles, rs, fin, s); else up_t<16, 9>(a, ntiles, rs, fin, s);

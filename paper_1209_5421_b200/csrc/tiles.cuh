@@ -2,6 +2,8 @@
 // finest level and the single-CTA tier (tiles.cu).
 #pragma once
 
+#include <cuda.h>
+
 #include "common.cuh"
 
 namespace auxb200 {
@@ -30,6 +32,10 @@ struct TileDown {
     double* rc;              // child's PCG right-hand side
     double* sc_child;        // child's scalars to reset (nullptr: none)
     int child_nval;          // index of the child's valid-step counter
+    // TMA tensor maps (filled by launch_tile_down): stencil planes, r_in, ap_prev
+    alignas(64) CUtensorMap m_val;
+    alignas(64) CUtensorMap m_r;
+    alignas(64) CUtensorMap m_ap;
 };
 
 // Up half (cycle.hpp:180-196) plus the PCG step's operator application:
@@ -53,13 +59,17 @@ struct TileUp {
     double* az;              // A z (interior)
     const double* ap0;       // mode 1: s0 = z . ap0
     int mode;                // 0: s0 = z.Az, s1 = r.z   1: s0 = z.ap0
+    // TMA tensor maps (filled by launch_tile_up): stencil planes, f, u_pre
+    alignas(64) CUtensorMap m_val;
+    alignas(64) CUtensorMap m_f;
+    alignas(64) CUtensorMap m_u;
 };
 
 // Launch the tile kernels; T = tile edge, pre/post = sweeps (1 or 2).
 bool tiles_supported(int w, int pre, int post);   // w: smaller edge of the owned rectangle
 int tile_edge(int w);
 // ntiles = tiles of the owned rectangle (tiles_x per row)
-void launch_tile_down(const TileDown& a, int ntiles, int pre, cudaStream_t s);
-void launch_tile_up(const TileUp& a, int ntiles, int post, RedState rs, Fin fin, cudaStream_t s);
+void launch_tile_down(TileDown& a, int ntiles, int pre, cudaStream_t s);
+void launch_tile_up(TileUp& a, int ntiles, int post, RedState rs, Fin fin, cudaStream_t s);
 
 }  // namespace auxb200
