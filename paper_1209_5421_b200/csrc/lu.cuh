@@ -125,38 +125,48 @@ __device__ inline void seq_lu_solve(const double* lu, const int* perm, int n, co
     }
 }
 
-// CTA-cooperative factorization of an n x n row-major matrix in global or
-// shared memory.  Every element update is the same single operation as in the
-// sequential loop, and the pivot is the first index of the strict maximum,
-// so the factors are bitwise those of lu_factor.  All threads of the block
-// must call it.  Returns the zero-pivot column or -1.
-__device__ inline int cta_lu_factor(double* a, int* perm, int n) {
+// CTA-cooperative factorization of an n x n row-major matrix (leading
+// dimension ld) in global or shared memory.  Every element update is the same
+// single operation as in the sequential loop, and the pivot is the first index
+// of the strict maximum (warp 0 scans rows k+lane, k+lane+32, ... with a strict
+// comparison, then a warp arg-max with ties to the lower row), so the factors
+// are bitwise those of lu_factor.  The trailing update runs one row per warp,
+// lanes along the columns.  All threads of the block (a multiple of 32) must
+// call it.  Returns the zero-pivot column or -1.
+__device__ inline int cta_lu_factor(double* a, int* perm, int n, int ld) {
     __shared__ int s_piv;
-    __shared__ double s_best;
     __shared__ int s_fail;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
     for (int i = threadIdx.x; i < n; i += blockDim.x) perm[i] = i;
     if (threadIdx.x == 0) s_fail = -1;
     __syncthreads();
     for (int k = 0; k < n; ++k) {
-        if (threadIdx.x == 0) {
-            int piv = k;
-            double best = fabs(a[(size_t)k * n + k]);
-            for (int r = k + 1; r < n; ++r) {
-                const double m = fabs(a[(size_t)r * n + k]);
+        if (wid == 0) {
+            double best = -1.0;
+            int piv = n;
+            for (int r = k + lane; r < n; r += 32) {
+                const double m = fabs(a[(size_t)r * ld + k]);
                 if (m > best) { best = m; piv = r; }
             }
-            s_piv = piv;
-            s_best = best;
-            if (best == 0.0) s_fail = k;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+                const int op = __shfl_xor_sync(0xffffffffu, piv, o);
+                if (ob > best || (ob == best && op < piv)) { best = ob; piv = op; }
+            }
+            if (lane == 0) {
+                s_piv = piv;
+                if (best == 0.0) s_fail = k;
+            }
         }
         __syncthreads();
         if (s_fail >= 0) return s_fail;
         const int piv = s_piv;
         if (piv != k) {
             for (int c = threadIdx.x; c < n; c += blockDim.x) {
-                const double t = a[(size_t)k * n + c];
-                a[(size_t)k * n + c] = a[(size_t)piv * n + c];
-                a[(size_t)piv * n + c] = t;
+                const double t = a[(size_t)k * ld + c];
+                a[(size_t)k * ld + c] = a[(size_t)piv * ld + c];
+                a[(size_t)piv * ld + c] = t;
             }
             if (threadIdx.x == 0) {
                 const int t = perm[k];
@@ -167,19 +177,17 @@ __device__ inline int cta_lu_factor(double* a, int* perm, int n) {
         __syncthreads();
         // multipliers, then the trailing update row by row
         for (int r = k + 1 + threadIdx.x; r < n; r += blockDim.x) {
-            const double m = a[(size_t)r * n + k] / a[(size_t)k * n + k];
-            a[(size_t)r * n + k] = m;
+            const double m = a[(size_t)r * ld + k] / a[(size_t)k * ld + k];
+            a[(size_t)r * ld + k] = m;
         }
         __syncthreads();
-        const int w = n - k - 1;
-        for (long e = threadIdx.x; e < (long)w * w; e += blockDim.x) {
-            const int r = k + 1 + static_cast<int>(e / w);
-            const int c = k + 1 + static_cast<int>(e % w);
-            a[(size_t)r * n + c] = __dsub_rn(a[(size_t)r * n + c], __dmul_rn(a[(size_t)r * n + k], a[(size_t)k * n + c]));
+        for (int r = k + 1 + wid; r < n; r += nw) {
+            const double m = a[(size_t)r * ld + k];
+            for (int c = k + 1 + lane; c < n; c += 32)
+                a[(size_t)r * ld + c] = __dsub_rn(a[(size_t)r * ld + c], __dmul_rn(m, a[(size_t)k * ld + c]));
         }
         __syncthreads();
     }
-    (void)s_best;
     return -1;
 }
 

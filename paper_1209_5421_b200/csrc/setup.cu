@@ -404,7 +404,7 @@ __global__ void k_factor_big(const int* __restrict__ ids, const int* __restrict_
             if (c < (unsigned)s) a[(size_t)q * s + c] = v[p];
         }
     __syncthreads();
-    const int zc = cta_lu_factor(a, perm + r0, s);
+    const int zc = cta_lu_factor(a, perm + r0, s, s);
     if (zc >= 0 && threadIdx.x == 0) atomicMin(err, (unsigned long long)lex_of_cm(g, gid));
 }
 
@@ -445,8 +445,21 @@ __device__ inline void lu_solve_unit(const double* lu, const int* perm, int n, i
     }
 }
 
-__device__ inline void lu_solve_unit_smem(const double* lu, const int* perm, int n, int j, double* x) {
-    lu_solve_unit(lu, perm, n, j, x);
+// Column j of LU^{-1} with the factors at leading dimension ld and the column
+// at stride xs (shared-memory scratch: xs = n puts the columns of consecutive
+// threads in consecutive words); same operations as lu_solve_unit.
+__device__ inline void lu_solve_col(const double* lu, int ld, const int* perm, int n, int j, double* x, int xs) {
+    for (int i = 0; i < n; ++i) x[(size_t)i * xs] = perm[i] == j ? 1.0 : 0.0;
+    for (int i = 1; i < n; ++i) {
+        double s = x[(size_t)i * xs];
+        for (int c = 0; c < i; ++c) s = __dsub_rn(s, __dmul_rn(lu[(size_t)i * ld + c], x[(size_t)c * xs]));
+        x[(size_t)i * xs] = s;
+    }
+    for (int i = n - 1; i >= 0; --i) {
+        double s = x[(size_t)i * xs];
+        for (int c = i + 1; c < n; ++c) s = __dsub_rn(s, __dmul_rn(lu[(size_t)i * ld + c], x[(size_t)c * xs]));
+        x[(size_t)i * xs] = s / lu[(size_t)i * ld + i];
+    }
 }
 
 __global__ void k_inv_cells(const int* __restrict__ bptr, const int* __restrict__ rp, const int* __restrict__ col,
@@ -497,25 +510,28 @@ __global__ void __launch_bounds__(64) k_factor_warp(const int* __restrict__ ids,
                                                     double* __restrict__ lu, int* __restrict__ perm,
                                                     unsigned long long* err, const int* __restrict__ inv_off,
                                                     double* __restrict__ inv) {
-    __shared__ double sa[2][kWarpLU * kWarpLU];
-    __shared__ double sx[2][kWarpLU * kWarpLU];
+    __shared__ double sa[2][kWarpLU * (kWarpLU + 1)];
+    __shared__ double sx[2][kWarpLU * (kWarpLU + 1)];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int task = blockIdx.x * 2 + w;
     if (task >= nids) return;
     const int gid = ids[task];
     const int r0 = bptr[gid], n = bptr[gid + 1] - r0;
     double* a = sa[w];
-    for (int e = lane; e < n * n; e += 32) a[e] = 0.0;
+    // odd row stride: lanes owning rows r hit different banks (stride n even
+    // would put a column of the block in one bank, a 32-way conflict)
+    const int ld = n | 1;
+    for (int e = lane; e < n * ld; e += 32) a[e] = 0.0;
     __syncwarp();
     if (lane < n)
         for (int p = rp[r0 + lane]; p < rp[r0 + lane + 1]; ++p) {
             const unsigned c = (unsigned)(col[p] - r0);
-            if (c < (unsigned)n) a[lane * n + c] = v[p];
+            if (c < (unsigned)n) a[lane * ld + c] = v[p];
         }
     int pm = lane;   // perm[lane]
     __syncwarp();
     for (int k = 0; k < n; ++k) {
-        double best = (lane >= k && lane < n) ? fabs(a[lane * n + k]) : -1.0;
+        double best = (lane >= k && lane < n) ? fabs(a[lane * ld + k]) : -1.0;
         int br = lane;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
@@ -529,9 +545,9 @@ __global__ void __launch_bounds__(64) k_factor_warp(const int* __restrict__ ids,
         }
         if (br != k) {
             for (int c = lane; c < n; c += 32) {
-                const double t = a[k * n + c];
-                a[k * n + c] = a[br * n + c];
-                a[br * n + c] = t;
+                const double t = a[k * ld + c];
+                a[k * ld + c] = a[br * ld + c];
+                a[br * ld + c] = t;
             }
             const int pk = __shfl_sync(0xffffffffu, pm, k), pb = __shfl_sync(0xffffffffu, pm, br);
             if (lane == k) pm = pb;
@@ -539,8 +555,8 @@ __global__ void __launch_bounds__(64) k_factor_warp(const int* __restrict__ ids,
         }
         __syncwarp();
         if (lane > k && lane < n) {
-            double* ar = a + lane * n;
-            const double* ak = a + k * n;
+            double* ar = a + lane * ld;
+            const double* ak = a + k * ld;
             const double m = ar[k] / ak[k];
             ar[k] = m;
             for (int c = k + 1; c < n; ++c) ar[c] = __dsub_rn(ar[c], __dmul_rn(m, ak[c]));
@@ -548,7 +564,7 @@ __global__ void __launch_bounds__(64) k_factor_warp(const int* __restrict__ ids,
         __syncwarp();
     }
     double* out = lu + off[gid];
-    for (int e = lane; e < n * n; e += 32) out[e] = a[e];
+    for (int e = lane; e < n * n; e += 32) out[e] = a[(e / n) * ld + e % n];
     if (lane < n) perm[r0 + lane] = pm;
     if (!inv) return;
     // column j = lane of A^-1: x = P e_j, forward, backward (reference order)
@@ -556,7 +572,7 @@ __global__ void __launch_bounds__(64) k_factor_warp(const int* __restrict__ ids,
     __syncwarp();
     if (lane < n) {
         const int j = lane;
-        for (int i = 0; i < n; ++i) x[i * n + j] = (__shfl_sync(0xffffffffu, pm, i) == j) ? 1.0 : 0.0;
+        for (int i = 0; i < n; ++i) x[i * ld + j] = (__shfl_sync(0xffffffffu, pm, i) == j) ? 1.0 : 0.0;
     } else {
         for (int i = 0; i < n; ++i) (void)__shfl_sync(0xffffffffu, pm, i);
     }
@@ -564,21 +580,21 @@ __global__ void __launch_bounds__(64) k_factor_warp(const int* __restrict__ ids,
     if (lane < n) {
         const int j = lane;
         for (int i = 1; i < n; ++i) {
-            double sm = x[i * n + j];
-            for (int c = 0; c < i; ++c) sm = __dsub_rn(sm, __dmul_rn(a[i * n + c], x[c * n + j]));
-            x[i * n + j] = sm;
+            double sm = x[i * ld + j];
+            for (int c = 0; c < i; ++c) sm = __dsub_rn(sm, __dmul_rn(a[i * ld + c], x[c * ld + j]));
+            x[i * ld + j] = sm;
         }
         for (int i = n - 1; i >= 0; --i) {
-            double sm = x[i * n + j];
-            for (int c = i + 1; c < n; ++c) sm = __dsub_rn(sm, __dmul_rn(a[i * n + c], x[c * n + j]));
-            x[i * n + j] = sm / a[i * n + i];
+            double sm = x[i * ld + j];
+            for (int c = i + 1; c < n; ++c) sm = __dsub_rn(sm, __dmul_rn(a[i * ld + c], x[c * ld + j]));
+            x[i * ld + j] = sm / a[i * ld + i];
         }
     }
     __syncwarp();
     double* iv = inv + inv_off[gid];   // column-major: iv[j * n + i] = (A^-1)(i, j)
     for (int e = lane; e < n * n; e += 32) {
         const int j = e / n, i = e - j * n;
-        iv[e] = x[i * n + j];
+        iv[e] = x[i * ld + j];
     }
 }
 
@@ -590,29 +606,41 @@ __global__ void __launch_bounds__(256) k_factor_cta_smem(const int* __restrict__
                                                         const double* __restrict__ v, Geo g,
                                                         const int* __restrict__ off, double* __restrict__ lu,
                                                         int* __restrict__ perm, unsigned long long* err,
-                                                        const int* __restrict__ inv_off, double* __restrict__ inv) {
+                                                        const int* __restrict__ inv_off, double* __restrict__ inv,
+                                                        int x_smem) {
     extern __shared__ double da[];
     const int gid = ids[blockIdx.x];
     const int r0 = bptr[gid], n = bptr[gid + 1] - r0;
-    for (long e = threadIdx.x; e < (long)n * n; e += blockDim.x) da[e] = 0.0;
+    const int ld = n | 1;   // odd row stride: no bank conflicts down a column
+    for (long e = threadIdx.x; e < (long)n * ld; e += blockDim.x) da[e] = 0.0;
     __syncthreads();
     for (int q = threadIdx.x; q < n; q += blockDim.x)
         for (int p = rp[r0 + q]; p < rp[r0 + q + 1]; ++p) {
             const unsigned c = (unsigned)(col[p] - r0);
-            if (c < (unsigned)n) da[(size_t)q * n + c] = v[p];
+            if (c < (unsigned)n) da[(size_t)q * ld + c] = v[p];
         }
     __syncthreads();
-    const int zc = cta_lu_factor(da, perm + r0, n);
+    const int zc = cta_lu_factor(da, perm + r0, n, ld);
     if (zc >= 0) {
         if (threadIdx.x == 0) atomicMin(err, (unsigned long long)lex_of_cm(g, gid));
         return;
     }
     double* out = lu + off[gid];
-    for (long e = threadIdx.x; e < (long)n * n; e += blockDim.x) out[e] = da[e];
+    for (long e = threadIdx.x; e < (long)n * n; e += blockDim.x) out[e] = da[(e / n) * ld + e % n];
     if (!inv) return;
     __syncthreads();
-    for (int j = threadIdx.x; j < n; j += blockDim.x)
-        lu_solve_unit_smem(da, perm + r0, n, j, inv + inv_off[gid] + (size_t)j * n);
+    double* iv = inv + inv_off[gid];   // column-major: iv[j * n + i] = (A^-1)(i, j)
+    if (x_smem) {   // columns in shared memory (x[i * n + j]), then one coalesced copy
+        double* x = da + (size_t)n * ld;
+        for (int j = threadIdx.x; j < n; j += blockDim.x) lu_solve_col(da, ld, perm + r0, n, j, x + j, n);
+        __syncthreads();
+        for (long e = threadIdx.x; e < (long)n * n; e += blockDim.x) {
+            const int j = (int)(e / n), i = (int)(e - (long)j * n);
+            iv[e] = x[(size_t)i * n + j];
+        }
+    } else {
+        for (int j = threadIdx.x; j < n; j += blockDim.x) lu_solve_col(da, ld, perm + r0, n, j, iv + (size_t)j * n, 1);
+    }
 }
 
 // check_color_locality (smoother.hpp:217-231): any nonzero coupling between
@@ -726,39 +754,34 @@ __global__ void k_dense_from_csr(const int* __restrict__ rp, const int* __restri
     }
 }
 
-// Coarsest level, n <= 128: factor (cta_lu_factor, reference order) with the
+// Coarsest level, n <= 112: factor (cta_lu_factor, reference order) with the
 // matrix in shared memory, then the explicit inverse's columns from the
 // shared factors (same operations as k_inverse).
 __global__ void __launch_bounds__(256) k_coarse_lu_inv_smem(double* a, int* perm, int n, int* zero_col,
                                                            const int* __restrict__ lex_of_storage,
                                                            double* __restrict__ work) {
     extern __shared__ double sl[];
-    for (int e = threadIdx.x; e < n * n; e += blockDim.x) sl[e] = a[e];
+    const int ld = n | 1;   // odd row stride: no bank conflicts down a column
+    for (int e = threadIdx.x; e < n * n; e += blockDim.x) sl[(e / n) * ld + e % n] = a[e];
     __syncthreads();
-    const int zc = cta_lu_factor(sl, perm, n);
+    const int zc = cta_lu_factor(sl, perm, n, ld);
     if (threadIdx.x == 0) *zero_col = zc;
     if (zc >= 0) return;
-    for (int e = threadIdx.x; e < n * n; e += blockDim.x) a[e] = sl[e];
+    for (int e = threadIdx.x; e < n * n; e += blockDim.x) a[e] = sl[(e / n) * ld + e % n];
     __syncthreads();
-    for (int js = threadIdx.x; js < n; js += blockDim.x) {
-        const int j = lex_of_storage[js];
-        double* x = work + (size_t)js * n;
-        for (int i = 0; i < n; ++i) x[i] = perm[i] == j ? 1.0 : 0.0;
-        for (int i = 1; i < n; ++i) {
-            double sm = x[i];
-            for (int q = 0; q < i; ++q) sm = __dsub_rn(sm, __dmul_rn(sl[i * n + q], x[q]));
-            x[i] = sm;
-        }
-        for (int i = n - 1; i >= 0; --i) {
-            double sm = x[i];
-            for (int q = i + 1; q < n; ++q) sm = __dsub_rn(sm, __dmul_rn(sl[i * n + q], x[q]));
-            x[i] = sm / sl[i * n + i];
-        }
+    // column js of the inverse in shared memory (x[i * n + js]), then to work
+    double* xs = sl + (size_t)n * ld;
+    for (int js = threadIdx.x; js < n; js += blockDim.x)
+        lu_solve_col(sl, ld, perm, n, lex_of_storage[js], xs + js, n);
+    __syncthreads();
+    for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+        const int js = e / n, i = e - js * n;
+        work[(size_t)js * n + i] = xs[(size_t)i * n + js];
     }
 }
 
 __global__ void k_cta_lu(double* a, int* perm, int n, int* zero_col) {
-    const int zc = cta_lu_factor(a, perm, n);
+    const int zc = cta_lu_factor(a, perm, n, n);
     if (threadIdx.x == 0) *zero_col = zc;
 }
 
@@ -955,12 +978,12 @@ void factor_coarsest(aux_hierarchy* h) {
     DBuf<double> work((size_t)nc * nc);
     h->c_work.alloc((size_t)2 * nc);
     h->c_inv.alloc((size_t)nc * nc);
-    if (nc <= 128) {
-        const size_t sm = (size_t)nc * nc * sizeof(double);
+    if (nc <= 112) {   // factors (odd leading dimension) + inverse columns in shared memory
+        const size_t sm = ((size_t)nc * (nc | 1) + (size_t)nc * nc) * sizeof(double);
         static bool attr = false;
         if (!attr) {
             AUX_CUDA(cudaFuncSetAttribute(k_coarse_lu_inv_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          128 * 128 * (int)sizeof(double)));
+                                          225 * 1024));
             attr = true;
         }
         k_coarse_lu_inv_smem<<<1, 256, sm, s>>>(h->c_lu.p, h->c_perm.p, nc, zc.p, h->c_lex.p, work.p);
@@ -971,7 +994,7 @@ void factor_coarsest(aux_hierarchy* h) {
     }
     const int z = read1(zc.p, s);
     if (z >= 0) throw_aux(AUX_SINGULAR_ERROR, "lu_factor: zero pivot at column " + std::to_string(z));
-    if (nc > 128) {
+    if (nc > 112) {
         k_inverse<<<grid_for(nc), kT, 0, s>>>(h->c_lu.p, h->c_perm.p, nc, h->c_lex.p, work.p, h->c_inv.p);
         AUX_LAUNCHED(1);
     }
@@ -1104,16 +1127,21 @@ void finest_blocks(aux_hierarchy* h, const Geo& gL, unsigned long long& sing, in
             if (!mid.empty()) {
                 DBuf<int> mid_d(mid.size());
                 AUX_CUDA(cudaMemcpyAsync(mid_d.p, mid.data(), sizeof(int) * mid.size(), cudaMemcpyHostToDevice, s));
-                const size_t sm = (size_t)mid_max * mid_max * sizeof(double);
+                // factors at an odd leading dimension, plus the inverse columns when they fit
+                constexpr size_t kMaxDyn = 225 * 1024;
+                const size_t lu_b = (size_t)mid_max * (mid_max | 1) * sizeof(double);
+                const size_t x_b = (size_t)mid_max * mid_max * sizeof(double);
+                const int x_smem = (h->gpu.block_solve == 0 && lu_b + x_b <= kMaxDyn) ? 1 : 0;
+                const size_t sm = lu_b + (x_smem ? x_b : 0);
                 static bool attr = false;
                 if (!attr) {
                     AUX_CUDA(cudaFuncSetAttribute(k_factor_cta_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                  (int)((size_t)kSmemLU * kSmemLU * sizeof(double))));
+                                                  (int)kMaxDyn));
                     attr = true;
                 }
                 k_factor_cta_smem<<<(unsigned)mid.size(), 256, sm, s>>>(
                     mid_d.p, F.bptr.p, F.rp.p, F.col.p, F.v.p, gL, F.cell_lu_off.p, F.big_lu.p, F.big_perm.p, err.p,
-                    h->gpu.block_solve == 0 ? F.inv_off.p : nullptr, h->gpu.block_solve == 0 ? F.inv.p : nullptr);
+                    h->gpu.block_solve == 0 ? F.inv_off.p : nullptr, h->gpu.block_solve == 0 ? F.inv.p : nullptr, x_smem);
                 AUX_LAUNCHED(1);
                 AUX_CUDA(cudaStreamSynchronize(s));
             }
