@@ -504,58 +504,70 @@ __global__ void k_size_flag(const int* __restrict__ bptr, int nL, int lo, int hi
         flag[g] = (s >= lo && s <= hi) ? 1 : 0;
     }
 }
+template <int G>
 __global__ void __launch_bounds__(64) k_factor_warp(const int* __restrict__ ids, int nids, const int* __restrict__ bptr,
                                                     const int* __restrict__ rp, const int* __restrict__ col,
                                                     const double* __restrict__ v, Geo g, const int* __restrict__ off,
                                                     double* __restrict__ lu, int* __restrict__ perm,
                                                     unsigned long long* err, const int* __restrict__ inv_off,
                                                     double* __restrict__ inv) {
-    __shared__ double sa[2][kWarpLU * (kWarpLU + 1)];
-    __shared__ double sx[2][kWarpLU * (kWarpLU + 1)];
+    // 32 / G blocks of up to G members per warp, G lanes each (lane r of a
+    // group owns row r); the k loop runs to the warp's largest block so every
+    // lane takes part in every shuffle
+    constexpr int BPW = 32 / G, LDM = G | 1;
+    __shared__ double sa[2 * BPW][G * LDM];
+    __shared__ double sx[2 * BPW][G * LDM];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int task = blockIdx.x * 2 + w;
-    if (task >= nids) return;
-    const int gid = ids[task];
-    const int r0 = bptr[gid], n = bptr[gid + 1] - r0;
-    double* a = sa[w];
-    // odd row stride: lanes owning rows r hit different banks (stride n even
-    // would put a column of the block in one bank, a 32-way conflict)
+    const int gl = lane % G, slot = w * BPW + lane / G;
+    const int task = blockIdx.x * 2 * BPW + slot;
+    const bool has = task < nids;
+    const int gid = has ? ids[task] : 0;
+    const int r0 = has ? bptr[gid] : 0, n = has ? bptr[gid + 1] - r0 : 0;
+    // odd row stride: lanes owning rows r hit different banks
     const int ld = n | 1;
-    for (int e = lane; e < n * ld; e += 32) a[e] = 0.0;
-    __syncwarp();
-    if (lane < n)
-        for (int p = rp[r0 + lane]; p < rp[r0 + lane + 1]; ++p) {
-            const unsigned c = (unsigned)(col[p] - r0);
-            if (c < (unsigned)n) a[lane * ld + c] = v[p];
-        }
-    int pm = lane;   // perm[lane]
-    __syncwarp();
-    for (int k = 0; k < n; ++k) {
-        double best = (lane >= k && lane < n) ? fabs(a[lane * ld + k]) : -1.0;
-        int br = lane;
+    int nmax = n;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
+    for (int o = 16; o > 0; o >>= 1) nmax = max(nmax, __shfl_xor_sync(0xffffffffu, nmax, o));
+    double* a = sa[slot];
+    for (int e = gl; e < n * ld; e += G) a[e] = 0.0;
+    __syncwarp();
+    if (gl < n)
+        for (int p = rp[r0 + gl]; p < rp[r0 + gl + 1]; ++p) {
+            const unsigned c = (unsigned)(col[p] - r0);
+            if (c < (unsigned)n) a[gl * ld + c] = v[p];
+        }
+    int pm = gl;   // perm[gl]
+    bool fail = false;
+    __syncwarp();
+    for (int k = 0; k < nmax; ++k) {
+        const bool act = k < n && !fail;
+        double best = (act && gl >= k && gl < n) ? fabs(a[gl * ld + k]) : -1.0;
+        int br = gl;
+#pragma unroll
+        for (int o = G / 2; o > 0; o >>= 1) {
             const double ob = __shfl_xor_sync(0xffffffffu, best, o);
             const int orow = __shfl_xor_sync(0xffffffffu, br, o);
             if (ob > best || (ob == best && orow < br)) { best = ob; br = orow; }
         }
-        if (best == 0.0) {
-            if (lane == 0) atomicMin(err, (unsigned long long)lex_of_cm(g, gid));
-            return;
+        if (act && best == 0.0) {
+            fail = true;
+            if (gl == 0) atomicMin(err, (unsigned long long)lex_of_cm(g, gid));
         }
-        if (br != k) {
-            for (int c = lane; c < n; c += 32) {
+        const bool go = act && !fail;
+        if (go && br != k)
+            for (int c = gl; c < n; c += G) {
                 const double t = a[k * ld + c];
                 a[k * ld + c] = a[br * ld + c];
                 a[br * ld + c] = t;
             }
-            const int pk = __shfl_sync(0xffffffffu, pm, k), pb = __shfl_sync(0xffffffffu, pm, br);
-            if (lane == k) pm = pb;
-            if (lane == br) pm = pk;
+        const int pk = __shfl_sync(0xffffffffu, pm, k, G), pb = __shfl_sync(0xffffffffu, pm, br, G);
+        if (go && br != k) {
+            if (gl == k) pm = pb;
+            if (gl == br) pm = pk;
         }
         __syncwarp();
-        if (lane > k && lane < n) {
-            double* ar = a + lane * ld;
+        if (go && gl > k && gl < n) {
+            double* ar = a + gl * ld;
             const double* ak = a + k * ld;
             const double m = ar[k] / ak[k];
             ar[k] = m;
@@ -563,22 +575,22 @@ __global__ void __launch_bounds__(64) k_factor_warp(const int* __restrict__ ids,
         }
         __syncwarp();
     }
-    double* out = lu + off[gid];
-    for (int e = lane; e < n * n; e += 32) out[e] = a[(e / n) * ld + e % n];
-    if (lane < n) perm[r0 + lane] = pm;
+    const bool ok = has && !fail;
+    if (ok) {
+        double* out = lu + off[gid];
+        for (int e = gl; e < n * n; e += G) out[e] = a[(e / n) * ld + e % n];
+        if (gl < n) perm[r0 + gl] = pm;
+    }
     if (!inv) return;
-    // column j = lane of A^-1: x = P e_j, forward, backward (reference order)
-    double* x = sx[w];   // column-major scratch: x[c * n + j] holds entry c of column j
-    __syncwarp();
-    if (lane < n) {
-        const int j = lane;
-        for (int i = 0; i < n; ++i) x[i * ld + j] = (__shfl_sync(0xffffffffu, pm, i) == j) ? 1.0 : 0.0;
-    } else {
-        for (int i = 0; i < n; ++i) (void)__shfl_sync(0xffffffffu, pm, i);
+    // column j = gl of A^-1: x = P e_j, forward, backward (reference order)
+    double* x = sx[slot];   // x[c * ld + j] holds entry c of column j
+    for (int i = 0; i < nmax; ++i) {
+        const int pmi = __shfl_sync(0xffffffffu, pm, i, G);
+        if (ok && gl < n && i < n) x[i * ld + gl] = (pmi == gl) ? 1.0 : 0.0;
     }
     __syncwarp();
-    if (lane < n) {
-        const int j = lane;
+    if (ok && gl < n) {
+        const int j = gl;
         for (int i = 1; i < n; ++i) {
             double sm = x[i * ld + j];
             for (int c = 0; c < i; ++c) sm = __dsub_rn(sm, __dmul_rn(a[i * ld + c], x[c * ld + j]));
@@ -591,10 +603,12 @@ __global__ void __launch_bounds__(64) k_factor_warp(const int* __restrict__ ids,
         }
     }
     __syncwarp();
-    double* iv = inv + inv_off[gid];   // column-major: iv[j * n + i] = (A^-1)(i, j)
-    for (int e = lane; e < n * n; e += 32) {
-        const int j = e / n, i = e - j * n;
-        iv[e] = x[i * ld + j];
+    if (ok) {
+        double* iv = inv + inv_off[gid];   // column-major: iv[j * n + i] = (A^-1)(i, j)
+        for (int e = gl; e < n * n; e += G) {
+            const int j = e / n, i = e - j * n;
+            iv[e] = x[i * ld + j];
+        }
     }
 }
 
@@ -1065,19 +1079,27 @@ void finest_blocks(aux_hierarchy* h, const Geo& gL, unsigned long long& sing, in
                                                     F.big_lu.p, F.big_perm.p, F.inv_off.p, F.inv.p);
             AUX_LAUNCHED(1);
         }
-        {   // 5..32 members: a warp per block
+        // 5..32 members: 4 blocks per warp up to 8 members, 2 up to 16, 1 up to 32
+        for (int cls = 0; cls < 3; ++cls) {
+            const int lo = cls == 0 ? 5 : cls == 1 ? 9 : 17, hi = cls == 0 ? 8 : cls == 1 ? 16 : kWarpLU;
             DBuf<int> f7(nL), p7(nL + 1);
-            k_size_flag<<<grid_for(nL), kT, 0, s>>>(F.bptr.p, nL, 5, kWarpLU, f7.p);
+            k_size_flag<<<grid_for(nL), kT, 0, s>>>(F.bptr.p, nL, lo, hi, f7.p);
             AUX_LAUNCHED(1);
             exclusive_scan(f7.p, p7.p, nL, s);
             const int n7 = read1(p7.p + nL, s);
             if (n7 > 0) {
                 DBuf<int> l7(n7);
                 k_compact<<<grid_for(nL), kT, 0, s>>>(f7.p, p7.p, nL, l7.p);
-                k_factor_warp<<<(unsigned)((n7 + 1) / 2), 64, 0, s>>>(l7.p, n7, F.bptr.p, F.rp.p, F.col.p, F.v.p, gL,
-                                                                     F.cell_lu_off.p, F.big_lu.p, F.big_perm.p, err.p,
-                                                                     inv_mode ? F.inv_off.p : nullptr,
-                                                                     inv_mode ? F.inv.p : nullptr);
+                const int per = 2 * (32 / (cls == 0 ? 8 : cls == 1 ? 16 : 32));   // blocks per 64-thread CTA
+                const unsigned grid = (unsigned)((n7 + per - 1) / per);
+                auto launch = [&](auto kern) {
+                    kern<<<grid, 64, 0, s>>>(l7.p, n7, F.bptr.p, F.rp.p, F.col.p, F.v.p, gL, F.cell_lu_off.p,
+                                             F.big_lu.p, F.big_perm.p, err.p, inv_mode ? F.inv_off.p : nullptr,
+                                             inv_mode ? F.inv.p : nullptr);
+                };
+                if (cls == 0) launch(k_factor_warp<8>);
+                else if (cls == 1) launch(k_factor_warp<16>);
+                else launch(k_factor_warp<32>);
                 AUX_LAUNCHED(2);
                 AUX_CUDA(cudaStreamSynchronize(s));
             }
