@@ -56,100 +56,129 @@ __device__ __forceinline__ int cmi(const Geo& g, int t1, int t2) {
 
 template <int T, int H>
 struct Tile {
-    static constexpr int RW = T + 2 * H;                   // staged cells per side
-    // plane positions per side: the box starts at an even plane column (a TMA
-    // box must start on a 16-byte boundary of its rows), so the a extent
-    // covers one more; both even so every plane group stays 128-byte aligned
-    static constexpr int PA = ((RW / 2 + 2) + 1) & ~1;
-    static constexpr int PB = ((RW / 2 + 1) + 1) & ~1;
+    static constexpr int RW = T + 2 * H;   // staged cells per side
+    // The staged box of colour c starts at plane column org[c & 1]: a TMA box
+    // must start on a 16-byte boundary of its rows, i.e. an even plane column.
+    // x0 = ox + T*tx - H has the parity of H; with H even both parities start
+    // at x0/2 (even), with H odd the even-x cells start at (x0+1)/2 (even) and
+    // the odd-x cells one column earlier, so their box starts two earlier.
+    static constexpr bool SH = (H & 1) != 0;
+    static constexpr int PA = SH ? RW / 2 + 1 : RW / 2;                 // even for every (T, H) used
+    static constexpr int PB = ((SH ? RW / 2 + 1 : RW / 2) + 1) & ~1;
     static constexpr int PP = PA * PB;
-    // shared memory (bytes): val[9][4][PB][PA] | u[4][PB][PA] | f[4][PB][PA] | ep[PB][PA] | act[4][PB][PA] | mbarriers
-    static constexpr size_t o_u = (size_t)36 * PP * 8;     // PP a multiple of 4: 128-byte multiples
-    static constexpr size_t o_f = o_u + (size_t)4 * PP * 8;
-    static constexpr size_t o_ep = o_f + (size_t)4 * PP * 8;
-    static constexpr size_t o_act = o_ep + (size_t)PP * 8;
-    static constexpr size_t o_bar = (o_act + 4 * PP + 15) & ~size_t(15);
-    static constexpr size_t bytes = o_bar + 16 + 128;      // + alignment slack of the dynamic base
+    // colour strides (doubles) of the vectors and of the 9-slot value blocks:
+    // every TMA destination starts on a 128-byte boundary
+    static constexpr int QS = (PP + 15) & ~15;
+    static constexpr int VS = (9 * PP + 15) & ~15;
+    static constexpr int EW = PA + 2;                                   // parent-correction row width
+    // shared memory (bytes): val[4][VS: 9][PB][PA] | u[4][QS] | f[4][QS] | ep[PB][EW] | act[4][QS] | mbarriers
+    static constexpr size_t o_u = (size_t)4 * VS * 8;
+    static constexpr size_t o_f = o_u + (size_t)4 * QS * 8;
+    static constexpr size_t o_ep = o_f + (size_t)4 * QS * 8;
+    static constexpr size_t o_act = o_ep + (size_t)PB * EW * 8;
+    static constexpr size_t o_bar = (o_act + 4 * QS + 15) & ~size_t(15);
+    static constexpr size_t bytes = o_bar + 16 + 128;                   // + alignment slack of the dynamic base
 };
 
 __device__ __forceinline__ unsigned char* align128(unsigned char* p) {
     return reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(p) + 127) & ~uintptr_t(127));
 }
 
-// Offset of the slot-S neighbour of a colour-C cell in the [colour][PB][PA] layout.
-template <int C, int S, int PA, int PB>
-__device__ __forceinline__ constexpr int noffp() {
-    constexpr int ux = (C & 1) + stencil_dx(S);
-    constexpr int uy = (C >> 1) + stencil_dy(S);
-    constexpr int nc = (ux & 1) | ((uy & 1) << 1);
-    constexpr int da = ux >> 1, db = uy >> 1;   // arithmetic shift: -1 >> 1 == -1
-    return (nc - C) * PA * PB + db * PA + da;
+// plane column where the box of x-parity p starts
+template <bool SH>
+__device__ __forceinline__ int org_of(int x0, int p) {
+    if (!SH) return x0 >> 1;
+    const int oe = (x0 + 1) >> 1;
+    return p ? oe - 2 : oe;
 }
 
-__device__ __forceinline__ int plane_a0(int x0) { return (x0 >> 1) & ~1; }   // even box start
+// Colour strides of a tile geometry (see Tile)
+template <int PA, int PB>
+struct Strides {
+    static constexpr int PP = PA * PB, QS = (PP + 15) & ~15, VS = (9 * PP + 15) & ~15;
+};
+
+// Offset of the slot-S neighbour of a colour-C cell in the [colour: QS][PB][PA]
+// vector layout (the x-parity origins differ by 2 columns when SH).
+template <int C, int S, int PA, int PB, bool SH>
+__device__ __forceinline__ constexpr int noffp() {
+    constexpr int p = C & 1;
+    constexpr int ux = p + stencil_dx(S);
+    constexpr int uy = (C >> 1) + stencil_dy(S);
+    constexpr int pn = ux & 1;
+    constexpr int nc = pn | ((uy & 1) << 1);
+    constexpr int dorg = SH ? (p == pn ? 0 : (p == 0 ? 2 : -2)) : 0;   // org[p] - org[pn]
+    constexpr int da = (ux >> 1) + dorg, db = uy >> 1;                // arithmetic shift: -1 >> 1 == -1
+    return (nc - C) * Strides<PA, PB>::QS + db * PA + da;
+}
+
+// val index of slot t of the cell at vector index s (colour C)
+template <int C, int PA, int PB>
+__device__ __forceinline__ constexpr int vslot(int t) {
+    return C * (Strides<PA, PB>::VS - Strides<PA, PB>::QS) + t * Strides<PA, PB>::PP;
+}
 
 // One colour pass of point_gs_sweep (smoother.hpp:81-86) on the cells of
 // colour C in [x0 + lo, x0 + hi) x [y0 + lo, y0 + hi).
-template <int C, int PA, int PB>
+template <int C, int PA, int PB, bool SH>
 __device__ __forceinline__ void gs_pass(const double* __restrict__ val, const double* __restrict__ f, double* u,
                                         int lo, int hi, int x0, int y0, bool from_zero) {
-    constexpr int PP = PA * PB;
+    constexpr int QS = Strides<PA, PB>::QS;
     const int i0 = lo + (((x0 + lo) ^ C) & 1), j0 = lo + (((y0 + lo) ^ (C >> 1)) & 1);
     const int na = (hi - i0 + 1) >> 1, nb = (hi - j0 + 1) >> 1;
-    const int a0 = ((x0 + i0) >> 1) - plane_a0(x0), b0 = ((y0 + j0) >> 1) - (y0 >> 1);
+    const int a0 = ((x0 + i0) >> 1) - org_of<SH>(x0, C & 1), b0 = ((y0 + j0) >> 1) - (y0 >> 1);
     for (int idx = threadIdx.x; idx < na * nb; idx += kTT) {
         const int j = idx / na;
-        const int s = C * PP + (b0 + j) * PA + a0 + (idx - j * na);
+        const int s = C * QS + (b0 + j) * PA + a0 + (idx - j * na);
         double sum = f[s];
         if (!from_zero) {
-            sum = __dsub_rn(sum, __dmul_rn(val[1 * 4 * PP + s], u[s + noffp<C, 1, PA, PB>()]));
-            sum = __dsub_rn(sum, __dmul_rn(val[2 * 4 * PP + s], u[s + noffp<C, 2, PA, PB>()]));
-            sum = __dsub_rn(sum, __dmul_rn(val[3 * 4 * PP + s], u[s + noffp<C, 3, PA, PB>()]));
-            sum = __dsub_rn(sum, __dmul_rn(val[4 * 4 * PP + s], u[s + noffp<C, 4, PA, PB>()]));
-            sum = __dsub_rn(sum, __dmul_rn(val[5 * 4 * PP + s], u[s + noffp<C, 5, PA, PB>()]));
-            sum = __dsub_rn(sum, __dmul_rn(val[6 * 4 * PP + s], u[s + noffp<C, 6, PA, PB>()]));
-            sum = __dsub_rn(sum, __dmul_rn(val[7 * 4 * PP + s], u[s + noffp<C, 7, PA, PB>()]));
-            sum = __dsub_rn(sum, __dmul_rn(val[8 * 4 * PP + s], u[s + noffp<C, 8, PA, PB>()]));
+            sum = __dsub_rn(sum, __dmul_rn(val[vslot<C, PA, PB>(1) + s], u[s + noffp<C, 1, PA, PB, SH>()]));
+            sum = __dsub_rn(sum, __dmul_rn(val[vslot<C, PA, PB>(2) + s], u[s + noffp<C, 2, PA, PB, SH>()]));
+            sum = __dsub_rn(sum, __dmul_rn(val[vslot<C, PA, PB>(3) + s], u[s + noffp<C, 3, PA, PB, SH>()]));
+            sum = __dsub_rn(sum, __dmul_rn(val[vslot<C, PA, PB>(4) + s], u[s + noffp<C, 4, PA, PB, SH>()]));
+            sum = __dsub_rn(sum, __dmul_rn(val[vslot<C, PA, PB>(5) + s], u[s + noffp<C, 5, PA, PB, SH>()]));
+            sum = __dsub_rn(sum, __dmul_rn(val[vslot<C, PA, PB>(6) + s], u[s + noffp<C, 6, PA, PB, SH>()]));
+            sum = __dsub_rn(sum, __dmul_rn(val[vslot<C, PA, PB>(7) + s], u[s + noffp<C, 7, PA, PB, SH>()]));
+            sum = __dsub_rn(sum, __dmul_rn(val[vslot<C, PA, PB>(8) + s], u[s + noffp<C, 8, PA, PB, SH>()]));
         }
-        u[s] = __ddiv_rn(sum, val[s]);
+        u[s] = __ddiv_rn(sum, val[vslot<C, PA, PB>(0) + s]);
     }
     __syncthreads();
 }
 
-template <int PA, int PB>
+template <int PA, int PB, bool SH>
 __device__ __forceinline__ void gs_pass_c(int c, const double* val, const double* f, double* u, int lo, int hi,
                                           int x0, int y0, bool from_zero) {
     switch (c) {   // c is a constant of the unrolled pass loop
-        case 0: gs_pass<0, PA, PB>(val, f, u, lo, hi, x0, y0, from_zero); break;
-        case 1: gs_pass<1, PA, PB>(val, f, u, lo, hi, x0, y0, from_zero); break;
-        case 2: gs_pass<2, PA, PB>(val, f, u, lo, hi, x0, y0, from_zero); break;
-        default: gs_pass<3, PA, PB>(val, f, u, lo, hi, x0, y0, from_zero); break;
+        case 0: gs_pass<0, PA, PB, SH>(val, f, u, lo, hi, x0, y0, from_zero); break;
+        case 1: gs_pass<1, PA, PB, SH>(val, f, u, lo, hi, x0, y0, from_zero); break;
+        case 2: gs_pass<2, PA, PB, SH>(val, f, u, lo, hi, x0, y0, from_zero); break;
+        default: gs_pass<3, PA, PB, SH>(val, f, u, lo, hi, x0, y0, from_zero); break;
     }
 }
 
 // (A x)_s of a colour-C cell in the ell_spmv order: from 0.0, slots 0..8
-template <int C, int PA, int PB>
+template <int C, int PA, int PB, bool SH>
 __device__ __forceinline__ double row9s(const double* __restrict__ val, const double* x, int s) {
-    constexpr int PP = PA * PB;
-    double y = __dadd_rn(0.0, __dmul_rn(val[s], x[s]));
-    y = __dadd_rn(y, __dmul_rn(val[1 * 4 * PP + s], x[s + noffp<C, 1, PA, PB>()]));
-    y = __dadd_rn(y, __dmul_rn(val[2 * 4 * PP + s], x[s + noffp<C, 2, PA, PB>()]));
-    y = __dadd_rn(y, __dmul_rn(val[3 * 4 * PP + s], x[s + noffp<C, 3, PA, PB>()]));
-    y = __dadd_rn(y, __dmul_rn(val[4 * 4 * PP + s], x[s + noffp<C, 4, PA, PB>()]));
-    y = __dadd_rn(y, __dmul_rn(val[5 * 4 * PP + s], x[s + noffp<C, 5, PA, PB>()]));
-    y = __dadd_rn(y, __dmul_rn(val[6 * 4 * PP + s], x[s + noffp<C, 6, PA, PB>()]));
-    y = __dadd_rn(y, __dmul_rn(val[7 * 4 * PP + s], x[s + noffp<C, 7, PA, PB>()]));
-    y = __dadd_rn(y, __dmul_rn(val[8 * 4 * PP + s], x[s + noffp<C, 8, PA, PB>()]));
+    double y = __dadd_rn(0.0, __dmul_rn(val[vslot<C, PA, PB>(0) + s], x[s]));
+    y = __dadd_rn(y, __dmul_rn(val[vslot<C, PA, PB>(1) + s], x[s + noffp<C, 1, PA, PB, SH>()]));
+    y = __dadd_rn(y, __dmul_rn(val[vslot<C, PA, PB>(2) + s], x[s + noffp<C, 2, PA, PB, SH>()]));
+    y = __dadd_rn(y, __dmul_rn(val[vslot<C, PA, PB>(3) + s], x[s + noffp<C, 3, PA, PB, SH>()]));
+    y = __dadd_rn(y, __dmul_rn(val[vslot<C, PA, PB>(4) + s], x[s + noffp<C, 4, PA, PB, SH>()]));
+    y = __dadd_rn(y, __dmul_rn(val[vslot<C, PA, PB>(5) + s], x[s + noffp<C, 5, PA, PB, SH>()]));
+    y = __dadd_rn(y, __dmul_rn(val[vslot<C, PA, PB>(6) + s], x[s + noffp<C, 6, PA, PB, SH>()]));
+    y = __dadd_rn(y, __dmul_rn(val[vslot<C, PA, PB>(7) + s], x[s + noffp<C, 7, PA, PB, SH>()]));
+    y = __dadd_rn(y, __dmul_rn(val[vslot<C, PA, PB>(8) + s], x[s + noffp<C, 8, PA, PB, SH>()]));
     return y;
 }
 
-template <int PA, int PB>
+template <int PA, int PB, bool SH>
 __device__ __forceinline__ double row9c(int c, const double* val, const double* x, int s) {
     switch (c) {
-        case 0: return row9s<0, PA, PB>(val, x, s);
-        case 1: return row9s<1, PA, PB>(val, x, s);
-        case 2: return row9s<2, PA, PB>(val, x, s);
-        default: return row9s<3, PA, PB>(val, x, s);
+        case 0: return row9s<0, PA, PB, SH>(val, x, s);
+        case 1: return row9s<1, PA, PB, SH>(val, x, s);
+        case 2: return row9s<2, PA, PB, SH>(val, x, s);
+        default: return row9s<3, PA, PB, SH>(val, x, s);
     }
 }
 
@@ -160,26 +189,52 @@ __device__ __forceinline__ void tile_origin(int ox, int oy, int tiles_x, int& x0
     y0 = oy + ty * T - H;
 }
 
+// (colour, b, a) of vector index i, and its level cell (t1, t2); false on
+// the padding between colour planes
+template <int PA, int PB, bool SH>
+__device__ __forceinline__ bool cell_of(int i, int x0, int y0, int& c, int& t1, int& t2) {
+    constexpr int QS = Strides<PA, PB>::QS;
+    c = i / QS;
+    const int r = i - c * QS, b = r / PA, aa = r - b * PA;
+    t1 = 2 * (org_of<SH>(x0, c & 1) + aa) + (c & 1);
+    t2 = 2 * ((y0 >> 1) + b) + (c >> 1);
+    return r < PA * PB;
+}
+
 // Staged positions outside the level: identity rows, zero right-hand side.
-template <int PA, int PB>
+template <int PA, int PB, bool SH>
 __device__ __forceinline__ void fix_off_level(double* val, double* f, int x0, int y0, int w) {
-    constexpr int PP = PA * PB;
-    const int ap0 = plane_a0(x0), bp0 = y0 >> 1;
-    for (int i = threadIdx.x; i < 4 * PP; i += kTT) {
-        const int c = i / PP, r = i - c * PP, b = r / PA, aa = r - b * PA;
-        const int t1 = 2 * (ap0 + aa) + (c & 1), t2 = 2 * (bp0 + b) + (c >> 1);
+    constexpr int QS = Strides<PA, PB>::QS, VS = Strides<PA, PB>::VS;
+    for (int i = threadIdx.x; i < 4 * QS; i += kTT) {
+        int c, t1, t2;
+        if (!cell_of<PA, PB, SH>(i, x0, y0, c, t1, t2)) continue;
         if ((unsigned)t1 >= (unsigned)w || (unsigned)t2 >= (unsigned)w) {
-            val[i] = 1.0;
+            val[i + c * (VS - QS)] = 1.0;   // slot 0
             f[i] = 0.0;
         }
     }
+}
+
+// TMA requests of one tile: the 9 stencil slots of each colour (4 boxes),
+// or one vector (4 boxes of one colour plane each)
+template <int PA, int PB, bool SH>
+__device__ __forceinline__ void tma_val(double* val, const CUtensorMap* m, int x0, int y0, uint64_t* bar) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+        tma_load_4d(val + c * Strides<PA, PB>::VS, m, org_of<SH>(x0, c & 1), y0 >> 1, c, 0, bar);
+}
+template <int PA, int PB, bool SH>
+__device__ __forceinline__ void tma_vec(double* v, const CUtensorMap* m, int x0, int y0, uint64_t* bar) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) tma_load_3d(v + c * Strides<PA, PB>::QS, m, org_of<SH>(x0, c & 1), y0 >> 1, c, bar);
 }
 
 // ---------------------------------------------------------------- down
 template <int T, int H>
 __global__ void __launch_bounds__(kTT) k_tile_down(const __grid_constant__ TileDown a) {
     using L = Tile<T, H>;
-    constexpr int RW = L::RW, PA = L::PA, PB = L::PB, PP = L::PP, TP = T / 2;
+    constexpr int RW = L::RW, PA = L::PA, PB = L::PB, PP = L::PP, QS = L::QS, TP = T / 2;
+    constexpr bool SH = L::SH;
     extern __shared__ unsigned char smraw[];
     unsigned char* sm = align128(smraw);
     double* val = reinterpret_cast<double*>(sm);
@@ -189,7 +244,6 @@ __global__ void __launch_bounds__(kTT) k_tile_down(const __grid_constant__ TileD
     int x0, y0;
     tile_origin<T, H>(a.ox, a.oy, a.tiles_x, x0, y0);
     const int w = 1 << a.g.k;
-    const int ap0 = plane_a0(x0), bp0 = y0 >> 1;
     const bool upd = a.ap_prev != nullptr;
     pdl_trigger();
     if (threadIdx.x == 0) {   // stencil values are constant during the solve: requested before the wait
@@ -197,13 +251,13 @@ __global__ void __launch_bounds__(kTT) k_tile_down(const __grid_constant__ TileD
         mbar_init(&bar[1], 1);
         fence_mbar_init();
         mbar_arrive_expect_tx(&bar[0], 36u * PP * 8u);
-        tma_load_4d(val, &a.m_val, ap0, bp0, 0, 0, &bar[0]);
+        tma_val<PA, PB, SH>(val, &a.m_val, x0, y0, &bar[0]);
     }
     pdl_wait();
     if (threadIdx.x == 0) {
         mbar_arrive_expect_tx(&bar[1], (upd ? 8u : 4u) * PP * 8u);
-        tma_load_3d(f, &a.m_r, ap0, bp0, 0, &bar[1]);
-        if (upd) tma_load_3d(u, &a.m_ap, ap0, bp0, 0, &bar[1]);   // A p of the previous step, into u
+        tma_vec<PA, PB, SH>(f, &a.m_r, x0, y0, &bar[1]);
+        if (upd) tma_vec<PA, PB, SH>(u, &a.m_ap, x0, y0, &bar[1]);   // A p of the previous step, into u
     }
     if (a.sc_child && blockIdx.x == 0 && threadIdx.x == 0) {   // child's PCG starts afresh
         a.sc_child[2] = 0.0;
@@ -212,40 +266,42 @@ __global__ void __launch_bounds__(kTT) k_tile_down(const __grid_constant__ TileD
     const double na = upd ? -a.sc[0] : 0.0;
     __syncthreads();   // barrier init visible before anyone waits on it
     mbar_wait(&bar[1], 0);
-    for (int i = threadIdx.x; i < 4 * PP; i += kTT) {
+    for (int i = threadIdx.x; i < 4 * QS; i += kTT) {   // (the padding between planes is never read)
         if (upd) f[i] = __dadd_rn(f[i], __dmul_rn(na, u[i]));   // axpy(-alpha, ap, r); zeros stay zero
         u[i] = 0.0;
     }
     mbar_wait(&bar[0], 0);
-    if (x0 < 0 || y0 < 0 || x0 + RW > w || y0 + RW > w) fix_off_level<PA, PB>(val, f, x0, y0, w);
+    if (x0 < 0 || y0 < 0 || x0 + RW > w || y0 + RW > w) fix_off_level<PA, PB, SH>(val, f, x0, y0, w);
     __syncthreads();
     constexpr int NP = H / 4;   // pre sweeps
 #pragma unroll
     for (int k = 1; k <= 4 * NP; ++k) {
         const int D = H + 1 - k;
-        gs_pass_c<PA, PB>((k - 1) & 3, val, f, u, H - D, H + T + D, x0, y0, k == 1);
+        gs_pass_c<PA, PB, SH>((k - 1) & 3, val, f, u, H - D, H + T + D, x0, y0, k == 1);
     }
     // interior outputs: pre-smoothed iterate, updated residual (plane rows of
     // T/2 consecutive words per colour)
-    const int ai = ((x0 + H) >> 1) - ap0, bi = ((y0 + H) >> 1) - bp0;
+    const int X0 = (x0 + H) >> 1, Y0 = (y0 + H) >> 1;   // first interior plane position
+    const int bi = Y0 - (y0 >> 1);
     for (int idx = threadIdx.x; idx < 4 * TP * TP; idx += kTT) {
         const int c = idx / (TP * TP), r = idx - c * TP * TP, pb = r / TP, pa = r - pb * TP;
-        const int s = c * PP + (bi + pb) * PA + ai + pa;
-        const int gi = (c << a.g.lq) + (((y0 + H) >> 1) + pb) * (1 << a.g.lh) + ((x0 + H) >> 1) + pa;
+        const int s = c * QS + (bi + pb) * PA + X0 - org_of<SH>(x0, c & 1) + pa;
+        const int gi = (c << a.g.lq) + (Y0 + pb) * (1 << a.g.lh) + X0 + pa;
         a.u_pre[gi] = u[s];
         if (a.r_out) a.r_out[gi] = f[s];
     }
     // residual r = f - A u of the four children (colours 0..3 at one plane
     // position), summed from 0.0 in member order SW, SE, NW, NE into the parent
+    const int ae = X0 - org_of<SH>(x0, 0), ao = X0 - org_of<SH>(x0, 1);
     for (int idx = threadIdx.x; idx < TP * TP; idx += kTT) {
         const int pb = idx / TP, pa = idx - pb * TP;
-        const int s0 = (bi + pb) * PA + ai + pa;
+        const int se = (bi + pb) * PA + ae + pa, so = (bi + pb) * PA + ao + pa;
         double sum = 0.0;
-        sum = __dadd_rn(sum, __dsub_rn(f[s0], row9s<0, PA, PB>(val, u, s0)));
-        sum = __dadd_rn(sum, __dsub_rn(f[PP + s0], row9s<1, PA, PB>(val, u, PP + s0)));
-        sum = __dadd_rn(sum, __dsub_rn(f[2 * PP + s0], row9s<2, PA, PB>(val, u, 2 * PP + s0)));
-        sum = __dadd_rn(sum, __dsub_rn(f[3 * PP + s0], row9s<3, PA, PB>(val, u, 3 * PP + s0)));
-        a.rc[cmi(a.gc, ((x0 + H) >> 1) + pa, ((y0 + H) >> 1) + pb)] = sum;
+        sum = __dadd_rn(sum, __dsub_rn(f[se], row9s<0, PA, PB, SH>(val, u, se)));
+        sum = __dadd_rn(sum, __dsub_rn(f[QS + so], row9s<1, PA, PB, SH>(val, u, QS + so)));
+        sum = __dadd_rn(sum, __dsub_rn(f[2 * QS + se], row9s<2, PA, PB, SH>(val, u, 2 * QS + se)));
+        sum = __dadd_rn(sum, __dsub_rn(f[3 * QS + so], row9s<3, PA, PB, SH>(val, u, 3 * QS + so)));
+        a.rc[cmi(a.gc, X0 + pa, Y0 + pb)] = sum;
     }
 }
 
@@ -253,7 +309,8 @@ __global__ void __launch_bounds__(kTT) k_tile_down(const __grid_constant__ TileD
 template <int T, int H>
 __global__ void __launch_bounds__(kTT) k_tile_up(const __grid_constant__ TileUp a, RedState rs, Fin fin) {
     using L = Tile<T, H>;
-    constexpr int RW = L::RW, PA = L::PA, PB = L::PB, PP = L::PP, TP = T / 2;
+    constexpr int RW = L::RW, PA = L::PA, PB = L::PB, PP = L::PP, QS = L::QS, TP = T / 2, EW = L::EW;
+    constexpr bool SH = L::SH;
     extern __shared__ unsigned char smraw[];
     unsigned char* sm = align128(smraw);
     double* val = reinterpret_cast<double*>(sm);
@@ -265,25 +322,25 @@ __global__ void __launch_bounds__(kTT) k_tile_up(const __grid_constant__ TileUp 
     int x0, y0;
     tile_origin<T, H>(a.ox, a.oy, a.tiles_x, x0, y0);
     const int w = 1 << a.g.k;
-    const int ap0 = plane_a0(x0), bp0 = y0 >> 1;
+    const int omin = org_of<SH>(x0, 1), bp0 = y0 >> 1;   // parents' first plane column / row
     pdl_trigger();
     if (threadIdx.x == 0) {   // constant data first (before the wait)
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 1);
         fence_mbar_init();
         mbar_arrive_expect_tx(&bar[0], 36u * PP * 8u);
-        tma_load_4d(val, &a.m_val, ap0, bp0, 0, 0, &bar[0]);
+        tma_val<PA, PB, SH>(val, &a.m_val, x0, y0, &bar[0]);
     }
-    for (int i = threadIdx.x; i < 4 * PP; i += kTT) {
-        const int c = i / PP, r = i - c * PP, b = r / PA, aa = r - b * PA;
-        const int t1 = 2 * (ap0 + aa) + (c & 1), t2 = 2 * (bp0 + b) + (c >> 1);
-        act[i] = ((unsigned)t1 < (unsigned)w && (unsigned)t2 < (unsigned)w) ? a.act[cmi(a.g, t1, t2)] : 0;
+    for (int i = threadIdx.x; i < 4 * QS; i += kTT) {
+        int c, t1, t2;
+        const bool in = cell_of<PA, PB, SH>(i, x0, y0, c, t1, t2);
+        act[i] = (in && (unsigned)t1 < (unsigned)w && (unsigned)t2 < (unsigned)w) ? a.act[cmi(a.g, t1, t2)] : 0;
     }
     pdl_wait();
     if (threadIdx.x == 0) {
         mbar_arrive_expect_tx(&bar[1], 8u * PP * 8u);
-        tma_load_3d(f, &a.m_f, ap0, bp0, 0, &bar[1]);
-        tma_load_3d(u, &a.m_u, ap0, bp0, 0, &bar[1]);
+        tma_vec<PA, PB, SH>(f, &a.m_f, x0, y0, &bar[1]);
+        tma_vec<PA, PB, SH>(u, &a.m_u, x0, y0, &bar[1]);
     }
     // child correction per parent cell (= plane position): explicit, or
     // ((0 + alpha_0 p_0) + alpha_1 p_1) ... over the child's valid PCG steps
@@ -296,9 +353,9 @@ __global__ void __launch_bounds__(kTT) k_tile_up(const __grid_constant__ TileUp 
         for (int k = 0; k < 8; ++k) al[k] = k < nval ? a.sc_c[3 + a.c_ni + k] : 0.0;
     }
     const int wc = w >> 1;
-    for (int i = threadIdx.x; i < PP; i += kTT) {
-        const int b = i / PA, aa = i - b * PA;
-        const int c1 = ap0 + aa, c2 = bp0 + b;
+    for (int i = threadIdx.x; i < PB * EW; i += kTT) {
+        const int b = i / EW, aa = i - b * EW;
+        const int c1 = omin + aa, c2 = bp0 + b;
         double e = 0.0;
         if ((unsigned)c1 < (unsigned)wc && (unsigned)c2 < (unsigned)wc) {
             const int pc = cmi(a.gc, c1, c2);
@@ -314,26 +371,30 @@ __global__ void __launch_bounds__(kTT) k_tile_up(const __grid_constant__ TileUp 
     }
     __syncthreads();
     mbar_wait(&bar[1], 0);
-    for (int i = threadIdx.x; i < 4 * PP; i += kTT)
-        if (act[i]) u[i] = __dadd_rn(u[i], ep[i % PP]);   // off-level positions are inactive
+    for (int i = threadIdx.x; i < 4 * QS; i += kTT) {
+        if (!act[i]) continue;   // off-level positions and the padding are inactive
+        const int c = i / QS, r = i - c * QS, b = r / PA, aa = r - b * PA;
+        u[i] = __dadd_rn(u[i], ep[b * EW + aa + org_of<SH>(x0, c & 1) - omin]);
+    }
     mbar_wait(&bar[0], 0);
-    if (x0 < 0 || y0 < 0 || x0 + RW > w || y0 + RW > w) fix_off_level<PA, PB>(val, f, x0, y0, w);
+    if (x0 < 0 || y0 < 0 || x0 + RW > w || y0 + RW > w) fix_off_level<PA, PB, SH>(val, f, x0, y0, w);
     __syncthreads();
     constexpr int NP = (H - 1) / 4;   // post sweeps
 #pragma unroll
     for (int k = 1; k <= 4 * NP; ++k) {
         const int D = H - k;
-        gs_pass_c<PA, PB>(3 - ((k - 1) & 3), val, f, u, H - D, H + T + D, x0, y0, false);
+        gs_pass_c<PA, PB, SH>(3 - ((k - 1) & 3), val, f, u, H - D, H + T + D, x0, y0, false);
     }
     // A z on the tile, z and A z out, fused inner products
-    const int ai = ((x0 + H) >> 1) - ap0, bi = ((y0 + H) >> 1) - bp0;
+    const int X0 = (x0 + H) >> 1, Y0 = (y0 + H) >> 1;
+    const int bi = Y0 - bp0;
     double v[2] = {0.0, 0.0};
     for (int idx = threadIdx.x; idx < 4 * TP * TP; idx += kTT) {
         const int c = idx / (TP * TP), r = idx - c * TP * TP, pb = r / TP, pa = r - pb * TP;
-        const int s = c * PP + (bi + pb) * PA + ai + pa;
-        const int gi = (c << a.g.lq) + (((y0 + H) >> 1) + pb) * (1 << a.g.lh) + ((x0 + H) >> 1) + pa;
+        const int s = c * QS + (bi + pb) * PA + X0 - org_of<SH>(x0, c & 1) + pa;
+        const int gi = (c << a.g.lq) + (Y0 + pb) * (1 << a.g.lh) + X0 + pa;
         const double zi = u[s];
-        const double yi = row9c<PA, PB>(c, val, u, s);
+        const double yi = row9c<PA, PB, SH>(c, val, u, s);
         a.z[gi] = zi;
         a.az[gi] = yi;
         if (a.mode == 0) {
@@ -365,11 +426,11 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
-// dims (innermost first): plane a, plane b, colour [, slot]; box PA x PB x 4 [x 9]
+// dims (innermost first): plane a, plane b, colour [, slot]; box PA x PB x 1 [x 9]
 void encode_level_map(CUtensorMap* m, const double* base, const Geo& g, int PA, int PB, bool slots) {
     const cuuint64_t dims[4] = {(cuuint64_t)g.H, (cuuint64_t)g.H, 4, 9};
     const cuuint64_t strides[3] = {(cuuint64_t)g.H * 8, (cuuint64_t)g.nq * 8, (cuuint64_t)g.n * 8};
-    const cuuint32_t box[4] = {(cuuint32_t)PA, (cuuint32_t)PB, 4, 9};
+    const cuuint32_t box[4] = {(cuuint32_t)PA, (cuuint32_t)PB, 1, 9};
     const cuuint32_t es[4] = {1, 1, 1, 1};
     const CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, slots ? 4 : 3, const_cast<double*>(base), dims,
                                    strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
