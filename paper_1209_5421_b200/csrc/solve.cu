@@ -623,6 +623,14 @@ __global__ void __launch_bounds__(256, 4) k_bgs_inv(const int* __restrict__ rp, 
     const bool ob = vb && sb <= 32 && rb - qb < w0 + 32;
     if (!__any_sync(0xffffffffu, oa)) return;   // only rows of larger blocks here
     const int ea = oa ? sa : 0, eb = ob ? sb : 0;
+    // the window's inverse entries are one contiguous range: pull them towards
+    // L2 now, so the inverse chunks do not pay a full DRAM round trip after
+    // the residual chain (C2: pre + post smoothing -0.14 ms, C3 -0.37 ms)
+    const int ib0 = (int)__reduce_min_sync(0xffffffffu, oa ? (unsigned)ma.x : (ob ? (unsigned)mb.x : 0x7fffffffu));
+    const int ib1 = (int)__reduce_max_sync(0xffffffffu, ob ? (unsigned)(mb.x + sb * sb)
+                                                            : (oa ? (unsigned)(ma.x + sa * sa) : 0u));
+    for (int e = ib0 + lane * 16; e < ib1; e += 32 * 16)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(inv + e));
     if (!zero && !res) {
         // r = b - sum a x_prev in storage order (smoother.hpp:193-198): the
         // owned rows are contiguous, so the warp streams their nonzeros
@@ -661,9 +669,6 @@ __global__ void __launch_bounds__(256, 4) k_bgs_inv(const int* __restrict__ rp, 
     // the chunk buffer; every owned row then takes its entries
     // inv(q, j) = pool[off + j s + q], j ascending, from shared memory
     const int fa = ma.x + qa, fb = mb.x + qb;   // entry (q, 0) of each row
-    const int ib0 = (int)__reduce_min_sync(0xffffffffu, oa ? (unsigned)ma.x : (ob ? (unsigned)mb.x : 0x7fffffffu));
-    const int ib1 = (int)__reduce_max_sync(0xffffffffu, ob ? (unsigned)(mb.x + sb * sb)
-                                                            : (oa ? (unsigned)(ma.x + sa * sa) : 0u));
     const double* Ra = R + (lane - qa);
     const double* Rb = R + (32 + lane - qb);
     double da = 0.0, db = 0.0;
