@@ -645,8 +645,8 @@ __global__ void __launch_bounds__(256, 4) k_bgs_inv(const int* __restrict__ rp, 
 #pragma unroll
             for (int k = 0; k < kChunk / 32; ++k) {
                 const int p = cs + lane + 32 * k;
-                cc[k] = p < pb1 ? col[p] : -1;
-                vv[k] = p < pb1 ? v[p] : 0.0;
+                cc[k] = p < pb1 ? __ldcs(col + p) : -1;   // streamed: u stays in L2 for the gathers
+                vv[k] = p < pb1 ? __ldcs(v + p) : 0.0;
             }
             double xv[kChunk / 32];
 #pragma unroll
@@ -678,7 +678,7 @@ __global__ void __launch_bounds__(256, 4) k_bgs_inv(const int* __restrict__ rp, 
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
             const int e = cs + lane + 32 * k;
-            t[k] = e < ib1 ? inv[e] : 0.0;
+            t[k] = e < ib1 ? __ldcs(inv + e) : 0.0;
         }
 #pragma unroll
         for (int k = 0; k < 8; ++k) buf[lane + 32 * k] = t[k];
