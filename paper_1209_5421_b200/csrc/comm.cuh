@@ -27,6 +27,7 @@ struct Msg {
 
 struct Comm {
     int rank = 0, size = 1;
+    bool peers_warm = false;   // the coarse cycle's peer connections exist (solve.cu build_graph)
     virtual ~Comm() {}
     // in-place element-wise sum over all parts (device doubles)
     virtual void allreduce_sum(double* buf, int count, cudaStream_t s) = 0;

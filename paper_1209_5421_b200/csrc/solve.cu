@@ -1411,14 +1411,15 @@ void build_graph(aux_hierarchy* h, const aux_cycle_opts& o, RedState rs) {
     h->graph_valid = false;
     if (!h->gpu.use_graphs || h->direct_only || h->lv.size() < 2) return;
     Ctx c{h, h->stream, o, rs, false};
-    if (h->dist.comm && h->dist.comm->size > 1) {
-        // one eager pass first, so every NCCL peer connection the coarse cycle
-        // uses exists before the capture (NCCL connects peers lazily); the
-        // solve overwrites whatever it computed
+    if (h->dist.comm && h->dist.comm->size > 1 && !h->dist.comm->peers_warm) {
+        // one eager pass first (once per communicator), so every NCCL peer
+        // connection the coarse cycle uses exists before the capture (NCCL
+        // connects peers lazily); the solve overwrites whatever it computed
         const int64_t b0 = g_launches;
         coarse_root(c);
         g_launches = b0;
         AUX_CUDA(cudaStreamSynchronize(h->stream));
+        h->dist.comm->peers_warm = true;
     }
     const int64_t before = g_launches;
     cudaGraph_t g;
