@@ -134,18 +134,33 @@ aux_status aux_setup(const aux_csr_view* A, const double* xy, int64_t n_points, 
         const long n = A->n_rows;
         DBuf<int> rp(n + 1), col(A->nnz);
         DBuf<double> v(A->nnz), xy_d(2 * std::max<long>(n_points, 0));
+        // structure and coordinates first on the setup stream; the values (half
+        // the bytes) on a second stream, so the structure check and the
+        // coordinate-only phase of setup overlap their copy
+        struct Side {
+            cudaStream_t s = nullptr;
+            cudaEvent_t e = nullptr;
+            ~Side() {   // (destroyed before v: an error thrown mid-copy still waits for it)
+                if (s) cudaStreamSynchronize(s);
+                if (e) cudaEventDestroy(e);
+                if (s) cudaStreamDestroy(s);
+            }
+        } side;
+        AUX_CUDA(cudaStreamCreateWithFlags(&side.s, cudaStreamNonBlocking));
+        AUX_CUDA(cudaEventCreateWithFlags(&side.e, cudaEventDisableTiming));
         AUX_CUDA(cudaMemcpyAsync(rp.p, A->row_ptr, sizeof(int) * (n + 1), cudaMemcpyHostToDevice, h->stream));
-        if (A->nnz) {
-            AUX_CUDA(cudaMemcpyAsync(col.p, A->col_idx, sizeof(int) * A->nnz, cudaMemcpyHostToDevice, h->stream));
-            AUX_CUDA(cudaMemcpyAsync(v.p, A->values, sizeof(double) * A->nnz, cudaMemcpyHostToDevice, h->stream));
-        }
         if (n_points > 0)
             AUX_CUDA(cudaMemcpyAsync(xy_d.p, xy, sizeof(double) * 2 * n_points, cudaMemcpyHostToDevice, h->stream));
+        if (A->nnz) {
+            AUX_CUDA(cudaMemcpyAsync(col.p, A->col_idx, sizeof(int) * A->nnz, cudaMemcpyHostToDevice, h->stream));
+            AUX_CUDA(cudaMemcpyAsync(v.p, A->values, sizeof(double) * A->nnz, cudaMemcpyHostToDevice, side.s));
+        }
+        AUX_CUDA(cudaEventRecord(side.e, side.s));
         aux_csr_view dv = *A;
         dv.row_ptr = rp.p;
         dv.col_idx = col.p;
         dv.values = v.p;
-        setup_device(h, &dv, xy_d.p, (long)n_points);
+        setup_device(h, &dv, xy_d.p, (long)n_points, side.e);
         h->host_rp = A->row_ptr;
         h->host_col = A->col_idx;
         h->host_val = A->values;

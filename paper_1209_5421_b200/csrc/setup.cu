@@ -1193,9 +1193,9 @@ void finest_blocks(aux_hierarchy* h, const Geo& gL, unsigned long long& sing, in
 
 // validate_csr (sparse.hpp:101-116), diagonal > 0 and symmetry
 // (hierarchy.hpp:321-325), in the reference's precedence.
-void validate_input(aux_hierarchy* h, const aux_csr_view* A) {
+// CSR structure (validate_csr, sparse.hpp:101-116): row_ptr and col_idx only.
+void validate_structure(aux_hierarchy* h, const aux_csr_view* A) {
     cudaStream_t s = h->stream;
-    const aux_setup_opts& o = h->opts;
     const int n = A->n_rows;
     const long nnz = A->nnz;
     {
@@ -1221,6 +1221,17 @@ void validate_input(aux_hierarchy* h, const aux_csr_view* A) {
             if (kind == 2) throw_aux(AUX_STRUCTURE_ERROR, "CSR column index out of range in row " + std::to_string(r));
             throw_aux(AUX_STRUCTURE_ERROR, "CSR row " + std::to_string(r) + " not sorted by column");
         }
+    }
+}
+
+// Values: diagonal > 0 and symmetry (hierarchy.hpp:321-325).
+void validate_values(aux_hierarchy* h, const aux_csr_view* A) {
+    cudaStream_t s = h->stream;
+    const aux_setup_opts& o = h->opts;
+    const int n = A->n_rows;
+    {
+        DBuf<unsigned long long> err(2);
+        AUX_CUDA(cudaMemsetAsync(err.p, 0xff, 2 * sizeof(unsigned long long), s));
         // diagonal > 0 (hierarchy.hpp:321-323)
         if (n > 0) {
             k_diag<<<grid_for(n), kT, 0, s>>>(A->row_ptr, A->col_idx, A->values, n, err.p + 1);
@@ -1246,9 +1257,15 @@ void validate_input(aux_hierarchy* h, const aux_csr_view* A) {
     }
 }
 
+void validate_input(aux_hierarchy* h, const aux_csr_view* A) {
+    validate_structure(h, A);
+    validate_values(h, A);
+}
+
 // bounding_box (auxgrid.hpp:75-91) into h->box; non-finite -> argument_error,
 // degenerate -> geometry_error.
-void bounding_box(aux_hierarchy* h, const double* xy, long n) {
+// 0: box in h->box; 1: non-finite coordinate; 2: degenerate point set.
+int bbox_compute(aux_hierarchy* h, const double* xy, long n) {
     cudaStream_t s = h->stream;
     {
         DBuf<unsigned long long> bb(4);
@@ -1263,7 +1280,7 @@ void bounding_box(aux_hierarchy* h, const double* xy, long n) {
         AUX_CUDA(cudaMemcpyAsync(r, bb.p, sizeof r, cudaMemcpyDeviceToHost, s));
         AUX_CUDA(cudaMemcpyAsync(&badh, bad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
         AUX_CUDA(cudaStreamSynchronize(s));
-        if (badh) throw_aux(AUX_ARGUMENT_ERROR, "bounding_box: non-finite coordinate");
+        if (badh) return 1;
         auto val = [](unsigned long long k) {
             const unsigned long long b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
             double d;
@@ -1274,12 +1291,17 @@ void bounding_box(aux_hierarchy* h, const double* xy, long n) {
         h->box[1] = val(r[1]);
         h->box[2] = val(r[2]);
         h->box[3] = val(r[3]);
-        if (!(h->box[1] > h->box[0]) || !(h->box[3] > h->box[2]))
-            throw_aux(AUX_GEOMETRY_ERROR, "bounding_box: degenerate point set");
+        if (!(h->box[1] > h->box[0]) || !(h->box[3] > h->box[2])) return 2;
     }
+    return 0;
 }
+void bbox_throw(int code) {
+    if (code == 1) throw_aux(AUX_ARGUMENT_ERROR, "bounding_box: non-finite coordinate");
+    if (code == 2) throw_aux(AUX_GEOMETRY_ERROR, "bounding_box: degenerate point set");
+}
+void bounding_box(aux_hierarchy* h, const double* xy, long n) { bbox_throw(bbox_compute(h, xy, n)); }
 
-void setup_device(aux_hierarchy* h, const aux_csr_view* A, const double* xy, long n_points) {
+void setup_device(aux_hierarchy* h, const aux_csr_view* A, const double* xy, long n_points, cudaEvent_t values_ready) {
     cudaStream_t s = h->stream;
     const aux_setup_opts& o = h->opts;
     if (A->n_rows != A->n_cols) throw_aux(AUX_SIZE_ERROR, "setup_hierarchy: matrix not square");
@@ -1289,7 +1311,15 @@ void setup_device(aux_hierarchy* h, const aux_csr_view* A, const double* xy, lon
     const long nnz = A->nnz;
     h->n = n;
 
-    validate_input(h, A);
+    // reference error order: size -> CSR structure -> diagonal -> symmetry ->
+    // geometry.  The structure check and the coordinate-only phase (bounding
+    // box, binning, sort) may run while the values are still being copied;
+    // the value checks and the geometry verdict follow in the reference order.
+    validate_structure(h, A);
+    auto values_checked = [&] {
+        if (values_ready) AUX_CUDA(cudaStreamWaitEvent(s, values_ready, 0));
+        validate_values(h, A);
+    };
     h->opts.coarsest_size = std::max(o.coarsest_size, 4);
     const int coarsest_size = h->opts.coarsest_size;
 
@@ -1304,6 +1334,7 @@ void setup_device(aux_hierarchy* h, const aux_csr_view* A, const double* xy, lon
     h->lv[0].nnz = nnz;
 
     if (n <= coarsest_size) {   // direct-only hierarchy (hierarchy.hpp:339-344)
+        values_checked();
         h->direct_only = true;
         F.rp.alloc(n + 1);
         F.col.alloc(nnz);
@@ -1322,7 +1353,11 @@ void setup_device(aux_hierarchy* h, const aux_csr_view* A, const double* xy, lon
         return;
     }
 
-    bounding_box(h, xy, n);
+    const int bb = bbox_compute(h, xy, n);
+    if (bb != 0) {   // no binning of an invalid point set; report after the value checks
+        values_checked();
+        bbox_throw(bb);
+    }
     int depth = 0;
     {
         long cells = 1;
@@ -1365,6 +1400,7 @@ void setup_device(aux_hierarchy* h, const aux_csr_view* A, const double* xy, lon
     key.release();
     F.col.alloc(nnz);
     F.v.alloc(nnz);
+    values_checked();
     k_permute_csr<<<grid_for((long)n * 4), kT, 0, s>>>(A->row_ptr, A->col_idx, A->values, F.perm.p, F.iperm.p, n,
                                                         F.rp.p, F.col.p, F.v.p);
     AUX_LAUNCHED(1);

@@ -4,7 +4,11 @@
 namespace auxb200 {
 
 // Device setup_hierarchy; A's arrays and xy are device pointers.
-void setup_device(aux_hierarchy* h, const aux_csr_view* A, const double* xy, long n_points);
+// values_ready: the matrix values may still be in flight (host API: the
+// coordinate-only phase of setup overlaps their copy); the stream waits on it
+// before the first use of the values.
+void setup_device(aux_hierarchy* h, const aux_csr_view* A, const double* xy, long n_points,
+                  cudaEvent_t values_ready = nullptr);
 // PCG buffers of every coarse level for a given n_inner.
 void alloc_solve_levels(aux_hierarchy* h, int n_inner);
 // Device solve; b and u are device pointers in the caller's DoF order.
