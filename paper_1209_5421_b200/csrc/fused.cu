@@ -303,15 +303,23 @@ __device__ void coarse_solve(const FusedArgs& a, const double* inv, double* part
     } else {
         // column-major inverse: thread (row, quarter) sums its quarter of j
         // sequentially (conflict-free shared loads, r broadcast), then the four
-        // partials combine in order — the order of k_coarse_inv.
+        // partials combine in order — the order of k_coarse_inv.  r is first
+        // gathered into compact order (part[4 nc ..]) so the dot loop carries
+        // no index arithmetic.
         const int nc = a.nc, cs = (nc + 3) / 4;
+        double* rc = part + 4 * nc;
+        for (int j = threadIdx.x; j < nc; j += kThreads) {
+            const int c = j >> (2 * L.lh), pos = j & (L.nq - 1);
+            rc[j] = r[pidx(L, c, pos & (L.H - 1), pos >> L.lh)];
+        }
+        __syncthreads();
         for (int idx = threadIdx.x; idx < 4 * nc; idx += kThreads) {
             const int row = idx % nc, k = idx / nc;
+            const int j0 = k * cs, j1 = min(nc, (k + 1) * cs);
+            const double* iv = inv + (size_t)j0 * nc + row;
             double s = 0.0;
-            for (int j = k * cs; j < min(nc, (k + 1) * cs); ++j) {
-                const int c = j >> (2 * L.lh), pos = j & (L.nq - 1);
-                s = fma(inv[j * nc + row], r[pidx(L, c, pos & (L.H - 1), pos >> L.lh)], s);
-            }
+#pragma unroll 8
+            for (int j = j0; j < j1; ++j, iv += nc) s = fma(*iv, rc[j], s);
             part[k * nc + row] = s;
         }
         __syncthreads();
@@ -1165,7 +1173,7 @@ unsigned fused_layout(const aux_hierarchy* h, int m0, int ni, FusedArgs* a) {
         a->off_vec[q] = take((1 + 2 * (size_t)ni) * 4 * W2 * W2 * sizeof(double));
         a->off_act[q] = take(n);
     }
-    a->off_part = take(4 * (size_t)h->nc * sizeof(double));
+    a->off_part = take(5 * (size_t)h->nc * sizeof(double));   // 4 partial sums + compact r
     const size_t need = off;
     if (need > (size_t)kFusedSmemMax) return 0;
     const size_t inv_bytes = (size_t)h->nc * h->nc * sizeof(double);
