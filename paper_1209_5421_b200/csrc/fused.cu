@@ -229,35 +229,49 @@ struct RV {
     double v[4][9];
 };
 
+// The register-resident level is always 16 x 16 plane positions (nq ==
+// kThreads): its padded layout is compile-time, so every index below is an
+// immediate (the top tier level and the cluster tier's quadrants).
+constexpr int kRH = 16, kRW2 = kRH + 2, kRPP = kRW2 * kRW2;
+static_assert(kRH * kRH == kThreads, "register-resident level: one plane position per thread");
+__device__ __forceinline__ int pidx_r(int c, int a, int b) { return c * kRPP + (b + 1) * kRW2 + a + 1; }
+template <int C, int T>
+__device__ __forceinline__ constexpr int noff_r() {
+    constexpr int ux = (C & 1) + stencil_dx(T);
+    constexpr int uy = (C >> 1) + stencil_dy(T);
+    constexpr int nc = (ux & 1) | ((uy & 1) << 1);
+    return (nc - C) * kRPP + (uy >> 1) * kRW2 + (ux >> 1);
+}
+
 template <int C>
 __device__ __forceinline__ double row9_r(const SLevel& L, const RV& rv, int pi, const double* x) {
     const double* v = rv.v[C];
     double s = __dadd_rn(0.0, __dmul_rn(v[0], x[pi]));
-    s = __dadd_rn(s, __dmul_rn(v[1], x[pi + noff<C, 1>(L)]));
-    s = __dadd_rn(s, __dmul_rn(v[2], x[pi + noff<C, 2>(L)]));
-    s = __dadd_rn(s, __dmul_rn(v[3], x[pi + noff<C, 3>(L)]));
-    s = __dadd_rn(s, __dmul_rn(v[4], x[pi + noff<C, 4>(L)]));
-    s = __dadd_rn(s, __dmul_rn(v[5], x[pi + noff<C, 5>(L)]));
-    s = __dadd_rn(s, __dmul_rn(v[6], x[pi + noff<C, 6>(L)]));
-    s = __dadd_rn(s, __dmul_rn(v[7], x[pi + noff<C, 7>(L)]));
-    s = __dadd_rn(s, __dmul_rn(v[8], x[pi + noff<C, 8>(L)]));
+    s = __dadd_rn(s, __dmul_rn(v[1], x[pi + noff_r<C, 1>()]));
+    s = __dadd_rn(s, __dmul_rn(v[2], x[pi + noff_r<C, 2>()]));
+    s = __dadd_rn(s, __dmul_rn(v[3], x[pi + noff_r<C, 3>()]));
+    s = __dadd_rn(s, __dmul_rn(v[4], x[pi + noff_r<C, 4>()]));
+    s = __dadd_rn(s, __dmul_rn(v[5], x[pi + noff_r<C, 5>()]));
+    s = __dadd_rn(s, __dmul_rn(v[6], x[pi + noff_r<C, 6>()]));
+    s = __dadd_rn(s, __dmul_rn(v[7], x[pi + noff_r<C, 7>()]));
+    s = __dadd_rn(s, __dmul_rn(v[8], x[pi + noff_r<C, 8>()]));
     return s;
 }
 
 template <int C>
 __device__ __forceinline__ void gs_pass_r(const SLevel& L, const RV& rv, const double* f, double* x) {
     const int pos = threadIdx.x;
-    const int pi = pidx(L, C, pos & (L.H - 1), pos >> L.lh);
+    const int pi = pidx_r(C, pos & (kRH - 1), pos >> 4);
     const double* v = rv.v[C];
     double s = f[pi];
-    s = __dsub_rn(s, __dmul_rn(v[1], x[pi + noff<C, 1>(L)]));
-    s = __dsub_rn(s, __dmul_rn(v[2], x[pi + noff<C, 2>(L)]));
-    s = __dsub_rn(s, __dmul_rn(v[3], x[pi + noff<C, 3>(L)]));
-    s = __dsub_rn(s, __dmul_rn(v[4], x[pi + noff<C, 4>(L)]));
-    s = __dsub_rn(s, __dmul_rn(v[5], x[pi + noff<C, 5>(L)]));
-    s = __dsub_rn(s, __dmul_rn(v[6], x[pi + noff<C, 6>(L)]));
-    s = __dsub_rn(s, __dmul_rn(v[7], x[pi + noff<C, 7>(L)]));
-    s = __dsub_rn(s, __dmul_rn(v[8], x[pi + noff<C, 8>(L)]));
+    s = __dsub_rn(s, __dmul_rn(v[1], x[pi + noff_r<C, 1>()]));
+    s = __dsub_rn(s, __dmul_rn(v[2], x[pi + noff_r<C, 2>()]));
+    s = __dsub_rn(s, __dmul_rn(v[3], x[pi + noff_r<C, 3>()]));
+    s = __dsub_rn(s, __dmul_rn(v[4], x[pi + noff_r<C, 4>()]));
+    s = __dsub_rn(s, __dmul_rn(v[5], x[pi + noff_r<C, 5>()]));
+    s = __dsub_rn(s, __dmul_rn(v[6], x[pi + noff_r<C, 6>()]));
+    s = __dsub_rn(s, __dmul_rn(v[7], x[pi + noff_r<C, 7>()]));
+    s = __dsub_rn(s, __dmul_rn(v[8], x[pi + noff_r<C, 8>()]));
     x[pi] = __ddiv_rn(s, v[0]);
     __syncthreads();
 }
@@ -382,13 +396,13 @@ __device__ void cycle_down(const FusedArgs& a, const SLevel& L, PState& ps, cons
     }
     if (rv) {   // thread t: the children at plane position t (all four colours)
         const int t = threadIdx.x;
-        const int T1 = t & (L.H - 1), T2 = t >> L.lh;
+        const int T1 = t & (kRH - 1), T2 = t >> 4;
         const RV& r = *rv;
         double sum = 0.0;
-        sum = __dadd_rn(sum, __dsub_rn(f[pidx(L, 0, T1, T2)], row9_r<0>(L, r, pidx(L, 0, T1, T2), u)));
-        sum = __dadd_rn(sum, __dsub_rn(f[pidx(L, 1, T1, T2)], row9_r<1>(L, r, pidx(L, 1, T1, T2), u)));
-        sum = __dadd_rn(sum, __dsub_rn(f[pidx(L, 2, T1, T2)], row9_r<2>(L, r, pidx(L, 2, T1, T2), u)));
-        sum = __dadd_rn(sum, __dsub_rn(f[pidx(L, 3, T1, T2)], row9_r<3>(L, r, pidx(L, 3, T1, T2), u)));
+        sum = __dadd_rn(sum, __dsub_rn(f[pidx_r(0, T1, T2)], row9_r<0>(L, r, pidx_r(0, T1, T2), u)));
+        sum = __dadd_rn(sum, __dsub_rn(f[pidx_r(1, T1, T2)], row9_r<1>(L, r, pidx_r(1, T1, T2), u)));
+        sum = __dadd_rn(sum, __dsub_rn(f[pidx_r(2, T1, T2)], row9_r<2>(L, r, pidx_r(2, T1, T2), u)));
+        sum = __dadd_rn(sum, __dsub_rn(f[pidx_r(3, T1, T2)], row9_r<3>(L, r, pidx_r(3, T1, T2), u)));
         const int cq = (T1 & 1) | ((T2 & 1) << 1);
         Cc.r[pidx(Cc, cq, T1 >> 1, T2 >> 1)] = sum;
         __syncthreads();
@@ -469,8 +483,9 @@ __device__ __forceinline__ void spmv_color(const SLevel& L, const double* x, dou
 template <int C>
 __device__ __forceinline__ void spmv_color_r(const SLevel& L, const RV& rv, const double* x, double* y, const double* r,
                                            const double* w, int mode, double& s0, double& s1) {
-    for (int pos = threadIdx.x; pos < L.nq; pos += kThreads) {
-        const int pi = pidx(L, C, pos & (L.H - 1), pos >> L.lh);
+    {
+        const int pos = threadIdx.x;
+        const int pi = pidx_r(C, pos & (kRH - 1), pos >> 4);
         const double yi = row9_r<C>(L, rv, pi, x);
         y[pi] = yi;
         const double xi = x[pi];
