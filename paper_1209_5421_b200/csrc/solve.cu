@@ -1622,7 +1622,13 @@ void solve_device(aux_hierarchy* h, const double* b, long n_b, const aux_cycle_o
         for (size_t l = 1; l + 1 < h->lv.size(); ++l)
             if (h->lv[l].zero_diag_lex >= 0)
                 throw_aux(AUX_SINGULAR_ERROR, "zero diagonal at row " + std::to_string(h->lv[l].zero_diag_lex));
-        build_graph(h, *o, rs);
+        {
+            const auto tg0 = std::chrono::steady_clock::now();
+            build_graph(h, *o, rs);
+            if (g_trace.on)
+                fprintf(stderr, "[aux trace] graph build %.3f ms host\n",
+                        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tg0).count());
+        }
         Ctx c{h, s, *o, rs, h->prof.on};
         // colour-pass byte counts for the profile
         if (h->prof.on && !h->direct_only && h->lv.size() > 1) {
