@@ -55,3 +55,18 @@ def test_c3_16m(gpu_api):
     r = gpu_api.solve(s.A, s.b, h)
     assert r.converged and abs(r.iterations - 13) <= 1, r.iterations
     assert _true_rel_residual(s, r.u) <= 1.0e-6 * (1 + 1e-9)
+
+
+@pytest.mark.parametrize("opts", [dict(cluster_tier=False), dict(fused_max_cells=256), dict(fused_max_cells=64),
+                                  dict(use_graphs=False)])
+def test_full_size_tiers_agree(opts):
+    """C1 at full size through every coarse-tier configuration: the cluster
+    tier off, the single-CTA tier cut to 256 / 64 cells (more levels on the TMA
+    tile kernels), eager launches -- same iterations, solutions within the
+    parity tolerance of the default path."""
+    from paper_1209_5421_b200 import api
+    s = problems.jittered_p1(1025)
+    ref = api.solve(s.A, s.b, api.setup_hierarchy(s.A, s.coords))
+    r = api.solve(s.A, s.b, api.setup_hierarchy(s.A, s.coords, gpu=api.GpuOptions(**opts)))
+    assert r.iterations == ref.iterations
+    assert np.max(np.abs(r.u - ref.u)) / np.max(np.abs(ref.u)) <= 1e-12
