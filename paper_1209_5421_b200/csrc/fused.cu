@@ -138,13 +138,35 @@ __device__ __forceinline__ SLevel slev(const FusedArgs& a, unsigned char* sm, co
     return L;
 }
 
-struct PState {
-    int step;    // current step
-    int nval;    // completed (non-breakdown) steps
-    int pend;    // r -= alpha[step-1] A p[step-1] still to apply
-    double alpha[kFusedMaxInner];
-    double e[kFusedMaxInner];
+// PCG state of the tier's levels.  Every thread computes the same values, so
+// one copy lives in shared memory (TierSM, written by all threads with
+// identical values, never read-modify-written); the current level's step and
+// pending-update flag stay in registers and are saved / restored at level
+// changes.  (A per-thread array in local memory misses the small L1 that the
+// tier's shared-memory carve-out leaves: hundreds of cycles per access.)
+struct TierSM {
+    double alpha[kMaxFusedLevels][kFusedMaxInner];
+    double e[kMaxFusedLevels][kFusedMaxInner];
+    int nval[kMaxFusedLevels];
+    int step[kMaxFusedLevels];
+    int pend[kMaxFusedLevels];
 };
+struct PState {
+    int step;        // current step (register)
+    int pend;        // r -= alpha[step-1] A p[step-1] still to apply (register)
+    double* alpha;   // shared: alpha of the valid steps
+    double* e;       // shared: energies
+    int* nval;       // shared: completed (non-breakdown) steps
+};
+__device__ __forceinline__ PState ps_view(TierSM* ts, int q) {
+    PState p;
+    p.step = 0;
+    p.pend = 0;
+    p.alpha = ts->alpha[q];
+    p.e = ts->e[q];
+    p.nval = &ts->nval[q];
+    return p;
+}
 
 __device__ __forceinline__ void bsum2(double* red, int& par, double& x, double& y) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -433,10 +455,10 @@ __device__ void cycle_up(const FusedArgs& a, const SLevel& L, const SLevel& Cc, 
     PH_RESET
     const int po = L.n > 256 ? 0 : 16;
     (void)po;
-    // the child's alphas in registers (PState lives in local memory), and the
+    // the child's alphas in registers, and the
     // four children of a parent handled by one thread: the parent's
     // correction e is formed once, in the axpy order (cycle.hpp:124)
-    const int nval = cs.nval;
+    const int nval = *cs.nval;
     double al[kFusedMaxInner];
 #pragma unroll
     for (int k = 0; k < kFusedMaxInner; ++k) al[k] = k < nval ? cs.alpha[k] : 0.0;
@@ -587,7 +609,7 @@ __device__ bool pcg_step(const FusedArgs& a, const SLevel& L, PState& ps, double
     }
     if (dead) return true;   // nonlinear_pcg returns the current iterate
     ps.alpha[i] = alpha;
-    ps.nval = i + 1;
+    *ps.nval = i + 1;
     return i + 1 >= a.ni;
 }
 
@@ -653,35 +675,34 @@ __device__ __forceinline__ void tier_load_rv(const FusedArgs& a, unsigned char* 
 // top level's padded r; returns the top level's PCG state (alphas, nval), the
 // directions stay in shared memory.
 __device__ void tier_run(const FusedArgs& a, unsigned char* sm, const Geo* sgeo, const double* inv, double* red,
-                         const RV& rv0, bool top_reg, PState& top) {
+                         const RV& rv0, bool top_reg, TierSM* ts) {
     FCLK_START
     const int nl = a.last - a.m0 + 1;
     // ---- the K-cycle as an explicit state machine over (level, PCG step)
-    PState ps[kMaxFusedLevels];
     int par = 0;
     int q = 0;
-    ps[0].step = 0;
-    ps[0].nval = 0;
-    ps[0].pend = 0;
+    PState cur = ps_view(ts, 0);
+    *cur.nval = 0;
     bool resume = false;   // false: start cycle(q) for step; true: cycle(q) just finished
     double* part = reinterpret_cast<double*>(sm + a.off_part);
     FCLK_DECL
     while (true) {
         const SLevel L = slev(a, sm, sgeo, q);
         if (!resume) {
-            double* u = L.p + ps[q].step * 4 * L.PP;
+            double* u = L.p + cur.step * 4 * L.PP;
             if (q < nl - 1) {
                 FCLK_BEGIN
-                cycle_down(a, L, ps[q], slev(a, sm, sgeo, q + 1), u, (q == 0 && top_reg) ? &rv0 : nullptr);
+                cycle_down(a, L, cur, slev(a, sm, sgeo, q + 1), u, (q == 0 && top_reg) ? &rv0 : nullptr);
                 FCLK_END(0, q)
+                ts->step[q] = cur.step;   // the parent's registers, restored when the child returns
+                ts->pend[q] = cur.pend;
                 ++q;
-                ps[q].step = 0;
-                ps[q].nval = 0;
-                ps[q].pend = 0;
+                cur = ps_view(ts, q);
+                *cur.nval = 0;
                 continue;
             }
             FCLK_BEGIN
-            coarse_solve(a, inv, part, L, ps[q], u);
+            coarse_solve(a, inv, part, L, cur, u);
             FCLK_END(1, q)
             resume = true;
             if (a.coarse_mode != 0) continue;
@@ -690,15 +711,15 @@ __device__ void tier_run(const FusedArgs& a, unsigned char* sm, const Geo* sgeo,
             // residual is rounding noise), so the inverse mode takes
             // u = A_c^{-1} f as the whole nonlinear_pcg.  The LU mode
             // (coarse_mode 1) runs the reference's n_inner steps.
-            ps[q].alpha[0] = 1.0;
-            ps[q].nval = 1;
+            cur.alpha[0] = 1.0;
+            *cur.nval = 1;
         } else {
             FCLK_BEGIN
-            const bool done = pcg_step(a, L, ps[q], red, par, (q == 0 && top_reg) ? &rv0 : nullptr);
+            const bool done = pcg_step(a, L, cur, red, par, (q == 0 && top_reg) ? &rv0 : nullptr);
             FCLK_END(2, q)
             if (!done) {
-                ps[q].pend = 1;
-                ++ps[q].step;
+                cur.pend = 1;
+                ++cur.step;
                 resume = false;
                 continue;
             }
@@ -706,15 +727,18 @@ __device__ void tier_run(const FusedArgs& a, unsigned char* sm, const Geo* sgeo,
         // nonlinear_pcg(q) finished: back to the parent (one call site keeps
         // the kernel's code small — instruction fetch is a visible stall here)
         if (q == 0) break;
+        const PState child = cur;
         --q;
+        cur = ps_view(ts, q);
+        cur.step = ts->step[q];
+        cur.pend = ts->pend[q];
         const SLevel P = slev(a, sm, sgeo, q);
         FCLK_BEGIN
-        cycle_up(a, P, L, ps[q + 1], P.p + ps[q].step * 4 * P.PP, (q == 0 && top_reg) ? &rv0 : nullptr);
+        cycle_up(a, P, L, child, P.p + cur.step * 4 * P.PP, (q == 0 && top_reg) ? &rv0 : nullptr);
         FCLK_END(3, q)
         resume = true;
     }
     FCLK_REPORT
-    top = ps[0];
 }
 
 __global__ void __launch_bounds__(kThreads, 1) k_fused_pcg(const __grid_constant__ FusedArgs a) {
@@ -740,17 +764,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_pcg(const __grid_constant
     RV rv0;
     const bool top_reg = tier_top_reg(sgeo, nl);
     if (top_reg) tier_load_rv(a, sm, sgeo, rv0);
-    PState top;
-    tier_run(a, sm, sgeo, inv, red, rv0, top_reg, top);
+    __shared__ TierSM ts;
+    tier_run(a, sm, sgeo, inv, red, rv0, top_reg, &ts);
 
     // ---- u of nonlinear_pcg(m0) = ((0 + alpha_0 p_0) + alpha_1 p_1) ... to global memory
     const SLevel L0 = slev(a, sm, sgeo, 0);
     double* u0 = a.lv[a.m0].u;
+    const int nv0 = ts.nval[0];
     for (int ci = threadIdx.x; ci < L0.n; ci += kThreads) {
         const int c = ci >> (2 * L0.lh), pos = ci & (L0.nq - 1);
         const int pi = pidx(L0, c, pos & (L0.H - 1), pos >> L0.lh);
         double s = 0.0;
-        for (int k = 0; k < top.nval; ++k) s = __dadd_rn(s, __dmul_rn(top.alpha[k], L0.p[k * 4 * L0.PP + pi]));
+        for (int k = 0; k < nv0; ++k) s = __dadd_rn(s, __dmul_rn(ts.alpha[0][k], L0.p[k * 4 * L0.PP + pi]));
         u0[ci] = s;
     }
 }
@@ -886,6 +911,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_cluster_pcg(const __grid_consta
     __shared__ __align__(8) uint64_t bar;
     __shared__ double cred[2][kQuads][2];              // cluster inner products, double-buffered
     __shared__ double cpub[kFusedMaxInner + 1];        // the tier's alphas and nval, pushed to the quadrants
+    __shared__ TierSM ts;                               // the tier's PCG state (CTA 4)
+    __shared__ double qal[kFusedMaxInner], qe[kFusedMaxInner];   // the 64x64 level's alphas / energies
     const FusedArgs& a = ca.f;
     const int rank = (int)cluster_rank();
     const bool quad = rank < kQuads, tier = rank == kTierRank;
@@ -964,7 +991,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_cluster_pcg(const __grid_consta
         else { pa = -1; pb = kQH - (k - 3 * (kQW2 - 1)); }
         zslot = pidx(Q, c, pa, pb);
     }
-    double alpha[kFusedMaxInner], e[kFusedMaxInner];
+    double* alpha = qal;   // shared, same values from every thread (see TierSM)
+    double* e = qe;
     int nval = 0, par = 0;
     for (int i = 0; i < ni; ++i) {
         double* u = Q.p + i * 4 * kQPP;
@@ -1018,11 +1046,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_cluster_pcg(const __grid_consta
         CPH(3)
         // ---- the child's nonlinear_pcg on the tier CTA
         if (tier) {
-            PState top;
-            tier_run(a, sm, sgeo, inv, red, rv, top_reg, top);
+            tier_run(a, sm, sgeo, inv, red, rv, top_reg, &ts);
             if (t < kQuads) {
-                for (int k = 0; k < top.nval; ++k) st_cluster(&cpub[k], t, top.alpha[k]);
-                st_cluster(&cpub[kFusedMaxInner], t, (double)top.nval);
+                const int nv0 = ts.nval[0];
+                for (int k = 0; k < nv0; ++k) st_cluster(&cpub[k], t, ts.alpha[0][k]);
+                st_cluster(&cpub[kFusedMaxInner], t, (double)nv0);
             }
         }
         csync();

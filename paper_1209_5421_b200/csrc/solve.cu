@@ -752,7 +752,9 @@ __global__ void k_pcg_u(Span sp, PList pl, const double* __restrict__ sc, int ni
     GSTRIDE(j, sp.n) {
         const long i = span_idx(sp, j);
         double e = 0.0;
-        for (int k = 0; k < nval; ++k) e = __dadd_rn(e, __dmul_rn(sc[3 + ni + k], pl.p[k][i]));
+#pragma unroll
+        for (int k = 0; k < 8; ++k)   // compile-time indices: the pointer list stays in registers
+            if (k < nval) e = __dadd_rn(e, __dmul_rn(sc[3 + ni + k], pl.p[k][i]));
         u[i] = e;
     }
 }
