@@ -5,7 +5,11 @@ namespace auxb200 {
 
 constexpr int kFusedMaxInner = 8;
 constexpr int kMaxFusedLevels = 8;
-constexpr int kFusedSmemMax = 232448 - 2048;   // 227 KB per CTA minus the static reduction buffer
+#ifdef AUX_FUSED_CLOCKS   // debug build: the clock tables take static shared memory too
+constexpr int kFusedSmemMax = 232448 - 2048 - 512;
+#else
+constexpr int kFusedSmemMax = 232448 - 2048;   // 227 KB per CTA minus the static buffers (reductions, tier state)
+#endif
 
 // Global-memory descriptor of one level for the fused coarse kernel (fused.cu).
 struct FLevel {
