@@ -1424,12 +1424,34 @@ void build_graph(aux_hierarchy* h, const aux_cycle_opts& o, RedState rs) {
         h->dist.comm->peers_warm = true;
     }
     const int64_t before = g_launches;
-    cudaGraph_t g;
+    cudaGraph_t g = nullptr;
     AUX_CUDA(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
-    coarse_root(c);
-    AUX_CUDA(cudaStreamEndCapture(h->stream, &g));
-    h->graph_kernels = g_launches - before;
-    g_launches = before;
+    if (h->dist.comm && h->dist.comm->size > 1) {
+        // a capture the communication library refuses leaves the multi-GPU
+        // solve on eager launches instead of failing it (every rank runs the
+        // same code, so they all take the same branch)
+        bool ok = true;
+        try {
+            coarse_root(c);
+        } catch (const AuxError&) {
+            ok = false;
+        }
+        const cudaError_t ec = cudaStreamEndCapture(h->stream, &g);
+        const int64_t kern = g_launches - before;
+        g_launches = before;
+        if (!ok || ec != cudaSuccess || !g) {
+            (void)cudaGetLastError();
+            if (g) cudaGraphDestroy(g);
+            std::fprintf(stderr, "auxamg_b200: coarse-cycle capture over the communicator failed; eager launches\n");
+            return;
+        }
+        h->graph_kernels = kern;
+    } else {
+        coarse_root(c);
+        AUX_CUDA(cudaStreamEndCapture(h->stream, &g));
+        h->graph_kernels = g_launches - before;
+        g_launches = before;
+    }
     AUX_CUDA(cudaGraphInstantiate(&h->graph, g, 0));
     cudaGraphDestroy(g);
     h->graph_opts = o;
