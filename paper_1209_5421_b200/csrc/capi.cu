@@ -296,16 +296,16 @@ aux_status aux_solve(aux_hierarchy* h, const aux_csr_view* A, const double* b, i
         solve_device(h, bd.p, (long)n_b, &o, res, ud.p);
         if (res->u && n > 0 && h->dist.comm) {   // a part writes the entries of the DoFs it owns
             const long m = h->fine.n;
-            if (m > 0) {
-                const int* gs = owned_ascending(h);
-                gather_owned_sorted(h, ud.p, h->dist.u_stage_h);
+            if (m == n) {   // one part owns every DoF: u is already in caller order
+                AUX_CUDA(cudaMemcpyAsync(res->u, ud.p, sizeof(double) * n, cudaMemcpyDeviceToHost, h->stream));
                 AUX_CUDA(cudaStreamSynchronize(h->stream));
-                const double* uv = h->dist.u_stage_h;
-                if (gs[m - 1] - gs[0] == m - 1) {   // one contiguous run of caller ids
-                    std::memcpy(res->u + gs[0], uv, sizeof(double) * m);
-                } else {
-                    for (long i = 0; i < m; ++i) res->u[gs[i]] = uv[i];   // ascending ids: streaming writes
-                }
+            } else if (m > 0) {   // owned entries in ascending caller id, copied run by run
+                const std::vector<int>& runs = owned_runs(h);
+                double* uv = pinned_scratch((size_t)m);
+                gather_owned_sorted(h, ud.p, uv);
+                AUX_CUDA(cudaStreamSynchronize(h->stream));
+                for (size_t k = 0; k < runs.size(); k += 3)
+                    std::memcpy(res->u + runs[k], uv + runs[k + 1], sizeof(double) * (size_t)runs[k + 2]);
             }
         } else if (res->u && n > 0) {
             AUX_CUDA(cudaMemcpyAsync(res->u, ud.p, sizeof(double) * n, cudaMemcpyDeviceToHost, h->stream));

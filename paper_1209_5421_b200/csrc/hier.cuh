@@ -149,14 +149,11 @@ struct DistInfo {
     DBuf<double> dsum;        // raw inner products before the all-reduce
     DBuf<int> gid;            // local finest row -> caller DoF id
     // host write-back of a part's solution (aux_solve): local rows in ascending
-    // caller id, those ids, and a pinned staging buffer; built at the first solve
+    // caller id, and those ids as runs of consecutive caller ids (caller id
+    // start, position in the ascending order, length); built at the first solve
     DBuf<int> ord;
-    int* gid_sorted_h = nullptr;
-    double* u_stage_h = nullptr;
-    ~DistInfo() {
-        if (gid_sorted_h) cudaFreeHost(gid_sorted_h);
-        if (u_stage_h) cudaFreeHost(u_stage_h);
-    }
+    std::vector<int> runs;
+    bool runs_built = false;
 };
 
 constexpr int kTileBlock = 8;   // blocks up to this size: one thread per block

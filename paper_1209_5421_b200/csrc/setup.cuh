@@ -24,8 +24,11 @@ void gather_level_to_root(aux_hierarchy* h, int t, const std::vector<double*>& v
 // Multi-GPU write-back: the part's local rows ordered by ascending caller id
 // (host array, cached), and its solution entries gathered in that order into a
 // pinned host buffer (asynchronous on h->stream).
-const int* owned_ascending(aux_hierarchy* h);
+const std::vector<int>& owned_runs(aux_hierarchy* h);
 void gather_owned_sorted(aux_hierarchy* h, const double* u_global, double* host_out);
+// Page-locked host scratch of this thread, grown on demand and reused across
+// hierarchies (pinning per solve costs milliseconds).
+double* pinned_scratch(size_t doubles);
 // Exports (reference layout, host arrays).
 void export_level(const aux_hierarchy* h, int level, aux_level_export* x);
 void level_info(const aux_hierarchy* h, int level, aux_level_info* o);

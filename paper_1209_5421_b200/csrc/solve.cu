@@ -1553,21 +1553,49 @@ __global__ void k_gather_sorted(long m, const int* __restrict__ ord, const int* 
     GSTRIDE(i, m) out[i] = u_global[gid[ord[i]]];
 }
 
-const int* owned_ascending(aux_hierarchy* h) {
+double* pinned_scratch(size_t doubles) {
+    struct Arena {
+        double* p = nullptr;
+        size_t n = 0;
+        ~Arena() {
+            if (p) cudaFreeHost(p);
+        }
+    };
+    thread_local Arena a;
+    if (a.n < doubles) {
+        if (a.p) AUX_CUDA(cudaFreeHost(a.p));
+        a.p = nullptr;
+        a.n = 0;
+        AUX_CUDA(cudaHostAlloc(&a.p, sizeof(double) * doubles, cudaHostAllocDefault));
+        a.n = doubles;
+    }
+    return a.p;
+}
+
+const std::vector<int>& owned_runs(aux_hierarchy* h) {
     DistInfo& d = h->dist;
     const long m = h->fine.n;
-    if (d.gid_sorted_h) return d.gid_sorted_h;
+    if (d.runs_built) return d.runs;
     DBuf<unsigned> keys(m);
     d.ord.alloc(m);
     AUX_CUDA(cudaMemcpyAsync(keys.p, d.gid.p, sizeof(int) * m, cudaMemcpyDeviceToDevice, h->stream));
     int bits = 1;
     while (bits < 31 && (1L << bits) < (long)h->n) ++bits;
     radix_sort_pairs(keys.p, d.ord.p, m, bits, h->stream, true);
-    AUX_CUDA(cudaHostAlloc(&d.gid_sorted_h, sizeof(int) * m, cudaHostAllocDefault));
-    AUX_CUDA(cudaHostAlloc(&d.u_stage_h, sizeof(double) * m, cudaHostAllocDefault));
-    AUX_CUDA(cudaMemcpyAsync(d.gid_sorted_h, keys.p, sizeof(int) * m, cudaMemcpyDeviceToHost, h->stream));
+    int* gs = reinterpret_cast<int*>(pinned_scratch((size_t)(m + 1) / 2));
+    AUX_CUDA(cudaMemcpyAsync(gs, keys.p, sizeof(int) * m, cudaMemcpyDeviceToHost, h->stream));
     AUX_CUDA(cudaStreamSynchronize(h->stream));
-    return d.gid_sorted_h;
+    d.runs.clear();
+    for (long i = 0; i < m;) {
+        long k = i + 1;
+        while (k < m && gs[k] == gs[k - 1] + 1) ++k;
+        d.runs.push_back(gs[i]);
+        d.runs.push_back((int)i);
+        d.runs.push_back((int)(k - i));
+        i = k;
+    }
+    d.runs_built = true;
+    return d.runs;
 }
 
 void gather_owned_sorted(aux_hierarchy* h, const double* u_global, double* host_out) {
