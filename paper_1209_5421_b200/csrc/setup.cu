@@ -1519,6 +1519,7 @@ void setup_device(aux_hierarchy* h, const aux_csr_view* A, const double* xy, lon
 //   levels   global-layout arrays per part; the owned rectangle is computed,
 //            a ring of kRing cells is refreshed from the neighbours; a level
 //            stays distributed while the rectangle is >= 16 cells on each side
+//            and the level is wider than 512 cells (AUX_DIST_AGG_SIDE)
 //   agg      the first level below that is gathered on part 0, which builds
 //            the rest of the hierarchy exactly as on one GPU.
 namespace {
@@ -1798,6 +1799,12 @@ void setup_device_dist(aux_hierarchy* h, const aux_csr_view* A, const double* xy
     }
     if (h->lv[1].dist) exchange_level_values(h, 1, false);
     h->dist.agg = P > 1 ? 1 << 30 : 1;   // one part: every level is "on part 0"
+    // levels of at most agg_side^2 cells are gathered on part 0 (default 512:
+    // 256K cells, where a K-cycle visit on one B200 is ~50 us, about one
+    // distributed visit's compute plus its exchanges); AUX_DIST_AGG_SIDE=0
+    // keeps every tileable level distributed
+    const char* aes = std::getenv("AUX_DIST_AGG_SIDE");
+    const int agg_side = aes ? std::atoi(aes) : 512;
 
     // ---- structured coarsening: distributed while the rectangle allows tiles
     DBuf<int> ovf(1);
@@ -1816,7 +1823,11 @@ void setup_device_dist(aux_hierarchy* h, const aux_csr_view* A, const double* xy
         const int wn = 1 << (k - 1);
         if (cur.dist) {
             nx.own = Rect{cur.own.x0 / 2, cur.own.y0 / 2, cur.own.x1 / 2, cur.own.y1 / 2};
-            nx.dist = nx.own.w() >= 16 && nx.own.h() >= 16;
+            // distributed while each part keeps a tileable rectangle and the
+            // level is big enough for one GPU to be bandwidth- rather than
+            // latency-bound on it; below that, one GPU runs the level faster
+            // than P GPUs plus a halo exchange and an all-reduce per phase
+            nx.dist = nx.own.w() >= 16 && nx.own.h() >= 16 && wn > agg_side;
         } else {
             nx.own = Rect{0, 0, wn, wn};
             nx.dist = false;

@@ -15,13 +15,21 @@ pytestmark = [pytest.mark.gpu, pytest.mark.timeout(600)]
 U_TOL = 1e-12
 
 
+@pytest.fixture(params=["512", "0"], ids=["agg512", "deep"])
+def agg_side(request, monkeypatch):
+    """Default agglomeration (levels of <= 512^2 cells on part 0) and the
+    deepest distribution (every level with a tileable rectangle per part)."""
+    monkeypatch.setenv("AUX_DIST_AGG_SIDE", request.param)
+    return request.param
+
+
 @pytest.mark.parametrize("parts", [1, 2, 4, 8])
 @pytest.mark.parametrize("name,make", [
     ("jitter_257", lambda: problems.jittered_p1(257)),
     ("graded_257", lambda: problems.graded_p1(257, 1.3)),
     ("poisson5_300", lambda: problems.poisson5(300)),
 ])
-def test_parts_match_oracle(gpu_api, parts, name, make):
+def test_parts_match_oracle(gpu_api, parts, name, make, agg_side):
     s = make()
     u, res, st = gpu_api.solve_parts(s.A, s.coords, s.b, parts)
     ref = ob.CpuHierarchy("oracle", s.A, s.coords).solve(s.b)
@@ -44,7 +52,7 @@ def test_parts_match_oracle(gpu_api, parts, name, make):
     ("graded2_257", lambda: problems.graded_p1(257, 2.0)),          # dropped + same-colour couplings
     ("jump_257", lambda: problems.jittered_p1(257, jump=1e3)),      # jump coefficient (C4 family)
 ])
-def test_parts_hard_problems(gpu_api, parts, name, make):
+def test_parts_hard_problems(gpu_api, parts, name, make, agg_side):
     s = make()
     u, res, st = gpu_api.solve_parts(s.A, s.coords, s.b, parts)
     ref = ob.CpuHierarchy("oracle", s.A, s.coords).solve(s.b)
