@@ -771,11 +771,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_pcg(const __grid_constant
     const SLevel L0 = slev(a, sm, sgeo, 0);
     double* u0 = a.lv[a.m0].u;
     const int nv0 = ts.nval[0];
+    double al[kFusedMaxInner];   // compile-time indices: registers
+#pragma unroll
+    for (int k = 0; k < kFusedMaxInner; ++k) al[k] = k < nv0 ? ts.alpha[0][k] : 0.0;
     for (int ci = threadIdx.x; ci < L0.n; ci += kThreads) {
         const int c = ci >> (2 * L0.lh), pos = ci & (L0.nq - 1);
         const int pi = pidx(L0, c, pos & (L0.H - 1), pos >> L0.lh);
         double s = 0.0;
-        for (int k = 0; k < nv0; ++k) s = __dadd_rn(s, __dmul_rn(ts.alpha[0][k], L0.p[k * 4 * L0.PP + pi]));
+#pragma unroll
+        for (int k = 0; k < kFusedMaxInner; ++k)
+            if (k < nv0) s = __dadd_rn(s, __dmul_rn(al[k], L0.p[k * 4 * L0.PP + pi]));
         u0[ci] = s;
     }
 }
@@ -1183,11 +1188,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_cluster_pcg(const __grid_consta
     // ---- u = ((0 + alpha_0 p_0) + alpha_1 p_1) ... of the 64x64 level
     if (quad) {
         const int gpos = (kQH * qy + tb) * gH + kQH * qx + ta;
+        double al[kFusedMaxInner];   // compile-time indices: registers
+#pragma unroll
+        for (int k = 0; k < kFusedMaxInner; ++k) al[k] = k < nval ? alpha[k] : 0.0;
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-            const int pi = pidx(Q, c, ta, tb);
+            const int pi = pidx_r(c, ta, tb);
             double s = 0.0;
-            for (int k = 0; k < nval; ++k) s = __dadd_rn(s, __dmul_rn(alpha[k], Q.p[k * 4 * kQPP + pi]));
+#pragma unroll
+            for (int k = 0; k < kFusedMaxInner; ++k)
+                if (k < nval) s = __dadd_rn(s, __dmul_rn(al[k], Q.p[k * 4 * kQPP + pi]));
             ca.u[c * gq + gpos] = s;
         }
     }
