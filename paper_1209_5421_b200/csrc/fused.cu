@@ -943,6 +943,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_cluster_pcg(const __grid_consta
     Q.p = qv + 4 * kQPP;
     Q.ap = qv + (1 + ni) * 4 * kQPP;
     uint8_t* qact = sm + (size_t)(1 + 2 * ni) * 4 * kQPP * sizeof(double);
+    // the child's correction for this quadrant's parents (own + ghost ring),
+    // pushed by the tier CTA: 18 x 18 coarse cells
+    constexpr int kQE = kQH + 2;
+    double* qcorr = reinterpret_cast<double*>(sm + (((size_t)(1 + 2 * ni) * 4 * kQPP * sizeof(double) + 4 * kQPP + 15) &
+                                                    ~size_t(15)));
     // the tier's top level (32x32 cells) as seen from the quadrants
     SLevel T0;
     T0.k = 0; T0.lh = 4; T0.H = kQH; T0.nq = kQH * kQH; T0.n = 4 * T0.nq; T0.W2 = kQW2; T0.PP = kQPP;
@@ -1052,6 +1057,28 @@ __global__ void __launch_bounds__(kThreads, 1) k_cluster_pcg(const __grid_consta
         // ---- the child's nonlinear_pcg on the tier CTA
         if (tier) {
             tier_run(a, sm, sgeo, inv, red, rv, top_reg, &ts);
+            // e = ((0 + alpha_0 p_0) + alpha_1 p_1) ... per coarse cell, pushed to
+            // every quadrant whose parents (own cells and ghost ring) include it
+            {
+                const int nv0 = ts.nval[0];
+                double al[kFusedMaxInner];
+#pragma unroll
+                for (int k = 0; k < kFusedMaxInner; ++k) al[k] = k < nv0 ? ts.alpha[0][k] : 0.0;
+                for (int cell = t; cell < 4 * kQH * kQH; cell += kThreads) {
+                    const int A = cell & (2 * kQH - 1), B = cell / (2 * kQH);   // coarse cell (32 x 32)
+                    const int pc = pidx(T0, (A & 1) | ((B & 1) << 1), A >> 1, B >> 1);
+                    double e = 0.0;
+#pragma unroll
+                    for (int k = 0; k < kFusedMaxInner; ++k)
+                        if (k < nv0) e = __dadd_rn(e, __dmul_rn(al[k], T0.p[k * 4 * kQPP + pc]));
+#pragma unroll
+                    for (int q = 0; q < kQuads; ++q) {
+                        const int la = A - kQH * (q & 1) + 1, lb = B - kQH * (q >> 1) + 1;
+                        if ((unsigned)la < (unsigned)kQE && (unsigned)lb < (unsigned)kQE)
+                            st_cluster(qcorr + lb * kQE + la, (uint32_t)q, e);
+                    }
+                }
+            }
             if (t < kQuads) {
                 const int nv0 = ts.nval[0];
                 for (int k = 0; k < nv0; ++k) st_cluster(&cpub[k], t, ts.alpha[0][k]);
@@ -1078,24 +1105,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_cluster_pcg(const __grid_consta
                 else if (t < 2 * kQH) { pa2 = t - kQH; pb2 = gb; }
                 else { pa2 = ga; pb2 = gb; }
             }
-            auto parent = [&](int pa, int pb) {
-                const int A = kQH * qx + pa, B = kQH * qy + pb;
-                return pidx(T0, (A & 1) | ((B & 1) << 1), A >> 1, B >> 1);
-            };
-            const int pc1 = parent(ta, tb), pc2 = parent(pa2, pb2);
-            double d1[kFusedMaxInner], d2[kFusedMaxInner];
-#pragma unroll
-            for (int k = 0; k < kFusedMaxInner; ++k) {
-                d1[k] = k < cn ? ld_cluster(T0.p + k * 4 * kQPP + pc1, kTierRank) : 0.0;
-                d2[k] = (k < cn && gh) ? ld_cluster(T0.p + k * 4 * kQPP + pc2, kTierRank) : 0.0;
-            }
-            double e1 = 0.0, e2 = 0.0;
-#pragma unroll
-            for (int k = 0; k < kFusedMaxInner; ++k)
-                if (k < cn) {
-                    e1 = __dadd_rn(e1, __dmul_rn(al[k], d1[k]));
-                    e2 = __dadd_rn(e2, __dmul_rn(al[k], d2[k]));
-                }
+            (void)al;
+            const double e1 = qcorr[(tb + 1) * kQE + ta + 1];
+            const double e2 = gh ? qcorr[(pb2 + 1) * kQE + pa2 + 1] : 0.0;
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
                 const int pi = pidx(Q, c, ta, tb);
@@ -1244,7 +1256,8 @@ bool cluster_layout(const aux_hierarchy* h, int m, const FusedArgs& fa, ClusterA
     if (!h->gpu.cluster_tier || m < 1 || fa.m0 != m + 1 || fa.ni > kFusedMaxInner) return false;
     const Level& L = h->lv[m];
     if (L.dist || L.geo.H != 2 * kQH || h->lv[m + 1].geo.nq != kThreads || fa.last - fa.m0 + 1 < 2) return false;
-    const size_t quad = (size_t)(1 + 2 * fa.ni) * 4 * kQPP * sizeof(double) + 4 * kQPP;
+    const size_t quad = (((size_t)(1 + 2 * fa.ni) * 4 * kQPP * sizeof(double) + 4 * kQPP + 15) & ~size_t(15)) +
+                        (size_t)(kQH + 2) * (kQH + 2) * sizeof(double);   // vectors, act, pushed corrections
     if (quad > (size_t)kFusedSmemMax) return false;
     ca->f = fa;
     ca->g = L.geo;
