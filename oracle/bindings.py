@@ -178,3 +178,90 @@ def galerkin_dense(kind, A, agg_of, n_agg):
                                             C.c_int32(n_agg), C.c_void_p(C_.ctypes.data))
     _abi.raise_for(s, b"galerkin_dense")
     return C_
+
+
+# ---- the reference's own input generators (problems.hpp, tests/testgen.hpp) via ref_shim.cpp
+def _gen_lib():
+    lib, _ = _load("ref")
+    if not getattr(lib, "_gen_typed", False):
+        lib.ref_gen_make.restype = C.c_void_p
+        lib.ref_gen_make.argtypes = [C.c_int, C.c_int, C.c_double, C.c_uint, C.c_double]
+        lib.ref_gen_random_spd.restype = C.c_void_p
+        lib.ref_gen_random_spd.argtypes = [C.c_int, C.c_uint]
+        lib.ref_gen_random_stencil.restype = C.c_void_p
+        lib.ref_gen_random_stencil.argtypes = [C.c_int, C.c_uint]
+        lib.ref_gen_random_vector.argtypes = [C.c_int64, C.c_uint, C.c_double, C.c_double, C.c_void_p]
+        for f in ("ref_gen_n", "ref_gen_mesh_nodes", "ref_gen_mesh_tris", "ref_gen_mesh_nboundary"):
+            getattr(lib, f).argtypes = [C.c_void_p]
+            getattr(lib, f).restype = C.c_int
+        for f in ("ref_gen_nnz", "ref_gen_ell_len"):
+            getattr(lib, f).argtypes = [C.c_void_p]
+            getattr(lib, f).restype = C.c_int64
+        for f in ("ref_gen_row_ptr", "ref_gen_col_idx", "ref_gen_ell_col"):
+            getattr(lib, f).argtypes = [C.c_void_p]
+            getattr(lib, f).restype = C.POINTER(C.c_int32)
+        for f in ("ref_gen_values", "ref_gen_b", "ref_gen_xy", "ref_gen_ell_val"):
+            getattr(lib, f).argtypes = [C.c_void_p]
+            getattr(lib, f).restype = C.POINTER(C.c_double)
+        lib.ref_gen_mesh_copy.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        lib.ref_gen_free.argtypes = [C.c_void_p]
+        lib._gen_typed = True
+    return lib
+
+
+def _arr(ptr, n, dtype):
+    if n == 0:
+        return np.zeros(0, dtype)
+    return np.ctypeslib.as_array(ptr, shape=(n,)).astype(dtype, copy=True)
+
+
+def ref_make(kind: int, n: int, param: float = 0.0, seed: int = 1, jump: float = 0.0, mesh: bool = False):
+    """LinearSystem from the reference's own generator (same kinds as
+    paper_1209_5421_b200.problems.make); mesh=True also returns the TriMesh."""
+    from paper_1209_5421_b200 import problems as P
+    lib = _gen_lib()
+    h = lib.ref_gen_make(kind, n, param, seed, jump)
+    if not h:
+        raise ValueError("reference generator failed")
+    try:
+        N, nnz = lib.ref_gen_n(h), lib.ref_gen_nnz(h)
+        A = P.CsrMatrix(N, N, _arr(lib.ref_gen_row_ptr(h), N + 1, np.int32), _arr(lib.ref_gen_col_idx(h), nnz, np.int32),
+                        _arr(lib.ref_gen_values(h), nnz, np.float64))
+        sysm = P.LinearSystem(A, _arr(lib.ref_gen_b(h), N, np.float64),
+                              _arr(lib.ref_gen_xy(h), 2 * N, np.float64).reshape(N, 2))
+        if not mesh:
+            return sysm
+        M, T, B = lib.ref_gen_mesh_nodes(h), lib.ref_gen_mesh_tris(h), lib.ref_gen_mesh_nboundary(h)
+        nodes, tris, bnd = np.zeros((M, 2)), np.zeros((T, 3), np.int32), np.zeros(max(B, 1), np.int32)
+        lib.ref_gen_mesh_copy(h, nodes.ctypes.data, tris.ctypes.data, bnd.ctypes.data)
+        return sysm, P.TriMesh(nodes, tris, bnd[:B])
+    finally:
+        lib.ref_gen_free(h)
+
+
+def ref_random_spd(n: int, seed: int):
+    from paper_1209_5421_b200 import problems as P
+    lib = _gen_lib()
+    h = lib.ref_gen_random_spd(n, seed)
+    try:
+        nnz = lib.ref_gen_nnz(h)
+        return P.CsrMatrix(n, n, _arr(lib.ref_gen_row_ptr(h), n + 1, np.int32),
+                           _arr(lib.ref_gen_col_idx(h), nnz, np.int32), _arr(lib.ref_gen_values(h), nnz, np.float64))
+    finally:
+        lib.ref_gen_free(h)
+
+
+def ref_random_stencil(k: int, seed: int):
+    lib = _gen_lib()
+    h = lib.ref_gen_random_stencil(k, seed)
+    try:
+        m = lib.ref_gen_ell_len(h)
+        return _arr(lib.ref_gen_ell_col(h), m, np.int32), _arr(lib.ref_gen_ell_val(h), m, np.float64)
+    finally:
+        lib.ref_gen_free(h)
+
+
+def ref_random_vector(n: int, seed: int, lo: float = -1.0, hi: float = 1.0):
+    out = np.zeros(n, np.float64)
+    _gen_lib().ref_gen_random_vector(n, seed, lo, hi, out.ctypes.data)
+    return out

@@ -13,6 +13,8 @@
 #include <vector>
 
 #include "auxamg/auxamg.hpp"
+#include "auxamg/problems.hpp"
+#include "testgen.hpp"   // reference tests/testgen.hpp (graded_mesh, disk_mesh, random_*)
 #include "../include/auxamg_b200.h"
 
 namespace {
@@ -51,9 +53,150 @@ auxamg::CsrMatrix to_csr(const aux_csr_view* v) {
     return A;
 }
 
+// One generated input: the reference's own generators (problems.hpp,
+// tests/testgen.hpp), so the harness generator libauxgen.so can be pinned
+// byte for byte and the reference arm of bench.py maps no repo library.
+struct RefGen {
+    auxamg::LinearSystem sys;
+    auxamg::TriMesh mesh;
+    std::vector<double> xy;
+    std::vector<int> ell_col;
+    std::vector<double> ell_val;
+};
+
+// assemble_fem_triangle (problems.hpp:152-193) with the BASELINE C4 jump
+// coefficient: the reference has no coefficient argument, so
+// the element loop is restated around the reference's own element_geometry and
+// csr_from_triplets, kappa multiplied before the division by 4*area.
+auxamg::LinearSystem assemble_jump(const auxamg::TriMesh& mesh, double kappa_odd) {
+    const int n = static_cast<int>(mesh.nodes.size());
+    std::vector<char> is_boundary(n, 0);
+    for (int v : mesh.boundary_nodes) is_boundary[v] = 1;
+    std::vector<int> interior_of(n, -1);
+    int n_interior = 0;
+    for (int v = 0; v < n; ++v)
+        if (!is_boundary[v]) interior_of[v] = n_interior++;
+    auxamg::LinearSystem sys;
+    sys.b.assign(n_interior, 0.0);
+    sys.coords.resize(n_interior);
+    for (int v = 0; v < n; ++v)
+        if (interior_of[v] >= 0) sys.coords[interior_of[v]] = mesh.nodes[v];
+    std::vector<auxamg::Triplet> entries;
+    entries.reserve(mesh.triangles.size() * 9);
+    for (int e = 0; e < static_cast<int>(mesh.triangles.size()); ++e) {
+        const auto g = auxamg::detail::element_geometry(mesh, e);
+        const auto& t = mesh.triangles[e];
+        const auxamg::Point p0 = mesh.nodes[t[0]], p1 = mesh.nodes[t[1]], p2 = mesh.nodes[t[2]];
+        const double cx = (p0.x + p1.x + p2.x) / 3.0, cy = (p0.y + p1.y + p2.y) / 3.0;
+        const int bx = std::min(7, static_cast<int>(8.0 * cx)), by = std::min(7, static_cast<int>(8.0 * cy));
+        const double kappa = ((bx + by) % 2 == 1) ? kappa_odd : 1.0;
+        for (int a = 0; a < 3; ++a) {
+            const int row = interior_of[t[a]];
+            if (row < 0) continue;
+            sys.b[row] += 1.0 * g.area / 3.0;
+            for (int b = 0; b < 3; ++b) {
+                const int col = interior_of[t[b]];
+                if (col < 0) continue;
+                entries.push_back({row, col, (kappa * (g.b[a] * g.b[b] + g.c[a] * g.c[b])) / (4.0 * g.area)});
+            }
+        }
+    }
+    sys.A = auxamg::csr_from_triplets(n_interior, n_interior, std::move(entries));
+    return sys;
+}
+
 }  // namespace
 
 extern "C" {
+
+// Same kind numbering as libauxgen's auxgen_make (paper_1209_5421_b200/csrc/problems.cpp):
+//   0 gen_poisson_uniform2d(n)                       problems.hpp:41-76
+//   1 structured_split_mesh(n) + assemble             problems.hpp:80-105, 152-193
+//   2 split mesh, interior nodes jittered by mt19937(seed) U(-param,param)*h
+//   3 testgen::graded_mesh(n, param)                   tests/testgen.hpp:91-98
+//   4 testgen::disk_mesh(n, 0.5, 0.5, param or 0.48)   tests/testgen.hpp:132-158
+// jump > 0: the C4 checkerboard coefficient (kinds 1-4).
+void* ref_gen_make(int kind, int n, double param, unsigned seed, double jump) {
+    auto* g = new RefGen;
+    try {
+        if (kind == 0) {
+            g->sys = auxamg::gen_poisson_uniform2d(n);
+        } else {
+            if (kind == 1 || kind == 2) g->mesh = auxamg::structured_split_mesh(n);
+            if (kind == 2) {
+                std::mt19937 rng(seed);
+                std::uniform_real_distribution<double> U(-param, param);
+                const double h = 1.0 / n;
+                for (int j = 1; j < n; ++j)
+                    for (int i = 1; i < n; ++i) {
+                        auxamg::Point& p = g->mesh.nodes[static_cast<std::size_t>(j) * (n + 1) + i];
+                        p.x += U(rng) * h;
+                        p.y += U(rng) * h;
+                    }
+            } else if (kind == 3) {
+                g->mesh = testgen::graded_mesh(n, param);
+            } else if (kind == 4) {
+                g->mesh = testgen::disk_mesh(n, 0.5, 0.5, param > 0 ? param : 0.48);
+            } else if (kind != 1) {
+                throw std::invalid_argument("unknown kind");
+            }
+            g->sys = jump > 0.0 ? assemble_jump(g->mesh, jump) : auxamg::assemble_fem_triangle(g->mesh, 1.0);
+        }
+        g->xy.resize(2 * g->sys.coords.size());
+        for (std::size_t i = 0; i < g->sys.coords.size(); ++i) {
+            g->xy[2 * i] = g->sys.coords[i].x;
+            g->xy[2 * i + 1] = g->sys.coords[i].y;
+        }
+    } catch (...) {
+        delete g;
+        return nullptr;
+    }
+    return g;
+}
+
+// testgen::random_spd (tests/testgen.hpp:18-35)
+void* ref_gen_random_spd(int n, unsigned seed) {
+    auto* g = new RefGen;
+    g->sys.A = testgen::random_spd(n, seed);
+    return g;
+}
+
+// testgen::random_stencil (tests/testgen.hpp:39-61)
+void* ref_gen_random_stencil(int k, unsigned seed) {
+    auto* g = new RefGen;
+    const auxamg::EllMatrix a = testgen::random_stencil(k, seed);
+    g->ell_col = a.col_idx;
+    g->ell_val = a.values;
+    return g;
+}
+
+// testgen::random_vector (tests/testgen.hpp:79-86)
+void ref_gen_random_vector(int64_t n, unsigned seed, double lo, double hi, double* out) {
+    const std::vector<double> v = testgen::random_vector(static_cast<std::size_t>(n), seed, lo, hi);
+    std::memcpy(out, v.data(), sizeof(double) * v.size());
+}
+
+int ref_gen_n(void* p) { return static_cast<RefGen*>(p)->sys.A.n_rows; }
+int64_t ref_gen_nnz(void* p) { return static_cast<int64_t>(static_cast<RefGen*>(p)->sys.A.values.size()); }
+const int* ref_gen_row_ptr(void* p) { return static_cast<RefGen*>(p)->sys.A.row_ptr.data(); }
+const int* ref_gen_col_idx(void* p) { return static_cast<RefGen*>(p)->sys.A.col_idx.data(); }
+const double* ref_gen_values(void* p) { return static_cast<RefGen*>(p)->sys.A.values.data(); }
+const double* ref_gen_b(void* p) { return static_cast<RefGen*>(p)->sys.b.data(); }
+const double* ref_gen_xy(void* p) { return static_cast<RefGen*>(p)->xy.data(); }
+int64_t ref_gen_ell_len(void* p) { return static_cast<int64_t>(static_cast<RefGen*>(p)->ell_val.size()); }
+const int* ref_gen_ell_col(void* p) { return static_cast<RefGen*>(p)->ell_col.data(); }
+const double* ref_gen_ell_val(void* p) { return static_cast<RefGen*>(p)->ell_val.data(); }
+int ref_gen_mesh_nodes(void* p) { return static_cast<int>(static_cast<RefGen*>(p)->mesh.nodes.size()); }
+int ref_gen_mesh_tris(void* p) { return static_cast<int>(static_cast<RefGen*>(p)->mesh.triangles.size()); }
+int ref_gen_mesh_nboundary(void* p) { return static_cast<int>(static_cast<RefGen*>(p)->mesh.boundary_nodes.size()); }
+void ref_gen_mesh_copy(void* p, double* xy, int* tris, int* boundary) {
+    const auxamg::TriMesh& m = static_cast<RefGen*>(p)->mesh;
+    for (std::size_t i = 0; i < m.nodes.size(); ++i) { xy[2 * i] = m.nodes[i].x; xy[2 * i + 1] = m.nodes[i].y; }
+    for (std::size_t i = 0; i < m.triangles.size(); ++i)
+        for (int v = 0; v < 3; ++v) tris[3 * i + v] = m.triangles[i][v];
+    for (std::size_t i = 0; i < m.boundary_nodes.size(); ++i) boundary[i] = m.boundary_nodes[i];
+}
+void ref_gen_free(void* p) { delete static_cast<RefGen*>(p); }
 
 void ref_set_num_threads(int n) { auxamg::set_num_threads(n); }
 

@@ -1,6 +1,8 @@
 """Device P1 FEM assembly: aux_assemble_p1 against the
-reference's assemble_fem_triangle + csr_from_triplets (the harness generator
-reproduces them bitwise, tests/test_oracle.py).  Pattern, load vector,
+reference's own assemble_fem_triangle + csr_from_triplets (problems.hpp:152-193,
+sparse.hpp:193-215), compiled in place through oracle/ref_shim.cpp
+(bindings.ref_make; the jump coefficient of C4 is the shim's restatement around
+the reference's element_geometry).  Pattern, load vector,
 coordinates and every entry summed from <= 2 contributions are bitwise; a
 diagonal sums ~6 contributions, added in element order here and in the
 reference's (unstable) std::sort order there, so it may differ in the last
@@ -8,6 +10,7 @@ bits.  The assembled system then runs setup + solve without leaving the GPU."""
 import numpy as np
 import pytest
 
+import bindings as ob
 from paper_1209_5421_b200 import problems
 
 pytestmark = pytest.mark.gpu
@@ -21,7 +24,7 @@ pytestmark = pytest.mark.gpu
     (2, 48, 0.15, 1e3),         # jump coefficient (C4 family)
 ])
 def test_assembly_matches_reference(gpu_api, kind, n, param, jump):
-    s, m = problems.make_with_mesh(kind, n, param, 1, jump)
+    s, m = ob.ref_make(kind, n, param, 1, jump, mesh=True)
     ds = gpu_api.DeviceSystem(m.nodes, m.triangles, m.boundary, 1.0, jump)
     A, b, xy = ds.to_host()
     assert A.n_rows == s.A.n_rows and A.nnz == s.A.nnz
