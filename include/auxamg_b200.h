@@ -266,11 +266,16 @@ aux_status aux_galerkin_dense(const aux_csr_view* A, const int32_t* agg_of, int6
 /* ---- measurement hooks (bench.py; not part of the reference API) ---- */
 /* Number of kernels this library launched (graph nodes count per replay). */
 int64_t aux_launch_count(void);
-/* When enabled, the finest-level kernels of the next solves are bracketed by
- * CUDA events on their launch stream; read back per-kernel totals. */
+/* on = 1: the finest-level kernels and the coarse K-cycle of the next solves
+ * are bracketed by CUDA events on their launch stream; on = 2: additionally
+ * the level-1 (level L) tile kernels, with the coarse cycle launched eagerly
+ * instead of as a graph; 0 = off.  Read back per-kernel totals. */
 void aux_profile_enable(aux_hierarchy* h, int32_t on);
 /* kind: 0 = finest block-GS colour pass, 1 = finest SpMV (outer A z),
- *       2 = finest residual+restrict, 3 = level-L 9-point GS colour pass.
+ *       2 = finest residual+restrict, 3 = coarse K-cycle of one finest visit,
+ *       4 = level-L k_tile_down (pending PCG update, pre-smoothing GS,
+ *       residual, restriction), 5 = level-L k_tile_up (prolongation,
+ *       post-smoothing GS, ELL SpMV A z, inner products; mode 2 only).
  * Writes launches, total ms and algorithmic bytes per launch (mean). */
 aux_status aux_profile_read(const aux_hierarchy* h, int32_t kind, int64_t* launches,
                             double* total_ms, double* bytes_per_launch);

@@ -376,8 +376,9 @@ void aux_destroy(aux_hierarchy* h) { delete h; }
 int64_t aux_launch_count(void) { return g_launches; }
 
 void aux_profile_enable(aux_hierarchy* h, int32_t on) {
-    h->prof.on = on != 0;
-    for (int k = 0; k < 4; ++k) {
+    h->prof.on = on < 0 ? 0 : (on > 2 ? 2 : on);
+    h->graph_valid = false;   // mode 2 runs the coarse cycle eagerly; mode 0/1 recapture
+    for (int k = 0; k < kProfKinds; ++k) {
         h->prof.used[k] = 0;
         h->prof.bytes[k] = 0;
         h->prof.launches[k] = 0;
@@ -387,7 +388,7 @@ void aux_profile_enable(aux_hierarchy* h, int32_t on) {
 
 aux_status aux_profile_read(const aux_hierarchy* hc, int32_t kind, int64_t* launches, double* total_ms,
                             double* bytes_per_launch) {
-    if (kind < 0 || kind > 3) return AUX_ARGUMENT_ERROR;
+    if (kind < 0 || kind >= kProfKinds) return AUX_ARGUMENT_ERROR;
     auto* h = const_cast<aux_hierarchy*>(hc);
     return guarded(nullptr, 0, [&] {
         AUX_CUDA(cudaStreamSynchronize(h->stream));

@@ -159,13 +159,18 @@ struct DistInfo {
 constexpr int kTileBlock = 8;   // blocks up to this size: one thread per block
 constexpr int kWarpInvMax = 320;   // inverse mode: blocks up to this size are one CTA task of k_bgs_inv
 
+// Live CUDA-event profile of one solve (aux_profile_enable / aux_profile_read).
+// Kinds: 0 finest colour pass, 1 outer A z + dots, 2 finest residual +
+// restriction, 3 coarse K-cycle of one finest visit (graph replay), 4 / 5
+// k_tile_down / k_tile_up of level 1 (level L: eager launches, mode 2 only).
+constexpr int kProfKinds = 6;
 struct Profile {
-    bool on = false;
-    std::vector<cudaEvent_t> ev_begin[4], ev_end[4];
-    size_t used[4] = {0, 0, 0, 0};
-    double bytes[4] = {0, 0, 0, 0};
-    long long launches[4] = {0, 0, 0, 0};
-    double total_ms[4] = {0, 0, 0, 0};
+    int on = 0;   // 0 off, 1 finest kernels + coarse graph, 2 also level-1 tile kernels (no graph)
+    std::vector<cudaEvent_t> ev_begin[kProfKinds], ev_end[kProfKinds];
+    size_t used[kProfKinds] = {};
+    double bytes[kProfKinds] = {};
+    long long launches[kProfKinds] = {};
+    double total_ms[kProfKinds] = {};
 };
 
 }  // namespace auxb200

@@ -1173,7 +1173,12 @@ void pcg_tiles(Ctx& c, int m) {
         d.rc = C.pcg.r.p;
         d.sc_child = explicit_iterate(h, m + 1) ? nullptr : C.pcg.sc.p;
         d.child_nval = sc_nval(ni);
+        const bool prof_l = m == 1 && c.profile_finest && h->prof.on == 2;
+        if (prof_l) prof_begin(c, 4);
         launch_tile_down(d, ntiles, c.o.pre_sweeps, c.s);
+        // algorithmic bytes (each array once): stencil values, r in, pending
+        // update (A p, r out), pre-smoothed iterate out, child right-hand side out
+        if (prof_l) prof_end(c, 4, (double)sp.n * (72.0 + 8.0 + (i ? 16.0 : 0.0) + 8.0) + 8.0 * (double)C.n);
         if (L.dist) {
             if (i == 0) ring_exchange(c, m, {P.upre.p});
             else ring_exchange(c, m, {P.upre.p, R[i & 1]});
@@ -1205,7 +1210,13 @@ void pcg_tiles(Ctx& c, int m) {
         u.mode = i == 0 ? 0 : 1;
         const Route ru = route(c, L.dist, i == 0 ? Fin{1, sc, nullptr, sc + 3, sc + sc_alpha(ni, 0), sc + sc_nval(ni), 0}
                                                  : Fin{2, sc, sc + 3, nullptr});
+        if (prof_l) prof_begin(c, 5);
         launch_tile_up(u, ntiles, c.o.post_sweeps, c.rs, ru.launch, c.s);
+        // stencil values, active flags, f, pre-smoothed iterate, child
+        // correction (explicit iterate or its n_inner directions), z and A z out
+        if (prof_l)
+            prof_end(c, 5, (double)sp.n * (72.0 + 1.0 + 8.0 + 8.0 + 16.0) +
+                               8.0 * (double)C.n * (child_explicit ? 1.0 : (double)ni));
         routed(c, ru);
         if (i > 0) {
             for (int j = 1; j < i; ++j) {
@@ -1361,12 +1372,14 @@ void finest_cycle(Ctx& c, const double* f, double* u, double* snap) {
     AUX_LAUNCHED(2);
     prof_end(c, 2, 12.0 * F.nnz + 4.0 * (F.n + 1) + 16.0 * F.n + 4.0 * (C.n + 1) + 8.0 * C.n);
     g_trace.mark(c.s, 1);
+    prof_begin(c, 3);
     if (h->graph_valid) {
         AUX_CUDA(cudaGraphLaunch(h->graph, c.s));
         AUX_LAUNCHED(h->graph_kernels);
     } else {
         coarse_root(c);
     }
+    prof_end(c, 3, 0.0);
     g_trace.mark(c.s, 2);
     k_csr_prolong<<<blocks_for(F.n), 256, 0, c.s>>>(F.cell.p, F.n, u, C.pcg.u.p);
     AUX_LAUNCHED(1);
@@ -1412,6 +1425,7 @@ void build_graph(aux_hierarchy* h, const aux_cycle_opts& o, RedState rs) {
     }
     h->graph_valid = false;
     if (!h->gpu.use_graphs || h->direct_only || h->lv.size() < 2) return;
+    if (h->prof.on == 2) return;   // per-kernel profile of the level-1 tile kernels: eager launches
     Ctx c{h, h->stream, o, rs, false};
     if (h->dist.comm && h->dist.comm->size > 1 && !h->dist.comm->peers_warm) {
         // one eager pass first (once per communicator), so every NCCL peer
@@ -1681,7 +1695,7 @@ void solve_device(aux_hierarchy* h, const double* b, long n_b, const aux_cycle_o
                 fprintf(stderr, "[aux trace] graph build %.3f ms host\n",
                         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tg0).count());
         }
-        Ctx c{h, s, *o, rs, h->prof.on};
+        Ctx c{h, s, *o, rs, h->prof.on != 0};
         // colour-pass byte counts for the profile
         if (h->prof.on && !h->direct_only && h->lv.size() > 1) {
             const Geo& gL = h->lv[1].geo;
