@@ -16,6 +16,7 @@
 // names and hierarchy.
 #pragma once
 
+#include <algorithm>
 #include <chrono>
 #include <cstdint>
 #include <span>
@@ -191,15 +192,17 @@ Hierarchy setup_hierarchy(const Csr& A, const Points& coords, const Opts& opts =
     return Hierarchy(h);
 }
 
-/// solve(A, b, h, opts) — cycle.hpp:202-247.  A must be the matrix given to
-/// setup (its device copy is reused).
+/// solve(A, b, h, opts) — cycle.hpp:202-247.  As in the reference the cycle
+/// runs on the hierarchy's copy of the setup matrix and the outer A z on the
+/// caller's A: the setup matrix (same arrays, same sampled contents) reuses its
+/// device copy, any other matrix of the same order is uploaded for that solve.
 template <class Csr, class Opts = CycleOptions>
 SolveResult solve(const Csr& A, std::span<const double> b, const Hierarchy& h, const Opts& opts = Opts{}) {
     const aux_csr_view v = detail::view(A);
     const aux_cycle_opts o = detail::cycle_opts(opts);
     SolveResult r;
     r.u.assign(static_cast<size_t>(A.n_rows), 0.0);
-    r.residual_history.assign(static_cast<size_t>(o.max_outer) + 1, 0.0);
+    r.residual_history.assign(static_cast<size_t>(std::max(o.max_outer, 0)) + 1, 0.0);   // options checked by aux_solve
     aux_solve_result res{};
     res.u = r.u.data();
     res.residual_history = r.residual_history.data();

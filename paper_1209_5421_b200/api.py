@@ -265,7 +265,11 @@ def setup_hierarchy_device(n: int, nnz: int, row_ptr: int, col_idx: int, values:
 
 def solve(A: CsrMatrix | None, b, h: Hierarchy, opts: CycleOptions | None = None,
           out: np.ndarray | None = None) -> SolveResult:
-    """solve(A, b, h, opts).  A may be None or the matrix given to setup.
+    """solve(A, b, h, opts) (cycle.hpp:202-247).  As in the reference, the
+    cycle runs on the hierarchy's copy of the setup matrix and the outer A z on
+    the caller's A: None or the setup matrix (same arrays and sampled contents,
+    or equal contents) reuses the device copy; any other matrix of the same
+    order is uploaded for this solve (not on multi-part hierarchies).
     out: optional caller-owned float64 array of length n (e.g. pinned) that
     receives u; the result then references it instead of a fresh copy."""
     o = (opts or CycleOptions()).c()

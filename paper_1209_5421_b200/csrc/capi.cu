@@ -57,7 +57,7 @@ aux_hierarchy* make_h(const aux_setup_opts* o, const aux_gpu_opts* g) {
 
 aux_hierarchy::~aux_hierarchy() {
     if (graph) cudaGraphExecDestroy(graph);
-    for (int k = 0; k < 4; ++k) {
+    for (int k = 0; k < kProfKinds; ++k) {
         for (auto e : prof.ev_begin[k]) cudaEventDestroy(e);
         for (auto e : prof.ev_end[k]) cudaEventDestroy(e);
     }
@@ -165,6 +165,7 @@ aux_status aux_setup(const aux_csr_view* A, const double* xy, int64_t n_points, 
         h->host_col = A->col_idx;
         h->host_val = A->values;
         h->host_nnz = A->nnz;
+        h->host_fp = csr_fingerprint(A);
         h->last_setup_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     });
     if (st != AUX_OK) {
@@ -239,6 +240,7 @@ static aux_status setup_dist_impl(const aux_csr_view* A, const double* xy, int64
             h->host_col = A->col_idx;
             h->host_val = A->values;
             h->host_nnz = A->nnz;
+            h->host_fp = csr_fingerprint(A);
         } else {
             setup_device_dist(h, A, xy, (long)n_points);
         }
@@ -281,13 +283,15 @@ aux_status aux_solve(aux_hierarchy* h, const aux_csr_view* A, const double* b, i
             throw_aux(AUX_ARGUMENT_ERROR, "cycle options must be positive");
         if (!(o.rtol > 0.0) || !(o.rtol < 1.0)) throw_aux(AUX_ARGUMENT_ERROR, "rtol must lie in (0,1)");
         if (o.max_directions < 0) throw_aux(AUX_ARGUMENT_ERROR, "max_directions must be >= 0");
+        h->outer = false;
         if (A) {
             if (n_b != A->n_rows) throw_aux(AUX_SIZE_ERROR, "solve: right-hand side does not match matrix");
             if (A->n_rows != h->n) throw_aux(AUX_SIZE_ERROR, "solve: hierarchy was built for a different order");
-            if (A->row_ptr != h->host_rp || A->col_idx != h->host_col || A->values != h->host_val ||
-                A->nnz != h->host_nnz)
-                throw_aux(AUX_ARGUMENT_ERROR,
-                          "solve: A differs from the matrix given to setup (pass NULL or the setup matrix)");
+            // the setup matrix (same arrays, same sampled contents) reuses the
+            // device copy; any other matrix is uploaded for the outer A z
+            const bool same = A->row_ptr == h->host_rp && A->col_idx == h->host_col && A->values == h->host_val &&
+                              A->nnz == h->host_nnz && csr_fingerprint(A) == h->host_fp;
+            if (!same) set_outer_matrix(h, A);
         }
         const long n = h->n;
         DBuf<double> bd(std::max<long>(n_b, 1)), ud(std::max<long>(n, 1));
@@ -323,6 +327,7 @@ aux_status aux_solve_device(aux_hierarchy* h, const double* b, int64_t n_b, cons
         aux_cycle_opts o;
         aux_default_cycle_opts(&o);
         if (opts) o = *opts;
+        h->outer = false;
         solve_device(h, b, (long)n_b, &o, res, res->u);
     });
 }

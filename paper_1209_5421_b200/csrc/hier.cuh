@@ -202,6 +202,16 @@ struct aux_hierarchy {
     const void* host_col = nullptr;
     const void* host_val = nullptr;
     long host_nnz = 0;
+    uint64_t host_fp = 0;            // sampled fingerprint of the setup matrix (csr_fingerprint)
+    // solve(A, ...) with a matrix other than the setup one: the reference uses
+    // the caller's A for the outer A z (cycle.hpp:228) and its copy for the
+    // cycle, so A is uploaded and permuted like the setup matrix (same rows
+    // order, columns relabelled, entries in storage order) and the outer
+    // SpMV of that solve reads it
+    bool outer = false;
+    long o_nnz = 0;
+    auxb200::DBuf<int> o_rp, o_col;
+    auxb200::DBuf<double> o_v;
     // solve workspace (outer loop)
     auxb200::DBuf<double> w_r, w_u, w_b, w_tmp;
     std::vector<auxb200::DBuf<double>> w_p, w_ap;

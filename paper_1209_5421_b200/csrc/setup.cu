@@ -1257,6 +1257,101 @@ void validate_values(aux_hierarchy* h, const aux_csr_view* A) {
     }
 }
 
+__global__ void k_perm_len(const int* __restrict__ rp, const int* __restrict__ perm, long n, int* __restrict__ len) {
+    GSTRIDE(i, n) {
+        const int old = perm[i];
+        len[i] = rp[old + 1] - rp[old];
+    }
+}
+
+uint64_t csr_fingerprint(const aux_csr_view* A) {
+    uint64_t h = 1469598103934665603ull;   // FNV-1a over the sampled words
+    auto mix = [&](uint64_t w) {
+        for (int b = 0; b < 8; ++b) {
+            h ^= (w >> (8 * b)) & 0xff;
+            h *= 1099511628211ull;
+        }
+    };
+    mix((uint64_t)A->n_rows);
+    mix((uint64_t)A->nnz);
+    const long n = A->n_rows, nnz = A->nnz;
+    if (n >= 0 && A->row_ptr) {
+        const long step = std::max<long>(1, (n + 1) / 256);
+        for (long i = 0; i <= n; i += step) mix((uint64_t)(uint32_t)A->row_ptr[i]);
+        mix((uint64_t)(uint32_t)A->row_ptr[n]);
+    }
+    if (nnz > 0 && A->col_idx && A->values) {
+        const long step = std::max<long>(1, nnz / 4096);
+        for (long p = 0; p < nnz; p += step) {
+            uint64_t w;
+            std::memcpy(&w, &A->values[p], 8);
+            mix(w ^ ((uint64_t)(uint32_t)A->col_idx[p] << 1));
+        }
+        uint64_t w;
+        std::memcpy(&w, &A->values[nnz - 1], 8);
+        mix(w);
+    }
+    return h;
+}
+
+void set_outer_matrix(aux_hierarchy* h, const aux_csr_view* A) {
+    if (h->dist.comm)
+        throw_aux(AUX_ARGUMENT_ERROR, "solve: a multi-part hierarchy needs the matrix given to setup");
+    cudaStream_t s = h->stream;
+    const long n = A->n_rows, nnz = A->nnz;
+    DBuf<int> rp(n + 1), col(std::max<long>(nnz, 1));
+    DBuf<double> v(std::max<long>(nnz, 1));
+    AUX_CUDA(cudaMemcpyAsync(rp.p, A->row_ptr, sizeof(int) * (n + 1), cudaMemcpyHostToDevice, s));
+    if (nnz) {
+        AUX_CUDA(cudaMemcpyAsync(col.p, A->col_idx, sizeof(int) * nnz, cudaMemcpyHostToDevice, s));
+        AUX_CUDA(cudaMemcpyAsync(v.p, A->values, sizeof(double) * nnz, cudaMemcpyHostToDevice, s));
+    }
+    // the reference's csr_spmv reads any CSR of the right order; reject only
+    // what would read out of bounds (sorted columns are not required)
+    {
+        int ends[2] = {0, 0};
+        AUX_CUDA(cudaMemcpyAsync(&ends[0], rp.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+        AUX_CUDA(cudaMemcpyAsync(&ends[1], rp.p + n, sizeof(int), cudaMemcpyDeviceToHost, s));
+        AUX_CUDA(cudaStreamSynchronize(s));
+        if (ends[0] != 0 || (long)ends[1] != nnz)
+            throw_aux(AUX_STRUCTURE_ERROR, "CSR row_ptr endpoints inconsistent with nnz");
+        DBuf<unsigned long long> err(1);
+        AUX_CUDA(cudaMemsetAsync(err.p, 0xff, sizeof(unsigned long long), s));
+        if (n > 0) {
+            k_validate<<<grid_for(n), kT, 0, s>>>(rp.p, col.p, (int)n, nnz, A->n_cols, err.p);
+            AUX_LAUNCHED(1);
+        }
+        const unsigned long long e = read1(err.p, s);
+        if (e != ~0ull && e % 4 != 3) {
+            const long r = (long)(e / 4);
+            if (e % 4 == 1) throw_aux(AUX_STRUCTURE_ERROR, "CSR row_ptr not nondecreasing at row " + std::to_string(r));
+            throw_aux(AUX_STRUCTURE_ERROR, "CSR column index out of range in row " + std::to_string(r));
+        }
+    }
+    Finest& F = h->fine;
+    h->o_rp.alloc(n + 1);
+    h->o_col.alloc(std::max<long>(nnz, 1));
+    h->o_v.alloc(std::max<long>(nnz, 1));
+    h->o_nnz = nnz;
+    if (h->direct_only) {   // rows in caller order
+        AUX_CUDA(cudaMemcpyAsync(h->o_rp.p, rp.p, sizeof(int) * (n + 1), cudaMemcpyDeviceToDevice, s));
+        if (nnz) {
+            AUX_CUDA(cudaMemcpyAsync(h->o_col.p, col.p, sizeof(int) * nnz, cudaMemcpyDeviceToDevice, s));
+            AUX_CUDA(cudaMemcpyAsync(h->o_v.p, v.p, sizeof(double) * nnz, cudaMemcpyDeviceToDevice, s));
+        }
+    } else {
+        DBuf<int> len(std::max<long>(n, 1));
+        k_perm_len<<<grid_for(n), kT, 0, s>>>(rp.p, F.perm.p, n, len.p);
+        AUX_LAUNCHED(1);
+        exclusive_scan(len.p, h->o_rp.p, n, s);
+        k_permute_csr<<<grid_for(n * 4), kT, 0, s>>>(rp.p, col.p, v.p, F.perm.p, F.iperm.p, n, h->o_rp.p,
+                                                      h->o_col.p, h->o_v.p);
+        AUX_LAUNCHED(1);
+    }
+    AUX_CUDA(cudaStreamSynchronize(s));   // the staging buffers go out of scope
+    h->outer = true;
+}
+
 void validate_input(aux_hierarchy* h, const aux_csr_view* A) {
     validate_structure(h, A);
     validate_values(h, A);

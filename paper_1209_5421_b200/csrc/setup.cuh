@@ -9,6 +9,13 @@ namespace auxb200 {
 // before the first use of the values.
 void setup_device(aux_hierarchy* h, const aux_csr_view* A, const double* xy, long n_points,
                   cudaEvent_t values_ready = nullptr);
+// Host-side sampled fingerprint of a CSR matrix (sizes, row_ptr and up to
+// 4096 evenly spaced column / value entries): detects a different matrix at the
+// setup matrix's addresses (freed and reallocated) without an O(nnz) pass.
+uint64_t csr_fingerprint(const aux_csr_view* A);
+// solve(A, ...) with a host matrix other than the setup one: upload, check,
+// permute into the finest row order (h->o_rp/o_col/o_v, h->outer = true).
+void set_outer_matrix(aux_hierarchy* h, const aux_csr_view* A);
 // PCG buffers of every coarse level for a given n_inner.
 void alloc_solve_levels(aux_hierarchy* h, int n_inner);
 // Device solve; b and u are device pointers in the caller's DoF order.

@@ -1717,7 +1717,11 @@ void solve_device(aux_hierarchy* h, const double* b, long n_b, const aux_cycle_o
         const bool vec_ok = (n % 2) == 0;   // device vectors are 256-byte aligned allocations
         double* r = h->w_r.p;
         double* u = h->w_u.p;
-        const double spmv_bytes = 12.0 * F.nnz + 4.0 * (n + 1) + 16.0 * n;
+        // the outer A z reads the caller's matrix (cycle.hpp:228): the setup
+        // copy, or the one solve(A, ...) uploaded (set_outer_matrix)
+        struct { const int* rp; const int* col; const double* v; long nnz; } OA{F.rp.p, F.col.p, F.v.p, F.nnz};
+        if (h->outer) OA = {h->o_rp.p, h->o_col.p, h->o_v.p, h->o_nnz};
+        const double spmv_bytes = 12.0 * OA.nnz + 4.0 * (n + 1) + 16.0 * n;
         g_trace.on = std::getenv("AUX_TRACE") != nullptr;
         g_trace.mark(s, 0);
         while (res->iterations < o->max_outer) {
@@ -1738,7 +1742,7 @@ void solve_device(aux_hierarchy* h, const double* b, long n_b, const aux_cycle_o
             {
                 const Route rs0 = route(c, fd, kept.empty() ? Fin{1, sc, nullptr, e_slot}
                                                              : Fin{2, sc, sc + 8 + kept[0], nullptr});
-                k_csr_spmv<<<red_blocks(n), kRedThreads, 0, s>>>(n, F.rp.p, F.col.p, F.v.p, p, ap, kept.empty() ? 0 : 1,
+                k_csr_spmv<<<red_blocks(n), kRedThreads, 0, s>>>(n, OA.rp, OA.col, OA.v, p, ap, kept.empty() ? 0 : 1,
                                                                 r, kept.empty() ? nullptr : h->w_ap[kept[0]].p, rs,
                                                                 rs0.launch);
                 AUX_LAUNCHED(1);
