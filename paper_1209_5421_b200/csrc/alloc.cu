@@ -1,6 +1,8 @@
 // alloc.cu — process-wide caching device allocator (see hier.cuh).
 #include <map>
 #include <mutex>
+#include <set>
+#include <tuple>
 
 #include "hier.cuh"
 
@@ -15,18 +17,27 @@ namespace {
 // before releasing its buffers).  The multi-part test transport drives one
 // part per thread, each on its own stream.
 std::mutex g_mu;   // guards cudaMalloc / cudaFree of the retry path
+// Blocks are keyed by (device, rounded size): a block is only handed to a
+// request on the device it was allocated on.
+using Key = std::pair<int, size_t>;
 struct Cache {
-    std::multimap<size_t, void*> m;   // rounded size -> cached block
+    std::multimap<Key, void*> m;   // (device, rounded size) -> cached block
     ~Cache() {   // thread exit: the blocks go back to the driver
         for (auto& kv : m) cudaFree(kv.second);
     }
-    auto find(size_t r) { return m.find(r); }
+    auto find(const Key& r) { return m.find(r); }
     auto end() { return m.end(); }
-    void erase(std::multimap<size_t, void*>::iterator it) { m.erase(it); }
-    void emplace(size_t r, void* p) { m.emplace(r, p); }
-    void clear() {
-        for (auto& kv : m) cudaFree(kv.second);
-        m.clear();
+    void erase(std::multimap<Key, void*>::iterator it) { m.erase(it); }
+    void emplace(const Key& r, void* p) { m.emplace(r, p); }
+    void clear(int dev) {   // the current device's blocks
+        for (auto it = m.begin(); it != m.end();) {
+            if (it->first.first == dev) {
+                cudaFree(it->second);
+                it = m.erase(it);
+            } else {
+                ++it;
+            }
+        }
     }
 };
 thread_local Cache g_free;
@@ -44,10 +55,17 @@ size_t round_size(size_t b) {
 
 }  // namespace
 
+int current_device() {
+    int d = 0;
+    if (cudaGetDevice(&d) != cudaSuccess) d = 0;
+    return d;
+}
+
 void* dev_alloc(size_t bytes) {
+    const int dev = current_device();
     const size_t r = round_size(bytes);
     {
-        auto it = g_free.find(r);
+        auto it = g_free.find(Key{dev, r});
         if (it != g_free.end()) {
             void* p = it->second;
             g_free.erase(it);
@@ -61,7 +79,7 @@ void* dev_alloc(size_t bytes) {
         (void)cudaGetLastError();
         std::lock_guard<std::mutex> lk(g_mu);
         cudaDeviceSynchronize();
-        g_free.clear();
+        g_free.clear(dev);
         e = cudaMalloc(&p, r);
     }
     if (e != cudaSuccess) throw_aux(AUX_CUDA_ERROR, std::string("cudaMalloc: ") + cudaGetErrorString(e));
@@ -70,7 +88,19 @@ void* dev_alloc(size_t bytes) {
 
 void dev_free(void* p, size_t bytes) {
     if (!p) return;
-    g_free.emplace(round_size(bytes), p);
+    cudaPointerAttributes at{};
+    const int dev = cudaPointerGetAttributes(&at, p) == cudaSuccess ? at.device : current_device();
+    g_free.emplace(Key{dev, round_size(bytes)}, p);
+}
+
+void ensure_smem_impl(const void* func, int bytes) {
+    static std::mutex mu;
+    static std::set<std::tuple<const void*, int, int>> done;
+    const int dev = current_device();
+    std::lock_guard<std::mutex> lk(mu);
+    if (done.count({func, dev, bytes})) return;
+    AUX_CUDA(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    done.insert({func, dev, bytes});
 }
 
 }  // namespace auxb200

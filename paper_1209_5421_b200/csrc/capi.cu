@@ -110,6 +110,7 @@ aux_status aux_setup_device(const aux_csr_view* A, const double* xy, int64_t n_p
     *out = nullptr;
     aux_hierarchy* h = nullptr;
     const aux_status st = guarded(msg, msg_len, [&] {
+        DeviceGuard dg(gpu ? gpu->device : 0);
         h = make_h(opts, gpu);
         const auto t0 = std::chrono::steady_clock::now();
         setup_device(h, A, xy, (long)n_points);
@@ -128,6 +129,7 @@ aux_status aux_setup(const aux_csr_view* A, const double* xy, int64_t n_points, 
     *out = nullptr;
     aux_hierarchy* h = nullptr;
     const aux_status st = guarded(msg, msg_len, [&] {
+        DeviceGuard dg(gpu ? gpu->device : 0);
         h = make_h(opts, gpu);
         const auto t0 = std::chrono::steady_clock::now();
         if (A->n_rows < 0 || A->nnz < 0) throw_aux(AUX_SIZE_ERROR, "setup_hierarchy: negative size");
@@ -188,7 +190,7 @@ void aux_local_group_destroy(void* g) { local_group_destroy(static_cast<LocalGro
 int32_t aux_nccl_unique_id(uint8_t id[128]) { return nccl_unique_id(id) ? 1 : 0; }
 void* aux_comm_create_nccl(const uint8_t id[128], int32_t nranks, int32_t rank, int32_t device) {
     try {
-        AUX_CUDA(cudaSetDevice(device));
+        DeviceGuard dg(device);
         return make_nccl_comm(id, nranks, rank);
     } catch (...) {
         return nullptr;
@@ -204,13 +206,18 @@ static aux_status setup_dist_impl(const aux_csr_view* A, const double* xy, int64
     const aux_status st = guarded(msg, msg_len, [&] {
         if (!d || d->nparts < 1 || d->rank < 0 || d->rank >= d->nparts)
             throw_aux(AUX_ARGUMENT_ERROR, "aux_dist_opts: bad part count or rank");
+        if (d->transport < 0 || d->transport > 2)
+            throw_aux(AUX_ARGUMENT_ERROR, "aux_dist_opts: transport must be 0 (local), 1 (NCCL id) or 2 (communicator)");
+        DeviceGuard dg(gpu ? gpu->device : 0);
         h = make_h(opts, gpu);
         const auto t0 = std::chrono::steady_clock::now();
         if (d->transport == 0) {
-            if (!d->local_group) throw_aux(AUX_ARGUMENT_ERROR, "aux_dist_opts: local transport needs a group");
+            if (!d->local_group || !is_local_group(d->local_group))
+                throw_aux(AUX_ARGUMENT_ERROR, "aux_dist_opts: local transport needs a group (aux_local_group_create)");
             h->dist.comm = make_local_comm(static_cast<LocalGroup*>(d->local_group), d->rank);
         } else if (d->transport == 2) {
-            if (!d->local_group) throw_aux(AUX_ARGUMENT_ERROR, "aux_dist_opts: transport 2 needs a communicator");
+            if (!d->local_group || !is_comm(d->local_group))
+                throw_aux(AUX_ARGUMENT_ERROR, "aux_dist_opts: transport 2 needs a communicator (aux_comm_create_nccl)");
             h->dist.comm = static_cast<Comm*>(d->local_group);
             h->dist.owns_comm = false;
             if (h->dist.comm->size != d->nparts || h->dist.comm->rank != d->rank)
@@ -267,6 +274,7 @@ aux_status aux_setup_dist_device(const aux_csr_view* A, const double* xy, int64_
 int32_t aux_part_rows(const aux_hierarchy* h) { return h->fine.n; }
 aux_status aux_part_dofs(const aux_hierarchy* h, int32_t* ids) {
     return guarded(nullptr, 0, [&] {
+        DeviceGuard dg(h->gpu.device);
         const int32_t* src = h->dist.comm ? h->dist.gid.p : h->fine.perm.p;
         AUX_CUDA(cudaMemcpy(ids, src, sizeof(int32_t) * h->fine.n, cudaMemcpyDeviceToHost));
     });
@@ -275,6 +283,7 @@ aux_status aux_part_dofs(const aux_hierarchy* h, int32_t* ids) {
 aux_status aux_solve(aux_hierarchy* h, const aux_csr_view* A, const double* b, int64_t n_b,
                      const aux_cycle_opts* opts, aux_solve_result* res, char* msg, size_t msg_len) {
     return guarded(msg, msg_len, [&] {
+        DeviceGuard dg(h->gpu.device);
         const auto t0 = std::chrono::steady_clock::now();
         aux_cycle_opts o;
         aux_default_cycle_opts(&o);
@@ -324,6 +333,7 @@ aux_status aux_solve(aux_hierarchy* h, const aux_csr_view* A, const double* b, i
 aux_status aux_solve_device(aux_hierarchy* h, const double* b, int64_t n_b, const aux_cycle_opts* opts,
                             aux_solve_result* res, char* msg, size_t msg_len) {
     return guarded(msg, msg_len, [&] {
+        DeviceGuard dg(h->gpu.device);
         aux_cycle_opts o;
         aux_default_cycle_opts(&o);
         if (opts) o = *opts;
@@ -360,23 +370,38 @@ int32_t aux_n_levels(const aux_hierarchy* h) { return (int32_t)h->lv.size(); }
 
 aux_status aux_level_info_get(const aux_hierarchy* h, int32_t level, aux_level_info* out) {
     if (level < 0 || level >= (int)h->lv.size()) return AUX_ARGUMENT_ERROR;
-    return guarded(nullptr, 0, [&] { level_info(h, level, out); });
+    return guarded(nullptr, 0, [&] {
+        DeviceGuard dg(h->gpu.device);
+        level_info(h, level, out);
+    });
 }
 
 aux_status aux_export_level(const aux_hierarchy* h, int32_t level, aux_level_export* out) {
     if (level < 0 || level >= (int)h->lv.size() || h->dist.comm) return AUX_ARGUMENT_ERROR;
-    return guarded(nullptr, 0, [&] { export_level(h, level, out); });
+    return guarded(nullptr, 0, [&] {
+        DeviceGuard dg(h->gpu.device);
+        export_level(h, level, out);
+    });
 }
 
 aux_status aux_export_coarsest(const aux_hierarchy* h, int32_t* n, double* lu, int32_t* perm) {
     return guarded(nullptr, 0, [&] {
+        DeviceGuard dg(h->gpu.device);
         int nn = 0;
         export_coarsest(h, &nn, lu, perm);
         *n = nn;
     });
 }
 
-void aux_destroy(aux_hierarchy* h) { delete h; }
+void aux_destroy(aux_hierarchy* h) {
+    if (!h) return;
+    const int dev = h->gpu.device;   // the buffers and the stream live there
+    int prev = -1;
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) cudaSetDevice(dev);
+    delete h;
+    if (prev >= 0 && prev != dev) cudaSetDevice(prev);
+}
 
 int64_t aux_launch_count(void) { return g_launches; }
 
@@ -396,6 +421,7 @@ aux_status aux_profile_read(const aux_hierarchy* hc, int32_t kind, int64_t* laun
     if (kind < 0 || kind >= kProfKinds) return AUX_ARGUMENT_ERROR;
     auto* h = const_cast<aux_hierarchy*>(hc);
     return guarded(nullptr, 0, [&] {
+        DeviceGuard dg(h->gpu.device);
         AUX_CUDA(cudaStreamSynchronize(h->stream));
         Profile& P = h->prof;
         double ms = 0.0;

@@ -7,6 +7,9 @@
 #include <mutex>
 #include <string>
 
+#include <mutex>
+#include <set>
+
 #include "comm.cuh"
 #include "hier.cuh"
 
@@ -76,11 +79,42 @@ struct LocalGroup {
     }
 };
 
+namespace {
+std::mutex g_reg_mu;
+std::set<const void*> g_groups, g_comms;
+}  // namespace
+
+bool is_local_group(const void* p) {
+    std::lock_guard<std::mutex> lk(g_reg_mu);
+    return g_groups.count(p) != 0;
+}
+bool is_comm(const void* p) {
+    std::lock_guard<std::mutex> lk(g_reg_mu);
+    return g_comms.count(p) != 0;
+}
+Comm::Comm() {
+    std::lock_guard<std::mutex> lk(g_reg_mu);
+    g_comms.insert(this);
+}
+Comm::~Comm() {
+    std::lock_guard<std::mutex> lk(g_reg_mu);
+    g_comms.erase(this);
+}
+
 LocalGroup* local_group_create(int parts) {
     if (parts < 1 || parts > 64) throw_aux(AUX_ARGUMENT_ERROR, "local group: 1..64 parts");
-    return new LocalGroup(parts);
+    LocalGroup* g = new LocalGroup(parts);
+    std::lock_guard<std::mutex> lk(g_reg_mu);
+    g_groups.insert(g);
+    return g;
 }
-void local_group_destroy(LocalGroup* g) { delete g; }
+void local_group_destroy(LocalGroup* g) {
+    {
+        std::lock_guard<std::mutex> lk(g_reg_mu);
+        g_groups.erase(g);
+    }
+    delete g;
+}
 
 namespace {
 

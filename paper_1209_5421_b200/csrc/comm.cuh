@@ -28,7 +28,8 @@ struct Msg {
 struct Comm {
     int rank = 0, size = 1;
     bool peers_warm = false;   // the coarse cycle's peer connections exist (solve.cu build_graph)
-    virtual ~Comm() {}
+    Comm();
+    virtual ~Comm();
     // in-place element-wise sum over all parts (device doubles)
     virtual void allreduce_sum(double* buf, int count, cudaStream_t s) = 0;
     // in-place element-wise max over all parts (device uint64)
@@ -46,6 +47,11 @@ struct LocalGroup;
 LocalGroup* local_group_create(int parts);
 void local_group_destroy(LocalGroup* g);
 Comm* make_local_comm(LocalGroup* g, int rank);
+
+// Handle checks of the C ABI's void* transport argument (aux_dist_opts):
+// registries of live groups / communicators, no dereference of the pointer.
+bool is_local_group(const void* p);
+bool is_comm(const void* p);
 
 // NCCL (one process per GPU).
 bool nccl_unique_id(unsigned char id[128]);

@@ -59,6 +59,29 @@ struct AuxError : std::runtime_error {
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// The dynamic shared-memory limit of a kernel is a per-device attribute: set
+// it once per (kernel, device, size) on the current device.
+void ensure_smem_impl(const void* func, int bytes);
+template <class K>
+inline void ensure_smem(K* kernel, size_t bytes) {
+    ensure_smem_impl(reinterpret_cast<const void*>(kernel), (int)bytes);
+}
+
+// Scoped current device: entry points that take a hierarchy run on its device
+// and restore the caller's afterwards.
+struct DeviceGuard {
+    int prev = -1, dev = -1;
+    explicit DeviceGuard(int d) : dev(d) {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        if (prev != d) AUX_CUDA(cudaSetDevice(d));
+    }
+    ~DeviceGuard() {
+        if (prev >= 0 && prev != dev) cudaSetDevice(prev);
+    }
+    DeviceGuard(const DeviceGuard&) = delete;
+    DeviceGuard& operator=(const DeviceGuard&) = delete;
+};
+
 // Host-side kernel launch counter (bench.py's gpu_launches).
 extern std::atomic<int64_t> g_launches;
 #define AUX_LAUNCHED(n) (::auxb200::g_launches += (n))

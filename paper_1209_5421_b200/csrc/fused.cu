@@ -1270,11 +1270,7 @@ bool cluster_layout(const aux_hierarchy* h, int m, const FusedArgs& fa, ClusterA
 }
 
 void launch_cluster_pcg(const ClusterArgs& a, cudaStream_t s) {
-    static bool attr_set = false;
-    if (!attr_set) {
-        AUX_CUDA(cudaFuncSetAttribute(k_cluster_pcg, cudaFuncAttributeMaxDynamicSharedMemorySize, kFusedSmemMax));
-        attr_set = true;
-    }
+    ensure_smem(k_cluster_pcg, kFusedSmemMax);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(kClusterCtas);
     cfg.blockDim = dim3(kThreads);
@@ -1294,11 +1290,7 @@ void launch_cluster_pcg(const ClusterArgs& a, cudaStream_t s) {
 }
 
 void launch_fused_pcg(const FusedArgs& a, cudaStream_t s) {
-    static bool attr_set = false;
-    if (!attr_set) {
-        AUX_CUDA(cudaFuncSetAttribute(k_fused_pcg, cudaFuncAttributeMaxDynamicSharedMemorySize, kFusedSmemMax));
-        attr_set = true;
-    }
+    ensure_smem(k_fused_pcg, kFusedSmemMax);
     launch_pdl(k_fused_pcg, dim3(1), dim3(kThreads), a.smem_bytes, s, a);
 }
 

@@ -994,12 +994,7 @@ void factor_coarsest(aux_hierarchy* h) {
     h->c_inv.alloc((size_t)nc * nc);
     if (nc <= 112) {   // factors (odd leading dimension) + inverse columns in shared memory
         const size_t sm = ((size_t)nc * (nc | 1) + (size_t)nc * nc) * sizeof(double);
-        static bool attr = false;
-        if (!attr) {
-            AUX_CUDA(cudaFuncSetAttribute(k_coarse_lu_inv_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          225 * 1024));
-            attr = true;
-        }
+        ensure_smem(k_coarse_lu_inv_smem, 225 * 1024);
         k_coarse_lu_inv_smem<<<1, 256, sm, s>>>(h->c_lu.p, h->c_perm.p, nc, zc.p, h->c_lex.p, work.p);
         AUX_LAUNCHED(1);
     } else {
@@ -1155,12 +1150,7 @@ void finest_blocks(aux_hierarchy* h, const Geo& gL, unsigned long long& sing, in
                 const size_t x_b = (size_t)mid_max * mid_max * sizeof(double);
                 const int x_smem = (h->gpu.block_solve == 0 && lu_b + x_b <= kMaxDyn) ? 1 : 0;
                 const size_t sm = lu_b + (x_smem ? x_b : 0);
-                static bool attr = false;
-                if (!attr) {
-                    AUX_CUDA(cudaFuncSetAttribute(k_factor_cta_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                  (int)kMaxDyn));
-                    attr = true;
-                }
+                ensure_smem(k_factor_cta_smem, (int)kMaxDyn);
                 k_factor_cta_smem<<<(unsigned)mid.size(), 256, sm, s>>>(
                     mid_d.p, F.bptr.p, F.rp.p, F.col.p, F.v.p, gL, F.cell_lu_off.p, F.big_lu.p, F.big_perm.p, err.p,
                     h->gpu.block_solve == 0 ? F.inv_off.p : nullptr, h->gpu.block_solve == 0 ? F.inv.p : nullptr, x_smem);

@@ -1304,11 +1304,7 @@ void finest_bgs_pass(Ctx& c, int color, const double* f, double* u, bool zero, d
         }
         if (j1 > jh) {
             const size_t need = (size_t)F.max_block * sizeof(double);
-            static bool attr = false;
-            if (!attr) {
-                AUX_CUDA(cudaFuncSetAttribute(k_bgs_inv_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-                attr = true;
-            }
+            ensure_smem(k_bgs_inv_cta, 200 * 1024);
             if (need > (size_t)200 * 1024) throw_aux(AUX_CAPACITY_ERROR, "block too large for the inverse smoother");
             k_bgs_inv_cta<<<(unsigned)(j1 - jh), 256, need, c.s>>>(F.rp.p, F.col.p, F.v.p, f, F.inv.p, F.big_ids.p,
                                                                   F.bptr.p, F.inv_off.p, xin, u, jh, z);
@@ -1336,11 +1332,7 @@ void finest_bgs_pass(Ctx& c, int color, const double* f, double* u, bool zero, d
     }
     if (j1 > jc) {   // more than 32 members: CTA per block
         const size_t need = ((size_t)F.max_block * F.max_block + F.max_block) * sizeof(double);
-        static bool attr = false;
-        if (!attr) {
-            AUX_CUDA(cudaFuncSetAttribute(k_bgs_cta<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-            attr = true;
-        }
+        ensure_smem(k_bgs_cta<true>, 200 * 1024);
         if (need <= (size_t)200 * 1024)
             k_bgs_cta<true><<<(unsigned)(j1 - jc), 128, need, c.s>>>(F.big_ids.p, F.cell_lu_off.p, F.big_lu.p,
                                                                      F.big_perm.p, F.bptr.p, res, xin, u,
@@ -1418,7 +1410,11 @@ void build_graph(aux_hierarchy* h, const aux_cycle_opts& o, RedState rs) {
         h->graph_valid = false;   // in-process parts synchronise through host barriers: no capture
         return;
     }
-    if (h->graph_valid && std::memcmp(&h->graph_opts, &o, sizeof o) == 0) return;
+    // the captured coarse cycle depends only on the inner-step and sweep counts
+    // (rtol, max_outer and max_directions act on the outer loop)
+    if (h->graph_valid && h->graph_opts.n_inner == o.n_inner && h->graph_opts.pre_sweeps == o.pre_sweeps &&
+        h->graph_opts.post_sweeps == o.post_sweeps)
+        return;
     if (h->graph) {
         cudaGraphExecDestroy(h->graph);
         h->graph = nullptr;

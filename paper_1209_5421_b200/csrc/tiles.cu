@@ -416,10 +416,6 @@ __global__ void __launch_bounds__(kTT) k_tile_up(const __grid_constant__ TileUp 
     if (grid_reduce<2>(v, rs, out) && threadIdx.x == 0) finalize(fin, out);
 }
 
-template <class K>
-void set_smem(K kernel, size_t bytes) {
-    AUX_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-}
 
 // ---- host: tensor maps of the colour-major level arrays
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -453,11 +449,7 @@ bool tiles_supported(int w, int pre, int post) { return w >= 16 && pre >= 1 && p
 
 template <int T, int H>
 static void down_t(TileDown& a, int ntiles, cudaStream_t s) {
-    static bool init = false;
-    if (!init) {
-        set_smem(k_tile_down<T, H>, Tile<T, H, false>::bytes);
-        init = true;
-    }
+    ensure_smem(k_tile_down<T, H>, Tile<T, H, false>::bytes);
     using L = Tile<T, H, false>;
     encode_level_map(&a.m_val, a.val, a.g, L::PAI, L::PBI, true);
     encode_level_map(&a.m_r, a.r_in, a.g, L::PAI, L::PBI, false);
@@ -467,11 +459,7 @@ static void down_t(TileDown& a, int ntiles, cudaStream_t s) {
 
 template <int T, int H>
 static void up_t(TileUp& a, int ntiles, RedState rs, Fin fin, cudaStream_t s) {
-    static bool init = false;
-    if (!init) {
-        set_smem(k_tile_up<T, H>, Tile<T, H, true>::bytes);
-        init = true;
-    }
+    ensure_smem(k_tile_up<T, H>, Tile<T, H, true>::bytes);
     using L = Tile<T, H, true>;
     encode_level_map(&a.m_val, a.val, a.g, L::PAI, L::PBI, true);
     encode_level_map(&a.m_f, a.f, a.g, L::PAI, L::PBI, false);

@@ -63,3 +63,23 @@ def test_no_gpu_setup_fails_loudly():
     s = problems.poisson5(10)
     with pytest.raises(api.AuxamgError):
         api.setup_hierarchy(s.A, s.coords)
+
+
+def test_dist_transport_validated_before_any_device_work():
+    """aux_dist_opts.transport outside {0, 1, 2} is an argument_error (no
+    device work: this runs without a GPU)."""
+    import ctypes as C
+    import numpy as np
+    from paper_1209_5421_b200 import _abi, api
+    rp = np.array([0, 1], np.int32)
+    ci = np.array([0], np.int32)
+    va = np.array([1.0])
+    xy = np.zeros(2)
+    v = _abi.CsrView(1, 1, 1, rp.ctypes.data, ci.ctypes.data, va.ctypes.data)
+    d = _abi.DistOpts()
+    d.nparts, d.rank, d.transport = 1, 0, 7
+    h = C.c_void_p()
+    msg = C.create_string_buffer(256)
+    st = api.lib().aux_setup_dist(C.byref(v), xy.ctypes.data, 1, None, None, C.byref(d), C.byref(h), msg, 256)
+    assert _abi.STATUS_TO_EXC[st] is _abi.ArgumentError, (st, msg.value)
+    assert b"transport" in msg.value
