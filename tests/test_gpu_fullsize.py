@@ -1,16 +1,31 @@
-"""BASELINE.json full-size configurations on the GPU, checked through
-size-independent properties (the oracle takes minutes at these sizes):
-the true residual ||b - A u|| / ||b|| recomputed on the host in float64
-meets rtol, the iteration counts match the reference's (SURVEY 8(c) goldens,
-measured with the reference itself), setup statistics match the survey's,
-and the two finest-smoother modes agree."""
+"""BASELINE.json full-size configurations on the GPU against the reference
+itself (oracle/_ref: the unmodified reference headers compiled in place, run
+with every host thread -- its results are bitwise independent of the thread
+count, parallel.hpp:1-9), on inputs byte-identical to the reference's own
+generators (tests/test_generators.py):
+
+  C1 jittered P1 n=1025, C2 graded_mesh(2049,1.3), C3 jittered P1 n=4097,
+  C4 jump 1e3 on the C3 mesh, C5 5-point n=4097 (the weak-scaling base).
+
+Per configuration: every exported hierarchy field bitwise (aggregation maps,
+member lists, active flags, colourings, every level's stencil pattern and
+values, block and coarsest LU factors, statistics / operator complexity),
+iterations within +-1 of the reference (and of SURVEY 8(c)'s goldens),
+||u - u_ref||_inf / ||u_ref||_inf <= 1e-12, and the true residual recomputed
+on the host meets rtol."""
+import os
+
 import numpy as np
 import pytest
 import scipy.sparse as sp
 
+import bindings as ob
 from paper_1209_5421_b200 import problems
+from test_gpu_parity import compare_exports
 
 pytestmark = [pytest.mark.gpu, pytest.mark.timeout(900)]
+
+U_TOL = 1e-12
 
 
 def _true_rel_residual(s, u):
@@ -18,21 +33,42 @@ def _true_rel_residual(s, u):
     return np.linalg.norm(s.b - A @ u) / np.linalg.norm(s.b)
 
 
-@pytest.mark.parametrize("name,make,iters,opcx", [
-    # graded(2049,1.3) -> 25 iterations, opcx 1.4280; jittered n=1025 -> 12, 1.4274
-    ("C2_graded_2049", lambda: problems.graded_p1(2049, 1.3), 25, 1.4280),
-    ("C1_jitter_1025", lambda: problems.jittered_p1(1025), 12, 1.4274),
-])
-def test_full_size_solve(gpu_api, name, make, iters, opcx):
+# name: (generator, SURVEY 8(c) golden iterations, golden operator complexity)
+FULL = {
+    "C1_jitter_1025": (lambda: problems.jittered_p1(1025), 12, 1.4274),
+    "C2_graded_2049": (lambda: problems.graded_p1(2049, 1.3), 25, 1.4280),
+    "C3_jitter_4097": (lambda: problems.jittered_p1(4097), 13, 1.4283),
+    "C4_jump1e3_4097": (lambda: problems.jittered_p1(4097, jump=1e3), 34, None),
+    "C5_poisson5_4097": (lambda: problems.poisson5(4097), 12, 1.5995),
+}
+
+
+@pytest.mark.skipif(not ob.available("ref"), reason="oracle/_ref not built")
+@pytest.mark.parametrize("name", list(FULL))
+def test_full_size_reference_parity(gpu_api, name):
+    make, golden_iters, golden_opcx = FULL[name]
     s = make()
+    ob.set_ref_threads(os.cpu_count() or 1)
+    ref = ob.CpuHierarchy("ref", s.A, s.coords)
+    rr = ref.solve(s.b)
     h = gpu_api.setup_hierarchy(s.A, s.coords)
-    st = h.stats()
-    assert round(st.operator_complexity, 4) == opcx
     r = gpu_api.solve(s.A, s.b, h)
-    assert r.converged and abs(r.iterations - iters) <= 1, r.iterations
+    # setup: every exported field bitwise
+    eo = ref.export()
+    del ref
+    eg = h.export()
+    compare_exports(eg, eo, exact_values=True)
+    if golden_opcx is not None:
+        assert round(eg["stats"]["operator_complexity"], 4) == golden_opcx
+    del eg, eo
+    # solve
+    assert r.converged and rr["converged"]
+    assert abs(r.iterations - rr["iterations"]) <= 1, (r.iterations, rr["iterations"])
+    assert abs(rr["iterations"] - golden_iters) <= 1, rr["iterations"]
+    err = np.max(np.abs(r.u - rr["u"])) / np.max(np.abs(rr["u"]))
+    assert err <= U_TOL, err
     assert _true_rel_residual(s, r.u) <= 1.0e-6 * (1 + 1e-9)
-    hist = np.array(r.residual_history)
-    assert hist[-1] <= 1e-6 * hist[0]
+    print(f"{name}: N={s.A.n_rows} iterations gpu={r.iterations} ref={rr['iterations']} max rel du={err:.2e}")
 
 
 def test_full_size_modes_agree():
@@ -45,16 +81,6 @@ def test_full_size_modes_agree():
         us.append((r.iterations, r.u))
     assert us[0][0] == us[1][0]
     assert np.max(np.abs(us[0][1] - us[1][1])) / np.max(np.abs(us[1][1])) <= 1e-12
-
-
-def test_c3_16m(gpu_api):
-    """C3: jittered P1, N = 16,777,216 (13 iterations, opcx 1.4283)."""
-    s = problems.jittered_p1(4097)
-    h = gpu_api.setup_hierarchy(s.A, s.coords)
-    assert round(h.stats().operator_complexity, 4) == 1.4283
-    r = gpu_api.solve(s.A, s.b, h)
-    assert r.converged and abs(r.iterations - 13) <= 1, r.iterations
-    assert _true_rel_residual(s, r.u) <= 1.0e-6 * (1 + 1e-9)
 
 
 @pytest.mark.parametrize("opts", [dict(cluster_tier=False), dict(fused_max_cells=256), dict(fused_max_cells=64),
@@ -70,20 +96,3 @@ def test_full_size_tiers_agree(opts):
     r = api.solve(s.A, s.b, api.setup_hierarchy(s.A, s.coords, gpu=api.GpuOptions(**opts)))
     assert r.iterations == ref.iterations
     assert np.max(np.abs(r.u - ref.u)) / np.max(np.abs(ref.u)) <= 1e-12
-
-
-@pytest.mark.parametrize("name,make", [
-    ("C2_graded_2049", lambda: problems.graded_p1(2049, 1.3)),
-    ("C1_jitter_1025", lambda: problems.jittered_p1(1025)),
-])
-def test_full_size_oracle_parity(name, make):
-    """The headline configuration at full size against the oracle itself
-    (~20 s of single-threaded C at C2): same iterations, solution within the
-    parity bar (measured 6e-14 at C2)."""
-    import bindings as ob
-    from paper_1209_5421_b200 import api
-    s = make()
-    ref = ob.CpuHierarchy("oracle", s.A, s.coords).solve(s.b)
-    r = api.solve(s.A, s.b, api.setup_hierarchy(s.A, s.coords))
-    assert abs(r.iterations - ref["iterations"]) <= 1
-    assert np.max(np.abs(r.u - ref["u"])) / np.max(np.abs(ref["u"])) <= 1e-12
