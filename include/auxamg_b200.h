@@ -96,7 +96,9 @@ typedef struct aux_gpu_opts {
                                  0 = one kernel per colour pass / phase */
     int32_t cluster_tier;     /* the 64x64-cell level above a 32x32 single-CTA tier runs with
                                  that tier in one 5-CTA thread-block cluster (1, default) */
-    int32_t reserved;
+    int32_t stream_min_width; /* structured levels whose owned rectangle is at least this many
+                                 cells wide run the row-wavefront kernels (stream.cu) instead of
+                                 the overlapped tiles; 0 = default (1024), -1 = off */
 } aux_gpu_opts;
 
 /* auxamg::LocalityReport, hierarchy.hpp:37-44. */
@@ -260,6 +262,27 @@ void aux_system_destroy(aux_system* s);
  * arbitrary partition agg_of (n_rows entries, ids in [0, n_agg)) into the
  * caller's n_agg x n_agg row-major C, every element summed in the reference's
  * order (bitwise).  size_error if the map does not match the matrix. */
+/* ---- file readers, host code, multithreaded parse:
+ *   aux_read_matrix_market  <- read_matrix_market   matrix_market.hpp:33-104
+ *   aux_read_mesh           <- read_mesh            problems.hpp:201-310 (+ element_geometry checks)
+ *   aux_read_coords         <- read_coords          problems.hpp:313-330
+ *   aux_write_matrix_market <- write_matrix_market  matrix_market.hpp:106-120
+ * threads <= 0: all hardware threads.  io_error / parse_error (message ends in
+ * "(line N)", as parse_error::what()) / geometry_error as in the reference.
+ * aux_file_data_sizes: CSR (n_rows, n_cols, nnz); mesh (nodes, triangles,
+ * boundary nodes); coords (points, 0, 0).  aux_file_data_copy: CSR (row_ptr
+ * int32[n_rows+1], col_idx int32[nnz], values double[nnz]); mesh (nodes double
+ * [2 nodes] xy interleaved, triangles int32[3 triangles], boundary int32[]);
+ * coords (double[2 points]). */
+typedef struct aux_file_data aux_file_data;
+aux_status aux_read_matrix_market(const char* path, int32_t threads, aux_file_data** out, char* msg, size_t msg_len);
+aux_status aux_read_mesh(const char* path, int32_t threads, aux_file_data** out, char* msg, size_t msg_len);
+aux_status aux_read_coords(const char* path, int32_t threads, aux_file_data** out, char* msg, size_t msg_len);
+aux_status aux_file_data_sizes(const aux_file_data* d, int64_t* a, int64_t* b, int64_t* c);
+aux_status aux_file_data_copy(const aux_file_data* d, void* p0, void* p1, void* p2);
+void aux_file_data_destroy(aux_file_data* d);
+aux_status aux_write_matrix_market(const aux_csr_view* A, const char* path, char* msg, size_t msg_len);
+
 aux_status aux_galerkin_dense(const aux_csr_view* A, const int32_t* agg_of, int64_t n_agg_of, int32_t n_agg,
                               int32_t device, double* C, char* msg, size_t msg_len);
 

@@ -265,3 +265,88 @@ def ref_random_vector(n: int, seed: int, lo: float = -1.0, hi: float = 1.0):
     out = np.zeros(n, np.float64)
     _gen_lib().ref_gen_random_vector(n, seed, lo, hi, out.ctypes.data)
     return out
+
+
+# ---- the reference's file readers (matrix_market.hpp, problems.hpp:201-330) via ref_shim.cpp
+def _io_lib():
+    lib = _gen_lib()
+    if not getattr(lib, "_io_typed", False):
+        for f in ("ref_read_matrix_market", "ref_read_mesh"):
+            getattr(lib, f).argtypes = [C.c_char_p, C.POINTER(C.c_void_p), C.c_char_p, C.c_size_t]
+            getattr(lib, f).restype = C.c_int
+        lib.ref_read_coords.argtypes = [C.c_char_p, C.POINTER(C.c_void_p), C.POINTER(C.c_int64), C.c_char_p, C.c_size_t]
+        lib.ref_read_coords.restype = C.c_int
+        lib.ref_write_matrix_market.argtypes = [C.c_void_p, C.c_char_p, C.c_char_p, C.c_size_t]
+        lib.ref_write_matrix_market.restype = C.c_int
+        lib.ref_gen_ncols.argtypes = [C.c_void_p]
+        lib.ref_gen_ncols.restype = C.c_int
+        lib._io_typed = True
+    return lib
+
+
+def _ref_status(st, msg):
+    """(status, what()) of a reference call; status 0 = no exception."""
+    return st, msg.value.decode(errors="replace")
+
+
+def ref_read_matrix_market(path: str):
+    """(status, message, CsrMatrix or None) from auxamg::read_matrix_market."""
+    from paper_1209_5421_b200 import problems as P
+    lib = _io_lib()
+    h, msg = C.c_void_p(), C.create_string_buffer(512)
+    st = lib.ref_read_matrix_market(path.encode(), C.byref(h), msg, 512)
+    if st:
+        return st, msg.value.decode(errors="replace"), None
+    try:
+        n, m, nnz = lib.ref_gen_n(h), lib.ref_gen_ncols(h), lib.ref_gen_nnz(h)
+        A = P.CsrMatrix(n, m, _arr(lib.ref_gen_row_ptr(h), n + 1, np.int32), _arr(lib.ref_gen_col_idx(h), nnz, np.int32),
+                        _arr(lib.ref_gen_values(h), nnz, np.float64))
+        return 0, "", A
+    finally:
+        lib.ref_gen_free(h)
+
+
+def ref_read_mesh(path: str):
+    """(status, message, TriMesh or None) from auxamg::read_mesh."""
+    from paper_1209_5421_b200 import problems as P
+    lib = _io_lib()
+    h, msg = C.c_void_p(), C.create_string_buffer(512)
+    st = lib.ref_read_mesh(path.encode(), C.byref(h), msg, 512)
+    if st:
+        return st, msg.value.decode(errors="replace"), None
+    try:
+        M, T, B = lib.ref_gen_mesh_nodes(h), lib.ref_gen_mesh_tris(h), lib.ref_gen_mesh_nboundary(h)
+        nodes, tris, bnd = np.zeros((M, 2)), np.zeros((T, 3), np.int32), np.zeros(max(B, 1), np.int32)
+        lib.ref_gen_mesh_copy(h, nodes.ctypes.data, tris.ctypes.data, bnd.ctypes.data)
+        return 0, "", P.TriMesh(nodes, tris, bnd[:B])
+    finally:
+        lib.ref_gen_free(h)
+
+
+def ref_read_coords(path: str):
+    """(status, message, (N, 2) array or None) from auxamg::read_coords."""
+    lib = _io_lib()
+    h, msg, n = C.c_void_p(), C.create_string_buffer(512), C.c_int64()
+    st = lib.ref_read_coords(path.encode(), C.byref(h), C.byref(n), msg, 512)
+    if st:
+        return st, msg.value.decode(errors="replace"), None
+    try:
+        return 0, "", _arr(lib.ref_gen_xy(h), 2 * n.value, np.float64).reshape(n.value, 2)
+    finally:
+        lib.ref_gen_free(h)
+
+
+def ref_write_matrix_market(A, path: str) -> None:
+    lib = _io_lib()
+    rp = np.ascontiguousarray(A.row_ptr, np.int32)
+    ci = np.ascontiguousarray(A.col_idx, np.int32)
+    va = np.ascontiguousarray(A.values, np.float64)
+
+    class _View(C.Structure):
+        _fields_ = [("n_rows", C.c_int32), ("n_cols", C.c_int32), ("nnz", C.c_int64),
+                    ("row_ptr", C.c_void_p), ("col_idx", C.c_void_p), ("values", C.c_void_p)]
+    v = _View(A.n_rows, A.n_cols, int(va.size), rp.ctypes.data, ci.ctypes.data, va.ctypes.data)
+    msg = C.create_string_buffer(512)
+    st = lib.ref_write_matrix_market(C.byref(v), path.encode(), msg, 512)
+    if st:
+        raise OSError(msg.value.decode())

@@ -380,4 +380,43 @@ int ref_galerkin_dense(const aux_csr_view* Av, const int32_t* agg_of, int64_t n_
     });
 }
 
+// ---- the reference's file readers (matrix_market.hpp:33-120, problems.hpp:201-330):
+// results in a RefGen (CSR in sys.A, mesh in mesh, points in xy)
+int ref_read_matrix_market(const char* path, void** out, char* msg, size_t len) {
+    *out = nullptr;
+    auto* g = new RefGen;
+    const int st = guarded(msg, len, [&] { g->sys.A = auxamg::read_matrix_market(path); });
+    if (st != AUX_OK) delete g;
+    else *out = g;
+    return st;
+}
+int ref_gen_ncols(void* p) { return static_cast<RefGen*>(p)->sys.A.n_cols; }
+int ref_read_mesh(const char* path, void** out, char* msg, size_t len) {
+    *out = nullptr;
+    auto* g = new RefGen;
+    const int st = guarded(msg, len, [&] { g->mesh = auxamg::read_mesh(path); });
+    if (st != AUX_OK) delete g;
+    else *out = g;
+    return st;
+}
+int ref_read_coords(const char* path, void** out, int64_t* n, char* msg, size_t len) {
+    *out = nullptr;
+    auto* g = new RefGen;
+    const int st = guarded(msg, len, [&] {
+        const std::vector<auxamg::Point> pts = auxamg::read_coords(path);
+        g->xy.resize(2 * pts.size());
+        for (std::size_t i = 0; i < pts.size(); ++i) {
+            g->xy[2 * i] = pts[i].x;
+            g->xy[2 * i + 1] = pts[i].y;
+        }
+        *n = (int64_t)pts.size();
+    });
+    if (st != AUX_OK) delete g;
+    else *out = g;
+    return st;
+}
+int ref_write_matrix_market(const aux_csr_view* Av, const char* path, char* msg, size_t len) {
+    return guarded(msg, len, [&] { auxamg::write_matrix_market(to_csr(Av), path); });
+}
+
 }  // extern "C"

@@ -48,7 +48,13 @@ class IoError(AuxamgError):
 
 
 class ParseError(AuxamgError):
-    """auxamg::parse_error (errors.hpp:67-76)."""
+    """auxamg::parse_error (errors.hpp:67-76); .line is the 1-based line number."""
+
+    @property
+    def line(self) -> int:
+        import re
+        m = re.search(r"\(line (-?\d+)\)$", str(self))
+        return int(m.group(1)) if m else -1
 
 
 class DeviceError(AuxamgError):
@@ -96,7 +102,7 @@ class CycleOpts(C.Structure):
 class GpuOpts(C.Structure):
     _fields_ = [("device", C.c_int32), ("coarse_solve", C.c_int32), ("fused_max_cells", C.c_int32),
                 ("use_graphs", C.c_int32), ("block_solve", C.c_int32),
-                ("tile_kernels", C.c_int32), ("cluster_tier", C.c_int32), ("reserved", C.c_int32)]
+                ("tile_kernels", C.c_int32), ("cluster_tier", C.c_int32), ("stream_min_width", C.c_int32)]
 
 
 class DistOpts(C.Structure):

@@ -132,6 +132,7 @@ class GpuOptions:
     block_solve: int = 0         # 0 explicit block inverses, 1 stored LU in reference order
     tile_kernels: bool = True    # overlapped-tile kernels for the structured levels
     cluster_tier: bool = True    # 64x64 level + single-CTA tier in one thread-block cluster
+    stream_min_width: int = 0    # row-wavefront kernels from this level width (cells); 0 default, -1 off
 
     def c(self):
         o = _abi.GpuOpts()
@@ -140,6 +141,7 @@ class GpuOptions:
         o.block_solve = self.block_solve
         o.tile_kernels = int(self.tile_kernels)
         o.cluster_tier = int(self.cluster_tier)
+        o.stream_min_width = int(self.stream_min_width)
         return o
 
 
@@ -550,3 +552,77 @@ def galerkin_dense(A: CsrMatrix, agg_of, n_agg: int, device: int = 0) -> np.ndar
                                  msg, 512)
     _abi.raise_for(s, msg.raw)
     return out
+
+
+# ---------------------------------------------------------------- file readers
+def _file_lib():
+    L = lib()
+    if not getattr(L, "_io_typed", False):
+        vp, sz = C.c_void_p, C.c_size_t
+        for f in ("aux_read_matrix_market", "aux_read_mesh", "aux_read_coords"):
+            getattr(L, f).argtypes = [C.c_char_p, C.c_int32, C.POINTER(vp), C.c_char_p, sz]
+            getattr(L, f).restype = C.c_int
+        L.aux_file_data_sizes.argtypes = [vp, vp, vp, vp]
+        L.aux_file_data_sizes.restype = C.c_int
+        L.aux_file_data_copy.argtypes = [vp, vp, vp, vp]
+        L.aux_file_data_copy.restype = C.c_int
+        L.aux_file_data_destroy.argtypes = [vp]
+        L.aux_write_matrix_market.argtypes = [vp, C.c_char_p, C.c_char_p, sz]
+        L.aux_write_matrix_market.restype = C.c_int
+        L._io_typed = True
+    return L
+
+
+def _read(fn: str, path: str, threads: int):
+    L = _file_lib()
+    h, msg = C.c_void_p(), C.create_string_buffer(512)
+    st = getattr(L, fn)(os.fsencode(path), threads, C.byref(h), msg, 512)
+    _abi.raise_for(st, msg.raw)
+    a, b, c = C.c_int64(), C.c_int64(), C.c_int64()
+    L.aux_file_data_sizes(h, C.byref(a), C.byref(b), C.byref(c))
+    return L, h, a.value, b.value, c.value
+
+
+def read_matrix_market(path: str, threads: int = 0) -> CsrMatrix:
+    """read_matrix_market (matrix_market.hpp:33-104): coordinate real general /
+    symmetric, 1-based; symmetric storage expanded; parsed by `threads` host
+    threads (0: all)."""
+    L, h, n, m, nnz = _read("aux_read_matrix_market", path, threads)
+    try:
+        rp, ci, va = np.empty(n + 1, np.int32), np.empty(nnz, np.int32), np.empty(nnz, np.float64)
+        L.aux_file_data_copy(h, rp.ctypes.data, ci.ctypes.data, va.ctypes.data)
+        return CsrMatrix(int(n), int(m), rp, ci, va)
+    finally:
+        L.aux_file_data_destroy(h)
+
+
+def read_mesh(path: str, threads: int = 0):
+    """read_mesh (problems.hpp:201-310): NODES / ELEMENTS / optional BOUNDARY;
+    the boundary is the explicit list united with the free edges' endpoints."""
+    from .problems import TriMesh
+    L, h, nn, ne, nb = _read("aux_read_mesh", path, threads)
+    try:
+        nodes, tris, bnd = np.empty((nn, 2)), np.empty((ne, 3), np.int32), np.empty(nb, np.int32)
+        L.aux_file_data_copy(h, nodes.ctypes.data, tris.ctypes.data, bnd.ctypes.data)
+        return TriMesh(nodes, tris, bnd)
+    finally:
+        L.aux_file_data_destroy(h)
+
+
+def read_coords(path: str, threads: int = 0) -> np.ndarray:
+    """read_coords (problems.hpp:313-330): one "x y" per non-blank line, (N, 2)."""
+    L, h, n, _, _ = _read("aux_read_coords", path, threads)
+    try:
+        xy = np.empty((n, 2))
+        L.aux_file_data_copy(h, xy.ctypes.data, None, None)
+        return xy
+    finally:
+        L.aux_file_data_destroy(h)
+
+
+def write_matrix_market(A: CsrMatrix, path: str) -> None:
+    """write_matrix_market (matrix_market.hpp:106-120): general, %.17g values."""
+    A = _prep_csr(A)
+    msg = C.create_string_buffer(512)
+    st = _file_lib().aux_write_matrix_market(C.byref(_csr_view(A)), os.fsencode(path), msg, 512)
+    _abi.raise_for(st, msg.raw)

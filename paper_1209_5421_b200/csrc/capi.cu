@@ -46,6 +46,7 @@ aux_hierarchy* make_h(const aux_setup_opts* o, const aux_gpu_opts* g) {
     if (o) h->opts = *o;
     if (g) h->gpu = *g;
     AUX_CUDA(cudaSetDevice(h->gpu.device));
+    AUX_CUDA(cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, h->gpu.device));
     AUX_CUDA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
     h->red_partials.alloc((size_t)kMaxRedBlocks * 4);
     h->red_ticket.alloc(1);

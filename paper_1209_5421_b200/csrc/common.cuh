@@ -201,9 +201,9 @@ inline int red_blocks(long n) {
 // Block-level sum of NV values per thread into smem; returns true in the
 // last-finishing block, where out[v] holds the grid total (fixed-shape tree
 // over block partials => run-to-run deterministic for a fixed grid).
-template <int NV>
+template <int NV, int NW = kRedThreads / 32>
 __device__ bool grid_reduce(double (&v)[NV], const RedState& rs, double (&out)[NV]) {
-    __shared__ double sm[NV][kRedThreads / 32];
+    __shared__ double sm[NV][NW];
     __shared__ bool last;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #pragma unroll
@@ -216,7 +216,7 @@ __device__ bool grid_reduce(double (&v)[NV], const RedState& rs, double (&out)[N
 #pragma unroll
         for (int i = 0; i < NV; ++i) {
             double s = 0.0;
-            for (int w = 0; w < kRedThreads / 32; ++w) s += sm[i][w];
+            for (int w = 0; w < NW; ++w) s += sm[i][w];
             out[i] = s;
         }
         return true;
@@ -225,7 +225,7 @@ __device__ bool grid_reduce(double (&v)[NV], const RedState& rs, double (&out)[N
 #pragma unroll
         for (int i = 0; i < NV; ++i) {
             double s = 0.0;
-            for (int w = 0; w < kRedThreads / 32; ++w) s += sm[i][w];
+            for (int w = 0; w < NW; ++w) s += sm[i][w];
             rs.partials[blockIdx.x * NV + i] = s;
         }
         __threadfence();
@@ -249,7 +249,7 @@ __device__ bool grid_reduce(double (&v)[NV], const RedState& rs, double (&out)[N
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
         double s = 0.0;
-        for (int w = 0; w < kRedThreads / 32; ++w) s += sm[i][w];
+        for (int w = 0; w < NW; ++w) s += sm[i][w];
         out[i] = s;
     }
     if (threadIdx.x == 0) *rs.ticket = 0u;

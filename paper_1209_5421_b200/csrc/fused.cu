@@ -980,6 +980,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_cluster_pcg(const __grid_consta
         }
     }
     pdl_wait();
+    __syncthreads();   // the zero fill above covers Q.r: finish it before any thread stores its residual
     if (quad) {
         const int gpos = (kQH * qy + tb) * gH + kQH * qx + ta;
 #pragma unroll

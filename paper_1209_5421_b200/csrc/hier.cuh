@@ -177,6 +177,7 @@ struct Profile {
 
 struct aux_hierarchy {
     int device = 0;
+    int sm_count = 148;
     cudaStream_t stream = nullptr;
     aux_setup_opts opts{};
     aux_gpu_opts gpu{};

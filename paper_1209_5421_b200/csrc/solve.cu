@@ -1151,6 +1151,11 @@ void pcg_tiles(Ctx& c, int m) {
     const Rect own = L.own;
     const int T = tile_edge(std::min(own.w(), own.h()));
     const int tx = own.w() / T, ntiles = tx * (own.h() / T);
+    // large levels: the row-wavefront kernels (stream.cu) instead of the tiles
+    const int smw = h->gpu.stream_min_width == 0 ? 1024 : h->gpu.stream_min_width;
+    const bool stream = smw > 0 && own.w() >= smw && own.h() >= 16 && c.o.pre_sweeps == 1 && c.o.post_sweeps == 1;
+    int s_nbx = 0, s_yb = 0, s_blocks = 0;
+    if (stream) stream_blocks(own.w(), own.h(), h->sm_count, s_nbx, s_yb, s_blocks);
     const bool child_agg = L.dist && (m + 1 == h->dist.agg);
     const bool child_explicit = explicit_iterate(h, m + 1) || child_agg;
     Span sp = flat_span(L.n);
@@ -1162,6 +1167,10 @@ void pcg_tiles(Ctx& c, int m) {
         d.gc = C.geo;
         d.ox = own.x0;
         d.oy = own.y0;
+        d.ow = own.w();
+        d.oh = own.h();
+        d.nbx = s_nbx;
+        d.yb = s_yb;
         d.tiles_x = tx;
         d.tiles_x_edge = T;
         d.val = L.val.p;
@@ -1175,7 +1184,8 @@ void pcg_tiles(Ctx& c, int m) {
         d.child_nval = sc_nval(ni);
         const bool prof_l = m == 1 && c.profile_finest && h->prof.on == 2;
         if (prof_l) prof_begin(c, 4);
-        launch_tile_down(d, ntiles, c.o.pre_sweeps, c.s);
+        if (stream) launch_stream_down(d, s_blocks, c.s);
+        else launch_tile_down(d, ntiles, c.o.pre_sweeps, c.s);
         // algorithmic bytes (each array once): stencil values, r in, pending
         // update (A p, r out), pre-smoothed iterate out, child right-hand side out
         if (prof_l) prof_end(c, 4, (double)sp.n * (72.0 + 8.0 + (i ? 16.0 : 0.0) + 8.0) + 8.0 * (double)C.n);
@@ -1194,6 +1204,10 @@ void pcg_tiles(Ctx& c, int m) {
         u.gc = C.geo;
         u.ox = own.x0;
         u.oy = own.y0;
+        u.ow = own.w();
+        u.oh = own.h();
+        u.nbx = s_nbx;
+        u.yb = s_yb;
         u.tiles_x = tx;
         u.tiles_x_edge = T;
         u.val = L.val.p;
@@ -1211,7 +1225,8 @@ void pcg_tiles(Ctx& c, int m) {
         const Route ru = route(c, L.dist, i == 0 ? Fin{1, sc, nullptr, sc + 3, sc + sc_alpha(ni, 0), sc + sc_nval(ni), 0}
                                                  : Fin{2, sc, sc + 3, nullptr});
         if (prof_l) prof_begin(c, 5);
-        launch_tile_up(u, ntiles, c.o.post_sweeps, c.rs, ru.launch, c.s);
+        if (stream) launch_stream_up(u, s_blocks, c.rs, ru.launch, c.s);
+        else launch_tile_up(u, ntiles, c.o.post_sweeps, c.rs, ru.launch, c.s);
         // stencil values, active flags, f, pre-smoothed iterate, child
         // correction (explicit iterate or its n_inner directions), z and A z out
         if (prof_l)

@@ -21,6 +21,8 @@ inline int sc_size(int ni) { return 4 + 2 * ni; }
 struct TileDown {
     Geo g, gc;
     int ox, oy;              // owned rectangle origin (global cells); tiles cover it
+    int ow, oh;              // owned rectangle size (cells)
+    int nbx, yb;             // row-wavefront blocking (stream.cu): x-blocks, plane rows per y-block
     int tiles_x;
     int tiles_x_edge;        // tile edge T (tile_edge of the owned rectangle)
     const double* val;
@@ -44,6 +46,8 @@ struct TileDown {
 struct TileUp {
     Geo g, gc;
     int ox, oy;
+    int ow, oh;
+    int nbx, yb;
     int tiles_x;
     int tiles_x_edge;
     const double* val;
@@ -71,5 +75,11 @@ int tile_edge(int w);
 // ntiles = tiles of the owned rectangle (tiles_x per row)
 void launch_tile_down(TileDown& a, int ntiles, int pre, cudaStream_t s);
 void launch_tile_up(TileUp& a, int ntiles, int post, RedState rs, Fin fin, cudaStream_t s);
+
+// Row-wavefront kernels for large levels (stream.cu; one pre / post sweep):
+// the same visit halves as the tile kernels, bitwise the same cell values.
+void stream_blocks(int ow, int oh, int sms, int& nbx, int& yb, int& nblocks);
+void launch_stream_down(TileDown& a, int nblocks, cudaStream_t s);
+void launch_stream_up(TileUp& a, int nblocks, RedState rs, Fin fin, cudaStream_t s);
 
 }  // namespace auxb200

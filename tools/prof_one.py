@@ -1,4 +1,5 @@
-"""One setup + a short solve for ncu captures:  python tools/prof_one.py graded2049 [max_outer]"""
+"""One setup + a short solve for ncu captures:  python tools/prof_one.py graded2049 [max_outer]
+(STREAM=<cells>: GpuOptions.stream_min_width)"""
 import os
 import sys
 
@@ -14,6 +15,6 @@ elif name.startswith("graded"):
     s = problems.graded_p1(int(name[6:]), 1.3)
 else:
     s = problems.poisson5(int(name[3:]))
-h = api.setup_hierarchy(s.A, s.coords)
+h = api.setup_hierarchy(s.A, s.coords, gpu=api.GpuOptions(stream_min_width=int(os.environ.get("STREAM", "0"))))
 r = api.solve(s.A, s.b, h, api.CycleOptions(max_outer=max_outer))
 print("iterations", r.iterations)

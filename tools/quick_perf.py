@@ -1,6 +1,7 @@
 """Quick GPU timing probe (not the bench contract): setup + solve times for a
 few BASELINE configurations through the C ABI.  FUSED=<cells> sets
-GpuOptions.fused_max_cells, CLUSTER=0 turns the cluster tier off; AUX_TRACE=1 prints the device-time breakdown."""
+GpuOptions.fused_max_cells, CLUSTER=0 turns the cluster tier off, STREAM=<cells>
+sets GpuOptions.stream_min_width (-1 off); AUX_TRACE=1 prints the device-time breakdown."""
 import os
 import sys
 import time
@@ -22,7 +23,8 @@ for name in cfgs:
     tg = time.time() - t
     for rep in range(3):
         t0 = time.time()
-        h = api.setup_hierarchy(s.A, s.coords, gpu=api.GpuOptions(fused_max_cells=fused, cluster_tier=os.environ.get("CLUSTER", "1") != "0"))
+        h = api.setup_hierarchy(s.A, s.coords, gpu=api.GpuOptions(fused_max_cells=fused, cluster_tier=os.environ.get("CLUSTER", "1") != "0",
+                                                                  stream_min_width=int(os.environ.get("STREAM", "0"))))
         t1 = time.time()
         for k in range(2):
             ts = time.time()
