@@ -20,10 +20,13 @@ Rules (reference anchors: auxgrid.hpp:95-121 for the cells):
 """
 from __future__ import annotations
 
+import os
+
 import numpy as np
 
 RING = 10
 MIN_EDGE = 16
+AGG_SIDE = 512   # default AUX_DIST_AGG_SIDE of the library (setup.cu)
 
 
 def part_grid(parts: int) -> tuple[int, int]:
@@ -115,18 +118,26 @@ class Partition:
         g = self.ghosts(rank)
         return np.bincount(self.owner[g], minlength=self.parts)
 
-    def level_plan(self, coarsest_size: int = 64) -> list[dict]:
+    def level_plan(self, coarsest_size: int = 64, agg_side: int | None = None) -> list[dict]:
         """Structured levels (k = L, L-1, ...) with their global size and
-        whether they are distributed (setup_device_dist): level L always (P > 1),
-        then while part 0's rectangle keeps >= MIN_EDGE cells per side; the
-        first level below that (and any still-distributed coarsest level) is
-        gathered on part 0."""
+        whether they are distributed, as setup_device_dist decides
+        (csrc/setup.cu): level L always (P > 1); below it a level stays
+        distributed while part 0's rectangle keeps >= MIN_EDGE cells per side
+        AND the level is wider than `agg_side` cells (the library's
+        AUX_DIST_AGG_SIDE, default 512: a K-cycle visit of a 256K-cell level
+        costs about one distributed visit's compute plus its halo exchanges and
+        all-reduces, so smaller levels run faster gathered on part 0;
+        agg_side=0 keeps every tileable level distributed).  The first level
+        below that (and any still-distributed coarsest level) is gathered on
+        part 0."""
+        if agg_side is None:
+            agg_side = int(os.environ.get("AUX_DIST_AGG_SIDE", AGG_SIDE))
         out, k, dist = [], self.depth, self.parts > 1
         while True:
             w = 1 << k
             x0, y0, x1, y1 = level_rect(w, self.parts, 0)
             if k < self.depth:
-                dist = dist and (x1 - x0) >= MIN_EDGE and (y1 - y0) >= MIN_EDGE
+                dist = dist and (x1 - x0) >= MIN_EDGE and (y1 - y0) >= MIN_EDGE and w > agg_side
             out.append({"k": k, "n": w * w, "dist": dist})
             if not (k > 0 and w * w > coarsest_size):
                 break

@@ -49,13 +49,18 @@ def test_ring_boxes_pair_up(parts):
 
 def test_level_plan_agglomerates_once():
     s = problems.jittered_p1(513)   # L = 9, 512 x 512 level-L cells
+    # deep plan (AUX_DIST_AGG_SIDE=0): distributed while the rectangles stay tileable
     for parts, first_gathered_k in ((2, 4), (4, 4), (8, 5)):
-        plan = pt.Partition(s.A, s.coords, parts).level_plan()
+        plan = pt.Partition(s.A, s.coords, parts).level_plan(agg_side=0)
         d = [lv["dist"] for lv in plan]
         assert d[0] and not d[-1]
         assert d == sorted(d, reverse=True)            # distributed levels come first
         k_agg = next(lv["k"] for lv in plan if not lv["dist"])
         assert k_agg == first_gathered_k
+    # the library's default (agg_side 512): only level L (512 wide) stays distributed
+    for parts in (2, 4, 8):
+        plan = pt.Partition(s.A, s.coords, parts).level_plan(agg_side=512)
+        assert [lv["dist"] for lv in plan][:2] == [True, False]
 
 
 # ---------------------------------------------------------------- 2 gloo ranks
