@@ -50,7 +50,7 @@ __device__ int g_fclk_launch;
     __shared__ unsigned long long s_clk[16];        \
     __shared__ unsigned s_cnt[16];                  \
     if (threadIdx.x < 16) { s_clk[threadIdx.x] = 0; s_cnt[threadIdx.x] = 0; } \
-    Tm::sync();                                     \
+    __syncthreads();                                \
     long long fclk_t0 = 0;
 #define FCLK_BEGIN fclk_t0 = clock64();
 #define FCLK_END(T, Q)                                                        \
@@ -89,29 +89,6 @@ constexpr double kBreak = 1e-300;
 #endif
 constexpr int kThreads = AUX_FUSED_THREADS;
 constexpr int kWarps = kThreads / 32;
-
-// Execution teams of the single-CTA tier.  Levels of at most kWarpTierMax
-// cells (the 256- and 64-cell levels below a 1K top level) run on warp 0
-// alone: a colour pass there has 64 cells, so a CTA barrier (and the wait for
-// seven idle warps) would cost more than the pass; the warp team syncs with
-// __syncwarp and reduces with shuffles only.  The other warps wait at one
-// barrier until warp 0 returns from the whole sub-recursion.
-#ifndef AUX_WARP_TIER_MAX
-#define AUX_WARP_TIER_MAX 256
-#endif
-constexpr int kWarpTierMax = AUX_WARP_TIER_MAX;
-struct TeamCta {
-    static constexpr bool kCta = true;
-    static constexpr int N = kThreads;
-    __device__ __forceinline__ static int rank() { return (int)threadIdx.x; }
-    __device__ __forceinline__ static void sync() { __syncthreads(); }
-};
-struct TeamWarp {
-    static constexpr bool kCta = false;
-    static constexpr int N = 32;
-    __device__ __forceinline__ static int rank() { return (int)(threadIdx.x & 31); }
-    __device__ __forceinline__ static void sync() { __syncwarp(); }
-};
 
 // Level view in shared memory.  Compact arrays (val, act) are indexed by the
 // colour-major cell index; vectors by the padded index
@@ -191,13 +168,7 @@ __device__ __forceinline__ PState ps_view(TierSM* ts, int q) {
     return p;
 }
 
-template <class Tm>
 __device__ __forceinline__ void bsum2(double* red, int& par, double& x, double& y) {
-    if constexpr (!Tm::kCta) {   // one warp: butterfly sums, identical in every lane
-        x = warp_sum(x);
-        y = warp_sum(y);
-        return;
-    }
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     x = warp_sum(x);
     y = warp_sum(y);
@@ -253,22 +224,21 @@ __device__ __forceinline__ double gs_cell(const SLevel& L, int ci, int pi, doubl
 
 // One colour pass.  Inactive cells have f = 0 and an identity row, so the
 // update leaves them at 0 like the reference, which skips them.
-template <class Tm, int C>
+template <int C>
 __device__ __forceinline__ void gs_pass(const SLevel& L, const double* f, double* x) {
-    for (int pos = Tm::rank(); pos < L.nq; pos += Tm::N) {
+    for (int pos = threadIdx.x; pos < L.nq; pos += kThreads) {
         const int a = pos & (L.H - 1), b = pos >> L.lh;
         const int pi = pidx(L, C, a, b);
         x[pi] = gs_cell<C>(L, (C * L.nq) + pos, pi, f[pi], x);
     }
-    Tm::sync();
+    __syncthreads();
 }
 
-template <class Tm>
 __device__ __forceinline__ void gs_sweep(const SLevel& L, const double* f, double* x, bool fwd) {
     if (fwd) {
-        gs_pass<Tm, 0>(L, f, x); gs_pass<Tm, 1>(L, f, x); gs_pass<Tm, 2>(L, f, x); gs_pass<Tm, 3>(L, f, x);
+        gs_pass<0>(L, f, x); gs_pass<1>(L, f, x); gs_pass<2>(L, f, x); gs_pass<3>(L, f, x);
     } else {
-        gs_pass<Tm, 3>(L, f, x); gs_pass<Tm, 2>(L, f, x); gs_pass<Tm, 1>(L, f, x); gs_pass<Tm, 0>(L, f, x);
+        gs_pass<3>(L, f, x); gs_pass<2>(L, f, x); gs_pass<1>(L, f, x); gs_pass<0>(L, f, x);
     }
 }
 
@@ -338,23 +308,22 @@ __device__ __forceinline__ void gs_sweep_r(const SLevel& L, const RV& rv, const 
 
 // Coarsest solve (cycle.hpp:152-155).  The coarsest level's vectors are padded
 // too; the inverse is stored in colour-major (compact) order.
-template <class Tm>
 __device__ void coarse_solve(const FusedArgs& a, const double* inv, double* part, const SLevel& L, PState& ps,
                              double* u) {
     double* r = L.r;
     if (ps.pend) {
         const double na = -ps.alpha[ps.step - 1];
         const double* ap = L.ap + (ps.step - 1) * 4 * L.PP;
-        for (int ci = Tm::rank(); ci < L.n; ci += Tm::N) {
+        for (int ci = threadIdx.x; ci < L.n; ci += kThreads) {
             const int c = ci >> (2 * L.lh), pos = ci & (L.nq - 1);
             const int pi = pidx(L, c, pos & (L.H - 1), pos >> L.lh);
             r[pi] = __dadd_rn(r[pi], __dmul_rn(na, ap[pi]));
         }
-        Tm::sync();
+        __syncthreads();
         ps.pend = 0;
     }
     if (a.coarse_mode == 1) {
-        if (Tm::rank() == 0) {
+        if (threadIdx.x == 0) {
             double* b = a.work;
             double* x = a.work + a.nc;
             for (int ci = 0; ci < a.nc; ++ci) {
@@ -375,12 +344,12 @@ __device__ void coarse_solve(const FusedArgs& a, const double* inv, double* part
         // no index arithmetic.
         const int nc = a.nc, cs = (nc + 3) / 4;
         double* rc = part + 4 * nc;
-        for (int j = Tm::rank(); j < nc; j += Tm::N) {
+        for (int j = threadIdx.x; j < nc; j += kThreads) {
             const int c = j >> (2 * L.lh), pos = j & (L.nq - 1);
             rc[j] = r[pidx(L, c, pos & (L.H - 1), pos >> L.lh)];
         }
-        Tm::sync();
-        for (int idx = Tm::rank(); idx < 4 * nc; idx += Tm::N) {
+        __syncthreads();
+        for (int idx = threadIdx.x; idx < 4 * nc; idx += kThreads) {
             const int row = idx % nc, k = idx / nc;
             const int j0 = k * cs, j1 = min(nc, (k + 1) * cs);
             const double* iv = inv + (size_t)j0 * nc + row;
@@ -389,14 +358,14 @@ __device__ void coarse_solve(const FusedArgs& a, const double* inv, double* part
             for (int j = j0; j < j1; ++j, iv += nc) s = fma(*iv, rc[j], s);
             part[k * nc + row] = s;
         }
-        Tm::sync();
-        for (int row = Tm::rank(); row < nc; row += Tm::N) {
+        __syncthreads();
+        for (int row = threadIdx.x; row < nc; row += kThreads) {
             const int c = row >> (2 * L.lh), pos = row & (L.nq - 1);
             u[pidx(L, c, pos & (L.H - 1), pos >> L.lh)] =
                 ((part[row] + part[nc + row]) + part[2 * nc + row]) + part[3 * nc + row];
         }
     }
-    Tm::sync();
+    __syncthreads();
 }
 
 // Restricted residual of the colour-C children (hierarchy.hpp:267-277 order:
@@ -411,7 +380,6 @@ __device__ __forceinline__ double child_resid(const SLevel& L, int T1, int T2, c
 // Pre-smoothing from u = 0 (cycle.hpp:170-171) and the restricted residual
 // (cycle.hpp:173-178).  The first pass applies the pending PCG residual
 // update of this level, relaxes colour 0 from zero and writes u = 0 elsewhere.
-template <class Tm>
 __device__ void cycle_down(const FusedArgs& a, const SLevel& L, PState& ps, const SLevel& Cc, double* u,
                            const RV* rv) {
     PH_RESET
@@ -421,7 +389,7 @@ __device__ void cycle_down(const FusedArgs& a, const SLevel& L, PState& ps, cons
     const bool pend = ps.pend != 0;
     const double na = pend ? -ps.alpha[ps.step - 1] : 0.0;
     const double* ap = L.ap + (ps.step > 0 ? ps.step - 1 : 0) * 4 * L.PP;
-    for (int ci = Tm::rank(); ci < L.n; ci += Tm::N) {
+    for (int ci = threadIdx.x; ci < L.n; ci += kThreads) {
         const int c = ci >> (2 * L.lh), pos = ci & (L.nq - 1);
         const int pi = pidx(L, c, pos & (L.H - 1), pos >> L.lh);
         double fi = f[pi];
@@ -432,39 +400,39 @@ __device__ void cycle_down(const FusedArgs& a, const SLevel& L, PState& ps, cons
         u[pi] = c == 0 ? __ddiv_rn(fi, L.val[ci]) : 0.0;
     }
     ps.pend = 0;
-    Tm::sync();
+    __syncthreads();
     PH(po + 0)
-    if constexpr (Tm::kCta) {
-        if (rv) {
-            gs_pass_r<1>(L, *rv, f, u);
-            gs_pass_r<2>(L, *rv, f, u);
-            gs_pass_r<3>(L, *rv, f, u);
-            for (int sw = 1; sw < a.pre; ++sw) gs_sweep_r(L, *rv, f, u, true);
-            // thread t: the children at plane position t (all four colours)
-            const int t = threadIdx.x;
-            const int T1 = t & (kRH - 1), T2 = t >> 4;
-            const RV& r = *rv;
-            double sum = 0.0;
-            sum = __dadd_rn(sum, __dsub_rn(f[pidx_r(0, T1, T2)], row9_r<0>(L, r, pidx_r(0, T1, T2), u)));
-            sum = __dadd_rn(sum, __dsub_rn(f[pidx_r(1, T1, T2)], row9_r<1>(L, r, pidx_r(1, T1, T2), u)));
-            sum = __dadd_rn(sum, __dsub_rn(f[pidx_r(2, T1, T2)], row9_r<2>(L, r, pidx_r(2, T1, T2), u)));
-            sum = __dadd_rn(sum, __dsub_rn(f[pidx_r(3, T1, T2)], row9_r<3>(L, r, pidx_r(3, T1, T2), u)));
-            const int cq = (T1 & 1) | ((T2 & 1) << 1);
-            Cc.r[pidx(Cc, cq, T1 >> 1, T2 >> 1)] = sum;
-            __syncthreads();
-            PH(po + 4)
-            return;
-        }
+    if (rv) {
+        gs_pass_r<1>(L, *rv, f, u);
+        gs_pass_r<2>(L, *rv, f, u);
+        gs_pass_r<3>(L, *rv, f, u);
+        for (int sw = 1; sw < a.pre; ++sw) gs_sweep_r(L, *rv, f, u, true);
+    } else {
+        gs_pass<1>(L, f, u);
+        PH(po + 1)
+        gs_pass<2>(L, f, u);
+        PH(po + 2)
+        gs_pass<3>(L, f, u);
+        PH(po + 3)
+        for (int sw = 1; sw < a.pre; ++sw) gs_sweep(L, f, u, true);
     }
-    gs_pass<Tm, 1>(L, f, u);
-    PH(po + 1)
-    gs_pass<Tm, 2>(L, f, u);
-    PH(po + 2)
-    gs_pass<Tm, 3>(L, f, u);
-    PH(po + 3)
-    for (int sw = 1; sw < a.pre; ++sw) gs_sweep<Tm>(L, f, u, true);
+    if (rv) {   // thread t: the children at plane position t (all four colours)
+        const int t = threadIdx.x;
+        const int T1 = t & (kRH - 1), T2 = t >> 4;
+        const RV& r = *rv;
+        double sum = 0.0;
+        sum = __dadd_rn(sum, __dsub_rn(f[pidx_r(0, T1, T2)], row9_r<0>(L, r, pidx_r(0, T1, T2), u)));
+        sum = __dadd_rn(sum, __dsub_rn(f[pidx_r(1, T1, T2)], row9_r<1>(L, r, pidx_r(1, T1, T2), u)));
+        sum = __dadd_rn(sum, __dsub_rn(f[pidx_r(2, T1, T2)], row9_r<2>(L, r, pidx_r(2, T1, T2), u)));
+        sum = __dadd_rn(sum, __dsub_rn(f[pidx_r(3, T1, T2)], row9_r<3>(L, r, pidx_r(3, T1, T2), u)));
+        const int cq = (T1 & 1) | ((T2 & 1) << 1);
+        Cc.r[pidx(Cc, cq, T1 >> 1, T2 >> 1)] = sum;
+        __syncthreads();
+        PH(po + 4)
+        return;
+    }
     // restriction into the child's PCG residual
-    for (int Q = Tm::rank(); Q < Cc.n; Q += Tm::N) {
+    for (int Q = threadIdx.x; Q < Cc.n; Q += kThreads) {
         const int cq = Q >> (2 * Cc.lh), pos = Q & (Cc.nq - 1);
         const int ac = pos & (Cc.H - 1), bc = pos >> Cc.lh;
         const int T1 = 2 * ac + (cq & 1), T2 = 2 * bc + (cq >> 1);   // coarse cell = fine plane coords
@@ -475,14 +443,13 @@ __device__ void cycle_down(const FusedArgs& a, const SLevel& L, PState& ps, cons
         sum = __dadd_rn(sum, child_resid<3>(L, T1, T2, f, u));
         Cc.r[pidx(Cc, cq, ac, bc)] = sum;
     }
-    Tm::sync();
+    __syncthreads();
     PH(po + 4)
 }
 
 // u_i += ec[parent(i)] on active cells (cycle.hpp:191-194) with
 // ec = ((0 + alpha_0 p_0) + alpha_1 p_1) ... the child's PCG iterate, then the
 // transposed post-smoothing (cycle.hpp:196).
-template <class Tm>
 __device__ void cycle_up(const FusedArgs& a, const SLevel& L, const SLevel& Cc, const PState& cs, double* u,
                          const RV* rv) {
     PH_RESET
@@ -495,7 +462,7 @@ __device__ void cycle_up(const FusedArgs& a, const SLevel& L, const SLevel& Cc, 
     double al[kFusedMaxInner];
 #pragma unroll
     for (int k = 0; k < kFusedMaxInner; ++k) al[k] = k < nval ? cs.alpha[k] : 0.0;
-    for (int pos = Tm::rank(); pos < L.nq; pos += Tm::N) {
+    for (int pos = threadIdx.x; pos < L.nq; pos += kThreads) {
         const int A = pos & (L.H - 1), B = pos >> L.lh;   // parent cell (A, B) on the child level
         const int pc = pidx(Cc, (A & 1) | ((B & 1) << 1), A >> 1, B >> 1);
         double e = 0.0;
@@ -509,24 +476,19 @@ __device__ void cycle_up(const FusedArgs& a, const SLevel& L, const SLevel& Cc, 
             u[pi] = __dadd_rn(u[pi], e);
         }
     }
-    Tm::sync();
+    __syncthreads();
     PH(po + 5)
     for (int sw = 0; sw < a.post; ++sw) {
-        if constexpr (Tm::kCta) {
-            if (rv) {
-                gs_sweep_r(L, *rv, L.r, u, false);
-                continue;
-            }
-        }
-        gs_sweep<Tm>(L, L.r, u, false);
+        if (rv) gs_sweep_r(L, *rv, L.r, u, false);
+        else gs_sweep(L, L.r, u, false);
     }
     PH(po + 6)
 }
 
-template <class Tm, int C>
+template <int C>
 __device__ __forceinline__ void spmv_color(const SLevel& L, const double* x, double* y, const double* r,
                                            const double* w, int mode, double& s0, double& s1) {
-    for (int pos = Tm::rank(); pos < L.nq; pos += Tm::N) {
+    for (int pos = threadIdx.x; pos < L.nq; pos += kThreads) {
         const int pi = pidx(L, C, pos & (L.H - 1), pos >> L.lh);
         const double yi = row9<C>(L, C * L.nq + pos, pi, x);
         y[pi] = yi;
@@ -561,7 +523,6 @@ __device__ __forceinline__ void spmv_color_r(const SLevel& L, const RV& rv, cons
 // After the preconditioner application of step i: A z, the A-orthogonalisation
 // against the kept directions (cycle.hpp:84-97) and alpha (cycle.hpp:123).
 // Returns true when this PCG is finished (breakdown or last step).
-template <class Tm>
 __device__ bool pcg_step(const FusedArgs& a, const SLevel& L, PState& ps, double* red, int& par, const RV* rv) {
     const int vs = 4 * L.PP;
     const int i = ps.step;
@@ -574,13 +535,13 @@ __device__ bool pcg_step(const FusedArgs& a, const SLevel& L, PState& ps, double
     PH_RESET
     const int po = L.n > 256 ? 0 : 16;
     (void)po;
-    if (Tm::kCta && rv) {
+    if (rv) {
         spmv_color_r<0>(L, *rv, p, ap, L.r, L.ap, mode, s0, s1);
         spmv_color_r<1>(L, *rv, p, ap, L.r, L.ap, mode, s0, s1);
         spmv_color_r<2>(L, *rv, p, ap, L.r, L.ap, mode, s0, s1);
         spmv_color_r<3>(L, *rv, p, ap, L.r, L.ap, mode, s0, s1);
-    } else if (L.n <= Tm::N) {   // all four colours at once, one cell per thread
-        const int ci = Tm::rank();
+    } else if (L.n <= kThreads) {   // all four colours at once, one cell per thread
+        const int ci = threadIdx.x;
         if (ci < L.n) {
             const int c = ci >> (2 * L.lh), pos = ci & (L.nq - 1);
             const int pi = pidx(L, c, pos & (L.H - 1), pos >> L.lh);
@@ -601,12 +562,12 @@ __device__ bool pcg_step(const FusedArgs& a, const SLevel& L, PState& ps, double
             }
         }
     } else {
-        spmv_color<Tm, 0>(L, p, ap, L.r, L.ap, mode, s0, s1);
-        spmv_color<Tm, 1>(L, p, ap, L.r, L.ap, mode, s0, s1);
-        spmv_color<Tm, 2>(L, p, ap, L.r, L.ap, mode, s0, s1);
-        spmv_color<Tm, 3>(L, p, ap, L.r, L.ap, mode, s0, s1);
+        spmv_color<0>(L, p, ap, L.r, L.ap, mode, s0, s1);
+        spmv_color<1>(L, p, ap, L.r, L.ap, mode, s0, s1);
+        spmv_color<2>(L, p, ap, L.r, L.ap, mode, s0, s1);
+        spmv_color<3>(L, p, ap, L.r, L.ap, mode, s0, s1);
     }
-    bsum2<Tm>(red, par, s0, s1);
+    bsum2(red, par, s0, s1);
     PH(po + 7)
     if (i == 0) {
         ps.e[0] = s0;
@@ -621,7 +582,7 @@ __device__ bool pcg_step(const FusedArgs& a, const SLevel& L, PState& ps, double
             const bool fin = (j == i);
             const double* wj = L.ap + j * vs;
             double t0 = 0.0, t1 = 0.0;
-            for (int ci = Tm::rank(); ci < L.n; ci += Tm::N) {
+            for (int ci = threadIdx.x; ci < L.n; ci += kThreads) {
                 const int c = ci >> (2 * L.lh), pos = ci & (L.nq - 1);
                 const int q = pidx(L, c, pos & (L.H - 1), pos >> L.lh);
                 const double pq = __dadd_rn(p[q], __dmul_rn(beta, pj[q]));
@@ -635,7 +596,7 @@ __device__ bool pcg_step(const FusedArgs& a, const SLevel& L, PState& ps, double
                     t0 = __dadd_rn(t0, __dmul_rn(pq, wj[q]));
                 }
             }
-            bsum2<Tm>(red, par, t0, t1);
+            bsum2(red, par, t0, t1);
             PH(po + 8)
             if (fin) {
                 ps.e[i] = t0;
@@ -710,53 +671,38 @@ __device__ __forceinline__ void tier_load_rv(const FusedArgs& a, unsigned char* 
         for (int t = 0; t < 9; ++t) rv.v[c][t] = L0.val[t * L0.n + c * L0.nq + threadIdx.x];
 }
 
-// nonlinear_pcg on tier level q0 with the K-cycle below it, right-hand side
-// already in the level's padded r, as an explicit state machine over (level,
-// PCG step) run by team Tm.  The CTA team hands the levels from qw down to
-// warp 0 (TeamWarp) and waits for it at one barrier; the child's PCG state
-// (alphas, valid steps) is in shared memory.
-template <class Tm>
-__device__ void tier_pcg(const FusedArgs& a, unsigned char* sm, const Geo* sgeo, const double* inv, double* red,
-                         const RV& rv0, bool top_reg, TierSM* ts, int q0, int qw) {
+// nonlinear_pcg(m0) with the K-cycle below it, right-hand side already in the
+// top level's padded r; returns the top level's PCG state (alphas, nval), the
+// directions stay in shared memory.
+__device__ void tier_run(const FusedArgs& a, unsigned char* sm, const Geo* sgeo, const double* inv, double* red,
+                         const RV& rv0, bool top_reg, TierSM* ts) {
     FCLK_START
     const int nl = a.last - a.m0 + 1;
+    // ---- the K-cycle as an explicit state machine over (level, PCG step)
     int par = 0;
-    int q = q0;
-    PState cur = ps_view(ts, q0);
+    int q = 0;
+    PState cur = ps_view(ts, 0);
     *cur.nval = 0;
     bool resume = false;   // false: start cycle(q) for step; true: cycle(q) just finished
     double* part = reinterpret_cast<double*>(sm + a.off_part);
     FCLK_DECL
     while (true) {
         const SLevel L = slev(a, sm, sgeo, q);
-        const RV* rv = (Tm::kCta && q == 0 && top_reg) ? &rv0 : nullptr;
         if (!resume) {
             double* u = L.p + cur.step * 4 * L.PP;
             if (q < nl - 1) {
                 FCLK_BEGIN
-                cycle_down<Tm>(a, L, cur, slev(a, sm, sgeo, q + 1), u, rv);
+                cycle_down(a, L, cur, slev(a, sm, sgeo, q + 1), u, (q == 0 && top_reg) ? &rv0 : nullptr);
                 FCLK_END(0, q)
                 ts->step[q] = cur.step;   // the parent's registers, restored when the child returns
                 ts->pend[q] = cur.pend;
-                if (Tm::kCta && q + 1 == qw) {   // the levels below run on warp 0
-                    if (threadIdx.x < 32) tier_pcg<TeamWarp>(a, sm, sgeo, inv, red, rv0, top_reg, ts, qw, qw);
-                    __syncthreads();
-                    const PState child = ps_view(ts, qw);
-                    cur.step = ts->step[q];
-                    cur.pend = ts->pend[q];
-                    FCLK_BEGIN
-                    cycle_up<Tm>(a, L, slev(a, sm, sgeo, qw), child, u, rv);
-                    FCLK_END(3, q)
-                    resume = true;
-                    continue;
-                }
                 ++q;
                 cur = ps_view(ts, q);
                 *cur.nval = 0;
                 continue;
             }
             FCLK_BEGIN
-            coarse_solve<Tm>(a, inv, part, L, cur, u);
+            coarse_solve(a, inv, part, L, cur, u);
             FCLK_END(1, q)
             resume = true;
             if (a.coarse_mode != 0) continue;
@@ -769,7 +715,7 @@ __device__ void tier_pcg(const FusedArgs& a, unsigned char* sm, const Geo* sgeo,
             *cur.nval = 1;
         } else {
             FCLK_BEGIN
-            const bool done = pcg_step<Tm>(a, L, cur, red, par, rv);
+            const bool done = pcg_step(a, L, cur, red, par, (q == 0 && top_reg) ? &rv0 : nullptr);
             FCLK_END(2, q)
             if (!done) {
                 cur.pend = 1;
@@ -780,7 +726,7 @@ __device__ void tier_pcg(const FusedArgs& a, unsigned char* sm, const Geo* sgeo,
         }
         // nonlinear_pcg(q) finished: back to the parent (one call site keeps
         // the kernel's code small — instruction fetch is a visible stall here)
-        if (q == q0) break;
+        if (q == 0) break;
         const PState child = cur;
         --q;
         cur = ps_view(ts, q);
@@ -788,27 +734,11 @@ __device__ void tier_pcg(const FusedArgs& a, unsigned char* sm, const Geo* sgeo,
         cur.pend = ts->pend[q];
         const SLevel P = slev(a, sm, sgeo, q);
         FCLK_BEGIN
-        cycle_up<Tm>(a, P, L, child, P.p + cur.step * 4 * P.PP, (Tm::kCta && q == 0 && top_reg) ? &rv0 : nullptr);
+        cycle_up(a, P, L, child, P.p + cur.step * 4 * P.PP, (q == 0 && top_reg) ? &rv0 : nullptr);
         FCLK_END(3, q)
         resume = true;
     }
-    if constexpr (Tm::kCta) {
-        FCLK_REPORT
-    }
-}
-
-// nonlinear_pcg(m0) with the K-cycle below it; returns the top level's PCG
-// state (alphas, nval), the directions stay in shared memory.
-__device__ void tier_run(const FusedArgs& a, unsigned char* sm, const Geo* sgeo, const double* inv, double* red,
-                         const RV& rv0, bool top_reg, TierSM* ts) {
-    const int nl = a.last - a.m0 + 1;
-    int qw = nl;   // first level run by warp 0 (the top level always by the CTA)
-    for (int q = 1; q < nl; ++q)
-        if (sgeo[q].n <= kWarpTierMax) {
-            qw = q;
-            break;
-        }
-    tier_pcg<TeamCta>(a, sm, sgeo, inv, red, rv0, top_reg, ts, 0, qw);
+    FCLK_REPORT
 }
 
 __global__ void __launch_bounds__(kThreads, 1) k_fused_pcg(const __grid_constant__ FusedArgs a) {
