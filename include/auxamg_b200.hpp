@@ -44,6 +44,7 @@ using geometry_error = auxamg::geometry_error;
 using definiteness_error = auxamg::definiteness_error;
 using singular_error = auxamg::singular_error;
 using io_error = auxamg::io_error;
+using parse_error = auxamg::parse_error;
 #else
 class error : public std::runtime_error { public: using std::runtime_error::runtime_error; };
 class size_error : public error { public: using error::error; };
@@ -54,6 +55,15 @@ class geometry_error : public error { public: using error::error; };
 class definiteness_error : public error { public: using error::error; };
 class singular_error : public error { public: using error::error; };
 class io_error : public error { public: using error::error; };
+class parse_error : public error {
+public:
+    parse_error(const std::string& what, long line)
+        : error(what + " (line " + std::to_string(line) + ")"), line_(line) {}
+    long line() const noexcept { return line_; }
+
+private:
+    long line_;
+};
 #endif
 /// Device failure (no reference analogue).
 class device_error : public error { public: using error::error; };
@@ -69,8 +79,13 @@ inline void throw_status(aux_status s, const char* msg) {
         case AUX_GEOMETRY_ERROR: throw geometry_error(m);
         case AUX_DEFINITENESS_ERROR: throw definiteness_error(m);
         case AUX_SINGULAR_ERROR: throw singular_error(m);
-        case AUX_IO_ERROR:
-        case AUX_PARSE_ERROR: throw io_error(m);
+        case AUX_IO_ERROR: throw io_error(m);
+        case AUX_PARSE_ERROR: {   // what() ends in " (line N)" (errors.hpp:67-76)
+            const size_t k = m.rfind(" (line ");
+            if (k != std::string::npos && m.size() > k + 8 && m.back() == ')')
+                throw parse_error(m.substr(0, k), std::stol(m.substr(k + 7, m.size() - k - 8)));
+            throw parse_error(m, -1);
+        }
         default: throw device_error(m);
     }
 }
@@ -93,7 +108,9 @@ struct CycleOptions {
     int max_directions = 0;
 };
 
-/// auxamg::SolveResult (cycle.hpp:47-55).
+/// auxamg::SolveResult (cycle.hpp:47-55).  Converts to any struct with the
+/// reference's field names (e.g. auxamg::SolveResult itself), so a caller
+/// written against the reference keeps its result types.
 struct SolveResult {
     std::vector<double> u;
     std::vector<double> residual_history;
@@ -102,14 +119,39 @@ struct SolveResult {
     double setup_seconds = 0.0;
     double solve_seconds = 0.0;
     double total_seconds = 0.0;
+
+    template <class T>
+        requires requires(T t) { t.u; t.residual_history; t.iterations; t.converged; t.solve_seconds; }
+    operator T() const {
+        T t{};
+        t.u = u;
+        t.residual_history = residual_history;
+        t.iterations = iterations;
+        t.converged = converged;
+        t.setup_seconds = setup_seconds;
+        t.solve_seconds = solve_seconds;
+        t.total_seconds = total_seconds;
+        return t;
+    }
 };
 
-/// auxamg::HierarchyStats (hierarchy.hpp:388-393).
+/// auxamg::HierarchyStats (hierarchy.hpp:388-393); converts like SolveResult.
 struct HierarchyStats {
     int levels = 0;
     std::vector<long> sizes;
     std::vector<long> nnz;
     double operator_complexity = 1.0;
+
+    template <class T>
+        requires requires(T t) { t.levels; t.sizes; t.nnz; t.operator_complexity; }
+    operator T() const {
+        T t{};
+        t.levels = levels;
+        t.sizes.assign(sizes.begin(), sizes.end());
+        t.nnz.assign(nnz.begin(), nnz.end());
+        t.operator_complexity = operator_complexity;
+        return t;
+    }
 };
 
 /// Device-resident auxamg::Hierarchy; move-only RAII owner of the GPU state.
@@ -235,5 +277,40 @@ inline HierarchyStats stats(const Hierarchy& h) {
 
 /// set_num_threads(n) — parallel.hpp:43-45; accepted, no effect on the GPU path.
 inline void set_num_threads(int n) { aux_set_num_threads(n); }
+
+/// read_matrix_market(path) — matrix_market.hpp:33-104, multithreaded parse;
+/// Csr is any CSR type with the reference's fields (auxamg::CsrMatrix).
+template <class Csr>
+Csr read_matrix_market(const std::string& path, int threads = 0) {
+    aux_file_data* d = nullptr;
+    char msg[512];
+    throw_status(aux_read_matrix_market(path.c_str(), threads, &d, msg, sizeof msg), msg);
+    int64_t n = 0, m = 0, nnz = 0;
+    aux_file_data_sizes(d, &n, &m, &nnz);
+    Csr A{};
+    A.n_rows = static_cast<int>(n);
+    A.n_cols = static_cast<int>(m);
+    A.row_ptr.resize(static_cast<size_t>(n) + 1);
+    A.col_idx.resize(static_cast<size_t>(nnz));
+    A.values.resize(static_cast<size_t>(nnz));
+    aux_file_data_copy(d, A.row_ptr.data(), A.col_idx.data(), A.values.data());
+    aux_file_data_destroy(d);
+    return A;
+}
+
+/// read_coords(path) — problems.hpp:313-330; Point is any {double x, y}.
+template <class Point>
+std::vector<Point> read_coords(const std::string& path, int threads = 0) {
+    static_assert(sizeof(Point) == 2 * sizeof(double), "points must be {double x, y}");
+    aux_file_data* d = nullptr;
+    char msg[512];
+    throw_status(aux_read_coords(path.c_str(), threads, &d, msg, sizeof msg), msg);
+    int64_t n = 0;
+    aux_file_data_sizes(d, &n, nullptr, nullptr);
+    std::vector<Point> pts(static_cast<size_t>(n));
+    aux_file_data_copy(d, pts.data(), nullptr, nullptr);
+    aux_file_data_destroy(d);
+    return pts;
+}
 
 }  // namespace auxamg_b200

@@ -350,3 +350,27 @@ def ref_write_matrix_market(A, path: str) -> None:
     st = lib.ref_write_matrix_market(C.byref(v), path.encode(), msg, 512)
     if st:
         raise OSError(msg.value.decode())
+
+
+def ref_assemble(mesh):
+    """LinearSystem from the reference's assemble_fem_triangle (problems.hpp:152-193, f = 1)."""
+    from paper_1209_5421_b200 import problems as P
+    lib = _io_lib()
+    if not getattr(lib, "_asm_typed", False):
+        lib.ref_assemble_mesh.restype = C.c_void_p
+        lib.ref_assemble_mesh.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_int]
+        lib._asm_typed = True
+    nd = np.ascontiguousarray(mesh.nodes, np.float64)
+    tr = np.ascontiguousarray(mesh.triangles, np.int32)
+    bd = np.ascontiguousarray(mesh.boundary, np.int32)
+    h = lib.ref_assemble_mesh(nd.ctypes.data, nd.shape[0], tr.ctypes.data, tr.shape[0], bd.ctypes.data, bd.size)
+    if not h:
+        raise ValueError("reference assembly failed")
+    try:
+        N, nnz = lib.ref_gen_n(h), lib.ref_gen_nnz(h)
+        A = P.CsrMatrix(N, N, _arr(lib.ref_gen_row_ptr(h), N + 1, np.int32), _arr(lib.ref_gen_col_idx(h), nnz, np.int32),
+                        _arr(lib.ref_gen_values(h), nnz, np.float64))
+        return P.LinearSystem(A, _arr(lib.ref_gen_b(h), N, np.float64),
+                              _arr(lib.ref_gen_xy(h), 2 * N, np.float64).reshape(N, 2))
+    finally:
+        lib.ref_gen_free(h)

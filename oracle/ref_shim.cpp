@@ -415,6 +415,28 @@ int ref_read_coords(const char* path, void** out, int64_t* n, char* msg, size_t 
     else *out = g;
     return st;
 }
+// assemble_fem_triangle (problems.hpp:152-193, f = 1) of a given mesh
+void* ref_assemble_mesh(const double* xy, int n_nodes, const int* tris, int n_tris, const int* bnd, int n_bnd) {
+    auto* g = new RefGen;
+    try {
+        g->mesh.nodes.resize(n_nodes);
+        for (int i = 0; i < n_nodes; ++i) g->mesh.nodes[i] = {xy[2 * i], xy[2 * i + 1]};
+        g->mesh.triangles.resize(n_tris);
+        for (int e = 0; e < n_tris; ++e) g->mesh.triangles[e] = {tris[3 * e], tris[3 * e + 1], tris[3 * e + 2]};
+        g->mesh.boundary_nodes.assign(bnd, bnd + n_bnd);
+        g->sys = auxamg::assemble_fem_triangle(g->mesh, 1.0);
+        g->xy.resize(2 * g->sys.coords.size());
+        for (std::size_t i = 0; i < g->sys.coords.size(); ++i) {
+            g->xy[2 * i] = g->sys.coords[i].x;
+            g->xy[2 * i + 1] = g->sys.coords[i].y;
+        }
+    } catch (...) {
+        delete g;
+        return nullptr;
+    }
+    return g;
+}
+
 int ref_write_matrix_market(const aux_csr_view* Av, const char* path, char* msg, size_t len) {
     return guarded(msg, len, [&] { auxamg::write_matrix_market(to_csr(Av), path); });
 }

@@ -122,11 +122,15 @@ struct Finest {
     int big_cta_begin[4] = {0, 0, 0, 0};        // within a colour: first block with > 32 members
     DBuf<int> big_ids;        // cell ids (colour-major), sorted by colour
     DBuf<double> scratch;     // 2N: colour-pass residuals + big-block solutions
-    // block_solve = 0: explicit inverse of every block (s >= 1), column-major
-    // s*s at inv_off[g]; per row {inv_off of its cell, q | s << 16}
-    DBuf<double> inv;
+    // block_solve = 0: explicit inverse of every block, column-major s x s:
+    // blocks of <= kSmallBlock members in the row-anchored pool inv_s (at
+    // kSmallBlock * first row), larger ones at inv_off[g] in inv; per row one
+    // byte meta8 = q | s << 4 (0xff when s > 15) and, for rows of blocks above
+    // kSmallBlock, rmeta = {inv_off of its cell, q | s << 16}
+    DBuf<double> inv, inv_s;
     DBuf<int> inv_off;        // n_L + 1
-    DBuf<int2> rmeta;         // N
+    DBuf<int2> rmeta;         // N (read for rows of larger blocks only)
+    DBuf<uint8_t> meta8;      // N
     int big_huge_begin[4] = {0, 0, 0, 0};       // within a colour: first block with > kWarpInvMax members
     int color_row[5] = {0, 0, 0, 0, 0};   // first finest row of each colour class (+ N)
     bool color_clean = true;  // check_color_locality (smoother.hpp:217-231) empty
@@ -158,6 +162,7 @@ struct DistInfo {
 
 constexpr int kTileBlock = 8;   // blocks up to this size: one thread per block
 constexpr int kWarpInvMax = 320;   // inverse mode: blocks up to this size are one CTA task of k_bgs_inv
+constexpr int kSmallBlock = 4;     // inverse mode: blocks up to this size use the row-anchored pool
 
 // Live CUDA-event profile of one solve (aux_profile_enable / aux_profile_read).
 // Kinds: 0 finest colour pass, 1 outer A z + dots, 2 finest residual +

@@ -364,17 +364,17 @@ __device__ __forceinline__ bool factor_small(const int* __restrict__ rp, const i
 }
 
 // factor_blocks (smoother.hpp:129-156) for 2 <= s <= 16: one thread extracts the
-// principal block and factors it (lu_factor order): s <= 6 in registers (and
-// inverted there when inv_off is given), otherwise in place in the pool.
+// principal block and factors it (lu_factor order) in registers, inverted
+// there into the row-anchored pool when inv_s is given (block_solve = 0).
 __global__ void k_factor_cells(const int* __restrict__ bptr, const int* __restrict__ rp, const int* __restrict__ col,
                                const double* __restrict__ v, Geo g, const int* __restrict__ off,
                                double* __restrict__ lu, int* __restrict__ perm, unsigned long long* err,
-                               const int* __restrict__ inv_off, double* __restrict__ inv) {
+                               double* __restrict__ inv_s) {
     GSTRIDE(gid, g.n) {
         const int r0 = bptr[gid], s = bptr[gid + 1] - r0;
         if (s < 2 || s > 4) continue;   // 5+ members: k_factor_warp / k_factor_cta_smem / k_factor_big
         {
-            double* iv = inv_off ? inv + inv_off[gid] : nullptr;
+            double* iv = inv_s ? inv_s + (size_t)kSmallBlock * r0 : nullptr;   // row-anchored pool
             double* f = lu + off[gid];
             bool ok = true;
             switch (s) {
@@ -415,18 +415,27 @@ __global__ void k_factor_big(const int* __restrict__ ids, const int* __restrict_
 // from the reference-order LU factors (columns = LU solves of unit vectors)
 // and stored column-major, so the lanes owning the rows of one block read
 // consecutive addresses.  Singletons store 1 / a_ii.
+// Blocks of <= kSmallBlock members keep their inverse in a row-anchored pool
+// (column-major s x s at kSmallBlock * first row; s^2 <= kSmallBlock * s), so
+// a colour pass finds it from the row index alone and loads a window's
+// inverses with one coalesced burst; larger blocks use the offset pool.
 __global__ void k_inv_sizes(const int* __restrict__ bptr, int nL, int* __restrict__ cnt) {
     GSTRIDE(g, nL) {
         const int s = bptr[g + 1] - bptr[g];
-        cnt[g] = s * s;
+        cnt[g] = s <= kSmallBlock ? 0 : s * s;
     }
 }
 
+// per row: one byte q | s << 4 for blocks of <= 15 members (0xff beyond), and
+// for rows of blocks above kSmallBlock the pool offset + (q, s) in rmeta
 __global__ void k_rmeta(const int* __restrict__ bptr, const int* __restrict__ inv_off, int nL,
-                        int2* __restrict__ meta) {
+                        int2* __restrict__ meta, uint8_t* __restrict__ meta8) {
     GSTRIDE(g, nL) {
         const int r0 = bptr[g], s = bptr[g + 1] - r0, off = inv_off[g];
-        for (int q = 0; q < s; ++q) meta[r0 + q] = make_int2(off, q | (s << 16));
+        for (int q = 0; q < s; ++q) {
+            meta8[r0 + q] = s <= 15 ? (uint8_t)(q | (s << 4)) : (uint8_t)0xff;
+            if (s > kSmallBlock) meta[r0 + q] = make_int2(off, q | (s << 16));
+        }
     }
 }
 
@@ -463,18 +472,15 @@ __device__ inline void lu_solve_col(const double* lu, int ld, const int* perm, i
 }
 
 __global__ void k_inv_cells(const int* __restrict__ bptr, const int* __restrict__ rp, const int* __restrict__ col,
-                            const double* __restrict__ v, int nL, const int* __restrict__ lu_off,
-                            const double* __restrict__ lu, const int* __restrict__ perm,
-                            const int* __restrict__ inv_off, double* __restrict__ inv) {
+                            const double* __restrict__ v, int nL, double* __restrict__ inv_s) {
     GSTRIDE(g, nL) {
         const int r0 = bptr[g], s = bptr[g + 1] - r0;
-        double* out = inv + inv_off[g];
         if (s == 1) {
             double d = 0.0;
             for (int p = rp[r0]; p < rp[r0 + 1]; ++p)
                 if (col[p] == r0) d = v[p];
-            out[0] = 1.0 / d;
-        }   // s >= 2: inverted where it is factored (k_factor_cells / k_factor_warp / k_factor_cta_smem)
+            inv_s[(size_t)kSmallBlock * r0] = 1.0 / d;
+        }   // 2 <= s <= 4: inverted where factored (k_factor_cells); s >= 5: the offset pool
     }
 }
 
@@ -1061,17 +1067,17 @@ void finest_blocks(aux_hierarchy* h, const Geo& gL, unsigned long long& sing, in
             const int pool = read1(F.inv_off.p + nL, s);
             F.inv.alloc(std::max(pool, 1));
             F.rmeta.alloc(n);
-            k_rmeta<<<grid_for(nL), kT, 0, s>>>(F.bptr.p, F.inv_off.p, nL, F.rmeta.p);
+            F.meta8.alloc(n);
+            F.inv_s.alloc((size_t)kSmallBlock * n);
+            k_rmeta<<<grid_for(nL), kT, 0, s>>>(F.bptr.p, F.inv_off.p, nL, F.rmeta.p, F.meta8.p);
             AUX_LAUNCHED(1);
         }
         const bool inv_mode = h->gpu.block_solve == 0;
         k_factor_cells<<<grid_for(nL), kT, 0, s>>>(F.bptr.p, F.rp.p, F.col.p, F.v.p, gL, F.cell_lu_off.p, F.big_lu.p,
-                                                   F.big_perm.p, err.p, inv_mode ? F.inv_off.p : nullptr,
-                                                   inv_mode ? F.inv.p : nullptr);
+                                                   F.big_perm.p, err.p, inv_mode ? F.inv_s.p : nullptr);
         AUX_LAUNCHED(1);
         if (inv_mode) {   // singletons: 1 / a_ii
-            k_inv_cells<<<grid_for(nL), kT, 0, s>>>(F.bptr.p, F.rp.p, F.col.p, F.v.p, nL, F.cell_lu_off.p,
-                                                    F.big_lu.p, F.big_perm.p, F.inv_off.p, F.inv.p);
+            k_inv_cells<<<grid_for(nL), kT, 0, s>>>(F.bptr.p, F.rp.p, F.col.p, F.v.p, nL, F.inv_s.p);
             AUX_LAUNCHED(1);
         }
         // 5..32 members: 4 blocks per warp up to 8 members, 2 up to 16, 1 up to 32

@@ -555,15 +555,20 @@ __device__ __forceinline__ double resid_fma(const int* __restrict__ rp, const in
     return s;
 }
 
+constexpr int kSmallInvWords = 5 * 32;   // row-anchored inverses of window rows 0..39 (blocks start in 0..31)
+
 __global__ void __launch_bounds__(256, 4) k_bgs_inv(const int* __restrict__ rp, const int* __restrict__ col,
                                                 const double* __restrict__ v, const double* __restrict__ b,
-                                                const int2* __restrict__ meta, const double* __restrict__ inv,
+                                                const uint8_t* __restrict__ meta8, const int2* __restrict__ meta,
+                                                const double* __restrict__ inv_s, const double* __restrict__ inv,
                                                 const int* __restrict__ big_ids, const int* __restrict__ bptr,
                                                 const int* __restrict__ inv_off, const double* xin, double* xout,
                                                 const double* __restrict__ res, int r0, int r1, int j0, int nbig,
                                                 int zero) {
     static_assert(kWarpInvMax >= 64 + 256, "window buffer");
+    static_assert(kSmallInvWords >= kSmallBlock * 31 + kSmallBlock * kSmallBlock, "small-block inverse window");
     __shared__ double sr[8][kWarpInvMax];
+    __shared__ double si[8][kSmallInvWords];
     const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
     if ((int)blockIdx.x < nbig) {   // one block of 33..kWarpInvMax members per CTA
         const int g = big_ids[j0 + blockIdx.x];
@@ -610,25 +615,46 @@ __global__ void __launch_bounds__(256, 4) k_bgs_inv(const int* __restrict__ rp, 
     if (w0 >= r1) return;
     const int ra = w0 + lane, rb = w0 + 32 + lane;
     const bool va = ra < r1, vb = rb < r1;
-    // every load whose address is known up front is issued together
-    const int2 ma = va ? meta[ra] : make_int2(0, 0);
-    const int2 mb = vb ? meta[rb] : make_int2(0, 0);
+    // every load whose address is known up front is issued together, the
+    // inverses of the window's small blocks first (row-anchored pool: one
+    // coalesced burst that depends on nothing)
+    double isv[kSmallInvWords / 32];
+#pragma unroll
+    for (int k = 0; k < kSmallInvWords / 32; ++k) {
+        const long e = (long)kSmallBlock * w0 + lane + 32 * k;
+        isv[k] = e < (long)kSmallBlock * r1 ? __ldcs(inv_s + e) : 0.0;
+    }
+    const unsigned m8a = va ? meta8[ra] : 0u, m8b = vb ? meta8[rb] : 0u;
     const int pa0 = va ? rp[ra] : 0, pa1 = va ? rp[ra + 1] : 0;
     const int pc0 = vb ? rp[rb] : 0, pc1 = vb ? rp[rb + 1] : 0;
     const double* bres = (res && !zero) ? res : b;   // precomputed residual rows (split mode)
     double acc_a = va ? bres[ra] : 0.0, acc_b = vb ? bres[rb] : 0.0;
     const double xa = (va && !zero) ? xin[ra] : 0.0, xb = (vb && !zero) ? xin[rb] : 0.0;
-    const int qa = ma.y & 0xffff, sa = ma.y >> 16, qb = mb.y & 0xffff, sb = mb.y >> 16;
+    // (q, s) from the byte; rows of blocks above kSmallBlock read rmeta
+    // (pool offset, and q / s beyond 15)
+    int qa = m8a & 15, sa = m8a >> 4, qb = m8b & 15, sb = m8b >> 4;
+    int2 ma = make_int2(0, 0), mb = make_int2(0, 0);
+    if (va && (m8a == 0xffu || sa > kSmallBlock)) {
+        ma = meta[ra];
+        qa = ma.y & 0xffff;
+        sa = ma.y >> 16;
+    }
+    if (vb && (m8b == 0xffu || sb > kSmallBlock)) {
+        mb = meta[rb];
+        qb = mb.y & 0xffff;
+        sb = mb.y >> 16;
+    }
     const bool oa = va && sa <= 32 && ra - qa >= w0;
     const bool ob = vb && sb <= 32 && rb - qb < w0 + 32;
     if (!__any_sync(0xffffffffu, oa)) return;   // only rows of larger blocks here
-    const int ea = oa ? sa : 0, eb = ob ? sb : 0;
-    // the window's inverse entries are one contiguous range: pull them towards
-    // L2 now, so the inverse chunks do not pay a full DRAM round trip after
-    // the residual chain (C2: pre + post smoothing -0.14 ms, C3 -0.37 ms)
-    const int ib0 = (int)__reduce_min_sync(0xffffffffu, oa ? (unsigned)ma.x : (ob ? (unsigned)mb.x : 0x7fffffffu));
-    const int ib1 = (int)__reduce_max_sync(0xffffffffu, ob ? (unsigned)(mb.x + sb * sb)
-                                                            : (oa ? (unsigned)(ma.x + sa * sa) : 0u));
+    const bool sma = oa && sa <= kSmallBlock, smb = ob && sb <= kSmallBlock;   // row-anchored inverses
+    const int ea = (oa && !sma) ? sa : 0, eb = (ob && !smb) ? sb : 0;           // offset-pool inverses
+    // the window's offset-pool entries are one contiguous range: pull them
+    // towards L2 now, so the inverse chunks do not pay a full DRAM round trip
+    // after the residual chain
+    const int ib0 = (int)__reduce_min_sync(0xffffffffu, ea ? (unsigned)ma.x : (eb ? (unsigned)mb.x : 0x7fffffffu));
+    const int ib1 = (int)__reduce_max_sync(0xffffffffu, eb ? (unsigned)(mb.x + sb * sb)
+                                                            : (ea ? (unsigned)(ma.x + sa * sa) : 0u));
     for (int e = ib0 + lane * 16; e < ib1; e += 32 * 16)
         asm volatile("prefetch.global.L2 [%0];" ::"l"(inv + e));
     if (!zero && !res) {
@@ -664,6 +690,22 @@ __global__ void __launch_bounds__(256, 4) k_bgs_inv(const int* __restrict__ rp, 
     }
     R[lane] = oa ? acc_a : 0.0;
     R[32 + lane] = ob ? acc_b : 0.0;
+    double* SI = si[wl];
+#pragma unroll
+    for (int k = 0; k < kSmallInvWords / 32; ++k) SI[lane + 32 * k] = isv[k];
+    __syncwarp();
+    // blocks of <= kSmallBlock members: inv(q, j) = pool[kSmallBlock c0 + j s + q], j ascending
+    double da = 0.0, db = 0.0;
+    if (sma) {
+        const int c0 = lane - qa;   // window-local first row of the block (>= 0)
+        const double* iv = SI + kSmallBlock * c0 + qa;
+        for (int j = 0; j < sa; ++j) da = fma(iv[j * sa], R[c0 + j], da);
+    }
+    if (smb) {
+        const int c0 = 32 + lane - qb;
+        const double* iv = SI + kSmallBlock * c0 + qb;
+        for (int j = 0; j < sb; ++j) db = fma(iv[j * sb], R[c0 + j], db);
+    }
     // delta = A_gg^{-1} r_g: the inverses of the owned blocks are one
     // contiguous range of the pool (cell order), streamed coalesced through
     // the chunk buffer; every owned row then takes its entries
@@ -671,7 +713,6 @@ __global__ void __launch_bounds__(256, 4) k_bgs_inv(const int* __restrict__ rp, 
     const int fa = ma.x + qa, fb = mb.x + qb;   // entry (q, 0) of each row
     const double* Ra = R + (lane - qa);
     const double* Rb = R + (32 + lane - qb);
-    double da = 0.0, db = 0.0;
     for (int cs = ib0; cs < ib1; cs += 256) {
         __syncwarp();
         double t[8];
@@ -1312,7 +1353,7 @@ void finest_bgs_pass(Ctx& c, int color, const double* f, double* u, bool zero, d
         const long ctas = (jh - jm) + ((long)(r1 - r0) + 255) / 256;
         const double* resid = nullptr;   // residual rows computed in the kernel
         if (ctas > 0) {
-            k_bgs_inv<<<(unsigned)ctas, 256, 0, c.s>>>(F.rp.p, F.col.p, F.v.p, f, F.rmeta.p, F.inv.p,
+            k_bgs_inv<<<(unsigned)ctas, 256, 0, c.s>>>(F.rp.p, F.col.p, F.v.p, f, F.meta8.p, F.rmeta.p, F.inv_s.p, F.inv.p,
                                                                    F.big_ids.p, F.bptr.p, F.inv_off.p, xin, u, resid,
                                                                    r0, r1, jm, jh - jm, z);
             AUX_LAUNCHED(1);

@@ -10,9 +10,14 @@ or `--backend reference` (the reference compiled in place, oracle/_ref).
     python -m paper_1209_5421_b200.runner --gen poisson2d --n 257 --n 513 --format csv
     python -m paper_1209_5421_b200.runner --gen graded --n 2049 --backend b200 --format jsonl
 
-File sources (Matrix Market, meshes) are the reference's I/O and out of scope
-(DESIGN.md section 8); `--gen` accepts the reference's `poisson2d` plus the
-harness families of SURVEY 8(d): `split`, `jitter`, `graded`, `disk`, `jump`.
+Sources as in load_problem (runner.hpp:64-83): `--gen` (the reference's
+`poisson2d` plus the harness families of SURVEY 8(d): `split`, `jitter`,
+`graded`, `disk`, `jump`), `--matrix F --coords F` (Matrix Market + one "x y"
+line per DoF, b = 1) or `--mesh F` (P1 assembly, f = 1) -- files parsed by the
+library's multithreaded readers (csrc/io.cpp); with the b200 backend a mesh
+is assembled on the GPU (aux_assemble_p1).  `--gpus P` runs the multi-GPU
+code path with P parts of one process on this process's device (the
+in-process transport); one process per GPU is bench.py's torchrun path.
 """
 from __future__ import annotations
 
@@ -93,17 +98,41 @@ def _solve_reference(sysm, setup_opts, cycle_opts, threads):
     return st, res, setup_s
 
 
-def run_one(gen: str, size: int, backend: str = "b200", gpus: int = 1, setup_opts=None, cycle_opts=None,
-            threads: int = 1) -> RunReport:
+def load_problem(gen: str | None, size: int, matrix: str = "", coords: str = "", mesh: str = "",
+                 backend: str = "b200", threads: int = 0) -> problems.LinearSystem:
+    """load_problem (runner.hpp:64-83): one source -> LinearSystem."""
+    from . import api
+    if gen:
+        if gen not in GENERATORS:
+            raise api.ArgumentError(f"unknown generator '{gen}'")
+        return GENERATORS[gen](size)
+    if matrix:
+        if not coords:
+            raise api.ArgumentError("--matrix requires --coords (the method needs DoF coordinates)")
+        A = api.read_matrix_market(matrix, threads)
+        xy = api.read_coords(coords, threads)
+        if xy.shape[0] != A.n_rows:
+            raise api.SizeError("coordinate count does not match matrix order")
+        return problems.LinearSystem(A, np.ones(A.n_rows), xy)
+    m = api.read_mesh(mesh, threads)
+    if backend == "b200":   # assemble_fem_triangle on the GPU (SURVEY 8(f) rank 1)
+        A, b, xy = api.DeviceSystem(m.nodes, m.triangles, m.boundary).to_host()
+        return problems.LinearSystem(A, b, xy)
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle"))
+    import bindings as ob
+    return ob.ref_assemble(m)
+
+
+def run_one(gen: str | None, size: int, backend: str = "b200", gpus: int = 1, setup_opts=None, cycle_opts=None,
+            threads: int = 1, matrix: str = "", coords: str = "", mesh: str = "") -> RunReport:
     """run_one (runner.hpp:87-112): problem, setup, stats, solve, timings."""
     from . import api
     setup_opts = setup_opts or api.SetupOptions()
     cycle_opts = cycle_opts or api.CycleOptions()
-    if gen not in GENERATORS:
-        raise api.ArgumentError(f"unknown generator '{gen}'")
     t0 = time.perf_counter()
-    sysm = GENERATORS[gen](size)
-    rep = RunReport(label=f"{gen}-{size}", n=sysm.A.n_rows, nnz=sysm.A.nnz)
+    sysm = load_problem(gen, size, matrix, coords, mesh, backend)
+    label = f"{gen}-{size}" if gen else (matrix or mesh)
+    rep = RunReport(label=label, n=sysm.A.n_rows, nnz=sysm.A.nnz)
     if backend == "b200":
         st, r, setup_s = _solve_b200(sysm, gpus, setup_opts, cycle_opts)
     elif backend == "reference":
@@ -152,8 +181,11 @@ def write_jsonl(reports, out) -> None:
 def main(argv=None) -> int:
     from . import api
     ap = argparse.ArgumentParser(description="auxamg batch runner with a B200 backend")
-    ap.add_argument("--gen", required=True, choices=sorted(GENERATORS))
-    ap.add_argument("--n", type=int, action="append", required=True)
+    ap.add_argument("--gen", default="")
+    ap.add_argument("--n", type=int, action="append", default=[])
+    ap.add_argument("--matrix", default="")
+    ap.add_argument("--coords", default="")
+    ap.add_argument("--mesh", default="")
     ap.add_argument("--backend", default="b200", choices=["b200", "reference"])
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--threads", type=int, default=1)
@@ -168,7 +200,14 @@ def main(argv=None) -> int:
     try:
         co = api.CycleOptions(n_inner=a.n_inner, max_outer=a.max_outer, rtol=a.rtol)
         so = api.SetupOptions(coarsest_size=a.coarsest)
-        reports = [run_one(a.gen, n, a.backend, a.gpus, so, co, a.threads) for n in a.n]
+        if sum(bool(x) for x in (a.gen, a.matrix, a.mesh)) != 1:
+            raise api.ArgumentError("exactly one of --gen, --matrix, --mesh must be given")
+        if a.gen and not a.n:
+            raise api.ArgumentError("--gen requires at least one --n")
+        if a.gen:
+            reports = [run_one(a.gen, n, a.backend, a.gpus, so, co, a.threads) for n in a.n]
+        else:
+            reports = [run_one(None, 0, a.backend, a.gpus, so, co, a.threads, a.matrix, a.coords, a.mesh)]
     except api.ArgumentError as e:   # auxamg_cli.cpp:83-92: argument errors -> 1, others -> 3
         print(f"error: {e}", file=sys.stderr)
         return 1
