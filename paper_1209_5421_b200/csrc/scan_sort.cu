@@ -172,7 +172,9 @@ void exclusive_scan(const int* in, int* out, long n, cudaStream_t s) {
     k_scan_final<<<static_cast<unsigned>(nb), kScanThreads, 0, s>>>(in, n, bsum.p, out);
     AUX_LAUNCHED(3);
     AUX_CUDA(cudaGetLastError());
-    AUX_CUDA(cudaStreamSynchronize(s));   // bsum is freed on return
+    // no synchronisation: bsum goes back to this thread's allocator cache and
+    // is only handed out again to work of this thread, ordered on its stream
+    // (alloc.cu), so the scan stays asynchronous
 }
 
 void radix_sort_pairs(unsigned* keys, int* vals, long n, int nbits, cudaStream_t s, bool iota_vals) {
@@ -203,7 +205,7 @@ void radix_sort_pairs(unsigned* keys, int* vals, long n, int nbits, cudaStream_t
         AUX_CUDA(cudaMemcpyAsync(keys, ka, sizeof(unsigned) * n, cudaMemcpyDeviceToDevice, s));
         AUX_CUDA(cudaMemcpyAsync(vals, va, sizeof(int) * n, cudaMemcpyDeviceToDevice, s));
     }
-    AUX_CUDA(cudaStreamSynchronize(s));
+    // (scratch buffers return to the stream-ordered cache: no synchronisation)
 }
 
 }  // namespace auxb200

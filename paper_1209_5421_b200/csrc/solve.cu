@@ -652,10 +652,11 @@ __global__ void __launch_bounds__(256, 4) k_bgs_inv(const int* __restrict__ rp, 
     // the window's offset-pool entries are one contiguous range: pull them
     // towards L2 now, so the inverse chunks do not pay a full DRAM round trip
     // after the residual chain
-    const int ib0 = (int)__reduce_min_sync(0xffffffffu, ea ? (unsigned)ma.x : (eb ? (unsigned)mb.x : 0x7fffffffu));
+    int ib0 = (int)__reduce_min_sync(0xffffffffu, ea ? (unsigned)ma.x : (eb ? (unsigned)mb.x : 0x7fffffffu));
     const int ib1 = (int)__reduce_max_sync(0xffffffffu, eb ? (unsigned)(mb.x + sb * sb)
                                                             : (ea ? (unsigned)(ma.x + sa * sa) : 0u));
-    for (int e = ib0 + lane * 16; e < ib1; e += 32 * 16)
+    if (ib0 > ib1) ib0 = ib1;   // no offset-pool block in this window: empty range
+    for (long e = (long)ib0 + lane * 16; e < ib1; e += 32 * 16)
         asm volatile("prefetch.global.L2 [%0];" ::"l"(inv + e));
     if (!zero && !res) {
         // r = b - sum a x_prev in storage order (smoother.hpp:193-198): the
