@@ -59,8 +59,8 @@ PROFILE_KINDS = {0: "finest block Gauss-Seidel colour pass (k_bgs_inv)",
                  1: "finest CSR SpMV + fused dots (k_csr_spmv)",
                  2: "finest residual + restriction (k_rows + k_restrict_cells)",
                  3: "coarse K-cycle below the finest level (graph replay per finest visit)",
-                 4: "level-L 9-point pre-smoothing GS + residual + restriction (k_tile_down)",
-                 5: "level-L 9-point post-smoothing GS + ELL SpMV + dots (k_tile_up)"}
+                 4: "level-L 9-point pre-smoothing GS + residual + restriction (k_stream_down; k_tile_down below 1024 cells wide)",
+                 5: "level-L 9-point post-smoothing GS + ELL SpMV + dots (k_stream_up; k_tile_up below 1024 cells wide)"}
 
 
 def scaled(cfg, world):
@@ -412,12 +412,16 @@ def main():
     kind = max((0, 1, 2), key=lambda k: prof[k][1])   # dominant HBM-bound kernel of the timed solve
     n_l, tot_ms, bytes_l = prof[kind]
     achieved = bytes_l / (tot_ms / n_l * 1e-3) / 1e9 if n_l else 0.0
-    traffic = None
-    try:
+    traffic, tdb = None, {}
+    try:   # ncu DRAM read+write bytes per launch (tools/traffic_from_ncu.py)
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            traffic = json.load(f).get(cfg_name, {}).get(str(kind))
+            tdb = json.load(f).get(cfg_name, {})
+        traffic = tdb.get(str(kind))
     except Exception:
         pass
+    for k, ent in zip(prof, kernels.values()):
+        if str(k) in tdb:
+            ent["traffic"] = tdb[str(k)]
 
     out = {
         "metric": METRIC, "value": value, "unit": "ms/MDOF", "n_gpus": world, "steps": args.steps,

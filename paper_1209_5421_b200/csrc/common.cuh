@@ -262,7 +262,7 @@ __device__ bool grid_reduce(double (&v)[NV], const RedState& rs, double (&out)[N
 constexpr double kBreakdown = 1e-300;   // breakdown_energy, cycle.hpp:78
 struct Fin {
     int op;                    // 0 none, 1 alpha (e=s0, alpha=s1/e), 2 beta (-s0/e_in), 3 store s0,
-                               // 5/6 raw s0 / (s0, s1) into e_out
+                               // 5/6 raw s0 / (s0, s1) into e_out, 7 beta into sc[1] and *e_out
     double* sc;                // [0]=alpha [1]=beta [2]=dead
     const double* e_in;
     double* e_out;             // op 1: energy slot; op 3: destination
@@ -284,6 +284,10 @@ __device__ __forceinline__ void finalize(const Fin& f, const double* s) {
         }
     } else if (f.op == 2) {
         f.sc[1] = -s[0] / *f.e_in;
+    } else if (f.op == 7) {
+        const double beta = -s[0] / *f.e_in;
+        f.sc[1] = beta;
+        *f.e_out = beta;
     } else if (f.op == 3) {
         *f.e_out = s[0];
     } else if (f.op == 5) {        // raw sums for a cross-GPU all-reduce (solve.cu routed())

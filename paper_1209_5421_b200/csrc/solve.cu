@@ -269,6 +269,76 @@ __global__ void __launch_bounds__(kRedThreads) k_update(long n, double* __restri
 
 // The outer update u += alpha p; r -= alpha ap; s0 = r.r (same arithmetic as
 // k_update with assign = 0, upd_r = 1, norm = 1) with 16-byte accesses.
+// Outer MGS (next_direction, cycle.hpp:84-97) with A p deferred: the steps
+// j < K-1 only update p (p += beta_j p_j) and form p . Ap_{j+1}; the last
+// kernel updates p and builds ap = (((Az + beta_0 Ap_0) + beta_1 Ap_1) ...)
+// per element in the same order the per-step updates would -- bitwise the
+// same vectors, 5K + 2 instead of 7K vector passes for K kept directions.
+constexpr int kMaxDeferred = 96;
+struct ApList {
+    const double* ap[kMaxDeferred];
+};
+__global__ void __launch_bounds__(kRedThreads) k_mgs_p_vec(long n, double* __restrict__ p,
+                                                          const double* __restrict__ pj,
+                                                          const double* __restrict__ w, const double* beta_in,
+                                                          RedState rs, Fin fin) {
+    pdl_trigger();
+    pdl_wait();
+    const double beta = *beta_in;
+    double v[1] = {0.0};
+    double2* p2 = reinterpret_cast<double2*>(p);
+    const double2* pj2 = reinterpret_cast<const double2*>(pj);
+    const double2* w2 = reinterpret_cast<const double2*>(w);
+    const long n2 = n / 2, stride = (long)gridDim.x * blockDim.x;
+    for (long k = blockIdx.x * (long)blockDim.x + threadIdx.x; k < n2; k += stride) {
+        const double2 P = p2[k], J = __ldcs(pj2 + k), W = w2[k];
+        double2 pn;
+        pn.x = __dadd_rn(P.x, __dmul_rn(beta, J.x));
+        pn.y = __dadd_rn(P.y, __dmul_rn(beta, J.y));
+        p2[k] = pn;
+        v[0] = __dadd_rn(v[0], __dmul_rn(pn.x, W.x));
+        v[0] = __dadd_rn(v[0], __dmul_rn(pn.y, W.y));
+    }
+    double out[1];
+    if (grid_reduce<1>(v, rs, out) && threadIdx.x == 0) finalize(fin, out);
+}
+
+__global__ void __launch_bounds__(kRedThreads) k_mgs_final_vec(long n, double* __restrict__ p,
+                                                              const double* __restrict__ pj, double* __restrict__ ap,
+                                                              ApList dirs, int nk, const double* __restrict__ betas,
+                                                              const double* __restrict__ r, RedState rs, Fin fin) {
+    pdl_trigger();
+    pdl_wait();
+    const double blast = betas[nk - 1];
+    double v[2] = {0.0, 0.0};
+    double2* p2 = reinterpret_cast<double2*>(p);
+    double2* a2 = reinterpret_cast<double2*>(ap);
+    const double2* pj2 = reinterpret_cast<const double2*>(pj);
+    const double2* r2 = reinterpret_cast<const double2*>(r);
+    const long n2 = n / 2, stride = (long)gridDim.x * blockDim.x;
+    for (long k = blockIdx.x * (long)blockDim.x + threadIdx.x; k < n2; k += stride) {
+        const double2 P = p2[k], J = __ldcs(pj2 + k), R = r2[k];
+        double2 A = a2[k];
+        for (int j = 0; j < nk; ++j) {   // the per-step axpy(beta_j, Ap_j, ap), in order
+            const double2 B = __ldcs(reinterpret_cast<const double2*>(dirs.ap[j]) + k);
+            const double bj = betas[j];
+            A.x = __dadd_rn(A.x, __dmul_rn(bj, B.x));
+            A.y = __dadd_rn(A.y, __dmul_rn(bj, B.y));
+        }
+        double2 pn;
+        pn.x = __dadd_rn(P.x, __dmul_rn(blast, J.x));
+        pn.y = __dadd_rn(P.y, __dmul_rn(blast, J.y));
+        p2[k] = pn;
+        a2[k] = A;
+        v[0] = __dadd_rn(v[0], __dmul_rn(pn.x, A.x));
+        v[0] = __dadd_rn(v[0], __dmul_rn(pn.y, A.y));
+        v[1] = __dadd_rn(v[1], __dmul_rn(R.x, pn.x));
+        v[1] = __dadd_rn(v[1], __dmul_rn(R.y, pn.y));
+    }
+    double out[2];
+    if (grid_reduce<2>(v, rs, out) && threadIdx.x == 0) finalize(fin, out);
+}
+
 __global__ void __launch_bounds__(kRedThreads) k_update_vec(long n, double* __restrict__ u,
                                                            const double* __restrict__ p, double* __restrict__ r,
                                                            const double* __restrict__ ap, const double* sc,
@@ -1704,7 +1774,8 @@ void solve_device(aux_hierarchy* h, const double* b, long n_b, const aux_cycle_o
         h->w_b.alloc(n);
         h->w_tmp.alloc(nx);
     }
-    if (h->w_sc.n < (size_t)(8 + o->max_outer + 1)) h->w_sc.alloc(8 + o->max_outer + 1);
+    // scalars: [0..7] alpha, beta, dead, ... | energies per slot | betas of one MGS sweep
+    if (h->w_sc.n < (size_t)(8 + 2 * (o->max_outer + 1))) h->w_sc.alloc(8 + 2 * (o->max_outer + 1));
     if (!h->direct_only && h->lv.size() > 1 && (int)h->lv[1].pcg.p.size() != o->n_inner) {
         alloc_solve_levels(h, o->n_inner);
         h->graph_valid = false;
@@ -1767,6 +1838,9 @@ void solve_device(aux_hierarchy* h, const double* b, long n_b, const aux_cycle_o
         }
         std::deque<int> kept;
         std::vector<char> in_use(slots, 0);
+        // AUX_MGS_DEFERRED=0: per-step A p updates (k_mgs_vec), the bitwise-identical reference point
+        const char* mgs_env = std::getenv("AUX_MGS_DEFERRED");
+        const bool defer_ap = !(mgs_env && mgs_env[0] == '0');
         const bool vec_ok = (n % 2) == 0;   // device vectors are 256-byte aligned allocations
         double* r = h->w_r.p;
         double* u = h->w_u.p;
@@ -1792,9 +1866,13 @@ void solve_device(aux_hierarchy* h, const double* b, long n_b, const aux_cycle_o
             g_trace.mark(s, 3);
             ghost_exchange(c, p);
             prof_begin(c, 1);
+            // deferred A p (k_mgs_p_vec / k_mgs_final_vec): the betas of this sweep at betas[j]
+            double* betas = sc + 8 + o->max_outer + 1;
+            const bool deferred = defer_ap && vec_ok && !kept.empty() && (int)kept.size() <= kMaxDeferred;
             {
                 const Route rs0 = route(c, fd, kept.empty() ? Fin{1, sc, nullptr, e_slot}
-                                                             : Fin{2, sc, sc + 8 + kept[0], nullptr});
+                                                 : deferred ? Fin{7, sc, sc + 8 + kept[0], betas}
+                                                            : Fin{2, sc, sc + 8 + kept[0], nullptr});
                 k_csr_spmv<<<red_blocks(n), kRedThreads, 0, s>>>(n, OA.rp, OA.col, OA.v, p, ap, kept.empty() ? 0 : 1,
                                                                 r, kept.empty() ? nullptr : h->w_ap[kept[0]].p, rs,
                                                                 rs0.launch);
@@ -1802,7 +1880,23 @@ void solve_device(aux_hierarchy* h, const double* b, long n_b, const aux_cycle_o
                 routed(c, rs0);
             }
             prof_end(c, 1, spmv_bytes + (kept.empty() ? 16.0 : 8.0) * n);
-            if (!kept.empty()) {
+            if (deferred) {
+                for (size_t j = 1; j < kept.size(); ++j) {
+                    const Route rj = route(c, fd, Fin{7, sc, sc + 8 + kept[j], betas + j});
+                    k_mgs_p_vec<<<red_blocks(n / 2), kRedThreads, 0, s>>>(n, p, h->w_p[kept[j - 1]].p,
+                                                                         h->w_ap[kept[j]].p, betas + (j - 1), rs,
+                                                                         rj.launch);
+                    AUX_LAUNCHED(1);
+                    routed(c, rj);
+                }
+                ApList dl{};
+                for (size_t j = 0; j < kept.size(); ++j) dl.ap[j] = h->w_ap[kept[j]].p;
+                const Route rf = route(c, fd, Fin{1, sc, nullptr, e_slot});
+                k_mgs_final_vec<<<red_blocks(n / 2), kRedThreads, 0, s>>>(n, p, h->w_p[kept.back()].p, ap, dl,
+                                                                         (int)kept.size(), betas, r, rs, rf.launch);
+                AUX_LAUNCHED(1);
+                routed(c, rf);
+            } else if (!kept.empty()) {
                 for (size_t j = 1; j < kept.size(); ++j) {
                     const Route rj = route(c, fd, Fin{2, sc, sc + 8 + kept[j], nullptr});
                     if (vec_ok)

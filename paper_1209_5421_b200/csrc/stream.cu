@@ -168,7 +168,13 @@ __device__ __forceinline__ double row9(const double (&v)[9], const double* ring,
 // issued at its start (nothing it loads depends on the ring), so a phase costs
 // one memory latency plus five short smem chains; the stencil values of row
 // p+1 stay in registers and serve A z of that row in the next phase.
-__global__ void __launch_bounds__(kST, 2) k_stream_up(const __grid_constant__ TileUp a, RedState rs, Fin fin) {
+#ifndef AUX_STREAM_MINB
+#define AUX_STREAM_MINB 2
+#endif
+#ifndef AUX_STREAM_CARRY
+#define AUX_STREAM_CARRY 1   // 1: row p's stencil values carried in registers; 0: re-read (L2) for A z
+#endif
+__global__ void __launch_bounds__(kST, AUX_STREAM_MINB) k_stream_up(const __grid_constant__ TileUp a, RedState rs, Fin fin) {
     extern __shared__ double dsm[];
     double* ring = dsm;
     pdl_trigger();
@@ -207,8 +213,10 @@ __global__ void __launch_bounds__(kST, 2) k_stream_up(const __grid_constant__ Ti
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
             fp[c] = fc[c];
+#if AUX_STREAM_CARRY
 #pragma unroll
             for (int t = 0; t < 9; ++t) vp[c][t] = vc[c][t];
+#endif
         }
         const int r1 = p + 1, r2 = p + 2;
         const bool pas = live(r1, B.b0 - 2, B.b1 + 1), pas10 = pas && r1 >= B.b0 - 1;
@@ -260,6 +268,12 @@ __global__ void __launch_bounds__(kST, 2) k_stream_up(const __grid_constant__ Ti
         __syncthreads();
         // ---- z = u, A z and the step's inner products at row p (interior)
         if (spm) {
+#if !AUX_STREAM_CARRY
+            load9<0>(g, a.val, p, col, vp[0]);
+            load9<1>(g, a.val, p, col, vp[1]);
+            load9<2>(g, a.val, p, col, vp[2]);
+            load9<3>(g, a.val, p, col, vp[3]);
+#endif
             double y[4];
             y[0] = row9<0>(vp[0], ring, p, sc);
             y[1] = row9<1>(vp[1], ring, p, sc);
@@ -289,7 +303,7 @@ __global__ void __launch_bounds__(kST, 2) k_stream_up(const __grid_constant__ Ti
 // Phase p: pass0(p+1) | pass1(p+1) | pass2(p) | pass3(p) | residual(p-1),
 // barriers between stages, all loads at the phase start (row p-1's values for
 // the residual were read one or two phases earlier and hit L2).
-__global__ void __launch_bounds__(kST, 2) k_stream_down(const __grid_constant__ TileDown a) {
+__global__ void __launch_bounds__(kST, AUX_STREAM_MINB) k_stream_down(const __grid_constant__ TileDown a) {
     extern __shared__ double dsm[];
     double* ring = dsm;
     double* fring = dsm + kSD * 4 * kSRW;

@@ -334,3 +334,21 @@ def test_cluster_tier_lu_coarse_and_determinism(gpu_api):
     assert abs(r1.iterations - ref["iterations"]) <= 1
     assert np.max(np.abs(r1.u - ref["u"])) / np.max(np.abs(ref["u"])) <= U_TOL
     assert np.array_equal(r1.u, r2.u)
+
+
+@pytest.mark.parametrize("name,opts", [("jitter_48", dict()), ("graded_64", dict()), ("jump_48", dict(max_directions=3)),
+                                       ("graded2_40", dict(n_inner=3))])
+def test_outer_mgs_deferred_ap_bitwise(gpu_api, name, opts, monkeypatch):
+    """The outer MGS with A p deferred to one final pass (k_mgs_p_vec /
+    k_mgs_final_vec) builds bitwise the same directions as the per-step
+    updates (AUX_MGS_DEFERRED=0): identical u, history and iterations."""
+    s = PROBS[name]
+    g = gpu_api.GpuOptions(block_solve=1) if name == "graded2_40" else None
+    co = gpu_api.CycleOptions(**opts)
+    h = gpu_api.setup_hierarchy(s.A, s.coords, gpu=g)
+    r1 = gpu_api.solve(s.A, s.b, h, co)
+    monkeypatch.setenv("AUX_MGS_DEFERRED", "0")
+    r0 = gpu_api.solve(s.A, s.b, h, co)
+    assert r1.iterations == r0.iterations
+    assert np.array_equal(r1.u, r0.u)
+    assert np.array_equal(np.asarray(r1.residual_history), np.asarray(r0.residual_history))
