@@ -8,18 +8,17 @@
 //   k_count / scan                    member_ptr + active flags   (hierarchy.hpp:94-98)
 //   k_permute_csr                     finest rows grouped by aggregate, entries in
 //                                     caller storage order, columns relabelled
-//   k_cells_fused                     one warp-streamed pass over the permuted rows:
-//                                     assemble_coarse_finest (hierarchy.hpp:141-192,
-//                                     each entry summed into one of 9 register
-//                                     accumulators in the reference's order, so values
-//                                     are bitwise equal), factor_blocks for blocks of
-//                                     <= 4 members (+ inverses) and check_color_locality
-//   k_block_check / k_factor_warp/cta/big  factor_blocks of larger blocks (smoother.hpp:129-156)
+//   k_galerkin_L                      assemble_coarse_finest     (hierarchy.hpp:141-192):
+//                                     one thread per aggregate streams its contiguous
+//                                     rows and sums each entry into one of 9 register
+//                                     accumulators in the reference's order (the
+//                                     (agg_i, agg_j) sort is the aggregation sort above
+//                                     plus the 9-way slot key), so values are bitwise equal
+//   k_block_check / k_factor_big      factor_blocks (smoother.hpp:129-156)
 //   k_coarsen                         assemble_coarse_structured + coarsen_active
 //   k_dense / cta LU / k_inverse      dense_from_ell + lu_factor for the coarsest level
 #include <algorithm>
 #include <cstring>
-#include <type_traits>
 #include <numeric>
 #include <vector>
 
@@ -317,153 +316,71 @@ __global__ void k_lu_sizes(const int* __restrict__ bptr, int nL, int* __restrict
     }
 }
 
+// Blocks of S <= 4 members: extract, factor (reg_lu_factor: lu_factor's
+// operation order) and, for block_solve = 0, invert in registers.
+template <int S>
+__device__ __forceinline__ bool factor_small(const int* __restrict__ rp, const int* __restrict__ col,
+                                             const double* __restrict__ v, int r0, double* __restrict__ lu,
+                                             int* __restrict__ perm, double* __restrict__ inv) {
+    double a[S][S];
+#pragma unroll
+    for (int i = 0; i < S; ++i)
+#pragma unroll
+        for (int j = 0; j < S; ++j) a[i][j] = 0.0;
+#pragma unroll
+    for (int q = 0; q < S; ++q)
+        for (int p = rp[r0 + q]; p < rp[r0 + q + 1]; ++p) {
+            const int c = col[p] - r0;
+            const double x = v[p];
+#pragma unroll
+            for (int j = 0; j < S; ++j)
+                if (c == j) a[q][j] = x;
+        }
+    int pm[S];
+    if (!reg_lu_factor<S>(a, pm)) return false;
+#pragma unroll
+    for (int i = 0; i < S; ++i) {
+        perm[r0 + i] = pm[i];
+#pragma unroll
+        for (int j = 0; j < S; ++j) lu[i * S + j] = a[i][j];
+    }
+    if (inv) {   // column j of A^-1 = LU solve of e_j, column-major
+#pragma unroll
+        for (int j = 0; j < S; ++j) {
+            double e[S], x[S];
+#pragma unroll
+            for (int i = 0; i < S; ++i) e[i] = i == j ? 1.0 : 0.0;
+            reg_lu_solve<S>(a, pm, e, x);
+#pragma unroll
+            for (int i = 0; i < S; ++i) inv[j * S + i] = x[i];
+        }
+    }
+    return true;
+}
 
-// ---- one streaming pass over the finest rows for every per-cell setup
-// product that reads them: the level-L Galerkin row (assemble_coarse_finest,
-// hierarchy.hpp:141-192), the principal-block LU factors and inverses of
-// blocks of <= 4 members (factor_blocks, smoother.hpp:129-156; singletons
-// 1 / a_ii) and check_color_locality (smoother.hpp:217-231).  A warp takes 32
-// consecutive cells (their rows are contiguous in the permuted CSR): the lanes
-// stage chunks of the nonzeros coalesced in shared memory (column, value,
-// column's cell), then lane l walks cell l's entries in storage order, so
-// every sum runs in the reference's order exactly as in the thread-per-cell
-// kernels it replaces.  Blocks of 5+ members are factored by the warp / CTA
-// kernels as before.
-constexpr int kCfChunk = 256;
-__global__ void __launch_bounds__(256) k_cells_fused(const int* __restrict__ bptr, const int* __restrict__ rp,
-                                                     const int* __restrict__ col, const double* __restrict__ v,
-                                                     const int* __restrict__ cell, Geo g, int lump,
-                                                     double* __restrict__ val, int* __restrict__ dcnt,
-                                                     double* __restrict__ dmass, unsigned long long* total,
-                                                     const int* __restrict__ lu_off, double* __restrict__ lu,
-                                                     int* __restrict__ perm, unsigned long long* err,
-                                                     double* __restrict__ inv_s, int* color_flag) {
-    __shared__ int s_col[8][kCfChunk];
-    __shared__ int s_cc[8][kCfChunk];
-    __shared__ double s_v[8][kCfChunk];
-    const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
-    const int g0 = (blockIdx.x * 8 + wl) * 32;
-    if (g0 >= g.n) return;
-    const int gid = g0 + lane;
-    const bool valid = gid < g.n;
-    const int r0 = valid ? bptr[gid] : 0, r1 = valid ? bptr[gid + 1] : 0, sz = r1 - r0;
-    const int p0 = valid ? rp[r0] : 0, p1 = valid ? rp[r1] : 0;
-    const int P0 = __shfl_sync(0xffffffffu, p0, 0);
-    const int last = min(31, g.n - 1 - g0);
-    const int P1 = __shfl_sync(0xffffffffu, p1, last);
-    int t1 = 0, t2 = 0;
-    if (valid) xy_of_cm(g, gid, t1, t2);
-    double acc[9];
-#pragma unroll
-    for (int t = 0; t < 9; ++t) acc[t] = 0.0;
-    int nd = 0;
-    double mass = 0.0, diag = 0.0;
-    double a[4][4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) a[i][j] = 0.0;
-    bool ccol = false;
-    int q = 0, rowend = (valid && sz > 0) ? rp[r0 + 1] : 0;
-    const bool small = sz >= 2 && sz <= 4;
-    for (int cs = P0; cs < P1; cs += kCfChunk) {
-#pragma unroll
-        for (int k = 0; k < kCfChunk / 32; ++k) {
-            const int p = cs + lane + 32 * k;
-            int c = 0, cc = -1;
-            double x = 0.0;
-            if (p < P1) {
-                c = __ldcs(col + p);
-                x = __ldcs(v + p);
-                cc = cell[c];
+// factor_blocks (smoother.hpp:129-156) for 2 <= s <= 16: one thread extracts the
+// principal block and factors it (lu_factor order) in registers, inverted
+// there into the row-anchored pool when inv_s is given (block_solve = 0).
+__global__ void k_factor_cells(const int* __restrict__ bptr, const int* __restrict__ rp, const int* __restrict__ col,
+                               const double* __restrict__ v, Geo g, const int* __restrict__ off,
+                               double* __restrict__ lu, int* __restrict__ perm, unsigned long long* err,
+                               double* __restrict__ inv_s) {
+    GSTRIDE(gid, g.n) {
+        const int r0 = bptr[gid], s = bptr[gid + 1] - r0;
+        if (s < 2 || s > 4) continue;   // 5+ members: k_factor_warp / k_factor_cta_smem / k_factor_big
+        {
+            double* iv = inv_s ? inv_s + (size_t)kSmallBlock * r0 : nullptr;   // row-anchored pool
+            double* f = lu + off[gid];
+            bool ok = true;
+            switch (s) {
+                case 2: ok = factor_small<2>(rp, col, v, r0, f, perm, iv); break;
+                case 3: ok = factor_small<3>(rp, col, v, r0, f, perm, iv); break;
+                default: ok = factor_small<4>(rp, col, v, r0, f, perm, iv); break;
             }
-            s_col[wl][lane + 32 * k] = c;
-            s_v[wl][lane + 32 * k] = x;
-            s_cc[wl][lane + 32 * k] = cc;
-        }
-        __syncwarp();
-        const int pe = min(p1, cs + kCfChunk);
-        for (int p = max(p0, cs); p < pe; ++p) {
-            while (p >= rowend) rowend = rp[r0 + (++q) + 1];   // the row of entry p
-            const double x = s_v[wl][p - cs];
-            const int c = s_col[wl][p - cs], cc = s_cc[wl][p - cs];
-            if (val) {   // Galerkin: slot of the column's cell relative to this cell
-                int u1, u2;
-                xy_of_cm(g, cc, u1, u2);
-                const int slot = stencil_slot(u1 - t1, u2 - t2);
-                if (slot < 0) {
-                    if (lump) acc[0] = __dadd_rn(acc[0], x);
-                    ++nd;
-                    mass = __dadd_rn(mass, fabs(x));
-                } else {
-#pragma unroll
-                    for (int t = 0; t < 9; ++t)
-                        if (slot == t) acc[t] = __dadd_rn(acc[t], x);
-                }
-            }
-            if (small) {   // principal block entries (entries outside the pattern stay 0.0)
-                const int j = c - r0;
-#pragma unroll
-                for (int i = 0; i < 4; ++i)
-#pragma unroll
-                    for (int jj = 0; jj < 4; ++jj)
-                        if (q == i && j == jj) a[i][jj] = x;
-            } else if (sz == 1 && c == r0) {
-                diag = x;
-            }
-            if (x != 0.0 && cc != gid && (cc >> g.lq) == (gid >> g.lq)) ccol = true;
-        }
-        __syncwarp();
-    }
-    if (__any_sync(0xffffffffu, ccol) && lane == 0) atomicOr(color_flag, 1);
-    if (!valid) return;
-    if (val) {
-        if (sz == 0) acc[0] = 1.0;   // inactive identity row (preset_stencil, hierarchy.hpp:121-131)
-#pragma unroll
-        for (int t = 0; t < 9; ++t) val[(size_t)t * g.n + gid] = acc[t];
-        if (nd) {
-            dcnt[gid] = nd;
-            dmass[gid] = mass;
-            atomicAdd(total, (unsigned long long)nd);
+            if (!ok) atomicMin(err, (unsigned long long)lex_of_cm(g, (int)gid));
+            continue;
         }
     }
-    if (sz == 1 && inv_s) inv_s[(size_t)kSmallBlock * r0] = 1.0 / diag;
-    if (!small) return;
-    auto fin = [&](auto sc) {
-        constexpr int S = decltype(sc)::value;
-        double b[S][S];
-#pragma unroll
-        for (int i = 0; i < S; ++i)
-#pragma unroll
-            for (int j = 0; j < S; ++j) b[i][j] = a[i][j];
-        int pm[S];
-        if (!reg_lu_factor<S>(b, pm)) {
-            atomicMin(err, (unsigned long long)lex_of_cm(g, gid));
-            return;
-        }
-        double* f = lu + lu_off[gid];
-#pragma unroll
-        for (int i = 0; i < S; ++i) {
-            perm[r0 + i] = pm[i];
-#pragma unroll
-            for (int j = 0; j < S; ++j) f[i * S + j] = b[i][j];
-        }
-        if (inv_s) {   // column j of A^-1 = LU solve of e_j, column-major, row-anchored pool
-            double* iv = inv_s + (size_t)kSmallBlock * r0;
-#pragma unroll
-            for (int j = 0; j < S; ++j) {
-                double e[S], x[S];
-#pragma unroll
-                for (int i = 0; i < S; ++i) e[i] = i == j ? 1.0 : 0.0;
-                reg_lu_solve<S>(b, pm, e, x);
-#pragma unroll
-                for (int i = 0; i < S; ++i) iv[j * S + i] = x[i];
-            }
-        }
-    };
-    if (sz == 2) fin(std::integral_constant<int, 2>{});
-    else if (sz == 3) fin(std::integral_constant<int, 3>{});
-    else fin(std::integral_constant<int, 4>{});
 }
 
 // Extract and factor one block of more than 16 members per CTA.
@@ -549,6 +466,18 @@ __device__ inline void lu_solve_col(const double* lu, int ld, const int* perm, i
     }
 }
 
+__global__ void k_inv_cells(const int* __restrict__ bptr, const int* __restrict__ rp, const int* __restrict__ col,
+                            const double* __restrict__ v, int nL, double* __restrict__ inv_s) {
+    GSTRIDE(g, nL) {
+        const int r0 = bptr[g], s = bptr[g + 1] - r0;
+        if (s == 1) {
+            double d = 0.0;
+            for (int p = rp[r0]; p < rp[r0 + 1]; ++p)
+                if (col[p] == r0) d = v[p];
+            inv_s[(size_t)kSmallBlock * r0] = 1.0 / d;
+        }   // 2 <= s <= 4: inverted where factored (k_factor_cells); s >= 5: the offset pool
+    }
+}
 
 // Blocks of more than 16 members: one CTA per block, one column per thread.
 __global__ void k_inv_big(const int* __restrict__ ids, const int* __restrict__ bptr, const int* __restrict__ lu_off,
@@ -726,6 +655,20 @@ __global__ void __launch_bounds__(256) k_factor_cta_smem(const int* __restrict__
         }
     } else {
         for (int j = threadIdx.x; j < n; j += blockDim.x) lu_solve_col(da, ld, perm + r0, n, j, iv + (size_t)j * n, 1);
+    }
+}
+
+// check_color_locality (smoother.hpp:217-231): any nonzero coupling between
+// two distinct blocks of the same colour => keep per-colour snapshots.
+__global__ void k_color_check(const int* __restrict__ rp, const int* __restrict__ col, const double* __restrict__ v,
+                              const int* __restrict__ cell, long n, int lq, int* flag) {
+    GSTRIDE(i, n) {
+        const int gi = cell[i];
+        for (int p = rp[i]; p < rp[i + 1]; ++p) {
+            if (v[p] == 0.0) continue;
+            const int gj = cell[col[p]];
+            if (gi != gj && (gi >> lq) == (gj >> lq)) { atomicOr(flag, 1); break; }
+        }
     }
 }
 
@@ -1078,28 +1021,16 @@ void alloc_solve_levels(aux_hierarchy* h, int n_inner) {
     AUX_CUDA(cudaStreamSynchronize(h->stream));
 }
 
-// Level-L Galerkin outputs filled by the fused finest-cell pass (nullptr: the
-// caller assembles level L itself, as the multi-GPU setup does).
-struct GalerkinOut {
-    double* val;
-    int* dcnt;
-    double* dmass;
-    unsigned long long* total;
-    int lump;
-};
-
 // A: device CSR view (arrays not retained); xy: device coordinates.
 // factor_blocks (smoother.hpp:129-156) on the finest level: block census,
 // stored LU factors, explicit inverses (block_solve = 0), big-block lists and
 // check_color_locality.  Returns the lowest singular aggregate (~0: none) and
 // the colour-locality flag through the out-parameters.
-void finest_blocks(aux_hierarchy* h, const Geo& gL, unsigned long long& sing, int& color_flag,
-                   const GalerkinOut* gal) {
+void finest_blocks(aux_hierarchy* h, const Geo& gL, unsigned long long& sing, int& color_flag) {
     cudaStream_t s = h->stream;
     Finest& F = h->fine;
     const int n = F.n;
     const int nL = gL.n;
-    (void)n;
     {
         DBuf<unsigned long long> err(1);
         DBuf<int> flag(nL), mb(1);
@@ -1137,15 +1068,13 @@ void finest_blocks(aux_hierarchy* h, const Geo& gL, unsigned long long& sing, in
             AUX_LAUNCHED(1);
         }
         const bool inv_mode = h->gpu.block_solve == 0;
-        // blocks of <= 4 members, singletons, check_color_locality and (when
-        // asked) the level-L Galerkin rows in one pass over the finest rows
-        DBuf<int> cflag(1);
-        AUX_CUDA(cudaMemsetAsync(cflag.p, 0, sizeof(int), s));
-        k_cells_fused<<<(unsigned)((nL + 255) / 256), 256, 0, s>>>(
-            F.bptr.p, F.rp.p, F.col.p, F.v.p, F.cell.p, gL, gal ? gal->lump : 0, gal ? gal->val : nullptr,
-            gal ? gal->dcnt : nullptr, gal ? gal->dmass : nullptr, gal ? gal->total : nullptr, F.cell_lu_off.p,
-            F.big_lu.p, F.big_perm.p, err.p, inv_mode ? F.inv_s.p : nullptr, cflag.p);
+        k_factor_cells<<<grid_for(nL), kT, 0, s>>>(F.bptr.p, F.rp.p, F.col.p, F.v.p, gL, F.cell_lu_off.p, F.big_lu.p,
+                                                   F.big_perm.p, err.p, inv_mode ? F.inv_s.p : nullptr);
         AUX_LAUNCHED(1);
+        if (inv_mode) {   // singletons: 1 / a_ii
+            k_inv_cells<<<grid_for(nL), kT, 0, s>>>(F.bptr.p, F.rp.p, F.col.p, F.v.p, nL, F.inv_s.p);
+            AUX_LAUNCHED(1);
+        }
         // 5..32 members: 4 blocks per warp up to 8 members, 2 up to 16, 1 up to 32
         for (int cls = 0; cls < 3; ++cls) {
             const int lo = cls == 0 ? 5 : cls == 1 ? 9 : 17, hi = cls == 0 ? 8 : cls == 1 ? 16 : kWarpLU;
@@ -1244,6 +1173,10 @@ void finest_blocks(aux_hierarchy* h, const Geo& gL, unsigned long long& sing, in
             }
         }
         sing = read1(err.p, s);
+        DBuf<int> cflag(1);
+        AUX_CUDA(cudaMemsetAsync(cflag.p, 0, sizeof(int), s));
+        k_color_check<<<grid_for(n), kT, 0, s>>>(F.rp.p, F.col.p, F.v.p, F.cell.p, n, gL.lq, cflag.p);
+        AUX_LAUNCHED(1);
         color_flag = read1(cflag.p, s);
     }
 
@@ -1552,9 +1485,16 @@ void setup_device(aux_hierarchy* h, const aux_csr_view* A, const double* xy, lon
                                                         F.rp.p, F.col.p, F.v.p);
     AUX_LAUNCHED(1);
 
-    // ---- level L operator (assemble_coarse_finest) and the finest blocks,
-    // in one pass over the permuted rows (k_cells_fused); the singular-block
-    // error is reported before the strict-locality one, as in the reference
+    {
+        unsigned long long sing = ~0ull;
+        int color_flag = 0;
+        finest_blocks(h, gL, sing, color_flag);
+        if (sing != ~0ull)
+            throw_aux(AUX_DEFINITENESS_ERROR, "aggregate " + std::to_string(sing) + " has a singular block");
+        F.color_clean = color_flag == 0;
+    }
+
+    // ---- level L operator (assemble_coarse_finest)
     h->lv.emplace_back();
     {
         auxb200::Level& L1 = h->lv[1];
@@ -1571,14 +1511,9 @@ void setup_device(aux_hierarchy* h, const aux_csr_view* A, const double* xy, lon
         AUX_CUDA(cudaMemsetAsync(dcnt.p, 0, sizeof(int) * nL, s));
         AUX_CUDA(cudaMemsetAsync(tot.p, 0, sizeof(unsigned long long), s));
         const int lump = (o.lump_locality && !o.strict_locality) ? 1 : 0;
-        AUX_LAUNCHED(1);
-        const GalerkinOut gal{L1.val.p, dcnt.p, dmass.p, tot.p, lump};
-        unsigned long long sing = ~0ull;
-        int color_flag = 0;
-        finest_blocks(h, gL, sing, color_flag, &gal);
-        if (sing != ~0ull)
-            throw_aux(AUX_DEFINITENESS_ERROR, "aggregate " + std::to_string(sing) + " has a singular block");
-        F.color_clean = color_flag == 0;
+        k_galerkin_L<<<grid_for(nL), kT, 0, s>>>(F.bptr.p, F.rp.p, F.col.p, F.v.p, F.cell.p, gL, lump, L1.val.p,
+                                                   dcnt.p, dmass.p, tot.p);
+        AUX_LAUNCHED(2);
         const unsigned long long dropped = read1(tot.p, s);
         std::memset(&h->loc, 0, sizeof h->loc);
         if (dropped > 0) {
@@ -1892,7 +1827,7 @@ void setup_device_dist(aux_hierarchy* h, const aux_csr_view* A, const double* xy
     {
         unsigned long long sing = ~0ull;
         int color_flag = 0;
-        finest_blocks(h, gL, sing, color_flag, nullptr);
+        finest_blocks(h, gL, sing, color_flag);
         sing = ~allmax(h, ~sing);
         if (sing != ~0ull)
             throw_aux(AUX_DEFINITENESS_ERROR, "aggregate " + std::to_string(sing) + " has a singular block");

@@ -638,7 +638,7 @@ __global__ void __launch_bounds__(256, 4) k_bgs_inv(const int* __restrict__ rp, 
     static_assert(kWarpInvMax >= 64 + 256, "window buffer");
     static_assert(kSmallInvWords >= kSmallBlock * 31 + kSmallBlock * kSmallBlock, "small-block inverse window");
     __shared__ double sr[8][kWarpInvMax];
-    __shared__ double si[8][kSmallInvWords];
+    __shared__ double si[8][kSmallInvWords + kSmallInvWords / 16];   // swizzled: +1 word per 16
     const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
     if ((int)blockIdx.x < nbig) {   // one block of 33..kWarpInvMax members per CTA
         const int g = big_ids[j0 + blockIdx.x];
@@ -685,14 +685,12 @@ __global__ void __launch_bounds__(256, 4) k_bgs_inv(const int* __restrict__ rp, 
     if (w0 >= r1) return;
     const int ra = w0 + lane, rb = w0 + 32 + lane;
     const bool va = ra < r1, vb = rb < r1;
-    // every load whose address is known up front is issued together, the
-    // inverses of the window's small blocks first (row-anchored pool: one
-    // coalesced burst that depends on nothing)
-    double isv[kSmallInvWords / 32];
-#pragma unroll
-    for (int k = 0; k < kSmallInvWords / 32; ++k) {
-        const long e = (long)kSmallBlock * w0 + lane + 32 * k;
-        isv[k] = e < (long)kSmallBlock * r1 ? __ldcs(inv_s + e) : 0.0;
+    // every load whose address is known up front is issued together; the
+    // inverses of the window's small blocks (row-anchored pool, 10 lines that
+    // depend on nothing) are pulled towards L2 now and read after the residual
+    if (lane < kSmallInvWords / 16) {
+        const long e = (long)kSmallBlock * w0 + 16 * lane;
+        if (e < (long)kSmallBlock * r1) asm volatile("prefetch.global.L2 [%0];" ::"l"(inv_s + e));
     }
     const unsigned m8a = va ? meta8[ra] : 0u, m8b = vb ? meta8[rb] : 0u;
     const int pa0 = va ? rp[ra] : 0, pa1 = va ? rp[ra + 1] : 0;
@@ -762,20 +760,30 @@ __global__ void __launch_bounds__(256, 4) k_bgs_inv(const int* __restrict__ rp, 
     R[lane] = oa ? acc_a : 0.0;
     R[32 + lane] = ob ? acc_b : 0.0;
     double* SI = si[wl];
+    // (index i stored at i + i / 16: consecutive blocks sit 16 words apart and
+    // would otherwise read the same banks)
 #pragma unroll
-    for (int k = 0; k < kSmallInvWords / 32; ++k) SI[lane + 32 * k] = isv[k];
+    for (int k = 0; k < kSmallInvWords / 32; ++k) {
+        const int i = lane + 32 * k;
+        const long e = (long)kSmallBlock * w0 + i;
+        SI[i + (i >> 4)] = e < (long)kSmallBlock * r1 ? __ldcs(inv_s + e) : 0.0;
+    }
     __syncwarp();
     // blocks of <= kSmallBlock members: inv(q, j) = pool[kSmallBlock c0 + j s + q], j ascending
     double da = 0.0, db = 0.0;
     if (sma) {
         const int c0 = lane - qa;   // window-local first row of the block (>= 0)
-        const double* iv = SI + kSmallBlock * c0 + qa;
-        for (int j = 0; j < sa; ++j) da = fma(iv[j * sa], R[c0 + j], da);
+        for (int j = 0; j < sa; ++j) {
+            const int i = kSmallBlock * c0 + j * sa + qa;
+            da = fma(SI[i + (i >> 4)], R[c0 + j], da);
+        }
     }
     if (smb) {
         const int c0 = 32 + lane - qb;
-        const double* iv = SI + kSmallBlock * c0 + qb;
-        for (int j = 0; j < sb; ++j) db = fma(iv[j * sb], R[c0 + j], db);
+        for (int j = 0; j < sb; ++j) {
+            const int i = kSmallBlock * c0 + j * sb + qb;
+            db = fma(SI[i + (i >> 4)], R[c0 + j], db);
+        }
     }
     // delta = A_gg^{-1} r_g: the inverses of the owned blocks are one
     // contiguous range of the pool (cell order), streamed coalesced through
