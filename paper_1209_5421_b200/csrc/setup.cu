@@ -846,29 +846,6 @@ __global__ void k_own_flag(const unsigned* __restrict__ key, long n, Geo g, int 
 __global__ void k_mark_local(const int* __restrict__ l2s, int n_own, int* __restrict__ s2l) {
     GSTRIDE(l, n_own) s2l[l2s[l]] = (int)l;
 }
-// non-owned entries of each local row (sorted-order column index)
-__global__ void k_ghost_count(const int* __restrict__ l2s, int n_own, const int* __restrict__ perm,
-                              const int* __restrict__ rp, const int* __restrict__ col, const int* __restrict__ iperm,
-                              const int* __restrict__ s2l, int* __restrict__ cnt) {
-    GSTRIDE(l, n_own) {
-        const int c = perm[l2s[l]];
-        int k = 0;
-        for (int p = rp[c]; p < rp[c + 1]; ++p) k += s2l[iperm[col[p]]] < 0 ? 1 : 0;
-        cnt[l] = k;
-    }
-}
-__global__ void k_ghost_emit(const int* __restrict__ l2s, int n_own, const int* __restrict__ perm,
-                             const int* __restrict__ rp, const int* __restrict__ col, const int* __restrict__ iperm,
-                             const int* __restrict__ s2l, const int* __restrict__ off, unsigned* __restrict__ out) {
-    GSTRIDE(l, n_own) {
-        const int c = perm[l2s[l]];
-        int k = off[l];
-        for (int p = rp[c]; p < rp[c + 1]; ++p) {
-            const int j = iperm[col[p]];
-            if (s2l[j] < 0) out[k++] = (unsigned)j;
-        }
-    }
-}
 __global__ void k_owner_key(const int* __restrict__ idx, long m, const unsigned* __restrict__ key, Geo g, int PX,
                             int PY, unsigned* __restrict__ okey) {
     const int w = 1 << g.k;
@@ -887,36 +864,6 @@ __global__ void k_compact_u(const int* __restrict__ flag, const int* __restrict_
 }
 __global__ void k_ghost_map(const int* __restrict__ ghosts, int ng, int n_own, int* __restrict__ s2l) {
     GSTRIDE(i, ng) s2l[ghosts[i]] = n_own + (int)i;
-}
-__global__ void k_local_len(const int* __restrict__ l2s, int n_own, const int* __restrict__ perm,
-                            const int* __restrict__ rp, int* __restrict__ len, int* __restrict__ gid) {
-    GSTRIDE(l, n_own) {
-        const int c = perm[l2s[l]];
-        len[l] = rp[c + 1] - rp[c];
-        gid[l] = c;
-    }
-}
-// local rows (entries in the caller's storage order, columns relabelled to
-// local / ghost indices), four lanes per row (see k_permute_csr)
-__global__ void k_local_csr(const int* __restrict__ gid, int n_own, const int* __restrict__ rp,
-                            const int* __restrict__ col, const double* __restrict__ v, const int* __restrict__ iperm,
-                            const int* __restrict__ s2l, const int* __restrict__ rpl, int* __restrict__ coll,
-                            double* __restrict__ vl) {
-    const int sub = threadIdx.x & 3;
-    const long grp = (blockIdx.x * (long)blockDim.x + threadIdx.x) >> 2;
-    const long ng = ((long)gridDim.x * blockDim.x) >> 2;
-    for (long l = grp; l < n_own; l += ng) {
-        const int c = gid[l];
-        const int a = rp[c], b = rp[c + 1], o = rpl[l];
-        for (int p = a + sub; p < b; p += 4) {
-            coll[o + (p - a)] = s2l[iperm[col[p]]];
-            vl[o + (p - a)] = v[p];
-        }
-    }
-}
-__global__ void k_local_cell(const int* __restrict__ l2s, int n_own, const int* __restrict__ ghosts, int ng,
-                             const unsigned* __restrict__ key, int* __restrict__ cell) {
-    GSTRIDE(i, (long)n_own + ng) cell[i] = (int)key[i < n_own ? l2s[i] : ghosts[i - n_own]];
 }
 __global__ void k_count_i(const int* __restrict__ key, long n, int* cnt) {
     GSTRIDE(i, n) atomicAdd(&cnt[key[i]], 1);
@@ -947,9 +894,117 @@ __global__ void k_zero_diag_rect(Geo g, const double* __restrict__ val, const ui
         atomicMin(err, (unsigned long long)(i >> g.lq) * g.n + lex_of_cm(g, i));
     }
 }
-__global__ void k_inv_perm(const int* __restrict__ perm, long n, int* __restrict__ iperm) {
-    GSTRIDE(i, n) iperm[perm[i]] = (int)i;
+// ---- per-part setup over the part's own rows (DoF ids): validate_csr,
+// diagonal and symmetry of the owned rows, ghost lists by DoF id, local CSR.
+// Row keys are global DoF ids, so the minimum over all parts is the
+// reference's first failing row (sparse.hpp:101-116, hierarchy.hpp:321-325).
+__global__ void k_validate_rows(const int* __restrict__ rows, int m, const int* __restrict__ rp,
+                                const int* __restrict__ col, long nnz, int ncols, unsigned long long* err) {
+    GSTRIDE(l, m) {
+        const int r = rows[l];
+        const int a = rp[r], b = rp[r + 1];
+        unsigned long long key = ~0ull;
+        if (a > b) {
+            key = (unsigned long long)r * 4 + 1;
+        } else {
+            const long lo = a < 0 ? 0 : a, hi = b > nnz ? nnz : b;
+            if (a < 0 || b > nnz) key = (unsigned long long)r * 4 + 2;
+            for (long p = lo; p < hi && key == ~0ull; ++p) {
+                const int c = col[p];
+                if (c < 0 || c >= ncols) key = (unsigned long long)r * 4 + 2;
+                else if (p > a && col[p - 1] >= c) key = (unsigned long long)r * 4 + 3;
+            }
+        }
+        if (key != ~0ull) atomicMin(err, key);
+    }
 }
+__global__ void k_symm_rows(const int* __restrict__ rows, int m, const int* __restrict__ rp,
+                            const int* __restrict__ col, const double* __restrict__ v,
+                            unsigned long long* out /* [0]=defect [1]=scale */, unsigned long long* diag_err) {
+    double dmx = 0.0, smx = 0.0;
+    GSTRIDE(l, m) {
+        const int i = rows[l];
+        double dg = 0.0;
+        for (int p = rp[i]; p < rp[i + 1]; ++p) {
+            const int j = col[p];
+            const double a = v[p];
+            if (j == i) dg = a;
+            const double aa = fabs(a);
+            smx = (smx < aa) ? aa : smx;
+            const int lo = rp[j], hi = rp[j + 1];
+            const int q = find_col(col, lo, hi, i);
+            const double d = (q < hi && col[q] == i) ? fabs(a - v[q]) : aa;
+            dmx = (dmx < d) ? d : dmx;
+        }
+        if (dg <= 0.0) atomicMin(diag_err, (unsigned long long)i);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double d2 = __shfl_xor_sync(0xffffffffu, dmx, o);
+        const double s2 = __shfl_xor_sync(0xffffffffu, smx, o);
+        dmx = (dmx < d2) ? d2 : dmx;
+        smx = (smx < s2) ? s2 : smx;
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMax(&out[0], (unsigned long long)__double_as_longlong(dmx));
+        atomicMax(&out[1], (unsigned long long)__double_as_longlong(smx));
+    }
+}
+__global__ void k_slice_flag(long n, long lo, long hi, int* __restrict__ flag) {
+    GSTRIDE(i, n) flag[i] = (i >= lo && i < hi) ? 1 : 0;
+}
+__global__ void k_gather_key(const int* __restrict__ ids, int m, const unsigned* __restrict__ key,
+                             unsigned* __restrict__ out) {
+    GSTRIDE(i, m) out[i] = key[ids[i]];
+}
+__global__ void k_ghost_count_id(const int* __restrict__ l2g, int n_own, const int* __restrict__ rp,
+                                 const int* __restrict__ col, const int* __restrict__ g2l, int* __restrict__ cnt) {
+    GSTRIDE(l, n_own) {
+        const int c = l2g[l];
+        int k = 0;
+        for (int p = rp[c]; p < rp[c + 1]; ++p) k += g2l[col[p]] < 0 ? 1 : 0;
+        cnt[l] = k;
+    }
+}
+__global__ void k_ghost_emit_id(const int* __restrict__ l2g, int n_own, const int* __restrict__ rp,
+                                const int* __restrict__ col, const int* __restrict__ g2l, const int* __restrict__ off,
+                                unsigned* __restrict__ out) {
+    GSTRIDE(l, n_own) {
+        const int c = l2g[l];
+        int k = off[l];
+        for (int p = rp[c]; p < rp[c + 1]; ++p)
+            if (g2l[col[p]] < 0) out[k++] = (unsigned)col[p];
+    }
+}
+__global__ void k_local_len_id(const int* __restrict__ l2g, int n_own, const int* __restrict__ rp,
+                               int* __restrict__ len) {
+    GSTRIDE(l, n_own) {
+        const int c = l2g[l];
+        len[l] = rp[c + 1] - rp[c];
+    }
+}
+// local rows (entries in the caller's storage order, columns relabelled to
+// local / ghost indices), four lanes per row (see k_permute_csr)
+__global__ void k_local_csr_id(const int* __restrict__ gid, int n_own, const int* __restrict__ rp,
+                               const int* __restrict__ col, const double* __restrict__ v, const int* __restrict__ g2l,
+                               const int* __restrict__ rpl, int* __restrict__ coll, double* __restrict__ vl) {
+    const int sub = threadIdx.x & 3;
+    const long grp = (blockIdx.x * (long)blockDim.x + threadIdx.x) >> 2;
+    const long ng = ((long)gridDim.x * blockDim.x) >> 2;
+    for (long l = grp; l < n_own; l += ng) {
+        const int c = gid[l];
+        const int a = rp[c], b = rp[c + 1], o = rpl[l];
+        for (int p = a + sub; p < b; p += 4) {
+            coll[o + (p - a)] = g2l[col[p]];
+            vl[o + (p - a)] = v[p];
+        }
+    }
+}
+__global__ void k_local_cell_id(const int* __restrict__ l2g, int n_own, const int* __restrict__ ghosts, int ng,
+                                const unsigned* __restrict__ key, int* __restrict__ cell) {
+    GSTRIDE(i, (long)n_own + ng) cell[i] = (int)key[i < n_own ? l2g[i] : ghosts[i - n_own]];
+}
+
 __global__ void k_gather_int(const int* __restrict__ idx, long n, const int* __restrict__ map, int* __restrict__ out) {
     GSTRIDE(i, n) out[i] = map[idx[i]];
 }
@@ -1589,10 +1644,15 @@ void setup_device(aux_hierarchy* h, const aux_csr_view* A, const double* xy, lon
 
 // ================================================================= multi-GPU setup
 //
-// One part of a distributed hierarchy.  Every part receives the
-// global (replicated) CSR and coordinates, runs the same validation and
-// bounding box, and owns one rectangle of level-L cells (quadtree subtree:
-// P = 2 halves, 4 quadrants, 8 half-quadrants, ...).
+// One part of a distributed hierarchy.  Every part sees the
+// global CSR and coordinates (the drop-in input) but reads only O(N/P) of the
+// matrix: the bounding box from its slice of the points + a MIN / MAX
+// all-reduce, one streaming pass over the points for the cell keys, then
+// validate_csr / diagonal / symmetry, the aggregation sort, the ghost lists
+// and the local CSR over its OWN rows only (verdicts all-reduced, so every
+// part raises the reference's error for the lowest failing row).  A part owns
+// one rectangle of level-L cells (quadtree subtree: P = 2 halves, 4
+// quadrants, 8 half-quadrants, ...).
 //   finest   the DoFs of its cells as local rows (global aggregation order),
 //            ghost DoFs as extra columns grouped by owner, exchange lists from
 //            a setup-time request/reply; blocks, inverses, Galerkin rows local
@@ -1656,13 +1716,68 @@ void setup_device_dist(aux_hierarchy* h, const aux_csr_view* A, const double* xy
     if (A->n_rows != A->n_cols) throw_aux(AUX_SIZE_ERROR, "setup_hierarchy: matrix not square");
     if (n_points != A->n_rows)
         throw_aux(AUX_SIZE_ERROR, "setup_hierarchy: coordinate count does not match matrix order");
-    validate_input(h, A);
     h->opts.coarsest_size = std::max(h->opts.coarsest_size, 4);
     const int coarsest_size = h->opts.coarsest_size;
     const int n = A->n_rows;
+    const long nnz = A->nnz;
     h->n = n;
+    // Every part reads only O(N/P) of the matrix: the row_ptr endpoints, its
+    // own rows (validation, symmetry look-ups into their columns' rows, ghost
+    // lists, local CSR); the O(N) work is one streaming pass over the
+    // coordinates for the cell keys (20 B per DoF) and the id -> local map.
+    {
+        int ends[2] = {0, 0};
+        if (n >= 0) {
+            AUX_CUDA(cudaMemcpyAsync(&ends[0], A->row_ptr, sizeof(int), cudaMemcpyDeviceToHost, s));
+            AUX_CUDA(cudaMemcpyAsync(&ends[1], A->row_ptr + n, sizeof(int), cudaMemcpyDeviceToHost, s));
+            AUX_CUDA(cudaStreamSynchronize(s));
+        }
+        if (ends[0] != 0 || (long)ends[1] != nnz)
+            throw_aux(AUX_STRUCTURE_ERROR, "CSR row_ptr endpoints inconsistent with nnz");
+    }
     if (n <= coarsest_size) throw_aux(AUX_ARGUMENT_ERROR, "distributed setup needs more DoFs than coarsest_size");
-    bounding_box(h, xy, n);
+    // ---- bounding_box (auxgrid.hpp:75-91): each part's slice of the points,
+    // then MIN / MAX over the parts (min as the max of the complemented
+    // order-preserving key); the verdict is reported after the value checks
+    int bbcode = 0;
+    {
+        const long lo = (long)n * rank / P, hi = (long)n * (rank + 1) / P;
+        DBuf<unsigned long long> bb(5);
+        DBuf<int> bad(1);
+        const unsigned long long init[4] = {~0ull, 0ull, ~0ull, 0ull};
+        AUX_CUDA(cudaMemcpyAsync(bb.p, init, sizeof init, cudaMemcpyHostToDevice, s));
+        AUX_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), s));
+        if (hi > lo) {
+            k_bbox<<<(unsigned)std::min<long>(148L * 8, std::max<long>(1, (hi - lo + kT - 1) / kT)), kT, 0, s>>>(
+                xy + 2 * lo, hi - lo, bb.p, bad.p);
+            AUX_LAUNCHED(1);
+        }
+        unsigned long long r[5];
+        int badh = 0;
+        AUX_CUDA(cudaMemcpyAsync(r, bb.p, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+        AUX_CUDA(cudaMemcpyAsync(&badh, bad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+        AUX_CUDA(cudaStreamSynchronize(s));
+        const unsigned long long m[5] = {~r[0], r[1], ~r[2], r[3], (unsigned long long)badh};
+        AUX_CUDA(cudaMemcpyAsync(bb.p, m, sizeof m, cudaMemcpyHostToDevice, s));
+        cm->allreduce_max(bb.p, 5, s);
+        AUX_CUDA(cudaMemcpyAsync(r, bb.p, sizeof r, cudaMemcpyDeviceToHost, s));
+        AUX_CUDA(cudaStreamSynchronize(s));
+        auto val = [](unsigned long long k) {
+            const unsigned long long b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+            double d;
+            std::memcpy(&d, &b, 8);
+            return d;
+        };
+        if (r[4]) {
+            bbcode = 1;
+        } else {
+            h->box[0] = val(~r[0]);
+            h->box[1] = val(r[1]);
+            h->box[2] = val(~r[2]);
+            h->box[3] = val(r[3]);
+            if (!(h->box[1] > h->box[0]) || !(h->box[3] > h->box[2])) bbcode = 2;
+        }
+    }
     int depth = 0;
     {
         long cells = 1;
@@ -1682,49 +1797,96 @@ void setup_device_dist(aux_hierarchy* h, const aux_csr_view* A, const double* xy
         throw_aux(AUX_ARGUMENT_ERROR, "problem too small for " + std::to_string(P) + " parts (level-L rectangle < 16)");
     const Rect ownL{h->dist.px * w / PX, h->dist.py * w / PY, (h->dist.px + 1) * w / PX, (h->dist.py + 1) * w / PY};
 
-    // ---- global aggregation (the same keys and stable sort as one GPU)
+    // ---- cell keys of every DoF; the owned DoFs (the rectangle's) in id order.
+    // With an invalid point set the parts validate id slices instead (the
+    // geometry error is raised after the matrix checks, as the reference).
     DBuf<unsigned> key(n);
-    DBuf<int> perm(n), iperm(n);
-    k_cellkey<<<grid_for(n), kT, 0, s>>>(xy, n, h->box[0], h->box[1], h->box[2], h->box[3], gL, key.p);
-    AUX_LAUNCHED(1);
-    radix_sort_pairs(key.p, perm.p, n, 2 * depth, s, true);
-    k_inv_perm<<<grid_for(n), kT, 0, s>>>(perm.p, n, iperm.p);
-    AUX_LAUNCHED(1);
-
-    // ---- owned rows (sorted order restricted to the rectangle)
     int n_own = 0;
-    DBuf<int> l2s, s2l(n);
+    DBuf<int> l2g;
     {
         DBuf<int> flag(n), pos(n + 1);
-        k_own_flag<<<grid_for(n), kT, 0, s>>>(key.p, n, gL, ownL.x0, ownL.y0, ownL.x1, ownL.y1, flag.p);
-        AUX_LAUNCHED(1);
+        if (bbcode == 0) {
+            k_cellkey<<<grid_for(n), kT, 0, s>>>(xy, n, h->box[0], h->box[1], h->box[2], h->box[3], gL, key.p);
+            k_own_flag<<<grid_for(n), kT, 0, s>>>(key.p, n, gL, ownL.x0, ownL.y0, ownL.x1, ownL.y1, flag.p);
+        } else {
+            k_slice_flag<<<grid_for(n), kT, 0, s>>>(n, (long)n * rank / P, (long)n * (rank + 1) / P, flag.p);
+        }
+        AUX_LAUNCHED(2);
         exclusive_scan(flag.p, pos.p, n, s);
         n_own = read1(pos.p + n, s);
-        l2s.alloc(std::max(n_own, 1));
-        k_compact<<<grid_for(n), kT, 0, s>>>(flag.p, pos.p, n, l2s.p);
-        AUX_CUDA(cudaMemsetAsync(s2l.p, 0xff, sizeof(int) * n, s));
-        k_mark_local<<<grid_for(n_own), kT, 0, s>>>(l2s.p, n_own, s2l.p);
-        AUX_LAUNCHED(2);
+        l2g.alloc(std::max(n_own, 1));
+        k_compact<<<grid_for(n), kT, 0, s>>>(flag.p, pos.p, n, l2g.p);
+        AUX_LAUNCHED(1);
     }
+    // ---- validate_csr, diagonal and symmetry over the owned rows; every part
+    // takes the same verdict (minimum failing row / maximum defect)
+    {
+        DBuf<unsigned long long> err(1);
+        AUX_CUDA(cudaMemsetAsync(err.p, 0xff, sizeof(unsigned long long), s));
+        if (n_own > 0) {
+            k_validate_rows<<<grid_for(n_own), kT, 0, s>>>(l2g.p, n_own, A->row_ptr, A->col_idx, nnz, A->n_cols,
+                                                           err.p);
+            AUX_LAUNCHED(1);
+        }
+        const unsigned long long e = ~allmax(h, ~read1(err.p, s));
+        if (e != ~0ull) {
+            const long r = (long)(e / 4);
+            const int kind = (int)(e % 4);
+            if (kind == 1) throw_aux(AUX_STRUCTURE_ERROR, "CSR row_ptr not nondecreasing at row " + std::to_string(r));
+            if (kind == 2) throw_aux(AUX_STRUCTURE_ERROR, "CSR column index out of range in row " + std::to_string(r));
+            throw_aux(AUX_STRUCTURE_ERROR, "CSR row " + std::to_string(r) + " not sorted by column");
+        }
+        DBuf<unsigned long long> sy(3);
+        const unsigned long long init[3] = {0ull, 0ull, ~0ull};
+        AUX_CUDA(cudaMemcpyAsync(sy.p, init, sizeof init, cudaMemcpyHostToDevice, s));
+        if (n_own > 0) {
+            k_symm_rows<<<grid_for(n_own), kT, 0, s>>>(l2g.p, n_own, A->row_ptr, A->col_idx, A->values, sy.p,
+                                                       sy.p + 2);
+            AUX_LAUNCHED(1);
+        }
+        unsigned long long syh[3];
+        AUX_CUDA(cudaMemcpyAsync(syh, sy.p, sizeof syh, cudaMemcpyDeviceToHost, s));
+        AUX_CUDA(cudaStreamSynchronize(s));
+        const unsigned long long dmin = ~allmax(h, ~syh[2]);
+        if (dmin != ~0ull) throw_aux(AUX_DEFINITENESS_ERROR, "nonpositive diagonal at row " + std::to_string(dmin));
+        const unsigned long long dfx = allmax(h, syh[0]), scx = allmax(h, syh[1]);
+        double defect, scale;
+        std::memcpy(&defect, &dfx, 8);
+        std::memcpy(&scale, &scx, 8);
+        scale = (1.0 < scale) ? scale : 1.0;
+        if (defect / scale > h->opts.symmetry_tol) throw_aux(AUX_STRUCTURE_ERROR, "matrix is not symmetric to tolerance");
+    }
+    bbox_throw(bbcode);
     if (allmax(h, n_own == 0 ? 1ull : 0ull))   // decided together: a lone throw would strand the others
         throw_aux(AUX_ARGUMENT_ERROR, "a part owns no DoFs (problem too small for the partition)");
 
-    // ---- ghost DoFs: sorted unique, grouped by owner part
+    // ---- owned rows in the aggregation order: the stable sort of the owned
+    // ids by cell key is the global stable sort restricted to the rectangle
+    {
+        DBuf<unsigned> okey(n_own);
+        k_gather_key<<<grid_for(n_own), kT, 0, s>>>(l2g.p, n_own, key.p, okey.p);
+        AUX_LAUNCHED(1);
+        radix_sort_pairs(okey.p, l2g.p, n_own, 2 * depth, s, false);
+    }
+    DBuf<int> g2l(n);   // DoF id -> local row (owned), n_own + ghost index, or -1
+    AUX_CUDA(cudaMemsetAsync(g2l.p, 0xff, sizeof(int) * n, s));
+    k_mark_local<<<grid_for(n_own), kT, 0, s>>>(l2g.p, n_own, g2l.p);
+    AUX_LAUNCHED(1);
+
+    // ---- ghost DoFs (columns owned elsewhere): unique ids, grouped by owner part
     int ng = 0;
     DBuf<int> ghosts;
     std::vector<int> gcount(P, 0);
     {
         DBuf<int> cnt(n_own), off(n_own + 1);
-        k_ghost_count<<<grid_for(n_own), kT, 0, s>>>(l2s.p, n_own, perm.p, A->row_ptr, A->col_idx, iperm.p, s2l.p,
-                                                     cnt.p);
+        k_ghost_count_id<<<grid_for(n_own), kT, 0, s>>>(l2g.p, n_own, A->row_ptr, A->col_idx, g2l.p, cnt.p);
         AUX_LAUNCHED(1);
         exclusive_scan(cnt.p, off.p, n_own, s);
         const int m = read1(off.p + n_own, s);
         if (m > 0) {
             DBuf<unsigned> gl(m);
             DBuf<int> dummy(m);
-            k_ghost_emit<<<grid_for(n_own), kT, 0, s>>>(l2s.p, n_own, perm.p, A->row_ptr, A->col_idx, iperm.p,
-                                                        s2l.p, off.p, gl.p);
+            k_ghost_emit_id<<<grid_for(n_own), kT, 0, s>>>(l2g.p, n_own, A->row_ptr, A->col_idx, g2l.p, off.p, gl.p);
             AUX_LAUNCHED(1);
             radix_sort_pairs(gl.p, dummy.p, m, bits_for(n), s, true);
             DBuf<int> uf(m), up(m + 1);
@@ -1742,7 +1904,7 @@ void setup_device_dist(aux_hierarchy* h, const aux_csr_view* A, const double* xy
             AUX_CUDA(cudaMemcpyAsync(ok.data(), okey.p, sizeof(unsigned) * ng, cudaMemcpyDeviceToHost, s));
             AUX_CUDA(cudaStreamSynchronize(s));
             for (unsigned o : ok) gcount[o]++;
-            k_ghost_map<<<grid_for(ng), kT, 0, s>>>(ghosts.p, ng, n_own, s2l.p);
+            k_ghost_map<<<grid_for(ng), kT, 0, s>>>(ghosts.p, ng, n_own, g2l.p);
             AUX_LAUNCHED(1);
         }
     }
@@ -1753,21 +1915,22 @@ void setup_device_dist(aux_hierarchy* h, const aux_csr_view* A, const double* xy
     F.n_ghost = ng;
     h->dist.gid.alloc(n_own);
     F.rp.alloc(n_own + 1);
+    AUX_CUDA(cudaMemcpyAsync(h->dist.gid.p, l2g.p, sizeof(int) * n_own, cudaMemcpyDeviceToDevice, s));
     {
         DBuf<int> len(n_own);
-        k_local_len<<<grid_for(n_own), kT, 0, s>>>(l2s.p, n_own, perm.p, A->row_ptr, len.p, h->dist.gid.p);
+        k_local_len_id<<<grid_for(n_own), kT, 0, s>>>(l2g.p, n_own, A->row_ptr, len.p);
         AUX_LAUNCHED(1);
         exclusive_scan(len.p, F.rp.p, n_own, s);
     }
     F.nnz = read1(F.rp.p + n_own, s);
     F.col.alloc(std::max<long>(F.nnz, 1));
     F.v.alloc(std::max<long>(F.nnz, 1));
-    k_local_csr<<<grid_for((long)n_own * 4), kT, 0, s>>>(h->dist.gid.p, n_own, A->row_ptr, A->col_idx, A->values,
-                                                          iperm.p, s2l.p, F.rp.p, F.col.p, F.v.p);
+    k_local_csr_id<<<grid_for((long)n_own * 4), kT, 0, s>>>(h->dist.gid.p, n_own, A->row_ptr, A->col_idx, A->values,
+                                                             g2l.p, F.rp.p, F.col.p, F.v.p);
     F.perm.alloc(n_own);
     AUX_CUDA(cudaMemcpyAsync(F.perm.p, h->dist.gid.p, sizeof(int) * n_own, cudaMemcpyDeviceToDevice, s));
     F.cell.alloc((size_t)n_own + ng);
-    k_local_cell<<<grid_for((long)n_own + ng), kT, 0, s>>>(l2s.p, n_own, ghosts.p, ng, key.p, F.cell.p);
+    k_local_cell_id<<<grid_for((long)n_own + ng), kT, 0, s>>>(l2g.p, n_own, ghosts.p, ng, key.p, F.cell.p);
     AUX_LAUNCHED(2);
     {
         DBuf<int> cnt(nL);
@@ -1815,7 +1978,7 @@ void setup_device_dist(aux_hierarchy* h, const aux_csr_view* A, const double* xy
         F.g_send_idx.alloc(std::max(ns, 1));
         F.g_send_buf.alloc(std::max(ns, 1));
         if (ns) {
-            k_gather_int<<<grid_for(ns), kT, 0, s>>>(req.p, ns, s2l.p, F.g_send_idx.p);
+            k_gather_int<<<grid_for(ns), kT, 0, s>>>(req.p, ns, g2l.p, F.g_send_idx.p);
             AUX_LAUNCHED(1);
         }
         F.g_peer.clear();

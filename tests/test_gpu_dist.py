@@ -129,3 +129,40 @@ def test_parts_full_size_c1(gpu_api, parts):
     A = sp.csr_matrix((s.A.values, s.A.col_idx, s.A.row_ptr), shape=(s.A.n_rows, s.A.n_rows))
     assert np.linalg.norm(s.b - A @ u) / np.linalg.norm(s.b) <= 1e-6 * (1 + 1e-9)
     assert round(st[0].operator_complexity, 4) == 1.4274
+
+
+def _corrupt_cases():
+    s = problems.jittered_p1(129)
+    n = s.A.n_rows
+    cases = {}
+    A = problems.CsrMatrix(n, n, s.A.row_ptr.copy(), s.A.col_idx.copy(), s.A.values.copy())
+    r = n - 7   # a late row: owned by another part than the first one
+    A.col_idx[A.row_ptr[r] + 1], A.col_idx[A.row_ptr[r]] = A.col_idx[A.row_ptr[r]], A.col_idx[A.row_ptr[r] + 1]
+    cases["unsorted_row"] = (A, s.coords)
+    A = problems.CsrMatrix(n, n, s.A.row_ptr.copy(), s.A.col_idx.copy(), s.A.values.copy())
+    for r in (n // 3, 2 * n // 3):   # two bad diagonals in different parts: the lower row is reported
+        p = A.row_ptr[r] + int(np.nonzero(A.col_idx[A.row_ptr[r]:A.row_ptr[r + 1]] == r)[0][0])
+        A.values[p] = -1.0
+    cases["bad_diagonals"] = (A, s.coords)
+    A = problems.CsrMatrix(n, n, s.A.row_ptr.copy(), s.A.col_idx.copy(), s.A.values.copy())
+    A.values[A.row_ptr[5] + 1] *= 1.5
+    cases["nonsymmetric"] = (A, s.coords)
+    xy = s.coords.copy()
+    xy[n - 3, 0] = np.nan
+    cases["nan_coordinate"] = (s.A, xy)
+    return cases, s.b
+
+
+@pytest.mark.parametrize("parts", [2, 4])
+def test_parts_errors_match_single_gpu(gpu_api, parts):
+    """Validation over each part's own rows with all-reduced verdicts: every
+    part raises exactly the error (class and message: lowest failing row) of
+    the single-GPU setup, which matches the reference's."""
+    cases, b = _corrupt_cases()
+    for name, (A, xy) in cases.items():
+        with pytest.raises(gpu_api.AuxamgError) as e1:
+            gpu_api.setup_hierarchy(A, xy)
+        with pytest.raises(gpu_api.AuxamgError) as ep:
+            gpu_api.solve_parts(A, xy, b, parts)
+        assert type(ep.value) is type(e1.value), (name, ep.value, e1.value)
+        assert str(ep.value) == str(e1.value), name
