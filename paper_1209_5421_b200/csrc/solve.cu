@@ -685,13 +685,7 @@ __global__ void __launch_bounds__(256, 4) k_bgs_inv(const int* __restrict__ rp, 
     if (w0 >= r1) return;
     const int ra = w0 + lane, rb = w0 + 32 + lane;
     const bool va = ra < r1, vb = rb < r1;
-    // every load whose address is known up front is issued together; the
-    // inverses of the window's small blocks (row-anchored pool, 10 lines that
-    // depend on nothing) are pulled towards L2 now and read after the residual
-    if (lane < kSmallInvWords / 16) {
-        const long e = (long)kSmallBlock * w0 + 16 * lane;
-        if (e < (long)kSmallBlock * r1) asm volatile("prefetch.global.L2 [%0];" ::"l"(inv_s + e));
-    }
+    // every load whose address is known up front is issued together
     const unsigned m8a = va ? meta8[ra] : 0u, m8b = vb ? meta8[rb] : 0u;
     const int pa0 = va ? rp[ra] : 0, pa1 = va ? rp[ra + 1] : 0;
     const int pc0 = vb ? rp[rb] : 0, pc1 = vb ? rp[rb + 1] : 0;
@@ -717,6 +711,13 @@ __global__ void __launch_bounds__(256, 4) k_bgs_inv(const int* __restrict__ rp, 
     if (!__any_sync(0xffffffffu, oa)) return;   // only rows of larger blocks here
     const bool sma = oa && sa <= kSmallBlock, smb = ob && sb <= kSmallBlock;   // row-anchored inverses
     const int ea = (oa && !sma) ? sa : 0, eb = (ob && !smb) ? sb : 0;           // offset-pool inverses
+    // the inverses of the window's small blocks (row-anchored pool: 10 lines
+    // known from the window alone) are pulled towards L2 now, read after the residual
+    const bool any_small = __any_sync(0xffffffffu, sma || smb);
+    if (any_small && lane < kSmallInvWords / 16) {
+        const long e = (long)kSmallBlock * w0 + 16 * lane;
+        if (e < (long)kSmallBlock * r1) asm volatile("prefetch.global.L2 [%0];" ::"l"(inv_s + e));
+    }
     // the window's offset-pool entries are one contiguous range: pull them
     // towards L2 now, so the inverse chunks do not pay a full DRAM round trip
     // after the residual chain
@@ -762,13 +763,15 @@ __global__ void __launch_bounds__(256, 4) k_bgs_inv(const int* __restrict__ rp, 
     double* SI = si[wl];
     // (index i stored at i + i / 16: consecutive blocks sit 16 words apart and
     // would otherwise read the same banks)
+    if (any_small) {
 #pragma unroll
-    for (int k = 0; k < kSmallInvWords / 32; ++k) {
-        const int i = lane + 32 * k;
-        const long e = (long)kSmallBlock * w0 + i;
-        SI[i + (i >> 4)] = e < (long)kSmallBlock * r1 ? __ldcs(inv_s + e) : 0.0;
+        for (int k = 0; k < kSmallInvWords / 32; ++k) {
+            const int i = lane + 32 * k;
+            const long e = (long)kSmallBlock * w0 + i;
+            SI[i + (i >> 4)] = e < (long)kSmallBlock * r1 ? __ldcs(inv_s + e) : 0.0;
+        }
+        __syncwarp();
     }
-    __syncwarp();
     // blocks of <= kSmallBlock members: inv(q, j) = pool[kSmallBlock c0 + j s + q], j ascending
     double da = 0.0, db = 0.0;
     if (sma) {
