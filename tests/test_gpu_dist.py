@@ -145,7 +145,9 @@ def _corrupt_cases():
         A.values[p] = -1.0
     cases["bad_diagonals"] = (A, s.coords)
     A = problems.CsrMatrix(n, n, s.A.row_ptr.copy(), s.A.col_idx.copy(), s.A.values.copy())
-    A.values[A.row_ptr[5] + 1] *= 1.5
+    r = n // 2
+    p = next(q for q in range(A.row_ptr[r], A.row_ptr[r + 1]) if A.col_idx[q] != r and A.values[q] != 0.0)
+    A.values[p] *= 1.5   # one off-diagonal entry of a middle row (its transpose is untouched)
     cases["nonsymmetric"] = (A, s.coords)
     xy = s.coords.copy()
     xy[n - 3, 0] = np.nan
