@@ -99,6 +99,8 @@ typedef struct aux_gpu_opts {
     int32_t stream_min_width; /* structured levels whose owned rectangle is at least this many
                                  cells wide run the row-wavefront kernels (stream.cu) instead of
                                  the overlapped tiles; 0 = default (1024), -1 = off */
+    int32_t cluster16;        /* the 128x128-cell level runs as one 16-CTA thread-block cluster
+                                 per visit half (cluster16.cu): 0 = default (on), -1 = off */
 } aux_gpu_opts;
 
 /* auxamg::LocalityReport, hierarchy.hpp:37-44. */

@@ -102,7 +102,8 @@ class CycleOpts(C.Structure):
 class GpuOpts(C.Structure):
     _fields_ = [("device", C.c_int32), ("coarse_solve", C.c_int32), ("fused_max_cells", C.c_int32),
                 ("use_graphs", C.c_int32), ("block_solve", C.c_int32),
-                ("tile_kernels", C.c_int32), ("cluster_tier", C.c_int32), ("stream_min_width", C.c_int32)]
+                ("tile_kernels", C.c_int32), ("cluster_tier", C.c_int32), ("stream_min_width", C.c_int32),
+                ("cluster16", C.c_int32)]
 
 
 class DistOpts(C.Structure):

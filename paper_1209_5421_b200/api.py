@@ -133,6 +133,7 @@ class GpuOptions:
     tile_kernels: bool = True    # overlapped-tile kernels for the structured levels
     cluster_tier: bool = True    # 64x64 level + single-CTA tier in one thread-block cluster
     stream_min_width: int = 0    # row-wavefront kernels from this level width (cells); 0 default, -1 off
+    cluster16: bool = True       # 128x128-cell level as one 16-CTA cluster per visit half
 
     def c(self):
         o = _abi.GpuOpts()
@@ -142,6 +143,7 @@ class GpuOptions:
         o.tile_kernels = int(self.tile_kernels)
         o.cluster_tier = int(self.cluster_tier)
         o.stream_min_width = int(self.stream_min_width)
+        o.cluster16 = 0 if self.cluster16 else -1
         return o
 
 

@@ -103,6 +103,28 @@ inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
     AUX_LAUNCHED(1);
 }
 
+// RN(a / b) in three dependent operations from y = rcp_or_zero(b):
+// q = RN(a y), r = a - b q (exact with an FMA), RN(q + r y).  By Markstein's
+// theorem (y within half an ulp of 1/b, q within one ulp of a/b) that is the
+// correctly rounded quotient, i.e. bitwise __ddiv_rn(a, b), whenever every
+// intermediate is a normal number (guaranteed by 2^-100 <= |b| <= 2^100 and
+// 2^-800 <= |q| <= 2^800); elsewhere (a = 0, tiny or huge operands, y = 0)
+// it falls back to __ddiv_rn.  tools/micro/markstein.cu compares the two
+// on 2.7e11 random and structured pairs (no difference).  __ddiv_rn is ~111
+// cycles of dependent latency on B200, this path ~25: it sits on the critical
+// path of every Gauss-Seidel cell update of the latency-bound coarse tier.
+__device__ __forceinline__ double rcp_or_zero(double b) {
+    const double ab = fabs(b);
+    return (ab >= 0x1p-100 && ab <= 0x1p+100) ? __drcp_rn(b) : 0.0;
+}
+static __device__ __noinline__ double ddiv_out_of_line(double a, double b) { return __ddiv_rn(a, b); }
+__device__ __forceinline__ double div_rcp(double a, double b, double y) {
+    const double q = __dmul_rn(a, y);
+    const double aq = fabs(q);   // with 2^-100 <= |y| <= 2^100: |a| >= 2^-900, remainder and result normal
+    if (aq >= 0x1p-800 && aq <= 0x1p+800) return __fma_rn(__fma_rn(-q, b, a), y, q);
+    return ddiv_out_of_line(a, b);   // rare: one shared copy keeps the latency-bound kernels' code small
+}
+
 // --------------------------------------------------------------- layout
 
 // Stencil offsets of slots 1..8 (hierarchy.hpp:48-50): E, NE, N, NW, W, SW, S, SE.

@@ -96,6 +96,7 @@ constexpr int kWarps = kThreads / 32;
 struct SLevel {
     int k, lh, H, nq, n, W2, PP;
     const double* val;
+    const double* rec;   // reciprocal of the diagonal (div_rcp), compact like val
     const uint8_t* act;
     double* r;
     double* p;    // p[i] = p + i*4*PP
@@ -129,6 +130,7 @@ __device__ __forceinline__ SLevel slev(const FusedArgs& a, unsigned char* sm, co
     L.W2 = g.H + 2;
     L.PP = L.W2 * L.W2;
     L.val = reinterpret_cast<const double*>(sm + a.off_val[q]);
+    L.rec = reinterpret_cast<const double*>(sm + a.off_rec[q]);
     L.act = reinterpret_cast<const uint8_t*>(sm + a.off_act[q]);
     double* v = reinterpret_cast<double*>(sm + a.off_vec[q]);
     const int vs = 4 * L.PP;
@@ -219,7 +221,7 @@ __device__ __forceinline__ double gs_cell(const SLevel& L, int ci, int pi, doubl
     s = __dsub_rn(s, __dmul_rn(v[6 * L.n], x[pi + noff<C, 6>(L)]));
     s = __dsub_rn(s, __dmul_rn(v[7 * L.n], x[pi + noff<C, 7>(L)]));
     s = __dsub_rn(s, __dmul_rn(v[8 * L.n], x[pi + noff<C, 8>(L)]));
-    return __ddiv_rn(s, v[0]);
+    return div_rcp(s, v[0], L.rec[ci]);
 }
 
 // One colour pass.  Inactive cells have f = 0 and an identity row, so the
@@ -249,6 +251,7 @@ __device__ __forceinline__ void gs_sweep(const SLevel& L, const double* f, doubl
 // shared-memory versions above (bitwise identical results).
 struct RV {
     double v[4][9];
+    double rc[4];   // rcp_or_zero(v[c][0])
 };
 
 // The register-resident level is always 16 x 16 plane positions (nq ==
@@ -294,7 +297,7 @@ __device__ __forceinline__ void gs_pass_r(const SLevel& L, const RV& rv, const d
     s = __dsub_rn(s, __dmul_rn(v[6], x[pi + noff_r<C, 6>()]));
     s = __dsub_rn(s, __dmul_rn(v[7], x[pi + noff_r<C, 7>()]));
     s = __dsub_rn(s, __dmul_rn(v[8], x[pi + noff_r<C, 8>()]));
-    x[pi] = __ddiv_rn(s, v[0]);
+    x[pi] = div_rcp(s, v[0], rv.rc[C]);
     __syncthreads();
 }
 
@@ -397,7 +400,7 @@ __device__ void cycle_down(const FusedArgs& a, const SLevel& L, PState& ps, cons
             fi = __dadd_rn(fi, __dmul_rn(na, ap[pi]));
             f[pi] = fi;
         }
-        u[pi] = c == 0 ? __ddiv_rn(fi, L.val[ci]) : 0.0;
+        u[pi] = c == 0 ? div_rcp(fi, L.val[ci], L.rec[ci]) : 0.0;
     }
     ps.pend = 0;
     __syncthreads();
@@ -657,6 +660,12 @@ __device__ void tier_stage(const FusedArgs& a, unsigned char* sm, Geo* sgeo, uin
         for (int i = threadIdx.x; i < nv2; i += kThreads) v[i] = make_double2(0.0, 0.0);
     }
     mbar_wait(bar, 0);
+    for (int q = 0; q < nl; ++q) {   // reciprocal diagonals (div_rcp); the callers barrier before use
+        const int n = a.lv[a.m0 + q].g.n;
+        const double* val = reinterpret_cast<const double*>(sm + a.off_val[q]);
+        double* rec = reinterpret_cast<double*>(sm + a.off_rec[q]);
+        for (int i = threadIdx.x; i < n; i += kThreads) rec[i] = rcp_or_zero(val[i]);
+    }
 }
 
 // Stencil values of the top level in registers when its colour planes have
@@ -669,6 +678,8 @@ __device__ __forceinline__ void tier_load_rv(const FusedArgs& a, unsigned char* 
     for (int c = 0; c < 4; ++c)
 #pragma unroll
         for (int t = 0; t < 9; ++t) rv.v[c][t] = L0.val[t * L0.n + c * L0.nq + threadIdx.x];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) rv.rc[c] = rcp_or_zero(rv.v[c][0]);
 }
 
 // nonlinear_pcg(m0) with the K-cycle below it, right-hand side already in the
@@ -937,6 +948,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_cluster_pcg(const __grid_consta
     Q.W2 = kQW2;
     Q.PP = kQPP;
     Q.val = nullptr;
+    Q.rec = nullptr;
     Q.act = nullptr;
     double* qv = reinterpret_cast<double*>(sm);
     Q.r = qv;
@@ -951,7 +963,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_cluster_pcg(const __grid_consta
     // the tier's top level (32x32 cells) as seen from the quadrants
     SLevel T0;
     T0.k = 0; T0.lh = 4; T0.H = kQH; T0.nq = kQH * kQH; T0.n = 4 * T0.nq; T0.W2 = kQW2; T0.PP = kQPP;
-    T0.val = nullptr; T0.act = nullptr;
+    T0.val = nullptr; T0.rec = nullptr; T0.act = nullptr;
     T0.r = reinterpret_cast<double*>(sm + a.off_vec[0]);
     T0.p = T0.r + 4 * kQPP;
     T0.ap = nullptr;
@@ -970,6 +982,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_cluster_pcg(const __grid_consta
         for (int c = 0; c < 4; ++c)
 #pragma unroll
             for (int s = 0; s < 9; ++s) rv.v[c][s] = __ldg(ca.val + (size_t)s * gN + c * gq + gpos);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) rv.rc[c] = rcp_or_zero(rv.v[c][0]);
         const int nv2 = (1 + 2 * ni) * 2 * kQPP;
         double2* v2 = reinterpret_cast<double2*>(qv);
         for (int i = t; i < nv2; i += kThreads) v2[i] = make_double2(0.0, 0.0);
@@ -1019,7 +1033,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_cluster_pcg(const __grid_consta
                     fi = __dadd_rn(fi, __dmul_rn(na, apv[pi]));
                     Q.r[pi] = fi;
                 }
-                u[pi] = c == 0 ? __ddiv_rn(fi, rv.v[0][0]) : 0.0;
+                u[pi] = c == 0 ? div_rcp(fi, rv.v[0][0], rv.rc[0]) : 0.0;
             }
             // ghost rings of colours 1..3 restart at zero (colour 0 is pushed)
             if (zslot >= 0) u[zslot] = 0.0;
@@ -1238,6 +1252,7 @@ unsigned fused_layout(const aux_hierarchy* h, int m0, int ni, FusedArgs* a) {
         a->off_val[q] = take(9 * n * sizeof(double));
         a->off_vec[q] = take((1 + 2 * (size_t)ni) * 4 * W2 * W2 * sizeof(double));
         a->off_act[q] = take(n);
+        a->off_rec[q] = take(n * sizeof(double));
     }
     a->off_part = take(5 * (size_t)h->nc * sizeof(double));   // 4 partial sums + compact r
     const size_t need = off;

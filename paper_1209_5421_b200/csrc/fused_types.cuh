@@ -37,6 +37,7 @@ struct FusedArgs {
     // shared-memory layout (bytes) of fused level q = m - m0
     unsigned off_val[kMaxFusedLevels];
     unsigned off_act[kMaxFusedLevels];
+    unsigned off_rec[kMaxFusedLevels];   // rcp_or_zero of the diagonal (slot 0), n doubles
     unsigned off_vec[kMaxFusedLevels];   // r, u, p[0..ni), ap[0..ni), n doubles each
     unsigned off_inv;                    // explicit inverse, if staged
     unsigned off_part;                   // 4*nc partial sums of the coarse mat-vec

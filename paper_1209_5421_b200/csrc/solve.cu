@@ -1279,6 +1279,8 @@ void pcg_tiles(Ctx& c, int m) {
     const bool stream = smw > 0 && own.w() >= smw && own.h() >= 16 && c.o.pre_sweeps == 1 && c.o.post_sweeps == 1;
     int s_nbx = 0, s_yb = 0, s_blocks = 0;
     if (stream) stream_blocks(own.w(), own.h(), h->sm_count, s_nbx, s_yb, s_blocks);
+    // the 128 x 128-cell level: one 16-CTA cluster per visit half (cluster16.cu)
+    const bool c16 = !L.dist && h->gpu.cluster16 >= 0 && !stream && c16_supported(L.geo) && ni <= 8;
     const bool child_agg = L.dist && (m + 1 == h->dist.agg);
     const bool child_explicit = explicit_iterate(h, m + 1) || child_agg;
     Span sp = flat_span(L.n);
@@ -1307,7 +1309,8 @@ void pcg_tiles(Ctx& c, int m) {
         d.child_nval = sc_nval(ni);
         const bool prof_l = m == 1 && c.profile_finest && h->prof.on == 2;
         if (prof_l) prof_begin(c, 4);
-        if (stream) launch_stream_down(d, s_blocks, c.s);
+        if (c16) launch_c16_down(d, c.o.pre_sweeps, c.s);
+        else if (stream) launch_stream_down(d, s_blocks, c.s);
         else launch_tile_down(d, ntiles, c.o.pre_sweeps, c.s);
         // algorithmic bytes (each array once): stencil values, r in, pending
         // update (A p, r out), pre-smoothed iterate out, child right-hand side out
@@ -1345,6 +1348,24 @@ void pcg_tiles(Ctx& c, int m) {
         u.az = P.ap[i].p;
         u.ap0 = P.ap[0].p;
         u.mode = i == 0 ? 0 : 1;
+        if (c16) {   // up half, A-orthogonalisation and alpha in one launch
+            C16Up cu{};
+            cu.t = u;
+            for (int k = 0; k < ni; ++k) {
+                cu.pj[k] = P.p[k].p;
+                cu.apj[k] = P.ap[k].p;
+            }
+            cu.sc = sc;
+            cu.step = i;
+            cu.ni = ni;
+            cu.post = c.o.post_sweeps;
+            if (prof_l) prof_begin(c, 5);
+            launch_c16_up(cu, c.s);
+            if (prof_l)
+                prof_end(c, 5, (double)sp.n * (72.0 + 1.0 + 8.0 + 8.0 + 16.0) +
+                                   8.0 * (double)C.n * (child_explicit ? 1.0 : (double)ni));
+            continue;
+        }
         const Route ru = route(c, L.dist, i == 0 ? Fin{1, sc, nullptr, sc + 3, sc + sc_alpha(ni, 0), sc + sc_nval(ni), 0}
                                                  : Fin{2, sc, sc + 3, nullptr});
         if (prof_l) prof_begin(c, 5);

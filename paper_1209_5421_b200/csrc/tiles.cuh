@@ -11,9 +11,9 @@ namespace auxb200 {
 // Scalar block of a level's nonlinear PCG (cycle.hpp:106-128) on the device:
 //   [0] alpha of the last step  [1] beta  [2] breakdown flag
 //   [3 + i] energy e_i          [3 + ni + i] alpha_i      [3 + 2 ni] valid steps
-inline int sc_alpha(int ni, int i) { return 3 + ni + i; }
-inline int sc_nval(int ni) { return 3 + 2 * ni; }
-inline int sc_size(int ni) { return 4 + 2 * ni; }
+__host__ __device__ inline int sc_alpha(int ni, int i) { return 3 + ni + i; }
+__host__ __device__ inline int sc_nval(int ni) { return 3 + 2 * ni; }
+__host__ __device__ inline int sc_size(int ni) { return 4 + 2 * ni; }
 
 // Down half of a K-cycle visit of one level (cycle.hpp:169-178):
 // the pending PCG residual update r -= alpha A p (cycle.hpp:125), pre-smoothing
@@ -81,5 +81,19 @@ void launch_tile_up(TileUp& a, int ntiles, int post, RedState rs, Fin fin, cudaS
 void stream_blocks(int ow, int oh, int sms, int& nbx, int& yb, int& nblocks);
 void launch_stream_down(TileDown& a, int nblocks, cudaStream_t s);
 void launch_stream_up(TileUp& a, int nblocks, RedState rs, Fin fin, cudaStream_t s);
+
+// 16-CTA cluster kernels for the 128 x 128-cell level (cluster16.cu): the
+// visit halves of the tile kernels, and the up half also runs the step's
+// A-orthogonalisation and alpha (what k_mgs_vec does after k_tile_up).
+struct C16Up {
+    TileUp t;                // z / az = P.p[step] / P.ap[step], ap0 = P.ap[0]
+    const double* pj[8];     // P.p[j]
+    const double* apj[8];    // P.ap[j]
+    double* sc;              // this level's scalars
+    int step, ni, post;
+};
+bool c16_supported(const Geo& g);
+void launch_c16_down(const TileDown& a, int pre, cudaStream_t s);
+void launch_c16_up(const C16Up& a, cudaStream_t s);
 
 }  // namespace auxb200

@@ -1,5 +1,5 @@
 """One setup + a short solve for ncu captures:  python tools/prof_one.py graded2049 [max_outer]
-(STREAM=<cells>: GpuOptions.stream_min_width)"""
+(STREAM=<cells>: GpuOptions.stream_min_width; NOGRAPH=1: eager launches, so ncu sees the coarse kernels)"""
 import os
 import sys
 
@@ -15,6 +15,7 @@ elif name.startswith("graded"):
     s = problems.graded_p1(int(name[6:]), 1.3)
 else:
     s = problems.poisson5(int(name[3:]))
-h = api.setup_hierarchy(s.A, s.coords, gpu=api.GpuOptions(stream_min_width=int(os.environ.get("STREAM", "0"))))
+h = api.setup_hierarchy(s.A, s.coords, gpu=api.GpuOptions(stream_min_width=int(os.environ.get("STREAM", "0")),
+                                                          use_graphs=os.environ.get("NOGRAPH", "0") != "1"))
 r = api.solve(s.A, s.b, h, api.CycleOptions(max_outer=max_outer))
 print("iterations", r.iterations)

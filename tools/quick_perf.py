@@ -1,7 +1,7 @@
 """Quick GPU timing probe (not the bench contract): setup + solve times for a
 few BASELINE configurations through the C ABI.  FUSED=<cells> sets
 GpuOptions.fused_max_cells, CLUSTER=0 turns the cluster tier off, STREAM=<cells>
-sets GpuOptions.stream_min_width (-1 off); AUX_TRACE=1 prints the device-time breakdown."""
+sets GpuOptions.stream_min_width (-1 off), C16=0 turns the 16-CTA cluster level off; AUX_TRACE=1 prints the device-time breakdown."""
 import os
 import sys
 import time
@@ -24,7 +24,8 @@ for name in cfgs:
     for rep in range(3):
         t0 = time.time()
         h = api.setup_hierarchy(s.A, s.coords, gpu=api.GpuOptions(fused_max_cells=fused, cluster_tier=os.environ.get("CLUSTER", "1") != "0",
-                                                                  stream_min_width=int(os.environ.get("STREAM", "0"))))
+                                                                  stream_min_width=int(os.environ.get("STREAM", "0")),
+                                                                  cluster16=os.environ.get("C16", "1") != "0"))
         t1 = time.time()
         for k in range(2):
             ts = time.time()
