@@ -46,6 +46,9 @@ __device__ __forceinline__ uint32_t c16_rank() {
 __device__ __forceinline__ void c16_sync() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
+// split cluster barrier: arrive early, wait just before the first remote store
+__device__ __forceinline__ void c16_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
+__device__ __forceinline__ void c16_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
 __device__ __forceinline__ void c16_st(const void* p, uint32_t rank, double v) {
     uint32_t ra;
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(p)), "r"(rank));
@@ -124,12 +127,13 @@ __device__ __forceinline__ void c16_push(double* u, int qx, int qy) {
     c16_st(u + bix(C, da, db), (uint32_t)(ny * 4 + nx), u[bix(C, sa, sb)]);
 }
 
-template <int C>
+template <int C, bool W = false>   // W: complete the split start-up barrier before the push
 __device__ __forceinline__ void c16_pass(const RV16& rv, const double (&f)[4], double* u, int ta, int tb, int qx,
                                          int qy) {
     const int pi = bix(C, ta, tb);
     u[pi] = c16_gs<C>(rv, f[C], u, pi);
     __syncthreads();
+    if (W) c16_wait();
     c16_push<C>(u, qx, qy);
     c16_sync();
 }
@@ -208,12 +212,14 @@ __global__ void __launch_bounds__(kC16T, 1) k_c16_down(const __grid_constant__ T
             if (a.r_out) a.r_out[ci] = f[c];
         }
     }
-    c16_sync();   // every CTA's zero fill before the first remote write (and the cluster is up)
+    __syncthreads();
+    c16_arrive();   // this CTA's zero fill is done (the neighbours wait for it before their first push)
     // sweep 0: colour 0 from zero, then colours 1..3; further sweeps: 0..3
     {
         const int pi = bix(0, ta, tb);
         u[pi] = div_rcp(f[0], rv.v[0][0], rv.rc[0]);
         __syncthreads();
+        c16_wait();
         c16_push<0>(u, qx, qy);
         c16_sync();
     }
@@ -272,7 +278,7 @@ __global__ void __launch_bounds__(kC16T, 1) k_c16_up(const __grid_constant__ C16
     };
     // u = u_pre + e on active cells: own plane position, and one ghost-ring
     // position for threads 0..67 (computed here with the neighbour's arithmetic)
-    auto prolong = [&](int a0, int b0) {
+    auto prolong = [&](int a0, int b0, int nc) {
         const int A = kBH * qx + a0, B = kBH * qy + b0;
         if (A < 0 || A >= g.H || B < 0 || B >= g.H) {
 #pragma unroll
@@ -281,30 +287,31 @@ __global__ void __launch_bounds__(kC16T, 1) k_c16_up(const __grid_constant__ C16
         }
         const double e = corr(A, B);
         const long cb = (long)B * g.H + A;
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
+        for (int c = 0; c < nc; ++c) {
             const long ci = ((long)c << g.lq) + cb;
             const double x = tu.u_pre[ci];
             u[bix(c, a0, b0)] = tu.act[ci] ? __dadd_rn(x, e) : x;
         }
     };
-    prolong(ta, tb);
-    if (t < 68) {
+    prolong(ta, tb, 4);
+    if (t < 68) {   // (in-level colour-3 ghosts: pushed by the neighbour before the first read)
         int ra, rb;
         if (t < 16) { ra = -1; rb = t; }
         else if (t < 32) { ra = kBH; rb = t - 16; }
         else if (t < 48) { ra = t - 32; rb = -1; }
         else if (t < 64) { ra = t - 48; rb = kBH; }
         else { ra = ((t - 64) & 1) ? kBH : -1; rb = ((t - 64) >> 1) ? kBH : -1; }
-        prolong(ra, rb);
+        prolong(ra, rb, 3);
     }
     double f[4];
 #pragma unroll
     for (int c = 0; c < 4; ++c) f[c] = tu.f[((long)c << g.lq) + gpos];
-    c16_sync();   // every CTA's ring filled before the first remote write
+    __syncthreads();
+    c16_arrive();   // (pairs with the c16_wait before the first push: the cluster is up)
     // transposed post-smoothing (cycle.hpp:196)
     for (int sw = 0; sw < a.post; ++sw) {
-        c16_pass<3>(rv, f, u, ta, tb, qx, qy);
+        if (sw == 0) c16_pass<3, true>(rv, f, u, ta, tb, qx, qy);
+        else c16_pass<3>(rv, f, u, ta, tb, qx, qy);
         c16_pass<2>(rv, f, u, ta, tb, qx, qy);
         c16_pass<1>(rv, f, u, ta, tb, qx, qy);
         c16_pass<0>(rv, f, u, ta, tb, qx, qy);

@@ -1127,7 +1127,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_cluster_pcg(const __grid_consta
             for (int c = 0; c < 4; ++c) {
                 const int pi = pidx(Q, c, ta, tb);
                 if (qact[pi]) u[pi] = __dadd_rn(u[pi], e1);
-                if (gh) {
+                // (colour-3 ghosts are not read before the neighbour pushes its
+                // post-smoothed colour 3, and that push may already be landing:
+                // leave them alone)
+                if (gh && c < 3) {
                     const int pj = pidx(Q, c, pa2, pb2);
                     if (qact[pj]) u[pj] = __dadd_rn(u[pj], e2);
                 }
