@@ -627,7 +627,13 @@ __device__ __forceinline__ double resid_fma(const int* __restrict__ rp, const in
 
 constexpr int kSmallInvWords = 5 * 32;   // row-anchored inverses of window rows 0..39 (blocks start in 0..31)
 
-__global__ void __launch_bounds__(256, 4) k_bgs_inv(const int* __restrict__ rp, const int* __restrict__ col,
+#ifndef AUX_BGS_MINB
+#define AUX_BGS_MINB 4
+#endif
+#ifndef AUX_BGS_CHUNK
+#define AUX_BGS_CHUNK 256
+#endif
+__global__ void __launch_bounds__(256, AUX_BGS_MINB) k_bgs_inv(const int* __restrict__ rp, const int* __restrict__ col,
                                                 const double* __restrict__ v, const double* __restrict__ b,
                                                 const uint8_t* __restrict__ meta8, const int2* __restrict__ meta,
                                                 const double* __restrict__ inv_s, const double* __restrict__ inv,
@@ -734,7 +740,7 @@ __global__ void __launch_bounds__(256, 4) k_bgs_inv(const int* __restrict__ rp, 
         // subtracts its products in order from shared memory
         const int pb0 = (int)__reduce_min_sync(0xffffffffu, oa ? (unsigned)pa0 : (ob ? (unsigned)pc0 : 0x7fffffffu));
         const int pb1 = (int)__reduce_max_sync(0xffffffffu, ob ? (unsigned)pc1 : (oa ? (unsigned)pa1 : 0u));
-        constexpr int kChunk = 256;
+        constexpr int kChunk = AUX_BGS_CHUNK;
         for (int cs = pb0; cs < pb1; cs += kChunk) {
             int cc[kChunk / 32];
             double vv[kChunk / 32];
