@@ -107,14 +107,31 @@ __device__ __forceinline__ int pidx(const SLevel& L, int c, int a, int b) {
     return c * L.PP + (b + 1) * L.W2 + a + 1;
 }
 
+// Geometry of a shared-memory level as compile-time constants (HC = its H >
+// 0) or L's runtime fields (HC = 0).  The tier's lower levels are nearly
+// always 8x8 / 4x4 plane positions; with their padded strides as immediates a
+// neighbour load is one instruction off a base register instead of an
+// address computation per load (the 16x16-cell level's phases are issue bound).
+constexpr int ilog2c(int v) { return v <= 1 ? 0 : 1 + ilog2c(v >> 1); }
+template <int HC> __device__ __forceinline__ int lgH(const SLevel& L) { return HC ? HC : L.H; }
+template <int HC> __device__ __forceinline__ int lgLH(const SLevel& L) { return HC ? ilog2c(HC) : L.lh; }
+template <int HC> __device__ __forceinline__ int lgW2(const SLevel& L) { return HC ? HC + 2 : L.W2; }
+template <int HC> __device__ __forceinline__ int lgPP(const SLevel& L) { return HC ? (HC + 2) * (HC + 2) : L.PP; }
+template <int HC> __device__ __forceinline__ int lgNQ(const SLevel& L) { return HC ? HC * HC : L.nq; }
+template <int HC> __device__ __forceinline__ int lgN(const SLevel& L) { return HC ? 4 * HC * HC : L.n; }
+template <int HC>
+__device__ __forceinline__ int pidxh(const SLevel& L, int c, int a, int b) {
+    return c * lgPP<HC>(L) + (b + 1) * lgW2<HC>(L) + a + 1;
+}
+
 // Offset of the slot-t neighbour of a colour-C cell in the padded layout.
-template <int C, int T>
+template <int C, int T, int HC = 0>
 __device__ __forceinline__ int noff(const SLevel& L) {
     constexpr int ux = (C & 1) + stencil_dx(T);
     constexpr int uy = (C >> 1) + stencil_dy(T);
     constexpr int nc = (ux & 1) | ((uy & 1) << 1);
     constexpr int da = ux >> 1, db = uy >> 1;   // arithmetic shift: -1 >> 1 == -1
-    return (nc - C) * L.PP + db * L.W2 + da;
+    return (nc - C) * lgPP<HC>(L) + db * lgW2<HC>(L) + da;
 }
 
 // sg: the fused levels' geometry, copied to shared memory once per launch
@@ -193,54 +210,55 @@ __device__ __forceinline__ void bsum2(double* red, int& par, double& x, double& 
 
 // (A x)_i for a colour-C cell (ell_spmv row, sparse.hpp:120-132): sum from 0.0,
 // slot order; off-grid and inactive-row slots hold exact zeros.
-template <int C>
+template <int C, int HC = 0>
 __device__ __forceinline__ double row9(const SLevel& L, int ci, int pi, const double* x) {
     const double* v = L.val + ci;
     double s = __dadd_rn(0.0, __dmul_rn(v[0], x[pi]));
-    s = __dadd_rn(s, __dmul_rn(v[1 * L.n], x[pi + noff<C, 1>(L)]));
-    s = __dadd_rn(s, __dmul_rn(v[2 * L.n], x[pi + noff<C, 2>(L)]));
-    s = __dadd_rn(s, __dmul_rn(v[3 * L.n], x[pi + noff<C, 3>(L)]));
-    s = __dadd_rn(s, __dmul_rn(v[4 * L.n], x[pi + noff<C, 4>(L)]));
-    s = __dadd_rn(s, __dmul_rn(v[5 * L.n], x[pi + noff<C, 5>(L)]));
-    s = __dadd_rn(s, __dmul_rn(v[6 * L.n], x[pi + noff<C, 6>(L)]));
-    s = __dadd_rn(s, __dmul_rn(v[7 * L.n], x[pi + noff<C, 7>(L)]));
-    s = __dadd_rn(s, __dmul_rn(v[8 * L.n], x[pi + noff<C, 8>(L)]));
+    s = __dadd_rn(s, __dmul_rn(v[1 * lgN<HC>(L)], x[pi + noff<C, 1, HC>(L)]));
+    s = __dadd_rn(s, __dmul_rn(v[2 * lgN<HC>(L)], x[pi + noff<C, 2, HC>(L)]));
+    s = __dadd_rn(s, __dmul_rn(v[3 * lgN<HC>(L)], x[pi + noff<C, 3, HC>(L)]));
+    s = __dadd_rn(s, __dmul_rn(v[4 * lgN<HC>(L)], x[pi + noff<C, 4, HC>(L)]));
+    s = __dadd_rn(s, __dmul_rn(v[5 * lgN<HC>(L)], x[pi + noff<C, 5, HC>(L)]));
+    s = __dadd_rn(s, __dmul_rn(v[6 * lgN<HC>(L)], x[pi + noff<C, 6, HC>(L)]));
+    s = __dadd_rn(s, __dmul_rn(v[7 * lgN<HC>(L)], x[pi + noff<C, 7, HC>(L)]));
+    s = __dadd_rn(s, __dmul_rn(v[8 * lgN<HC>(L)], x[pi + noff<C, 8, HC>(L)]));
     return s;
 }
 
 // Gauss-Seidel update of a colour-C cell (smoother.hpp:81-86).
-template <int C>
+template <int C, int HC = 0>
 __device__ __forceinline__ double gs_cell(const SLevel& L, int ci, int pi, double f, const double* x) {
     const double* v = L.val + ci;
     double s = f;
-    s = __dsub_rn(s, __dmul_rn(v[1 * L.n], x[pi + noff<C, 1>(L)]));
-    s = __dsub_rn(s, __dmul_rn(v[2 * L.n], x[pi + noff<C, 2>(L)]));
-    s = __dsub_rn(s, __dmul_rn(v[3 * L.n], x[pi + noff<C, 3>(L)]));
-    s = __dsub_rn(s, __dmul_rn(v[4 * L.n], x[pi + noff<C, 4>(L)]));
-    s = __dsub_rn(s, __dmul_rn(v[5 * L.n], x[pi + noff<C, 5>(L)]));
-    s = __dsub_rn(s, __dmul_rn(v[6 * L.n], x[pi + noff<C, 6>(L)]));
-    s = __dsub_rn(s, __dmul_rn(v[7 * L.n], x[pi + noff<C, 7>(L)]));
-    s = __dsub_rn(s, __dmul_rn(v[8 * L.n], x[pi + noff<C, 8>(L)]));
+    s = __dsub_rn(s, __dmul_rn(v[1 * lgN<HC>(L)], x[pi + noff<C, 1, HC>(L)]));
+    s = __dsub_rn(s, __dmul_rn(v[2 * lgN<HC>(L)], x[pi + noff<C, 2, HC>(L)]));
+    s = __dsub_rn(s, __dmul_rn(v[3 * lgN<HC>(L)], x[pi + noff<C, 3, HC>(L)]));
+    s = __dsub_rn(s, __dmul_rn(v[4 * lgN<HC>(L)], x[pi + noff<C, 4, HC>(L)]));
+    s = __dsub_rn(s, __dmul_rn(v[5 * lgN<HC>(L)], x[pi + noff<C, 5, HC>(L)]));
+    s = __dsub_rn(s, __dmul_rn(v[6 * lgN<HC>(L)], x[pi + noff<C, 6, HC>(L)]));
+    s = __dsub_rn(s, __dmul_rn(v[7 * lgN<HC>(L)], x[pi + noff<C, 7, HC>(L)]));
+    s = __dsub_rn(s, __dmul_rn(v[8 * lgN<HC>(L)], x[pi + noff<C, 8, HC>(L)]));
     return div_rcp(s, v[0], L.rec[ci]);
 }
 
 // One colour pass.  Inactive cells have f = 0 and an identity row, so the
 // update leaves them at 0 like the reference, which skips them.
-template <int C>
+template <int C, int HC = 0>
 __device__ __forceinline__ void gs_pass(const SLevel& L, const double* f, double* x) {
-    for (int pos = threadIdx.x; pos < L.nq; pos += kThreads) {
-        const int a = pos & (L.H - 1), b = pos >> L.lh;
-        const int pi = pidx(L, C, a, b);
-        x[pi] = gs_cell<C>(L, (C * L.nq) + pos, pi, f[pi], x);
+    for (int pos = threadIdx.x; pos < lgNQ<HC>(L); pos += kThreads) {
+        const int a = pos & (lgH<HC>(L) - 1), b = pos >> lgLH<HC>(L);
+        const int pi = pidxh<HC>(L, C, a, b);
+        x[pi] = gs_cell<C, HC>(L, (C * lgNQ<HC>(L)) + pos, pi, f[pi], x);
     }
     __syncthreads();
 }
 
+template <int HC = 0>
 __device__ __forceinline__ void gs_sweep(const SLevel& L, const double* f, double* x, bool fwd) {
     if (fwd) {
-        gs_pass<0>(L, f, x); gs_pass<1>(L, f, x); gs_pass<2>(L, f, x); gs_pass<3>(L, f, x);
+        gs_pass<0, HC>(L, f, x); gs_pass<1, HC>(L, f, x); gs_pass<2, HC>(L, f, x); gs_pass<3, HC>(L, f, x);
     } else {
-        gs_pass<3>(L, f, x); gs_pass<2>(L, f, x); gs_pass<1>(L, f, x); gs_pass<0>(L, f, x);
+        gs_pass<3, HC>(L, f, x); gs_pass<2, HC>(L, f, x); gs_pass<1, HC>(L, f, x); gs_pass<0, HC>(L, f, x);
     }
 }
 
@@ -311,15 +329,16 @@ __device__ __forceinline__ void gs_sweep_r(const SLevel& L, const RV& rv, const 
 
 // Coarsest solve (cycle.hpp:152-155).  The coarsest level's vectors are padded
 // too; the inverse is stored in colour-major (compact) order.
+template <int HC = 0>
 __device__ void coarse_solve(const FusedArgs& a, const double* inv, double* part, const SLevel& L, PState& ps,
                              double* u) {
     double* r = L.r;
     if (ps.pend) {
         const double na = -ps.alpha[ps.step - 1];
-        const double* ap = L.ap + (ps.step - 1) * 4 * L.PP;
-        for (int ci = threadIdx.x; ci < L.n; ci += kThreads) {
-            const int c = ci >> (2 * L.lh), pos = ci & (L.nq - 1);
-            const int pi = pidx(L, c, pos & (L.H - 1), pos >> L.lh);
+        const double* ap = L.ap + (ps.step - 1) * 4 * lgPP<HC>(L);
+        for (int ci = threadIdx.x; ci < lgN<HC>(L); ci += kThreads) {
+            const int c = ci >> (2 * lgLH<HC>(L)), pos = ci & (lgNQ<HC>(L) - 1);
+            const int pi = pidxh<HC>(L, c, pos & (lgH<HC>(L) - 1), pos >> lgLH<HC>(L));
             r[pi] = __dadd_rn(r[pi], __dmul_rn(na, ap[pi]));
         }
         __syncthreads();
@@ -330,13 +349,13 @@ __device__ void coarse_solve(const FusedArgs& a, const double* inv, double* part
             double* b = a.work;
             double* x = a.work + a.nc;
             for (int ci = 0; ci < a.nc; ++ci) {
-                const int c = ci >> (2 * L.lh), pos = ci & (L.nq - 1);
-                b[a.lex[ci]] = r[pidx(L, c, pos & (L.H - 1), pos >> L.lh)];
+                const int c = ci >> (2 * lgLH<HC>(L)), pos = ci & (lgNQ<HC>(L) - 1);
+                b[a.lex[ci]] = r[pidxh<HC>(L, c, pos & (lgH<HC>(L) - 1), pos >> lgLH<HC>(L))];
             }
             seq_lu_solve(a.lu, a.perm, a.nc, b, x);
             for (int ci = 0; ci < a.nc; ++ci) {
-                const int c = ci >> (2 * L.lh), pos = ci & (L.nq - 1);
-                u[pidx(L, c, pos & (L.H - 1), pos >> L.lh)] = x[a.lex[ci]];
+                const int c = ci >> (2 * lgLH<HC>(L)), pos = ci & (lgNQ<HC>(L) - 1);
+                u[pidxh<HC>(L, c, pos & (lgH<HC>(L) - 1), pos >> lgLH<HC>(L))] = x[a.lex[ci]];
             }
         }
     } else {
@@ -348,8 +367,8 @@ __device__ void coarse_solve(const FusedArgs& a, const double* inv, double* part
         const int nc = a.nc, cs = (nc + 3) / 4;
         double* rc = part + 4 * nc;
         for (int j = threadIdx.x; j < nc; j += kThreads) {
-            const int c = j >> (2 * L.lh), pos = j & (L.nq - 1);
-            rc[j] = r[pidx(L, c, pos & (L.H - 1), pos >> L.lh)];
+            const int c = j >> (2 * lgLH<HC>(L)), pos = j & (lgNQ<HC>(L) - 1);
+            rc[j] = r[pidxh<HC>(L, c, pos & (lgH<HC>(L) - 1), pos >> lgLH<HC>(L))];
         }
         __syncthreads();
         for (int idx = threadIdx.x; idx < 4 * nc; idx += kThreads) {
@@ -363,8 +382,8 @@ __device__ void coarse_solve(const FusedArgs& a, const double* inv, double* part
         }
         __syncthreads();
         for (int row = threadIdx.x; row < nc; row += kThreads) {
-            const int c = row >> (2 * L.lh), pos = row & (L.nq - 1);
-            u[pidx(L, c, pos & (L.H - 1), pos >> L.lh)] =
+            const int c = row >> (2 * lgLH<HC>(L)), pos = row & (lgNQ<HC>(L) - 1);
+            u[pidxh<HC>(L, c, pos & (lgH<HC>(L) - 1), pos >> lgLH<HC>(L))] =
                 ((part[row] + part[nc + row]) + part[2 * nc + row]) + part[3 * nc + row];
         }
     }
@@ -373,28 +392,30 @@ __device__ void coarse_solve(const FusedArgs& a, const double* inv, double* part
 
 // Restricted residual of the colour-C children (hierarchy.hpp:267-277 order:
 // children SW, SE, NW, NE == colours 0..3, sum from 0.0).
-template <int C>
+template <int C, int HC = 0>
 __device__ __forceinline__ double child_resid(const SLevel& L, int T1, int T2, const double* f, const double* u) {
-    const int pi = pidx(L, C, T1, T2);
-    const int ci = C * L.nq + (T2 << L.lh) + T1;
-    return __dsub_rn(f[pi], row9<C>(L, ci, pi, u));
+    const int pi = pidxh<HC>(L, C, T1, T2);
+    const int ci = C * lgNQ<HC>(L) + (T2 << lgLH<HC>(L)) + T1;
+    return __dsub_rn(f[pi], row9<C, HC>(L, ci, pi, u));
 }
 
 // Pre-smoothing from u = 0 (cycle.hpp:170-171) and the restricted residual
 // (cycle.hpp:173-178).  The first pass applies the pending PCG residual
 // update of this level, relaxes colour 0 from zero and writes u = 0 elsewhere.
+template <int HC = 0>
 __device__ void cycle_down(const FusedArgs& a, const SLevel& L, PState& ps, const SLevel& Cc, double* u,
                            const RV* rv) {
+    constexpr int HCC = HC / 2;   // the child level's geometry
     PH_RESET
-    const int po = L.n > 256 ? 0 : 16;
+    const int po = lgN<HC>(L) > 256 ? 0 : 16;
     (void)po;
     double* f = L.r;
     const bool pend = ps.pend != 0;
     const double na = pend ? -ps.alpha[ps.step - 1] : 0.0;
-    const double* ap = L.ap + (ps.step > 0 ? ps.step - 1 : 0) * 4 * L.PP;
-    for (int ci = threadIdx.x; ci < L.n; ci += kThreads) {
-        const int c = ci >> (2 * L.lh), pos = ci & (L.nq - 1);
-        const int pi = pidx(L, c, pos & (L.H - 1), pos >> L.lh);
+    const double* ap = L.ap + (ps.step > 0 ? ps.step - 1 : 0) * 4 * lgPP<HC>(L);
+    for (int ci = threadIdx.x; ci < lgN<HC>(L); ci += kThreads) {
+        const int c = ci >> (2 * lgLH<HC>(L)), pos = ci & (lgNQ<HC>(L) - 1);
+        const int pi = pidxh<HC>(L, c, pos & (lgH<HC>(L) - 1), pos >> lgLH<HC>(L));
         double fi = f[pi];
         if (pend) {
             fi = __dadd_rn(fi, __dmul_rn(na, ap[pi]));
@@ -411,13 +432,13 @@ __device__ void cycle_down(const FusedArgs& a, const SLevel& L, PState& ps, cons
         gs_pass_r<3>(L, *rv, f, u);
         for (int sw = 1; sw < a.pre; ++sw) gs_sweep_r(L, *rv, f, u, true);
     } else {
-        gs_pass<1>(L, f, u);
+        gs_pass<1, HC>(L, f, u);
         PH(po + 1)
-        gs_pass<2>(L, f, u);
+        gs_pass<2, HC>(L, f, u);
         PH(po + 2)
-        gs_pass<3>(L, f, u);
+        gs_pass<3, HC>(L, f, u);
         PH(po + 3)
-        for (int sw = 1; sw < a.pre; ++sw) gs_sweep(L, f, u, true);
+        for (int sw = 1; sw < a.pre; ++sw) gs_sweep<HC>(L, f, u, true);
     }
     if (rv) {   // thread t: the children at plane position t (all four colours)
         const int t = threadIdx.x;
@@ -429,22 +450,22 @@ __device__ void cycle_down(const FusedArgs& a, const SLevel& L, PState& ps, cons
         sum = __dadd_rn(sum, __dsub_rn(f[pidx_r(2, T1, T2)], row9_r<2>(L, r, pidx_r(2, T1, T2), u)));
         sum = __dadd_rn(sum, __dsub_rn(f[pidx_r(3, T1, T2)], row9_r<3>(L, r, pidx_r(3, T1, T2), u)));
         const int cq = (T1 & 1) | ((T2 & 1) << 1);
-        Cc.r[pidx(Cc, cq, T1 >> 1, T2 >> 1)] = sum;
+        Cc.r[pidxh<HCC>(Cc, cq, T1 >> 1, T2 >> 1)] = sum;
         __syncthreads();
         PH(po + 4)
         return;
     }
     // restriction into the child's PCG residual
-    for (int Q = threadIdx.x; Q < Cc.n; Q += kThreads) {
-        const int cq = Q >> (2 * Cc.lh), pos = Q & (Cc.nq - 1);
-        const int ac = pos & (Cc.H - 1), bc = pos >> Cc.lh;
+    for (int Q = threadIdx.x; Q < lgN<HCC>(Cc); Q += kThreads) {
+        const int cq = Q >> (2 * lgLH<HCC>(Cc)), pos = Q & (lgNQ<HCC>(Cc) - 1);
+        const int ac = pos & (lgH<HCC>(Cc) - 1), bc = pos >> lgLH<HCC>(Cc);
         const int T1 = 2 * ac + (cq & 1), T2 = 2 * bc + (cq >> 1);   // coarse cell = fine plane coords
         double sum = 0.0;
-        sum = __dadd_rn(sum, child_resid<0>(L, T1, T2, f, u));
-        sum = __dadd_rn(sum, child_resid<1>(L, T1, T2, f, u));
-        sum = __dadd_rn(sum, child_resid<2>(L, T1, T2, f, u));
-        sum = __dadd_rn(sum, child_resid<3>(L, T1, T2, f, u));
-        Cc.r[pidx(Cc, cq, ac, bc)] = sum;
+        sum = __dadd_rn(sum, child_resid<0, HC>(L, T1, T2, f, u));
+        sum = __dadd_rn(sum, child_resid<1, HC>(L, T1, T2, f, u));
+        sum = __dadd_rn(sum, child_resid<2, HC>(L, T1, T2, f, u));
+        sum = __dadd_rn(sum, child_resid<3, HC>(L, T1, T2, f, u));
+        Cc.r[pidxh<HCC>(Cc, cq, ac, bc)] = sum;
     }
     __syncthreads();
     PH(po + 4)
@@ -453,10 +474,12 @@ __device__ void cycle_down(const FusedArgs& a, const SLevel& L, PState& ps, cons
 // u_i += ec[parent(i)] on active cells (cycle.hpp:191-194) with
 // ec = ((0 + alpha_0 p_0) + alpha_1 p_1) ... the child's PCG iterate, then the
 // transposed post-smoothing (cycle.hpp:196).
+template <int HC = 0>
 __device__ void cycle_up(const FusedArgs& a, const SLevel& L, const SLevel& Cc, const PState& cs, double* u,
                          const RV* rv) {
+    constexpr int HCC = HC / 2;   // the child level's geometry
     PH_RESET
-    const int po = L.n > 256 ? 0 : 16;
+    const int po = lgN<HC>(L) > 256 ? 0 : 16;
     (void)po;
     // the child's alphas in registers, and the
     // four children of a parent handled by one thread: the parent's
@@ -465,17 +488,17 @@ __device__ void cycle_up(const FusedArgs& a, const SLevel& L, const SLevel& Cc, 
     double al[kFusedMaxInner];
 #pragma unroll
     for (int k = 0; k < kFusedMaxInner; ++k) al[k] = k < nval ? cs.alpha[k] : 0.0;
-    for (int pos = threadIdx.x; pos < L.nq; pos += kThreads) {
-        const int A = pos & (L.H - 1), B = pos >> L.lh;   // parent cell (A, B) on the child level
-        const int pc = pidx(Cc, (A & 1) | ((B & 1) << 1), A >> 1, B >> 1);
+    for (int pos = threadIdx.x; pos < lgNQ<HC>(L); pos += kThreads) {
+        const int A = pos & (lgH<HC>(L) - 1), B = pos >> lgLH<HC>(L);   // parent cell (A, B) on the child level
+        const int pc = pidxh<HCC>(Cc, (A & 1) | ((B & 1) << 1), A >> 1, B >> 1);
         double e = 0.0;
 #pragma unroll
         for (int k = 0; k < kFusedMaxInner; ++k)
-            if (k < nval) e = __dadd_rn(e, __dmul_rn(al[k], Cc.p[k * 4 * Cc.PP + pc]));
+            if (k < nval) e = __dadd_rn(e, __dmul_rn(al[k], Cc.p[k * 4 * lgPP<HCC>(Cc) + pc]));
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-            if (!L.act[c * L.nq + pos]) continue;
-            const int pi = pidx(L, c, A, B);
+            if (!L.act[c * lgNQ<HC>(L) + pos]) continue;
+            const int pi = pidxh<HC>(L, c, A, B);
             u[pi] = __dadd_rn(u[pi], e);
         }
     }
@@ -483,17 +506,17 @@ __device__ void cycle_up(const FusedArgs& a, const SLevel& L, const SLevel& Cc, 
     PH(po + 5)
     for (int sw = 0; sw < a.post; ++sw) {
         if (rv) gs_sweep_r(L, *rv, L.r, u, false);
-        else gs_sweep(L, L.r, u, false);
+        else gs_sweep<HC>(L, L.r, u, false);
     }
     PH(po + 6)
 }
 
-template <int C>
+template <int C, int HC = 0>
 __device__ __forceinline__ void spmv_color(const SLevel& L, const double* x, double* y, const double* r,
                                            const double* w, int mode, double& s0, double& s1) {
-    for (int pos = threadIdx.x; pos < L.nq; pos += kThreads) {
-        const int pi = pidx(L, C, pos & (L.H - 1), pos >> L.lh);
-        const double yi = row9<C>(L, C * L.nq + pos, pi, x);
+    for (int pos = threadIdx.x; pos < lgNQ<HC>(L); pos += kThreads) {
+        const int pi = pidxh<HC>(L, C, pos & (lgH<HC>(L) - 1), pos >> lgLH<HC>(L));
+        const double yi = row9<C, HC>(L, C * lgNQ<HC>(L) + pos, pi, x);
         y[pi] = yi;
         const double xi = x[pi];
         if (mode == 0) {
@@ -526,8 +549,9 @@ __device__ __forceinline__ void spmv_color_r(const SLevel& L, const RV& rv, cons
 // After the preconditioner application of step i: A z, the A-orthogonalisation
 // against the kept directions (cycle.hpp:84-97) and alpha (cycle.hpp:123).
 // Returns true when this PCG is finished (breakdown or last step).
+template <int HC = 0>
 __device__ bool pcg_step(const FusedArgs& a, const SLevel& L, PState& ps, double* red, int& par, const RV* rv) {
-    const int vs = 4 * L.PP;
+    const int vs = 4 * lgPP<HC>(L);
     const int i = ps.step;
     double* p = L.p + i * vs;
     double* ap = L.ap + i * vs;
@@ -536,24 +560,24 @@ __device__ bool pcg_step(const FusedArgs& a, const SLevel& L, PState& ps, double
     double s0 = 0.0, s1 = 0.0;
     const int mode = i == 0 ? 0 : 1;
     PH_RESET
-    const int po = L.n > 256 ? 0 : 16;
+    const int po = lgN<HC>(L) > 256 ? 0 : 16;
     (void)po;
     if (rv) {
         spmv_color_r<0>(L, *rv, p, ap, L.r, L.ap, mode, s0, s1);
         spmv_color_r<1>(L, *rv, p, ap, L.r, L.ap, mode, s0, s1);
         spmv_color_r<2>(L, *rv, p, ap, L.r, L.ap, mode, s0, s1);
         spmv_color_r<3>(L, *rv, p, ap, L.r, L.ap, mode, s0, s1);
-    } else if (L.n <= kThreads) {   // all four colours at once, one cell per thread
+    } else if (lgN<HC>(L) <= kThreads) {   // all four colours at once, one cell per thread
         const int ci = threadIdx.x;
-        if (ci < L.n) {
-            const int c = ci >> (2 * L.lh), pos = ci & (L.nq - 1);
-            const int pi = pidx(L, c, pos & (L.H - 1), pos >> L.lh);
+        if (ci < lgN<HC>(L)) {
+            const int c = ci >> (2 * lgLH<HC>(L)), pos = ci & (lgNQ<HC>(L) - 1);
+            const int pi = pidxh<HC>(L, c, pos & (lgH<HC>(L) - 1), pos >> lgLH<HC>(L));
             double yi;
             switch (c) {
-                case 0: yi = row9<0>(L, ci, pi, p); break;
-                case 1: yi = row9<1>(L, ci, pi, p); break;
-                case 2: yi = row9<2>(L, ci, pi, p); break;
-                default: yi = row9<3>(L, ci, pi, p); break;
+                case 0: yi = row9<0, HC>(L, ci, pi, p); break;
+                case 1: yi = row9<1, HC>(L, ci, pi, p); break;
+                case 2: yi = row9<2, HC>(L, ci, pi, p); break;
+                default: yi = row9<3, HC>(L, ci, pi, p); break;
             }
             ap[pi] = yi;
             const double xi = p[pi];
@@ -565,10 +589,10 @@ __device__ bool pcg_step(const FusedArgs& a, const SLevel& L, PState& ps, double
             }
         }
     } else {
-        spmv_color<0>(L, p, ap, L.r, L.ap, mode, s0, s1);
-        spmv_color<1>(L, p, ap, L.r, L.ap, mode, s0, s1);
-        spmv_color<2>(L, p, ap, L.r, L.ap, mode, s0, s1);
-        spmv_color<3>(L, p, ap, L.r, L.ap, mode, s0, s1);
+        spmv_color<0, HC>(L, p, ap, L.r, L.ap, mode, s0, s1);
+        spmv_color<1, HC>(L, p, ap, L.r, L.ap, mode, s0, s1);
+        spmv_color<2, HC>(L, p, ap, L.r, L.ap, mode, s0, s1);
+        spmv_color<3, HC>(L, p, ap, L.r, L.ap, mode, s0, s1);
     }
     bsum2(red, par, s0, s1);
     PH(po + 7)
@@ -585,9 +609,9 @@ __device__ bool pcg_step(const FusedArgs& a, const SLevel& L, PState& ps, double
             const bool fin = (j == i);
             const double* wj = L.ap + j * vs;
             double t0 = 0.0, t1 = 0.0;
-            for (int ci = threadIdx.x; ci < L.n; ci += kThreads) {
-                const int c = ci >> (2 * L.lh), pos = ci & (L.nq - 1);
-                const int q = pidx(L, c, pos & (L.H - 1), pos >> L.lh);
+            for (int ci = threadIdx.x; ci < lgN<HC>(L); ci += kThreads) {
+                const int c = ci >> (2 * lgLH<HC>(L)), pos = ci & (lgNQ<HC>(L) - 1);
+                const int q = pidxh<HC>(L, c, pos & (lgH<HC>(L) - 1), pos >> lgLH<HC>(L));
                 const double pq = __dadd_rn(p[q], __dmul_rn(beta, pj[q]));
                 const double aq = __dadd_rn(ap[q], __dmul_rn(beta, apj[q]));
                 p[q] = pq;
@@ -703,7 +727,11 @@ __device__ void tier_run(const FusedArgs& a, unsigned char* sm, const Geo* sgeo,
             double* u = L.p + cur.step * 4 * L.PP;
             if (q < nl - 1) {
                 FCLK_BEGIN
-                cycle_down(a, L, cur, slev(a, sm, sgeo, q + 1), u, (q == 0 && top_reg) ? &rv0 : nullptr);
+                const SLevel Cn = slev(a, sm, sgeo, q + 1);
+                if (q == 0 && top_reg) cycle_down<0>(a, L, cur, Cn, u, &rv0);
+                else if (L.H == 8) cycle_down<8>(a, L, cur, Cn, u, nullptr);
+                else if (L.H == 4) cycle_down<4>(a, L, cur, Cn, u, nullptr);
+                else cycle_down<0>(a, L, cur, Cn, u, nullptr);
                 FCLK_END(0, q)
                 ts->step[q] = cur.step;   // the parent's registers, restored when the child returns
                 ts->pend[q] = cur.pend;
@@ -713,7 +741,8 @@ __device__ void tier_run(const FusedArgs& a, unsigned char* sm, const Geo* sgeo,
                 continue;
             }
             FCLK_BEGIN
-            coarse_solve(a, inv, part, L, cur, u);
+            if (L.H == 4) coarse_solve<4>(a, inv, part, L, cur, u);
+            else coarse_solve<0>(a, inv, part, L, cur, u);
             FCLK_END(1, q)
             resume = true;
             if (a.coarse_mode != 0) continue;
@@ -726,7 +755,11 @@ __device__ void tier_run(const FusedArgs& a, unsigned char* sm, const Geo* sgeo,
             *cur.nval = 1;
         } else {
             FCLK_BEGIN
-            const bool done = pcg_step(a, L, cur, red, par, (q == 0 && top_reg) ? &rv0 : nullptr);
+            bool done;
+            if (q == 0 && top_reg) done = pcg_step<0>(a, L, cur, red, par, &rv0);
+            else if (L.H == 8) done = pcg_step<8>(a, L, cur, red, par, nullptr);
+            else if (L.H == 4) done = pcg_step<4>(a, L, cur, red, par, nullptr);
+            else done = pcg_step<0>(a, L, cur, red, par, nullptr);
             FCLK_END(2, q)
             if (!done) {
                 cur.pend = 1;
@@ -745,7 +778,11 @@ __device__ void tier_run(const FusedArgs& a, unsigned char* sm, const Geo* sgeo,
         cur.pend = ts->pend[q];
         const SLevel P = slev(a, sm, sgeo, q);
         FCLK_BEGIN
-        cycle_up(a, P, L, child, P.p + cur.step * 4 * P.PP, (q == 0 && top_reg) ? &rv0 : nullptr);
+        double* up = P.p + cur.step * 4 * P.PP;
+        if (q == 0 && top_reg) cycle_up<0>(a, P, L, child, up, &rv0);
+        else if (P.H == 8) cycle_up<8>(a, P, L, child, up, nullptr);
+        else if (P.H == 4) cycle_up<4>(a, P, L, child, up, nullptr);
+        else cycle_up<0>(a, P, L, child, up, nullptr);
         FCLK_END(3, q)
         resume = true;
     }
