@@ -117,6 +117,17 @@ class ClockSampler:
                                          stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
+        # let nvidia-smi finish starting up (NVML init, first sample) before the
+        # timed region opens: its start-up competes with the driver calls of the
+        # first timed steps (seen as a 5-8 ms per-step gap on some boxes)
+        t_end = time.time() + 3.0
+        while self.proc is not None and time.time() < t_end:
+            try:
+                if os.path.getsize(self.path) > 0:
+                    break
+            except OSError:
+                break
+            time.sleep(0.02)
         return self
 
     def __exit__(self, *a):
