@@ -56,14 +56,15 @@ __device__ int g_fclk_launch;
 #define FCLK_END(T, Q)                                                        \
     if (threadIdx.x == 0) { s_clk[(T) * 4 + ((Q) & 3)] += clock64() - fclk_t0; s_cnt[(T) * 4 + ((Q) & 3)]++; }
 __device__ unsigned long long g_ph[32], g_phn[32];
-__device__ long long g_ph_last;
-#define PH_RESET if (threadIdx.x == 0) g_ph_last = clock64();
+// (the phase start lives in a register: a global one cost thread 0 a memory
+// round trip per phase, which the next barrier made every thread wait for)
+#define PH_RESET long long ph_last_ = clock64();
 #define PH(ID)                                                                \
     if (threadIdx.x == 0) {                                                   \
         const long long t_ = clock64();                                       \
-        atomicAdd(&g_ph[ID], (unsigned long long)(t_ - g_ph_last));           \
+        atomicAdd(&g_ph[ID], (unsigned long long)(t_ - ph_last_));            \
         atomicAdd(&g_phn[ID], 1ull);                                          \
-        g_ph_last = t_;                                                       \
+        ph_last_ = t_;                                                        \
     }
 #define FCLK_REPORT                                                           \
     if (threadIdx.x == 0 && atomicAdd(&g_fclk_launch, 1) == 2) {            \
