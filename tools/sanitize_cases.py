@@ -9,6 +9,7 @@ Cases (each prints one line; exit code 1 if a solve fails to converge):
   lu        jittered n=65, block_solve=1, coarse_solve=1 (reference-order LU paths)
   nograph   jittered n=65 with CUDA graphs off (eager launches, PDL chains)
   dist      jittered n=129 split over 2 parts on one device (in-process transport)
+  c16       jittered n=257: the 128x128-cell level as 16-CTA clusters (cluster16.cu) + cluster tier
 """
 import os
 import sys
@@ -49,6 +50,7 @@ CASES = {
     "lu": lambda: run("lu", problems.jittered_p1(65), api.GpuOptions(block_solve=1, coarse_solve=1)),
     "nograph": lambda: run("nograph", problems.jittered_p1(65), api.GpuOptions(use_graphs=False)),
     "dist": lambda: run("dist", problems.jittered_p1(129), api.GpuOptions(), dist_parts=2),
+    "c16": lambda: run("c16", problems.jittered_p1(257), api.GpuOptions()),
 }
 
 if __name__ == "__main__":
