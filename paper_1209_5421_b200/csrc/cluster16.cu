@@ -102,39 +102,31 @@ __device__ __forceinline__ double c16_row9(const RV16& rv, const double* u, int 
     return y;
 }
 
-// Push this block's boundary cells of colour C into the neighbours' ghost
-// rings: threads 0..63 the four edges, 64..67 the four corners.
+// Push this thread's freshly computed colour-C value into the ghost rings of
+// the neighbours its plane position (ta, tb) borders; the cluster barrier
+// after the pass orders it (and the CTA's own stores) before any reader.
 template <int C>
-__device__ __forceinline__ void c16_push(double* u, int qx, int qy) {
-    const int t = threadIdx.x;
-    if (t >= 68) return;
-    int sa, sb, da, db, nx = qx, ny = qy;
-    if (t < 16) {            // left edge -> left neighbour's right ghost column
-        sa = 0; sb = t; da = kBH; db = t; nx = qx - 1;
-    } else if (t < 32) {     // right edge
-        sa = kBH - 1; sb = t - 16; da = -1; db = t - 16; nx = qx + 1;
-    } else if (t < 48) {     // bottom edge
-        sa = t - 32; sb = 0; da = t - 32; db = kBH; ny = qy - 1;
-    } else if (t < 64) {     // top edge
-        sa = t - 48; sb = kBH - 1; da = t - 48; db = -1; ny = qy + 1;
-    } else {                 // corners
-        const int cx = (t - 64) & 1, cy = (t - 64) >> 1;
-        sa = cx ? kBH - 1 : 0; sb = cy ? kBH - 1 : 0;
-        da = cx ? -1 : kBH; db = cy ? -1 : kBH;
-        nx = qx + (cx ? 1 : -1); ny = qy + (cy ? 1 : -1);
-    }
-    if (nx < 0 || nx > 3 || ny < 0 || ny > 3) return;
-    c16_st(u + bix(C, da, db), (uint32_t)(ny * 4 + nx), u[bix(C, sa, sb)]);
+__device__ __forceinline__ void c16_push_own(double* u, int qx, int qy, int ta, int tb, double val) {
+    const bool w = ta == 0 && qx > 0, e = ta == kBH - 1 && qx < 3;
+    const bool s = tb == 0 && qy > 0, n = tb == kBH - 1 && qy < 3;
+    if (w) c16_st(u + bix(C, kBH, tb), (uint32_t)(qy * 4 + qx - 1), val);
+    if (e) c16_st(u + bix(C, -1, tb), (uint32_t)(qy * 4 + qx + 1), val);
+    if (s) c16_st(u + bix(C, ta, kBH), (uint32_t)((qy - 1) * 4 + qx), val);
+    if (n) c16_st(u + bix(C, ta, -1), (uint32_t)((qy + 1) * 4 + qx), val);
+    if (w && s) c16_st(u + bix(C, kBH, kBH), (uint32_t)((qy - 1) * 4 + qx - 1), val);
+    if (e && s) c16_st(u + bix(C, -1, kBH), (uint32_t)((qy - 1) * 4 + qx + 1), val);
+    if (w && n) c16_st(u + bix(C, kBH, -1), (uint32_t)((qy + 1) * 4 + qx - 1), val);
+    if (e && n) c16_st(u + bix(C, -1, -1), (uint32_t)((qy + 1) * 4 + qx + 1), val);
 }
 
 template <int C, bool W = false>   // W: complete the split start-up barrier before the push
 __device__ __forceinline__ void c16_pass(const RV16& rv, const double (&f)[4], double* u, int ta, int tb, int qx,
                                          int qy) {
     const int pi = bix(C, ta, tb);
-    u[pi] = c16_gs<C>(rv, f[C], u, pi);
-    __syncthreads();
+    const double val = c16_gs<C>(rv, f[C], u, pi);
+    u[pi] = val;
     if (W) c16_wait();
-    c16_push<C>(u, qx, qy);
+    c16_push_own<C>(u, qx, qy, ta, tb, val);
     c16_sync();
 }
 
@@ -217,10 +209,10 @@ __global__ void __launch_bounds__(kC16T, 1) k_c16_down(const __grid_constant__ T
     // sweep 0: colour 0 from zero, then colours 1..3; further sweeps: 0..3
     {
         const int pi = bix(0, ta, tb);
-        u[pi] = div_rcp(f[0], rv.v[0][0], rv.rc[0]);
-        __syncthreads();
+        const double val = div_rcp(f[0], rv.v[0][0], rv.rc[0]);
+        u[pi] = val;
         c16_wait();
-        c16_push<0>(u, qx, qy);
+        c16_push_own<0>(u, qx, qy, ta, tb, val);
         c16_sync();
     }
     c16_pass<1>(rv, f, u, ta, tb, qx, qy);

@@ -303,9 +303,7 @@ __device__ __forceinline__ double row9_r(const SLevel& L, const RV& rv, int pi, 
 }
 
 template <int C>
-__device__ __forceinline__ void gs_pass_r(const SLevel& L, const RV& rv, const double* f, double* x) {
-    const int pos = threadIdx.x;
-    const int pi = pidx_r(C, pos & (kRH - 1), pos >> 4);
+__device__ __forceinline__ double gs_cell_r(const RV& rv, const double* f, const double* x, int pi) {
     const double* v = rv.v[C];
     double s = f[pi];
     s = __dsub_rn(s, __dmul_rn(v[1], x[pi + noff_r<C, 1>()]));
@@ -316,7 +314,13 @@ __device__ __forceinline__ void gs_pass_r(const SLevel& L, const RV& rv, const d
     s = __dsub_rn(s, __dmul_rn(v[6], x[pi + noff_r<C, 6>()]));
     s = __dsub_rn(s, __dmul_rn(v[7], x[pi + noff_r<C, 7>()]));
     s = __dsub_rn(s, __dmul_rn(v[8], x[pi + noff_r<C, 8>()]));
-    x[pi] = div_rcp(s, v[0], rv.rc[C]);
+    return div_rcp(s, v[0], rv.rc[C]);
+}
+template <int C>
+__device__ __forceinline__ void gs_pass_r(const SLevel& L, const RV& rv, const double* f, double* x) {
+    const int pos = threadIdx.x;
+    const int pi = pidx_r(C, pos & (kRH - 1), pos >> 4);
+    x[pi] = gs_cell_r<C>(rv, f, x, pi);
     __syncthreads();
 }
 
@@ -903,29 +907,26 @@ __device__ __forceinline__ double ld_cluster(const void* p, uint32_t rank) {
     return v;
 }
 
-// Push the quadrant boundary of colour C of x into the neighbours' ghost rings
-// (threads 0..32: 16 column cells, 16 row cells, the corner).
+// Push one freshly computed colour-C value of this thread's plane position
+// (ta, tb) into the neighbours' ghost rings when it sits on an edge facing
+// them; the cluster barrier after the pass orders it (and the CTA's own
+// stores) before any reader, so a pass needs no CTA barrier of its own.
 template <int C>
-__device__ __forceinline__ void q_push(const SLevel& L, double* x, int qx, int qy) {
-    const int t = threadIdx.x;
-    if (t > 2 * kQH) return;
+__device__ __forceinline__ void q_push_own(double* x, int qx, int qy, int ta, int tb, double val) {
     const int ea = qx == 0 ? kQH - 1 : 0, ga = qx == 0 ? -1 : kQH;   // my edge column, its ghost column
     const int eb = qy == 0 ? kQH - 1 : 0, gb = qy == 0 ? -1 : kQH;
-    int sa, sb, da, db, nqx = qx, nqy = qy;
-    if (t < kQH) {
-        sa = ea; sb = t; da = ga; db = t; nqx = 1 - qx;
-    } else if (t < 2 * kQH) {
-        sa = t - kQH; sb = eb; da = sa; db = gb; nqy = 1 - qy;
-    } else {
-        sa = ea; sb = eb; da = ga; db = gb; nqx = 1 - qx; nqy = 1 - qy;
-    }
-    st_cluster(x + pidx(L, C, da, db), (uint32_t)(nqy * 2 + nqx), x[pidx(L, C, sa, sb)]);
+    if (ta == ea) st_cluster(x + pidx_r(C, ga, tb), (uint32_t)(qy * 2 + (1 - qx)), val);
+    if (tb == eb) st_cluster(x + pidx_r(C, ta, gb), (uint32_t)((1 - qy) * 2 + qx), val);
+    if (ta == ea && tb == eb) st_cluster(x + pidx_r(C, ga, gb), (uint32_t)((1 - qy) * 2 + (1 - qx)), val);
 }
 
 template <int C>
 __device__ __forceinline__ void q_pass(const SLevel& L, const RV& rv, const double* f, double* x, int qx, int qy) {
-    gs_pass_r<C>(L, rv, f, x);   // ends with __syncthreads
-    q_push<C>(L, x, qx, qy);
+    const int t = threadIdx.x, ta = t & (kQH - 1), tb = t >> 4;
+    const int pi = pidx_r(C, ta, tb);
+    const double val = gs_cell_r<C>(rv, f, x, pi);
+    x[pi] = val;
+    q_push_own<C>(x, qx, qy, ta, tb, val);
 }
 
 // Block sum of (x, y) of the quadrant CTA, pushed to slot [par][rank] of every
@@ -1071,12 +1072,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_cluster_pcg(const __grid_consta
                     fi = __dadd_rn(fi, __dmul_rn(na, apv[pi]));
                     Q.r[pi] = fi;
                 }
-                u[pi] = c == 0 ? div_rcp(fi, rv.v[0][0], rv.rc[0]) : 0.0;
+                const double u0 = c == 0 ? div_rcp(fi, rv.v[0][0], rv.rc[0]) : 0.0;
+                u[pi] = u0;
+                if (c == 0) q_push_own<0>(u, qx, qy, ta, tb, u0);
             }
             // ghost rings of colours 1..3 restart at zero (colour 0 is pushed)
             if (zslot >= 0) u[zslot] = 0.0;
-            __syncthreads();
-            q_push<0>(Q, u, qx, qy);
         }
         csync();
         CPH(1)
