@@ -108,12 +108,14 @@ class ClockSampler:
     def __enter__(self):
         fd, self.path = tempfile.mkstemp(suffix=".csv")
         os.close(fd)
-        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+        q = ("index,clocks.sm,clocks.max.sm," + os.environ.get("AUX_SMI_POWER", "power.draw") + ",clocks_event_reasons.active,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
+            if os.environ.get("AUX_SMI_OFF"):
+                raise RuntimeError("sampler off")
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                          "--format=csv,noheader,nounits", "-lms", os.environ.get("AUX_SMI_MS", "500")],
                                          stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
@@ -334,10 +336,12 @@ def main():
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         iters = None
         setup_ms, solve_ms = [], []
+        step_ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
         with ClockSampler(local) as clk:
             barrier()
             ev0.record()
-            for _ in range(steps):
+            for k in range(steps):
+                step_ev[k].record()
                 h = setup_dev()
                 r = api.solve_device(h, d_b.data_ptr(), d_u.data_ptr(), N)
                 iters = r.iterations
@@ -345,10 +349,12 @@ def main():
                 setup_ms.append(a)
                 solve_ms.append(b)
                 del h
+            step_ev[steps].record()
             ev1.record()
             barrier()
         launches = api.launch_count() - launches0
         ms_step = maxr(ev0.elapsed_time(ev1)) / steps
+        steps_ms = [round(step_ev[k].elapsed_time(step_ev[k + 1]), 3) for k in range(steps)]
         u_dev = d_u.cpu().numpy()
         prof = {}
         if with_profile:
@@ -393,7 +399,7 @@ def main():
             assert np.array_equal(res.u[ids], u_dev[ids]), "host-API and device-API solutions differ"
         else:
             assert np.array_equal(res.u, u_dev), "host-API and device-API solutions differ"
-        return dict(ms_step=ms_step, e2e_ms=e2e_ms, iters=iters, launches=launches, clocks=clk.summary(),
+        return dict(ms_step=ms_step, e2e_ms=e2e_ms, iters=iters, launches=launches, clocks=clk.summary(), steps_ms=steps_ms,
                     setup_ms=statistics.median(setup_ms), solve_ms=statistics.median(solve_ms), prof=prof,
                     h2d=int(h2d), d2h=int(N * 8))
 
@@ -441,7 +447,7 @@ def main():
         "config": config_dict(cfg, N, nnz), "iterations": m["iters"],
         "parallelism": (f"quadtree-subtree partition over {world} GPUs, NCCL halo/ghost exchange + all-reduce, "
                         "coarse levels agglomerated on rank 0") if use_dist else "1 GPU",
-        "breakdown": {"setup_ms": m["setup_ms"], "solve_ms": solve_ms,
+        "breakdown": {"setup_ms": m["setup_ms"], "solve_ms": solve_ms, "steps_ms": m["steps_ms"],
                       "coarse_kcycle_ms": round(prof[3][1], 3) if 3 in prof else None},
         "e2e": {"value": m["e2e_ms"] / mdof, "unit": "ms/MDOF", "h2d_bytes_per_step": m["h2d"],
                 "d2h_bytes_per_step": m["d2h"]},
