@@ -10,7 +10,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_1209_5421_b200 import api, problems  # noqa: E402
 
-s = problems.graded_p1(2049, 1.3)
+s = problems.jittered_p1(int(sys.argv[1][6:])) if len(sys.argv) > 1 and sys.argv[1].startswith("jitter") else problems.graded_p1(2049, 1.3)
 N = s.A.n_rows
 pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()  # noqa: E731
 A_h = api.CsrMatrix(N, N, pin(s.A.row_ptr), pin(s.A.col_idx), pin(s.A.values))
