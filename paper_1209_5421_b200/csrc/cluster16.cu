@@ -25,6 +25,8 @@
 // Per-cell arithmetic is that of the tile kernels (bitwise colour-ordered
 // Gauss-Seidel, smoother.hpp:81-86; restriction sums in member order); only
 // the inner products' summation order differs.
+#include <atomic>
+
 #include "tiles.cuh"
 #include "tma.cuh"
 
@@ -415,14 +417,38 @@ void c16_launch(void (*kernel)(KArgs...), cudaStream_t s, Args&&... args) {
 
 }  // namespace
 
+// Per device: cluster launch supported and at least one 16-CTA cluster of
+// these kernels fits (a partitioned GPU may have smaller GPCs); otherwise the
+// level stays on the tile kernels.
 bool c16_supported(const Geo& g) {
-    static const int ok = [] {
-        int dev = 0, v = 0;
-        if (cudaGetDevice(&dev) != cudaSuccess) return 0;
-        if (cudaDeviceGetAttribute(&v, cudaDevAttrClusterLaunch, dev) != cudaSuccess) return 0;
-        return v;
-    }();
-    return ok && g.H == 4 * kBH;
+    if (g.H != 4 * kBH) return false;
+    static std::atomic<int> ok_dev[64];   // 0 unknown, 1 yes, 2 no
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return false;
+    int st = ok_dev[dev].load();
+    if (st == 0) {
+        int v = 0, nclusters = 0;
+        bool ok = cudaDeviceGetAttribute(&v, cudaDevAttrClusterLaunch, dev) == cudaSuccess && v;
+        for (int k = 0; ok && k < 2; ++k) {
+            const void* fn = k == 0 ? reinterpret_cast<const void*>(k_c16_down) : reinterpret_cast<const void*>(k_c16_up);
+            ok = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess;
+            cudaLaunchConfig_t cfg{};
+            cfg.gridDim = dim3(kC16);
+            cfg.blockDim = dim3(kC16T);
+            cudaLaunchAttribute at{};
+            at.id = cudaLaunchAttributeClusterDimension;
+            at.val.clusterDim.x = kC16;
+            at.val.clusterDim.y = 1;
+            at.val.clusterDim.z = 1;
+            cfg.attrs = &at;
+            cfg.numAttrs = 1;
+            ok = ok && cudaOccupancyMaxActiveClusters(&nclusters, fn, &cfg) == cudaSuccess && nclusters > 0;
+        }
+        (void)cudaGetLastError();
+        st = ok ? 1 : 2;
+        ok_dev[dev].store(st);
+    }
+    return st == 1;
 }
 
 void launch_c16_down(const TileDown& a, int pre, cudaStream_t s) { c16_launch(k_c16_down, s, a, pre); }
