@@ -370,6 +370,27 @@ __device__ void coarse_solve(const FusedArgs& a, const double* inv, double* part
         // gathered into compact order (part[4 nc ..]) so the dot loop carries
         // no index arithmetic.
         const int nc = a.nc, cs = (nc + 3) / 4;
+        if constexpr (HC == 4) {
+            if (nc == 64 && kThreads == 256) {   // the usual 8x8-cell coarsest level: no gather phase,
+                // thread (row, quarter k) reads its 16 columns' r straight from the padded
+                // layout (column j = 16 k + jj is colour k, plane position jj)
+                const int row = threadIdx.x & 63, k = threadIdx.x >> 6;
+                const double* iv = inv + (size_t)(16 * k) * 64 + row;
+                const double* rk = r + k * lgPP<4>(L);
+                double s = 0.0;
+#pragma unroll
+                for (int jj = 0; jj < 16; ++jj) s = fma(iv[jj * 64], rk[((jj >> 2) + 1) * lgW2<4>(L) + (jj & 3) + 1], s);
+                part[k * 64 + row] = s;
+                __syncthreads();
+                if (threadIdx.x < 64) {
+                    const int c = row >> 4, pos = row & 15;
+                    u[pidxh<4>(L, c, pos & 3, pos >> 2)] =
+                        ((part[row] + part[64 + row]) + part[128 + row]) + part[192 + row];
+                }
+                __syncthreads();
+                return;
+            }
+        }
         double* rc = part + 4 * nc;
         for (int j = threadIdx.x; j < nc; j += kThreads) {
             const int c = j >> (2 * lgLH<HC>(L)), pos = j & (lgNQ<HC>(L) - 1);
