@@ -754,7 +754,7 @@ __device__ void tier_run(const FusedArgs& a, unsigned char* sm, const Geo* sgeo,
             if (q < nl - 1) {
                 FCLK_BEGIN
                 const SLevel Cn = slev(a, sm, sgeo, q + 1);
-                if (q == 0 && top_reg) cycle_down<0>(a, L, cur, Cn, u, &rv0);
+                if (q == 0 && top_reg) cycle_down<kRH>(a, L, cur, Cn, u, &rv0);
                 else if (L.H == 8) cycle_down<8>(a, L, cur, Cn, u, nullptr);
                 else if (L.H == 4) cycle_down<4>(a, L, cur, Cn, u, nullptr);
                 else cycle_down<0>(a, L, cur, Cn, u, nullptr);
@@ -782,7 +782,7 @@ __device__ void tier_run(const FusedArgs& a, unsigned char* sm, const Geo* sgeo,
         } else {
             FCLK_BEGIN
             bool done;
-            if (q == 0 && top_reg) done = pcg_step<0>(a, L, cur, red, par, &rv0);
+            if (q == 0 && top_reg) done = pcg_step<kRH>(a, L, cur, red, par, &rv0);
             else if (L.H == 8) done = pcg_step<8>(a, L, cur, red, par, nullptr);
             else if (L.H == 4) done = pcg_step<4>(a, L, cur, red, par, nullptr);
             else done = pcg_step<0>(a, L, cur, red, par, nullptr);
@@ -805,7 +805,7 @@ __device__ void tier_run(const FusedArgs& a, unsigned char* sm, const Geo* sgeo,
         const SLevel P = slev(a, sm, sgeo, q);
         FCLK_BEGIN
         double* up = P.p + cur.step * 4 * P.PP;
-        if (q == 0 && top_reg) cycle_up<0>(a, P, L, child, up, &rv0);
+        if (q == 0 && top_reg) cycle_up<kRH>(a, P, L, child, up, &rv0);
         else if (P.H == 8) cycle_up<8>(a, P, L, child, up, nullptr);
         else if (P.H == 4) cycle_up<4>(a, P, L, child, up, nullptr);
         else cycle_up<0>(a, P, L, child, up, nullptr);
