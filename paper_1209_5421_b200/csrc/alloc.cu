@@ -1,8 +1,12 @@
 // alloc.cu — process-wide caching device allocator (see hier.cuh).
+#include <condition_variable>
+#include <thread>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <set>
 #include <tuple>
+#include <vector>
 
 #include "hier.cuh"
 
@@ -101,6 +105,109 @@ void ensure_smem_impl(const void* func, int bytes) {
     if (done.count({func, dev, bytes})) return;
     AUX_CUDA(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     done.insert({func, dev, bytes});
+}
+
+namespace {
+struct DriverPools {
+    std::mutex mu;
+    std::multimap<int, cudaStream_t> streams;    // device -> idle stream
+};
+DriverPools& pools() {
+    static DriverPools* p = new DriverPools();   // never destroyed: outlives every hierarchy
+    return *p;
+}
+}  // namespace
+
+cudaStream_t stream_pool_get() {
+    const int dev = current_device();
+    {
+        std::lock_guard<std::mutex> lk(pools().mu);
+        auto it = pools().streams.find(dev);
+        if (it != pools().streams.end()) {
+            cudaStream_t s = it->second;
+            pools().streams.erase(it);
+            return s;
+        }
+    }
+    cudaStream_t s = nullptr;
+    AUX_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    return s;
+}
+
+void stream_pool_put(cudaStream_t s) {   // the caller synchronised it
+    if (!s) return;
+    const int dev = current_device();
+    std::lock_guard<std::mutex> lk(pools().mu);
+    pools().streams.emplace(dev, s);
+}
+
+// A retired executable graph is destroyed by a background thread: the
+// destroy call blocks for 10+ ms whenever another process holds the driver
+// lock, and nothing waits for it.  (Re-targeting cached executables with
+// cudaGraphExecUpdate was tried: the update reports success for captures of
+// another hierarchy with the same topology, yet the replay is wrong.)
+cudaGraphExec_t graph_exec_acquire(cudaGraph_t g) {
+    cudaGraphExec_t e = nullptr;
+    AUX_CUDA(cudaGraphInstantiate(&e, g, 0));
+    return e;
+}
+
+namespace {
+struct Reaper {
+    std::mutex mu;
+    std::mutex busy;   // held while destroying: process exit waits for the batch, then stops the thread
+    std::condition_variable cv;
+    std::vector<std::pair<int, cudaGraphExec_t>> q;
+    bool started = false;
+    bool exiting = false;
+    void start() {
+        std::atexit([] {   // before the CUDA runtime's own teardown; leftovers go with the context
+            Reaper& r = reaper_ref();
+            {
+                std::lock_guard<std::mutex> lk(r.mu);
+                r.exiting = true;
+                r.cv.notify_one();
+            }
+            std::lock_guard<std::mutex> b(r.busy);   // a batch in progress finishes first
+        });
+        std::thread([this] {
+            for (;;) {
+                std::vector<std::pair<int, cudaGraphExec_t>> work;
+                std::unique_lock<std::mutex> b(busy, std::defer_lock);
+                {
+                    std::unique_lock<std::mutex> lk(mu);
+                    cv.wait(lk, [this] { return !q.empty() || exiting; });
+                    if (exiting) return;
+                    work.swap(q);
+                    b.lock();   // (taken under mu: exit either sees no batch or waits for this one)
+                }
+                for (auto& w : work) {
+                    cudaSetDevice(w.first);
+                    cudaGraphExecDestroy(w.second);
+                }
+            }
+        }).detach();
+    }
+    static Reaper& reaper_ref();
+};
+Reaper& Reaper::reaper_ref() {
+    static Reaper* r = new Reaper();   // never destroyed (detached thread)
+    return *r;
+}
+Reaper& reaper() { return Reaper::reaper_ref(); }
+}  // namespace
+
+void graph_exec_release(cudaGraphExec_t e) {   // no launch of e may still be in flight
+    if (!e) return;
+    Reaper& r = reaper();
+    std::lock_guard<std::mutex> lk(r.mu);
+    if (!r.started) {
+        r.start();
+        r.started = true;
+    }
+    if (r.exiting) return;   // the context goes away with the process
+    r.q.emplace_back(current_device(), e);
+    r.cv.notify_one();
 }
 
 }  // namespace auxb200

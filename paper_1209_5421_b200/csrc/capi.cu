@@ -47,7 +47,10 @@ aux_hierarchy* make_h(const aux_setup_opts* o, const aux_gpu_opts* g) {
     if (g) h->gpu = *g;
     AUX_CUDA(cudaSetDevice(h->gpu.device));
     AUX_CUDA(cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, h->gpu.device));
-    AUX_CUDA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+    {
+        HostCallTimer tm("stream_pool_get");
+        h->stream = stream_pool_get();
+    }
     h->red_partials.alloc((size_t)kMaxRedBlocks * 4);
     h->red_ticket.alloc(1);
     AUX_CUDA(cudaMemsetAsync(h->red_ticket.p, 0, sizeof(unsigned int), h->stream));
@@ -57,7 +60,12 @@ aux_hierarchy* make_h(const aux_setup_opts* o, const aux_gpu_opts* g) {
 }  // namespace
 
 aux_hierarchy::~aux_hierarchy() {
-    if (graph) cudaGraphExecDestroy(graph);
+    HostCallTimer tm_all("destroy (total)");
+    if (stream) cudaStreamSynchronize(stream);   // no launch of the graph still in flight
+    if (graph) {
+        HostCallTimer tm("graph_exec_release");
+        graph_exec_release(graph);
+    }
     for (int k = 0; k < kProfKinds; ++k) {
         for (auto e : prof.ev_begin[k]) cudaEventDestroy(e);
         for (auto e : prof.ev_end[k]) cudaEventDestroy(e);
@@ -70,7 +78,10 @@ aux_hierarchy::~aux_hierarchy() {
     lv.clear();
     w_p.clear();
     w_ap.clear();
-    if (stream) cudaStreamDestroy(stream);
+    if (stream) {
+        HostCallTimer tm("stream_pool_put");
+        stream_pool_put(stream);   // synchronised above
+    }
 }
 
 extern "C" {

@@ -20,6 +20,10 @@
 // column indices are implicit.
 #pragma once
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -124,6 +128,24 @@ __device__ __forceinline__ double div_rcp(double a, double b, double y) {
     if (aq >= 0x1p-800 && aq <= 0x1p+800) return __fma_rn(__fma_rn(-q, b, a), y, q);
     return ddiv_out_of_line(a, b);   // rare: one shared copy keeps the latency-bound kernels' code small
 }
+
+// AUX_HOSTCALL_TRACE=<ms>: report host-side driver calls of the per-step
+// path (stream / graph creation and destruction) that take longer than <ms>
+// (diagnostics for stalls caused by other processes' driver queries).
+struct HostCallTimer {
+    const char* name;
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    explicit HostCallTimer(const char* n) : name(n) {}
+    ~HostCallTimer() {
+        static const double thr = [] {
+            const char* e = std::getenv("AUX_HOSTCALL_TRACE");
+            return e ? std::atof(e) : -1.0;
+        }();
+        if (thr < 0) return;
+        const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        if (ms > thr) std::fprintf(stderr, "[aux hostcall] %s %.2f ms\n", name, ms);
+    }
+};
 
 // --------------------------------------------------------------- layout
 

@@ -19,6 +19,16 @@ namespace auxb200 {
 // returning its blocks.
 void* dev_alloc(size_t bytes);
 void dev_free(void* p, size_t bytes);
+// Per-hierarchy driver objects (alloc.cu): a solve that sets up and destroys
+// a hierarchy per system would otherwise create and destroy a stream and
+// destroy a graph every time, and those driver calls block for 10-15 ms
+// whenever another process (nvidia-smi, a monitoring agent) holds the driver
+// lock.  Streams are pooled (they come back idle); retired executable graphs
+// are destroyed by a background thread.
+cudaStream_t stream_pool_get();
+void stream_pool_put(cudaStream_t s);
+cudaGraphExec_t graph_exec_acquire(cudaGraph_t g);
+void graph_exec_release(cudaGraphExec_t e);
 
 // RAII device buffer.
 template <class T>

@@ -1581,7 +1581,7 @@ void build_graph(aux_hierarchy* h, const aux_cycle_opts& o, RedState rs) {
         h->graph_opts.post_sweeps == o.post_sweeps)
         return;
     if (h->graph) {
-        cudaGraphExecDestroy(h->graph);
+        graph_exec_release(h->graph);
         h->graph = nullptr;
     }
     h->graph_valid = false;
@@ -1600,6 +1600,7 @@ void build_graph(aux_hierarchy* h, const aux_cycle_opts& o, RedState rs) {
     }
     const int64_t before = g_launches;
     cudaGraph_t g = nullptr;
+    HostCallTimer tm_cap("coarse-cycle capture + instantiate");
     AUX_CUDA(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
     if (h->dist.comm && h->dist.comm->size > 1) {
         // a capture the communication library refuses leaves the multi-GPU
@@ -1627,7 +1628,10 @@ void build_graph(aux_hierarchy* h, const aux_cycle_opts& o, RedState rs) {
         h->graph_kernels = g_launches - before;
         g_launches = before;
     }
-    AUX_CUDA(cudaGraphInstantiate(&h->graph, g, 0));
+    {
+        HostCallTimer tm("graph_exec_acquire");
+        h->graph = graph_exec_acquire(g);
+    }
     cudaGraphDestroy(g);
     h->graph_opts = o;
     h->graph_valid = true;

@@ -24,9 +24,11 @@ for _ in range(3):
     api.solve_device(h, d[4].data_ptr(), du.data_ptr(), N)
     del h
 torch.cuda.synchronize()
-smi = subprocess.Popen(["nvidia-smi", "--query-gpu=clocks.sm,clocks_event_reasons.active", "--format=csv,noheader",
-                        "-lms", "50"], stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
-time.sleep(1.0)
+q = os.environ.get("SMI_Q", "clocks.sm,clocks_event_reasons.active")
+smi = None if q == "off" else subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader",
+                                               "-lms", os.environ.get("SMI_MS", "50")],
+                                              stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+time.sleep(float(os.environ.get("SMI_WAIT", "1.0")))
 for k in range(steps):
     t0 = time.perf_counter()
     h = api.setup_hierarchy_device(N, s.A.nnz, d[0].data_ptr(), d[1].data_ptr(), d[2].data_ptr(), d[3].data_ptr(), N)
@@ -38,4 +40,5 @@ for k in range(steps):
     t3 = time.perf_counter()
     print(f"step {k:2d}: host setup {1e3*(t1-t0):7.2f} (dev {a:6.2f})  solve {1e3*(t2-t1):7.2f} (dev {b:6.2f})  "
           f"destroy {1e3*(t3-t2):6.2f}", flush=True)
-smi.terminate()
+if smi is not None:
+    smi.terminate()
