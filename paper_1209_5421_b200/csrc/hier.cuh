@@ -237,6 +237,7 @@ struct aux_hierarchy {
     long graph_kernels = 0;
     aux_cycle_opts graph_opts{};
     bool graph_valid = false;
+    bool graph_pending = false;   // single GPU: captured at the first coarse visit, behind the finest kernels
     int fused_m0 = 1 << 30;          // first level run by the single-CTA kernel
     bool tiles = false;              // levels [1, fused_m0) run the overlapped-tile kernels
     auxb200::DBuf<auxb200::FLevel> d_flv;

@@ -1220,6 +1220,7 @@ void gather_root_v(aux_hierarchy* h, int t, const std::vector<double*>& vecs, cu
 }
 
 void pcg_tiles(Ctx& c, int m);
+void build_graph(aux_hierarchy* h, const aux_cycle_opts& o, RedState rs);
 
 // Levels whose nonlinear_pcg runs as one kernel that writes the iterate u
 // itself (single-CTA tier, cluster tier); elsewhere the parent sums alpha_k p_k.
@@ -1529,6 +1530,14 @@ void finest_cycle(Ctx& c, const double* f, double* u, double* snap) {
     AUX_LAUNCHED(2);
     prof_end(c, 2, 12.0 * F.nnz + 4.0 * (F.n + 1) + 16.0 * F.n + 4.0 * (C.n + 1) + 8.0 * C.n);
     g_trace.mark(c.s, 1);
+    if (h->graph_pending) {
+        h->graph_pending = false;
+        const auto tg0 = std::chrono::steady_clock::now();
+        build_graph(h, c.o, c.rs);
+        if (g_trace.on)
+            fprintf(stderr, "[aux trace] graph build %.3f ms host\n",
+                    std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tg0).count());
+    }
     prof_begin(c, 3);
     if (h->graph_valid) {
         AUX_CUDA(cudaGraphLaunch(h->graph, c.s));
@@ -1854,12 +1863,16 @@ void solve_device(aux_hierarchy* h, const double* b, long n_b, const aux_cycle_o
         for (size_t l = 1; l + 1 < h->lv.size(); ++l)
             if (h->lv[l].zero_diag_lex >= 0)
                 throw_aux(AUX_SINGULAR_ERROR, "zero diagonal at row " + std::to_string(h->lv[l].zero_diag_lex));
-        {
+        if (h->dist.comm && h->dist.comm->size > 1) {
             const auto tg0 = std::chrono::steady_clock::now();
             build_graph(h, *o, rs);
             if (g_trace.on)
                 fprintf(stderr, "[aux trace] graph build %.3f ms host\n",
                         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tg0).count());
+        } else {
+            // one GPU: (re)captured at the first coarse visit, so the host work
+            // overlaps the first finest smoothing already queued on the device
+            h->graph_pending = true;
         }
         Ctx c{h, s, *o, rs, h->prof.on != 0};
         // colour-pass byte counts for the profile
