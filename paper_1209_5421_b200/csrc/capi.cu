@@ -157,10 +157,10 @@ aux_status aux_setup(const aux_csr_view* A, const double* xy, int64_t n_points, 
             ~Side() {   // (destroyed before v: an error thrown mid-copy still waits for it)
                 if (s) cudaStreamSynchronize(s);
                 if (e) cudaEventDestroy(e);
-                if (s) cudaStreamDestroy(s);
+                if (s) stream_pool_put(s);
             }
         } side;
-        AUX_CUDA(cudaStreamCreateWithFlags(&side.s, cudaStreamNonBlocking));
+        side.s = stream_pool_get();
         AUX_CUDA(cudaEventCreateWithFlags(&side.e, cudaEventDisableTiming));
         AUX_CUDA(cudaMemcpyAsync(rp.p, A->row_ptr, sizeof(int) * (n + 1), cudaMemcpyHostToDevice, h->stream));
         if (n_points > 0)
