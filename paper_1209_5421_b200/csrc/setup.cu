@@ -1152,7 +1152,7 @@ void finest_blocks(aux_hierarchy* h, const Geo& gL, unsigned long long& sing, in
                 else if (cls == 1) launch(k_factor_warp<16>);
                 else launch(k_factor_warp<32>);
                 AUX_LAUNCHED(2);
-                AUX_CUDA(cudaStreamSynchronize(s));
+                // (l7 may go: a freed block is only reused by work ordered after this on the stream)
             }
         }
         DBuf<int> pos(nL + 1);
@@ -1166,9 +1166,8 @@ void finest_blocks(aux_hierarchy* h, const Geo& gL, unsigned long long& sing, in
             k_compact<<<grid_for(nL), kT, 0, s>>>(flag.p, pos.p, nL, F.big_ids.p);
             AUX_LAUNCHED(1);
             std::vector<int> ids(nbig), bp0(nbig), bp1(nbig);
-            AUX_CUDA(cudaMemcpyAsync(ids.data(), F.big_ids.p, sizeof(int) * nbig, cudaMemcpyDeviceToHost, s));
-            AUX_CUDA(cudaStreamSynchronize(s));
             std::vector<int> bptr_h(nL + 1);
+            AUX_CUDA(cudaMemcpyAsync(ids.data(), F.big_ids.p, sizeof(int) * nbig, cudaMemcpyDeviceToHost, s));
             AUX_CUDA(cudaMemcpyAsync(bptr_h.data(), F.bptr.p, sizeof(int) * (nL + 1), cudaMemcpyDeviceToHost, s));
             AUX_CUDA(cudaStreamSynchronize(s));
             // order: per colour, the warp class (<= 32 members) then the CTA
@@ -1211,7 +1210,6 @@ void finest_blocks(aux_hierarchy* h, const Geo& gL, unsigned long long& sing, in
                     mid_d.p, F.bptr.p, F.rp.p, F.col.p, F.v.p, gL, F.cell_lu_off.p, F.big_lu.p, F.big_perm.p, err.p,
                     h->gpu.block_solve == 0 ? F.inv_off.p : nullptr, h->gpu.block_solve == 0 ? F.inv.p : nullptr, x_smem);
                 AUX_LAUNCHED(1);
-                AUX_CUDA(cudaStreamSynchronize(s));
             }
             if (!huge.empty()) {   // beyond shared memory: factors in place in global memory
                 DBuf<int> hid(huge.size());
@@ -1224,15 +1222,16 @@ void finest_blocks(aux_hierarchy* h, const Geo& gL, unsigned long long& sing, in
                                                                    F.big_perm.p, F.inv_off.p, F.inv.p);
                     AUX_LAUNCHED(1);
                 }
-                AUX_CUDA(cudaStreamSynchronize(s));
             }
         }
-        sing = read1(err.p, s);
+        // the singular-block verdict and the colour check in one read-back
         DBuf<int> cflag(1);
         AUX_CUDA(cudaMemsetAsync(cflag.p, 0, sizeof(int), s));
         k_color_check<<<grid_for(n), kT, 0, s>>>(F.rp.p, F.col.p, F.v.p, F.cell.p, n, gL.lq, cflag.p);
         AUX_LAUNCHED(1);
-        color_flag = read1(cflag.p, s);
+        AUX_CUDA(cudaMemcpyAsync(&sing, err.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+        AUX_CUDA(cudaMemcpyAsync(&color_flag, cflag.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+        AUX_CUDA(cudaStreamSynchronize(s));
     }
 
 }
@@ -1602,20 +1601,30 @@ void setup_device(aux_hierarchy* h, const aux_csr_view* A, const double* xy, lon
         k_coarsen<<<grid_for(nx.n), kT, 0, s>>>(cur.geo, cur.val.p, cur.active.p, nx.geo, nx.val.p, nx.active.p, ovf.p);
         AUX_LAUNCHED(1);
     }
-    if (read1(ovf.p, s)) throw_aux(AUX_STRUCTURE_ERROR, "4-child coarsening escaped the 9-point stencil");
-
-    // ---- per-level nnz and zero-diagonal records
+    // ---- per-level nnz and zero-diagonal records, read back for all levels
+    // at once together with the coarsening overflow flag (one host sync
+    // instead of two per level)
     {
-        DBuf<unsigned long long> cnt(1), zd(1);
-        for (size_t l = 1; l < h->lv.size(); ++l) {
+        const size_t nlev = h->lv.size();
+        DBuf<unsigned long long> cz(2 * nlev);
+        AUX_CUDA(cudaMemsetAsync(cz.p, 0, sizeof(unsigned long long) * nlev, s));
+        AUX_CUDA(cudaMemsetAsync(cz.p + nlev, 0xff, sizeof(unsigned long long) * nlev, s));
+        for (size_t l = 1; l < nlev; ++l) {
             auxb200::Level& L = h->lv[l];
-            AUX_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long), s));
-            AUX_CUDA(cudaMemsetAsync(zd.p, 0xff, sizeof(unsigned long long), s));
-            k_level_nnz<<<grid_for(L.n, 4), kT, 0, s>>>(L.geo, L.active.p, cnt.p);
-            k_zero_diag<<<grid_for(L.n, 4), kT, 0, s>>>(L.geo, L.val.p, L.active.p, zd.p);
+            k_level_nnz<<<grid_for(L.n, 4), kT, 0, s>>>(L.geo, L.active.p, cz.p + l);
+            k_zero_diag<<<grid_for(L.n, 4), kT, 0, s>>>(L.geo, L.val.p, L.active.p, cz.p + nlev + l);
             AUX_LAUNCHED(2);
-            L.nnz = (long)read1(cnt.p, s);
-            const unsigned long long z = read1(zd.p, s);
+        }
+        std::vector<unsigned long long> hv(2 * nlev);
+        int ov = 0;
+        AUX_CUDA(cudaMemcpyAsync(hv.data(), cz.p, sizeof(unsigned long long) * 2 * nlev, cudaMemcpyDeviceToHost, s));
+        AUX_CUDA(cudaMemcpyAsync(&ov, ovf.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+        AUX_CUDA(cudaStreamSynchronize(s));
+        if (ov) throw_aux(AUX_STRUCTURE_ERROR, "4-child coarsening escaped the 9-point stencil");
+        for (size_t l = 1; l < nlev; ++l) {
+            auxb200::Level& L = h->lv[l];
+            L.nnz = (long)hv[l];
+            const unsigned long long z = hv[nlev + l];
             L.zero_diag_lex = z == ~0ull ? -1 : (int)(z % (unsigned long long)L.n);
         }
     }
