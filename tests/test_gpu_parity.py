@@ -352,3 +352,18 @@ def test_outer_mgs_deferred_ap_bitwise(gpu_api, name, opts, monkeypatch):
     assert r1.iterations == r0.iterations
     assert np.array_equal(r1.u, r0.u)
     assert np.array_equal(np.asarray(r1.residual_history), np.asarray(r0.residual_history))
+
+
+@pytest.mark.parametrize("opts", [dict(pre_sweeps=3, post_sweeps=3), dict(pre_sweeps=1, post_sweeps=3),
+                                  dict(n_inner=4), dict(n_inner=9), dict(n_inner=9, max_directions=1)])
+def test_uncommon_cycle_options(gpu_api, opts):
+    """Options outside the fast tiers' range (3 sweeps: no tile kernels; more than
+    8 inner steps: no single-CTA / cluster tier) run the generic per-phase path
+    and still match the oracle."""
+    s = problems.jittered_p1(129)
+    h = gpu_api.setup_hierarchy(s.A, s.coords)
+    res = gpu_api.solve(s.A, s.b, h, gpu_api.CycleOptions(**opts))
+    ref = ob.CpuHierarchy("oracle", s.A, s.coords).solve(s.b, ob.cycle_opts(**opts))
+    assert abs(res.iterations - ref["iterations"]) <= 1
+    err = np.max(np.abs(res.u - ref["u"])) / np.max(np.abs(ref["u"]))
+    assert err <= U_TOL, err
