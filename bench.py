@@ -81,11 +81,24 @@ def make_problem(cfg):
     return problems.make(cfg["kind"], cfg["n"], cfg["param"], 1, cfg["jump"])
 
 
+L2_BYTES = 126e6
+
+
+def input_bytes(N, nnz):
+    return 12 * nnz + 4 * (N + 1) + 24 * N
+
+
+def needs_flush(N, nnz):
+    """Inputs that fit the 126 MB L2 twice over get an explicit L2 flush before every timed step."""
+    return input_bytes(N, nnz) < 2 * L2_BYTES
+
+
 def config_dict(cfg, N, nnz):
     """The `config` object, identical in both arms."""
-    inputs = 12 * nnz + 4 * (N + 1) + 24 * N
-    return {"workload": cfg["name"], "N": int(N), "nnz": int(nnz), "rtol": 1e-6,
-            "l2": f"inputs {inputs / 1e6:.0f} MB > 126 MB L2 (no flush needed)"}
+    inputs = input_bytes(N, nnz)
+    l2 = (f"inputs {inputs / 1e6:.0f} MB > 2 x 126 MB L2 (no flush needed)" if not needs_flush(N, nnz) else
+          f"inputs {inputs / 1e6:.0f} MB < 2 x 126 MB L2: a 256 MB buffer is written (L2 flush) before every timed step")
+    return {"workload": cfg["name"], "N": int(N), "nnz": int(nnz), "rtol": 1e-6, "l2": l2}
 
 
 def peaks():
@@ -337,10 +350,19 @@ def main():
         iters = None
         setup_ms, solve_ms = [], []
         step_ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+        flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev) if needs_flush(N, nnz) else None
+
+        def l2_flush(k):
+            if flush is not None:   # (the library's own stream starts after this completes)
+                flush.fill_(k & 0xff)
+                torch.cuda.current_stream().synchronize()
+
+        l2_flush(0)   # the fill kernel loads lazily: not inside the timed region
         with ClockSampler(local) as clk:
             barrier()
             ev0.record()
             for k in range(steps):
+                l2_flush(k)
                 step_ev[k].record()
                 h = setup_dev()
                 r = api.solve_device(h, d_b.data_ptr(), d_u.data_ptr(), N)
@@ -385,7 +407,8 @@ def main():
         barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        for _ in range(steps):
+        for k in range(steps):
+            l2_flush(k)
             h = setup_host(A_h, xy_h)
             res = api.solve(A_h, b_h, h, out=u_h)
             del h
