@@ -6,10 +6,13 @@
 // moves ~3 MB: 7.7 + 11.5 us of tile kernels and ~8 us of MGS per step).  Here
 // CTA (qx, qy) of a 4x4 cluster owns the 32x32 cells of one block (thread t:
 // plane position t of all four colours, its 36 stencil values in registers),
-// and the blocks exchange through distributed shared memory: after every
-// colour pass a CTA pushes that colour's boundary cells into its (up to
-// eight) neighbours' ghost rings (st.shared::cluster) and one cluster barrier
-// separates the passes.  Inner products are per-CTA sums pushed to every CTA
+// and the blocks exchange through distributed shared memory: in every colour
+// pass the thread that updates a boundary cell pushes the new value into the
+// (up to eight) neighbours' ghost rings (st.shared::cluster), and one cluster
+// barrier separates the passes (no CTA barrier of its own); the start-up
+// barrier is split (arrive after the local fill, wait before the first push).
+// Gauss-Seidel divides through register-resident reciprocal diagonals
+// (common.cuh div_rcp: bitwise __ddiv_rn).  Inner products are per-CTA sums pushed to every CTA
 // and added in CTA order, so every CTA holds the same alpha / beta; the whole
 // A-orthogonalisation of the step (cycle.hpp:84-97) runs inside the up
 // kernel on register-resident z and A z.
@@ -19,7 +22,8 @@
 //               restriction into the child (cycle.hpp:173-178)
 //   k_c16_up    prolongation of the child's iterate on own + ghost cells
 //               (cycle.hpp:191-194, same arithmetic as the neighbour, so no
-//               exchange), transposed post-smoothing (cycle.hpp:196), A z,
+//               exchange; colour-3 ghosts are left to the neighbour's first
+//               post-smoothing push), transposed post-smoothing (cycle.hpp:196), A z,
 //               the step's inner products, MGS and alpha (cycle.hpp:106-128)
 //
 // Per-cell arithmetic is that of the tile kernels (bitwise colour-ordered
