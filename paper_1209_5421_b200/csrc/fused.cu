@@ -866,11 +866,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_pcg(const __grid_constant
 // (thread t: plane position t of all four colours, the 36 stencil values in
 // registers); CTA 4 runs the single-CTA tier (tier_run) for every
 // preconditioner application.  The CTAs exchange through distributed shared
-// memory: after every colour pass a quadrant pushes the updated boundary of
-// that colour into its three neighbours' ghost rings (st.shared::cluster),
-// the restriction stores straight into CTA 4's right-hand side, the
-// prolongation loads CTA 4's directions (ld.shared::cluster), and inner
-// products are per-CTA block sums pushed to every CTA and added in CTA order.
+// memory: in every colour pass the thread that updates a quadrant boundary
+// cell pushes the new value into the neighbours' ghost rings
+// (st.shared::cluster), the restriction stores straight into CTA 4's
+// right-hand side, CTA 4 pushes each coarse cell's combined correction to the
+// quadrants whose parents include it, and inner products are per-CTA block
+// sums pushed to every CTA and added in CTA order.
 // One cluster barrier (barrier.cluster arrive.release / wait.acquire)
 // separates dependent phases — it replaces a kernel boundary.  Per-element
 // arithmetic is that of the tile kernels (bitwise colour-ordered GS).
