@@ -919,15 +919,6 @@ __device__ __forceinline__ uint32_t mapa(const void* p, uint32_t rank) {
 __device__ __forceinline__ void st_cluster(const void* p, uint32_t rank, double v) {
     asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(mapa(p, rank)), "d"(v) : "memory");
 }
-// (not volatile, no memory clobber: the loads of one phase issue together;
-// ordering against the producer comes from the cluster barrier before them)
-__device__ __forceinline__ double ld_cluster(const void* p, uint32_t rank) {
-    uint32_t ra;
-    asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(p)), "r"(rank));
-    double v;
-    asm("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(ra));
-    return v;
-}
 
 // Push one freshly computed colour-C value of this thread's plane position
 // (ta, tb) into the neighbours' ghost rings when it sits on an edge facing
